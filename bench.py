@@ -1,0 +1,459 @@
+#!/usr/bin/env python
+"""Benchmark: walker-steps/sec for node2vec on R-MAT scale-24 (BASELINE.json configs[1]).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+One step = one full walk batch: every vertex of the R-MAT s24 ef16 graph
+(uniform [1,5) weights) starts one node2vec walker (a=p=0.5, b=q=2, 80
+steps, adaptive eRJS/eRVS with the device-calibrated cost ratio).  One
+process per GPU, graph replicated, no collective in the hot loop.  Scaling is weak: every rank walks
+one walker per vertex (global walker id = rank * V + v, so every rank draws
+distinct Philox streams) and `value` is the walker-steps of all ranks over the
+slowest rank's time.  Inputs are resident in HBM when
+the timed region starts; the graph (2.7 GB) is far larger than L2 (126 MB),
+so no L2 flush is needed between steps.
+
+--impl reference times the reference's own CPU run_queries
+(oracle/_ref/libdynwalk_ref.so, compiled from the reference sources) on the
+host cores, on a bounded walker sample of the same graph (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "walker-steps/sec (node2vec, R-MAT s24) at 1/2/4/8 B200; % of HBM roofline"
+UNIT = "walker-steps/s"
+TOPO_SEED, WEIGHT_SEED, WALK_SEED, PROFILE_SEED = 1, 2, 7, 5
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scale", type=int, default=24)
+    ap.add_argument("--walk-length", type=int, default=80)
+    ap.add_argument("--a", type=float, default=0.5)
+    ap.add_argument("--b", type=float, default=2.0)
+    ap.add_argument("--mode", default="adaptive")
+    ap.add_argument("--ratio", type=float, default=0.0, help="override the calibrated ratio")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-only", action="store_true",
+                    help="build + 1 warm walk + 1 walk, for ncu (no JSON line)")
+    return ap.parse_args()
+
+
+def workload(args) -> dict:
+    return {"workload": f"node2vec p={args.a:g} q={args.b:g}, walk length {args.walk_length}, "
+                        f"one walker per vertex, weighted R-MAT scale-{args.scale} ef16 "
+                        "(BASELINE configs[1])",
+            "graph": f"rmat s{args.scale} ef16 (A,B,C,D)=(.57,.19,.19,.05), mirrored, "
+                     "uniform[1,5) f32 weights",
+            "model": "node2vec", "a": args.a, "b": args.b, "walk_length": args.walk_length,
+            "mode": args.mode, "walkers": 2 ** args.scale,
+            "l2": "inputs larger than L2 (graph 2.7 GB vs 126 MB L2), no flush"}
+
+
+# ---------------------------------------------------------------- distributed
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def dist_init(world, local, backend):
+    import torch
+    import torch.distributed as dist
+    if world > 1 and not dist.is_initialized():
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+    return dist if world > 1 else None
+
+
+def reduce_max(x: float, dist, device) -> float:
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def reduce_sum(x: int, dist, device) -> int:
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.int64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return int(t.item())
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def ncu_traffic(scale: int):
+    """Per-launch DRAM bytes of the walk kernel from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_walk_kernel.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    if d.get("scale") != scale:
+        return None
+    return d.get("dram_bytes_per_launch")
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    world, rank, local = dist_env()
+    dist = dist_init(world, local, "nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import paper_2512_00705_b200 as dw
+
+    t0 = time.perf_counter()
+    dg = dw.DeviceGraph.rmat(args.scale, 16, seed=TOPO_SEED, weights="uniform", low=1.0,
+                             high=5.0, weight_seed=WEIGHT_SEED, devices=[local])
+    info = dg.info()
+    build_s = time.perf_counter() - t0
+    model = dw.Model("node2vec", a=args.a, b=args.b)
+    # one calibration (rank 0), broadcast so every shard makes the same decisions
+    ratio = args.ratio
+    t0 = time.perf_counter()
+    if ratio <= 0:
+        ratio = dw.profile_edge_cost_ratio(dg, model, seed=PROFILE_SEED) if rank == 0 else 0.0
+        if dist is not None:
+            t = torch.tensor([ratio], dtype=torch.float64, device=dev)
+            dist.broadcast(t, 0)
+            ratio = float(t.item())
+    calib_s = time.perf_counter() - t0
+
+    nv = info["num_vertices"]
+    # weak scaling: one walker per vertex on every rank, distinct global ids
+    lo, hi = 0, nv
+    n = nv
+    L = args.walk_length
+    opts = dw.RunOptions(mode=args.mode, walk_length=L, seed=WALK_SEED, edge_cost_ratio=ratio,
+                         qid_base=rank * nv)
+    lib = dw.load_library()
+    q = torch.arange(lo, hi, dtype=torch.int64, device=dev).to(torch.int32)
+    paths = torch.empty((max(n, 1), L + 1), dtype=torch.int32, device=dev)
+    lengths = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    mdesc, odesc = model.c(), opts.c()
+
+    def step():
+        rc = lib.dw_run_device(dg.h, 0, C.byref(mdesc), C.c_void_p(q.data_ptr()), n,
+                               C.byref(odesc), C.c_void_p(paths.data_ptr()),
+                               C.c_void_p(lengths.data_ptr()), C.c_void_p(stream.cuda_stream))
+        if rc:
+            raise dw.DynwalkError(rc, lib.dw_last_error().decode())
+        st = dw.RunStatsC()
+        rc = lib.dw_run_device_sync(dg.h, 0, C.byref(st))
+        if rc:
+            raise dw.DynwalkError(rc, lib.dw_last_error().decode())
+        return st
+
+    if args.profile_only:
+        step()
+        step()
+        torch.cuda.synchronize()
+        return
+    for _ in range(args.warmup):
+        step()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    kms, stats = [], None
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            st = step()
+            kms.append(st.kernel_ms)
+            stats = st
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    elapsed_ms = ev0.elapsed_time(ev1)
+    elapsed_ms = reduce_max(elapsed_ms, dist, dev)
+    walker_steps_rank = int(stats.steps - stats.dead_ends)
+    walker_steps = reduce_sum(walker_steps_rank, dist, dev)  # per step, all ranks
+    value = walker_steps * args.steps / (elapsed_ms / 1e3)
+    kernel_ms = reduce_max(float(np.mean(kms)), dist, dev)
+    alg_bytes = reduce_sum(int(stats.algorithmic_bytes), dist, dev)
+
+    # ---- e2e through the C ABI with pinned host buffers (H2D + D2H timed)
+    e2e = None
+    if args.e2e_steps > 0 and n > 0:
+        hq = C.c_void_p()
+        hp = C.c_void_p()
+        hl = C.c_void_p()
+        for buf, nbytes in ((hq, n * 4), (hp, n * (L + 1) * 4), (hl, n * 4)):
+            rc = lib.dw_host_alloc(nbytes, C.byref(buf))
+            if rc:
+                raise dw.DynwalkError(rc, lib.dw_last_error().decode())
+        qa = np.ctypeslib.as_array(C.cast(hq, dw.u32p), (n,))
+        qa[:] = np.arange(lo, hi, dtype=np.uint32)
+        st = dw.RunStatsC()
+
+        def e2e_step():
+            rc = lib.dw_run(dg.h, C.byref(mdesc), C.cast(hq, dw.u32p), n, C.byref(odesc),
+                            C.cast(hp, dw.u32p), C.cast(hl, dw.u32p), C.byref(st))
+            if rc:
+                raise dw.DynwalkError(rc, lib.dw_last_error().decode())
+
+        e2e_step()  # warm
+        if dist is not None:
+            dist.barrier()
+        ts = []
+        for _ in range(args.e2e_steps):
+            t0 = time.perf_counter()
+            e2e_step()
+            ts.append(time.perf_counter() - t0)
+        t_e2e = reduce_max(float(np.mean(ts)), dist, dev)
+        e2e = {"value": walker_steps / t_e2e, "unit": UNIT,
+               "h2d_bytes_per_step": reduce_sum(n * 4, dist, dev),
+               "d2h_bytes_per_step": reduce_sum(n * (L + 2) * 4, dist, dev),
+               "ms_per_step": t_e2e * 1e3,
+               "api": "dw_run (C ABI), pinned host queries/paths/lengths"}
+        for buf in (hq, hp, hl):
+            lib.dw_host_free(buf)
+
+    # ---- CPU baseline (oracle port, host cores), rank 0 at N=1 only
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_port(dg, args, ratio, nv)
+
+    if rank != 0:
+        return
+    pk = peaks()
+    achieved = alg_bytes / (kernel_ms / 1e3) / 1e9
+    traffic = ncu_traffic(args.scale)
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64 (bit-exact reference arithmetic), u32 ids",
+        "data": "synthetic R-MAT (deterministic Philox generator, on-device)",
+        "config": dict(workload(args), parallelism=f"walker-parallel x{world} (one walker per "
+                                                   "vertex per GPU, graph replicated)",
+                       edge_cost_ratio=ratio, edge_cost_ratio_source=(
+                           "override" if args.ratio > 0 else "device-calibrated (K4)")),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"],
+                     "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
+                     "peak_source": pk["source"], "kernel": "walk_kernel<Node2VecModel<true>,0>",
+                     "kernel_ms_per_launch": kernel_ms,
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "algorithmic_bytes_per_walker_step": alg_bytes / max(walker_steps, 1),
+                     "bytes_model": "SURVEY.md §8(d) minimal-sector model, counted per step "
+                                    "on the device"},
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+        "gpu_launches": int(stats.kernel_launches) * args.steps,
+        "walker_steps_per_step": walker_steps,
+        "stats": {k: int(getattr(stats, k)) for k in (
+            "steps", "select_erjs", "select_ervs", "trials", "weight_reads", "rng_draws",
+            "erjs_fallbacks", "dead_ends")},
+        "setup_s": {"graph_build": build_s, "calibration": calib_s},
+        "graph": info,
+    }
+    print(json.dumps(out), flush=True)
+
+
+def cpu_baseline_port(dg, args, ratio, nv) -> dict:
+    """The oracle (C restatement of the reference path, pthreads over all host
+    cores) on a bounded walker sample of the same graph and ratio."""
+    import oracle
+    a = dg.download()
+    og = oracle.Graph.from_csr(a["row"], a["col"], a["prop"])
+    del a
+    cores = os.cpu_count() or 1
+    m = oracle.Model("node2vec", a=args.a, b=args.b)
+    n = 1 << 14
+    rate = None
+    while True:
+        stride = max(1, nv // n)
+        q = np.arange(0, nv, stride, dtype=np.uint32)[:n]
+        t0 = time.perf_counter()
+        r = oracle.run(og, m, q, mode=args.mode, walk_length=args.walk_length, seed=WALK_SEED,
+                       ratio=ratio, rng="philox", threads=cores, keep_paths=False)
+        dt = time.perf_counter() - t0
+        ws = r.stats["steps"] - r.stats["dead_ends"]
+        rate = ws / dt
+        if dt >= args.cpu_seconds * 0.5 or n >= nv:
+            break
+        n = min(nv, int(n * max(2.0, args.cpu_seconds / max(dt, 1e-3))))
+    return {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{len(q)} walkers (every {stride}th vertex), {ws} walker-steps, "
+                      f"{dt:.1f} s, same graph/ratio/seed as the GPU run"}
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    # identical graph to the GPU arm, built on the CPU (oracle generator)
+    og = oracle.Graph.rmat_par(args.scale, 16, TOPO_SEED, 1.0, 5.0, WEIGHT_SEED, cores)
+    a = og.arrays()
+    del og
+    kind = "reference" if oracle.ref_available() else "port"
+    m = oracle.Model("node2vec", a=args.a, b=args.b)
+    nv = len(a["row"]) - 1
+    if kind == "reference":
+        g = oracle.RefGraph.from_csr(a["row"], a["col"], a["prop"])
+        del a
+        # the reference's own cost-model profile (cost_model.cpp:37-126), CLI seed
+        ratio = oracle.ref_profile_ratio(g, m, oracle.derive_seed(WALK_SEED, PROFILE_SEED))
+
+        def walk(q):
+            r = oracle.ref_run(g, m, q, mode=args.mode, walk_length=args.walk_length,
+                               seed=WALK_SEED, ratio=ratio, rng="mt19937", workers=cores,
+                               keep_paths=False)
+            return r.stats["steps"] - r.stats["dead_ends"], r.wall_ms / 1e3
+    else:
+        g = oracle.Graph.from_csr(a["row"], a["col"], a["prop"])
+        ratio = args.ratio if args.ratio > 0 else 1.2
+
+        def walk(q):
+            r = oracle.run(g, m, q, mode=args.mode, walk_length=args.walk_length,
+                           seed=WALK_SEED, ratio=ratio, rng="mt19937", threads=cores,
+                           keep_paths=False)
+            return r.stats["steps"] - r.stats["dead_ends"], r.wall_ms / 1e3
+    setup_s = time.perf_counter() - t0
+    # size the per-step sample to ~4 s of walking
+    n = 1 << 13
+    while True:
+        stride = max(1, nv // n)
+        q = np.arange(0, nv, stride, dtype=np.uint32)[:n]
+        ws, dt = walk(q)
+        if dt > 0.5 or n >= nv:
+            break
+        n *= 4
+    n = int(min(nv, max(n, n * 4.0 / max(dt, 1e-3))))
+    stride = max(1, nv // n)
+    q = np.arange(0, nv, stride, dtype=np.uint32)[:n]
+    for _ in range(args.warmup):
+        walk(q)
+    tot_ws, tot_t = 0, 0.0
+    for _ in range(args.steps):
+        ws, dt = walk(q)
+        tot_ws += ws
+        tot_t += dt
+    value = tot_ws / tot_t
+    sample = (f"{len(q)} walkers per step (every {stride}th vertex), {tot_ws // args.steps} "
+              f"walker-steps per step; time = RunStats.wall_ms")
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_t / args.steps * 1e3,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f64", "data": "synthetic R-MAT (same graph as the GPU arm, CPU-built)",
+           "impl": "reference",
+           "config": dict(workload(args), edge_cost_ratio=ratio,
+                          edge_cost_ratio_source="reference profile_edge_cost_ratio"
+                          if kind == "reference" else "fixed"),
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                            "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0},
+           "setup_s": setup_s}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+    world, _, _ = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -44,7 +44,7 @@ class OrcModel(C.Structure):
 class OrcOpts(C.Structure):
     _fields_ = [("mode", C.c_int), ("walk_length", C.c_uint32), ("seed", C.c_uint64),
                 ("cap_per_degree", C.c_uint64), ("edge_cost_ratio", C.c_double),
-                ("rng", C.c_int)]
+                ("rng", C.c_int), ("qid_base", C.c_uint64)]
 
 
 class OrcStats(C.Structure):
@@ -102,6 +102,9 @@ def lib() -> C.CDLL:
         L.orc_rmat_samples.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, u32p, u32p]
         L.orc_gen_rmat.restype = P
         L.orc_gen_rmat.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64]
+        L.orc_gen_rmat_par.restype = P
+        L.orc_gen_rmat_par.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, C.c_double,
+                                       C.c_double, C.c_uint64, C.c_int]
         L.orc_synth_philox.argtypes = [P, C.c_int, C.c_double, C.c_double, C.c_double,
                                        C.c_uint64]
         L.orc_run.argtypes = [P, C.POINTER(OrcModel), C.POINTER(OrcOpts), u32p, C.c_uint64,
@@ -249,6 +252,12 @@ class Graph:
     def rmat(scale, edge_factor, seed) -> "Graph":
         return Graph(lib().orc_gen_rmat(scale, edge_factor, seed))
 
+    @staticmethod
+    def rmat_par(scale, edge_factor, seed, low=1.0, high=5.0, weight_seed=0, threads=None):
+        threads = threads or os.cpu_count() or 1
+        return Graph(lib().orc_gen_rmat_par(scale, edge_factor, seed, low, high, weight_seed,
+                                            threads))
+
     def synth(self, kind: str, low=1.0, high=5.0, alpha=1.0, seed=0) -> "Graph":
         k = {"uniform": 0, "labels": 1, "pareto": 2, "degree": 3}[kind]
         if lib().orc_synth_weights(self.ptr, k, low, high, alpha, seed) != 0:
@@ -274,14 +283,15 @@ class RunResult:
 
 
 def run(g: Graph, model: Model, queries, mode="adaptive", walk_length=80, seed=0,
-        cap_per_degree=64, ratio=1.0, rng="philox", threads=1, keep_paths=True) -> RunResult:
+        cap_per_degree=64, ratio=1.0, rng="philox", threads=1, keep_paths=True,
+        qid_base=0) -> RunResult:
     """Oracle run_queries (runtime.cpp:192-247)."""
     q = np.ascontiguousarray(queries, np.uint32)
     paths = np.empty((len(q), walk_length + 1), np.uint32) if keep_paths else None
     lengths = np.empty(len(q), np.uint32)
     st = OrcStats()
     m = model.c()
-    o = OrcOpts(MODES[mode], walk_length, seed, cap_per_degree, ratio, RNG[rng])
+    o = OrcOpts(MODES[mode], walk_length, seed, cap_per_degree, ratio, RNG[rng], qid_base)
     import time
     t0 = time.perf_counter()
     rc = lib().orc_run(g.ptr, C.byref(m), C.byref(o), _ptr(q, u32p), len(q),

@@ -537,6 +537,213 @@ orc_graph* orc_gen_rmat(uint32_t scale, uint32_t edge_factor, uint64_t seed) {
     return g;
 }
 
+/* Parallel form of orc_gen_rmat for large scales (bench.py --impl reference
+ * input): the same samples, mirrored, as one sorted (src,dst) key array.  A
+ * full key sort equals Graph::build's per-slice stable sort by target here
+ * because duplicates are indistinguishable before weights are synthesized. */
+typedef struct {
+    uint32_t scale;
+    uint64_t ns, lo, hi;
+    uint64_t seed;
+    uint64_t* keys;
+    uint64_t loops;
+} rmat_task;
+
+static void* rmat_task_run(void* arg) {
+    rmat_task* t = (rmat_task*)arg;
+    const uint64_t chunk = 4096;
+    uint32_t s[4096], d[4096];
+    for (uint64_t b = t->lo; b < t->hi; b += chunk) {
+        const uint64_t n = b + chunk <= t->hi ? chunk : t->hi - b;
+        /* sample ids b..b+n: same draws as orc_rmat_samples */
+        const uint64_t ks = orc_derive_seed(t->seed, 0x726d6174ULL);
+        const uint64_t pk = orc_derive_seed(t->seed, 0x7065726dULL);
+        const uint32_t key[2] = {(uint32_t)ks, (uint32_t)(ks >> 32)};
+        for (uint64_t j = 0; j < n; ++j) {
+            const uint64_t i = b + j;
+            uint32_t u = 0, v = 0, rnd[4];
+            for (uint32_t lvl = 0; lvl < t->scale; ++lvl) {
+                if ((lvl & 3) == 0) {
+                    const uint32_t ctr[4] = {lvl >> 2, (uint32_t)i, (uint32_t)(i >> 32), 0x524d4154u};
+                    orc_philox4x32_10(ctr, key, rnd);
+                }
+                const uint32_t r = rnd[lvl & 3];
+                const uint32_t bu = r >= RMAT_TAB, bv = (r >= RMAT_TA && r < RMAT_TAB) || r >= RMAT_TABC;
+                u = (u << 1) | bu;
+                v = (v << 1) | bv;
+            }
+            s[j] = rmat_perm(u, t->scale, pk);
+            d[j] = rmat_perm(v, t->scale, pk);
+        }
+        for (uint64_t j = 0; j < n; ++j) {
+            const uint64_t i = b + j;
+            t->keys[i] = ((uint64_t)s[j] << 32) | d[j];
+            if (s[j] != d[j]) {
+                t->keys[t->ns + i] = ((uint64_t)d[j] << 32) | s[j];
+            } else {
+                t->keys[t->ns + i] = (uint64_t)(1ull << t->scale) << 32; /* sentinel, sorts last */
+                ++t->loops;
+            }
+        }
+    }
+    return NULL;
+}
+
+typedef struct {
+    const uint64_t* in;
+    uint64_t* out;
+    uint64_t lo, hi;
+    int shift;
+    uint64_t* hist; /* [2048] per task, then its offsets */
+} radix_task;
+
+static void* radix_count(void* arg) {
+    radix_task* t = (radix_task*)arg;
+    memset(t->hist, 0, 2048 * sizeof(uint64_t));
+    for (uint64_t i = t->lo; i < t->hi; ++i) ++t->hist[(t->in[i] >> t->shift) & 2047];
+    return NULL;
+}
+
+static void* radix_scatter(void* arg) {
+    radix_task* t = (radix_task*)arg;
+    for (uint64_t i = t->lo; i < t->hi; ++i) t->out[t->hist[(t->in[i] >> t->shift) & 2047]++] = t->in[i];
+    return NULL;
+}
+
+static void par_run(void* (*fn)(void*), void* tasks, size_t sz, int n) {
+    pthread_t th[256];
+    for (int i = 0; i < n; ++i) pthread_create(&th[i], NULL, fn, (char*)tasks + sz * (size_t)i);
+    for (int i = 0; i < n; ++i) pthread_join(th[i], NULL);
+}
+
+/* stable LSD radix sort, 11-bit digits, over the low `bits` bits */
+static uint64_t* radix_sort64(uint64_t* a, uint64_t* tmp, uint64_t n, int bits, int nt) {
+    radix_task* tk = (radix_task*)xmalloc(sizeof(radix_task) * (size_t)nt);
+    uint64_t* hist = (uint64_t*)xmalloc(sizeof(uint64_t) * 2048 * (size_t)nt);
+    for (int shift = 0; shift < bits; shift += 11) {
+        for (int t = 0; t < nt; ++t) {
+            tk[t].in = a;
+            tk[t].out = tmp;
+            tk[t].lo = n * (uint64_t)t / (uint64_t)nt;
+            tk[t].hi = n * (uint64_t)(t + 1) / (uint64_t)nt;
+            tk[t].shift = shift;
+            tk[t].hist = hist + 2048 * (size_t)t;
+        }
+        par_run(radix_count, tk, sizeof(radix_task), nt);
+        uint64_t run = 0;
+        for (int dgt = 0; dgt < 2048; ++dgt)
+            for (int t = 0; t < nt; ++t) {
+                const uint64_t c = tk[t].hist[dgt];
+                tk[t].hist[dgt] = run;
+                run += c;
+            }
+        par_run(radix_scatter, tk, sizeof(radix_task), nt);
+        uint64_t* sw = a;
+        a = tmp;
+        tmp = sw;
+    }
+    free(tk);
+    free(hist);
+    return a;
+}
+
+typedef struct {
+    orc_graph* g;
+    const uint64_t* keys;
+    uint64_t lo, hi;
+    int what; /* 0 col, 1 rows, 2 uniform props, 3 aggregates */
+    double low, high;
+    uint64_t seed;
+} fill_task;
+
+static uint64_t edge_draw(uint64_t seed, uint64_t e, uint32_t tag);
+
+static void* fill_run(void* arg) {
+    fill_task* t = (fill_task*)arg;
+    orc_graph* g = t->g;
+    if (t->what == 0) {
+        for (uint64_t e = t->lo; e < t->hi; ++e) g->col[e] = (uint32_t)t->keys[e];
+    } else if (t->what == 1) {
+        for (uint64_t v = t->lo; v < t->hi; ++v) { /* first key >= v<<32 */
+            uint64_t lo = 0, hi = g->ne;
+            while (lo < hi) {
+                const uint64_t mid = lo + (hi - lo) / 2;
+                if (t->keys[mid] < (v << 32)) lo = mid + 1; else hi = mid;
+            }
+            g->row[v] = lo;
+        }
+    } else if (t->what == 2) {
+        for (uint64_t e = t->lo; e < t->hi; ++e) {
+            const double u = (double)(edge_draw(t->seed, e, 0x57474854u) >> 11) * 0x1.0p-53;
+            g->prop[e] = (float)(t->low + u * (t->high - t->low));
+        }
+    } else {
+        for (uint64_t v = t->lo; v < t->hi; ++v) {
+            double mx = 0.0, sum = 0.0;
+            for (uint64_t e = g->row[v]; e != g->row[v + 1]; ++e) {
+                const double p = g->prop[e];
+                if (p > mx) mx = p;
+                sum += p;
+            }
+            g->nmax[v] = mx;
+            g->nsum[v] = sum;
+        }
+    }
+    return NULL;
+}
+
+static void par_fill(orc_graph* g, const uint64_t* keys, uint64_t n, int what, double low,
+                     double high, uint64_t seed, int nt) {
+    fill_task* tk = (fill_task*)xmalloc(sizeof(fill_task) * (size_t)nt);
+    for (int t = 0; t < nt; ++t) {
+        fill_task x = {g, keys, n * (uint64_t)t / (uint64_t)nt, n * (uint64_t)(t + 1) / (uint64_t)nt,
+                       what, low, high, seed};
+        tk[t] = x;
+    }
+    par_run(fill_run, tk, sizeof(fill_task), nt);
+    free(tk);
+}
+
+/* R-MAT + uniform[low,high) Philox weights (== orc_gen_rmat + orc_synth_philox
+ * kind 0), multi-threaded. */
+orc_graph* orc_gen_rmat_par(uint32_t scale, uint32_t edge_factor, uint64_t seed, double low,
+                            double high, uint64_t wseed, int nt) {
+    if (nt < 1) nt = 1;
+    if (nt > 256) nt = 256;
+    const uint64_t nv = 1ull << scale;
+    const uint64_t ns = (uint64_t)(edge_factor / 2) * nv;
+    uint64_t* keys = (uint64_t*)xmalloc(2 * ns * sizeof(uint64_t));
+    uint64_t* tmp = (uint64_t*)xmalloc(2 * ns * sizeof(uint64_t));
+    rmat_task* rt = (rmat_task*)xmalloc(sizeof(rmat_task) * (size_t)nt);
+    for (int t = 0; t < nt; ++t) {
+        rmat_task x = {scale, ns, ns * (uint64_t)t / (uint64_t)nt, ns * (uint64_t)(t + 1) / (uint64_t)nt,
+                       seed, keys, 0};
+        rt[t] = x;
+    }
+    par_run(rmat_task_run, rt, sizeof(rmat_task), nt);
+    uint64_t loops = 0;
+    for (int t = 0; t < nt; ++t) loops += rt[t].loops;
+    free(rt);
+    uint64_t* sorted = radix_sort64(keys, tmp, 2 * ns, 32 + (int)scale + 1, nt);
+    orc_graph* g = (orc_graph*)xmalloc(sizeof(orc_graph));
+    g->nv = (uint32_t)nv;
+    g->ne = 2 * ns - loops;
+    g->row = (uint64_t*)xmalloc((nv + 1) * sizeof(uint64_t));
+    g->col = (uint32_t*)xmalloc(g->ne * sizeof(uint32_t));
+    g->prop = (float*)xmalloc(g->ne * sizeof(float));
+    g->label = NULL;
+    g->nmax = (double*)xmalloc(nv * sizeof(double));
+    g->nsum = (double*)xmalloc(nv * sizeof(double));
+    par_fill(g, sorted, g->ne, 0, 0, 0, 0, nt);
+    par_fill(g, sorted, nv, 1, 0, 0, 0, nt);
+    g->row[nv] = g->ne;
+    free(keys);
+    free(tmp);
+    par_fill(g, NULL, g->ne, 2, low, high, wseed, nt);
+    par_fill(g, NULL, nv, 3, 0, 0, 0, nt);
+    return g;
+}
+
 static uint64_t edge_draw(uint64_t seed, uint64_t e, uint32_t tag) {
     const uint32_t ctr[4] = {(uint32_t)e, (uint32_t)(e >> 32), 0, tag};
     const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
@@ -583,7 +790,8 @@ int orc_synth_philox(orc_graph* g, int kind, double low, double high, double alp
         for (uint64_t e = 0; e < ne; ++e) {
             const double u =
                 ((double)(edge_draw(seed, e, 0x50415245u) >> 11) + 0.5) * 0x1.0p-53;
-            g->prop[e] = (float)pow(u, -inv);
+            /* alpha == 1: u^-1 as one correctly rounded division on both sides */
+            g->prop[e] = alpha == 1.0 ? (float)(1.0 / u) : (float)pow(u, -inv);
         }
         break;
     }
@@ -989,7 +1197,7 @@ static void* run_worker(void* arg) {
             if (sh->lengths) sh->lengths[i] = 0;
             continue;
         }
-        const int64_t len = walk_query(&c, sh->o, start, i, path, &ls, r);
+        const int64_t len = walk_query(&c, sh->o, start, sh->o->qid_base + i, path, &ls, r);
         if (len < 0) {
             pthread_mutex_lock(&g_err_mu);
             if (!sh->failed) {

@@ -57,6 +57,7 @@ typedef struct orc_opts {
     uint64_t cap_per_degree;
     double edge_cost_ratio;
     int rng; /* ORC_RNG_* */
+    uint64_t qid_base; /* global id of queries[0] (walker-stream key) */
 } orc_opts;
 
 /* Mirrors RunStats (include/dynwalk/runtime.hpp:53-73), GPU-relevant fields. */
@@ -97,6 +98,9 @@ void orc_rmat_samples(uint32_t scale, uint64_t nsamples, uint64_t seed, uint32_t
 orc_graph* orc_gen_rmat(uint32_t scale, uint32_t edge_factor, uint64_t seed);
 int orc_synth_philox(orc_graph* g, int kind, double low, double high, double alpha,
                      uint64_t seed);
+/* multi-threaded orc_gen_rmat + orc_synth_philox(uniform) for large scales */
+orc_graph* orc_gen_rmat_par(uint32_t scale, uint32_t edge_factor, uint64_t seed, double low,
+                            double high, uint64_t wseed, int nthreads);
 
 /* ---- walks ---- */
 int orc_run(const orc_graph* g, const orc_model* m, const orc_opts* o, const uint32_t* queries,

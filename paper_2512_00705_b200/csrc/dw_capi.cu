@@ -1,0 +1,663 @@
+// dw_capi.cu -- the C ABI (include/dynwalk_b200.h) over the device engine.
+//
+// Host side of the boundary: validation with the reference's error
+// semantics, per-device graph replicas, walker sharding, stream-ordered
+// H2D -> walk -> D2H pipelines, and RunStats assembly.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/dynwalk_b200.h"
+#include "dw_graph.cuh"
+#include "dw_walk.cuh"
+
+using dwb::DeviceGraphBuffers;
+typedef unsigned long long ull;
+
+namespace {
+
+thread_local std::string t_error;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    t_error = buf;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(DW_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CU(call, what)                                         \
+    do {                                                       \
+        cudaError_t e_ = (call);                               \
+        if (e_ != cudaSuccess) return cuda_fail(e_, what);     \
+    } while (0)
+
+constexpr int kMaxBatches = 64;
+
+struct Replica {
+    int device = 0;
+    int num_sms = 0;
+    cudaStream_t stream = nullptr;  // walk kernels
+    cudaStream_t copy = nullptr;    // H2D/D2H
+    DeviceGraphBuffers g;
+    ull* counters = nullptr;   // [kCNum]
+    ull* queues = nullptr;     // [kMaxBatches]
+    int* error = nullptr;
+    ull* error_info = nullptr;
+    // dw_run scratch
+    uint32_t* d_queries = nullptr;
+    uint32_t* d_paths = nullptr;
+    uint32_t* d_lengths = nullptr;
+    ull cap_q = 0, cap_paths = 0;
+    cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
+    std::vector<cudaEvent_t> ev_h2d, ev_walk;
+    // dw_run_device bookkeeping
+    bool pending = false;
+    ull pending_launches = 0;
+    ull pending_qbase = 0;
+};
+
+}  // namespace
+
+struct dw_graph_s {
+    uint32_t nv = 0;
+    ull ne = 0;
+    bool has_labels = false;
+    uint32_t max_degree = 0;
+    std::vector<Replica> reps;
+};
+
+namespace {
+
+int init_replica(Replica& r, int device) {
+    r.device = device;
+    CU(cudaSetDevice(device), "cudaSetDevice");
+    CU(cudaDeviceGetAttribute(&r.num_sms, cudaDevAttrMultiProcessorCount, device),
+       "cudaDeviceGetAttribute");
+    CU(cudaStreamCreateWithFlags(&r.stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    CU(cudaStreamCreateWithFlags(&r.copy, cudaStreamNonBlocking), "cudaStreamCreate");
+    CU(cudaMalloc(&r.counters, dwb::kCNum * sizeof(ull)), "cudaMalloc counters");
+    CU(cudaMalloc(&r.queues, kMaxBatches * sizeof(ull)), "cudaMalloc queues");
+    CU(cudaMalloc(&r.error, sizeof(int)), "cudaMalloc error");
+    CU(cudaMalloc(&r.error_info, sizeof(ull)), "cudaMalloc error");
+    CU(cudaEventCreate(&r.ev_start), "cudaEventCreate");
+    CU(cudaEventCreate(&r.ev_stop), "cudaEventCreate");
+    r.ev_h2d.resize(kMaxBatches);
+    r.ev_walk.resize(kMaxBatches);
+    for (int i = 0; i < kMaxBatches; ++i) {
+        CU(cudaEventCreateWithFlags(&r.ev_h2d[i], cudaEventDisableTiming), "cudaEventCreate");
+        CU(cudaEventCreateWithFlags(&r.ev_walk[i], cudaEventDisableTiming), "cudaEventCreate");
+    }
+    return DW_OK;
+}
+
+void free_replica(Replica& r) {
+    if (cudaSetDevice(r.device) != cudaSuccess) return;
+    if (r.stream) cudaStreamSynchronize(r.stream);
+    if (r.copy) cudaStreamSynchronize(r.copy);
+    cudaFree(r.g.nodes);
+    cudaFree(r.g.edges);
+    cudaFree(r.g.labels);
+    cudaFree(r.counters);
+    cudaFree(r.queues);
+    cudaFree(r.error);
+    cudaFree(r.error_info);
+    cudaFree(r.d_queries);
+    cudaFree(r.d_paths);
+    cudaFree(r.d_lengths);
+    if (r.ev_start) cudaEventDestroy(r.ev_start);
+    if (r.ev_stop) cudaEventDestroy(r.ev_stop);
+    for (auto e : r.ev_h2d) if (e) cudaEventDestroy(e);
+    for (auto e : r.ev_walk) if (e) cudaEventDestroy(e);
+    if (r.stream) cudaStreamDestroy(r.stream);
+    if (r.copy) cudaStreamDestroy(r.copy);
+}
+
+int resolve_devices(const int* devices, int ndev, std::vector<int>& out) {
+    int count = 0;
+    CU(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+    if (count < 1) return fail(DW_ECUDA, "no CUDA device available");
+    if (ndev < 1) return fail(DW_EINVAL, "worker count must be >= 1 (ndev=%d)", ndev);
+    out.clear();
+    for (int i = 0; i < ndev; ++i) {
+        const int d = devices ? devices[i] : i;
+        if (d < 0 || d >= count) return fail(DW_EINVAL, "device %d out of range (%d devices)", d, count);
+        out.push_back(d);
+    }
+    return DW_OK;
+}
+
+// Graph invariants the reference keeps by construction (graph.hpp:187-192).
+int validate_desc(const dw_graph_desc* d) {
+    if (!d || !d->row_offsets || (d->num_edges && (!d->col_indices || !d->edge_props)))
+        return fail(DW_EINVAL, "graph descriptor is missing arrays");
+    if ((ull)d->num_vertices >= DW_INVALID_VERTEX)
+        return fail(DW_EINVAL, "vertex id overflow: graph needs %u vertices", d->num_vertices);
+    const uint32_t nv = d->num_vertices;
+    if (d->row_offsets[0] != 0 || d->row_offsets[nv] != d->num_edges)
+        return fail(DW_EINVAL, "corrupt CSR: row_offsets must start at 0 and end at num_edges");
+    for (uint32_t v = 0; v < nv; ++v) {
+        const ull b = d->row_offsets[v], e = d->row_offsets[v + 1];
+        if (e < b) return fail(DW_EINVAL, "corrupt CSR: row_offsets decrease at vertex %u", v);
+        for (ull i = b; i < e; ++i) {
+            const uint32_t c = d->col_indices[i];
+            if (c >= nv)
+                return fail(DW_EINVAL, "vertex id %u out of range (num_vertices=%u)", c, nv);
+            if (i > b && d->col_indices[i - 1] > c)
+                return fail(DW_EINVAL, "adjacency slice of vertex %u is not sorted by target", v);
+            const float p = d->edge_props[i];
+            if (!(p > 0.0f) || !std::isfinite(p))
+                return fail(DW_EINVAL, "edge property must be strictly positive and finite, got %g",
+                            (double)p);
+        }
+    }
+    return DW_OK;
+}
+
+int upload_replica(Replica& r, const dw_graph_desc* d) {
+    CU(cudaSetDevice(r.device), "cudaSetDevice");
+    const uint32_t nv = d->num_vertices;
+    const ull ne = d->num_edges;
+    cudaStream_t s = r.stream;
+    ull* row = nullptr;
+    uint32_t* col = nullptr;
+    float* prop = nullptr;
+    double *nmax = nullptr, *nsum = nullptr;
+    CU(cudaMalloc(&row, (nv + 1ull) * sizeof(ull)), "cudaMalloc");
+    CU(cudaMalloc(&col, std::max<ull>(ne, 1) * sizeof(uint32_t)), "cudaMalloc");
+    CU(cudaMalloc(&prop, std::max<ull>(ne, 1) * sizeof(float)), "cudaMalloc");
+    CU(cudaMemcpyAsync(row, d->row_offsets, (nv + 1ull) * sizeof(ull), cudaMemcpyHostToDevice, s),
+       "H2D");
+    if (ne) {
+        CU(cudaMemcpyAsync(col, d->col_indices, ne * sizeof(uint32_t), cudaMemcpyHostToDevice, s),
+           "H2D");
+        CU(cudaMemcpyAsync(prop, d->edge_props, ne * sizeof(float), cudaMemcpyHostToDevice, s),
+           "H2D");
+    }
+    if (d->node_prop_max && d->node_prop_sum && nv) {
+        CU(cudaMalloc(&nmax, nv * sizeof(double)), "cudaMalloc");
+        CU(cudaMalloc(&nsum, nv * sizeof(double)), "cudaMalloc");
+        CU(cudaMemcpyAsync(nmax, d->node_prop_max, nv * sizeof(double), cudaMemcpyHostToDevice, s),
+           "H2D");
+        CU(cudaMemcpyAsync(nsum, d->node_prop_sum, nv * sizeof(double), cudaMemcpyHostToDevice, s),
+           "H2D");
+    }
+    r.g.nv = nv;
+    r.g.ne = ne;
+    CU(cudaMalloc(&r.g.nodes, std::max<uint32_t>(nv, 1) * sizeof(dwb::NodeRec)), "cudaMalloc nodes");
+    CU(cudaMalloc(&r.g.edges, std::max<ull>(ne, 1) * sizeof(dwb::EdgeRec)), "cudaMalloc edges");
+    if (d->edge_labels) {
+        CU(cudaMalloc(&r.g.labels, std::max<ull>(ne, 1) * sizeof(uint16_t)), "cudaMalloc labels");
+        if (ne)
+            CU(cudaMemcpyAsync(r.g.labels, d->edge_labels, ne * sizeof(uint16_t),
+                               cudaMemcpyHostToDevice, s),
+               "H2D");
+    }
+    CU(dwb::pack_graph(row, col, prop, nmax, nsum, r.g, s), "pack_graph");
+    CU(cudaStreamSynchronize(s), "upload");
+    cudaFree(row);
+    cudaFree(col);
+    cudaFree(prop);
+    cudaFree(nmax);
+    cudaFree(nsum);
+    return DW_OK;
+}
+
+int check_model(const dw_model_desc* m) {
+    if (!m) return fail(DW_EINVAL, "model descriptor is NULL");
+    if (m->kind < DW_MODEL_STATIC || m->kind > DW_MODEL_PR2)
+        return fail(DW_EINVAL,
+                    "unknown model kind %d (expected static, node2vec, metapath, pr2; DSL models "
+                    "need code generation)",
+                    m->kind);
+    if (m->kind == DW_MODEL_METAPATH) {
+        if (m->schema_len > DW_MAX_SCHEMA)
+            return fail(DW_EINVAL, "metapath schema longer than %d labels", DW_MAX_SCHEMA);
+        if (m->schema_len && !m->schema) return fail(DW_EINVAL, "metapath schema is NULL");
+    }
+    return DW_OK;
+}
+
+dwb::ModelParams model_params(const dw_model_desc* m) {
+    dwb::ModelParams mp;
+    std::memset(&mp, 0, sizeof mp);
+    mp.a = m->a;
+    mp.b = m->b;
+    mp.gamma = m->gamma;
+    if (m->kind == DW_MODEL_METAPATH) {
+        mp.schema_len = m->schema_len;
+        for (uint32_t i = 0; i < m->schema_len; ++i) mp.schema[i] = m->schema[i];
+    }
+    return mp;
+}
+
+const char* mode_name(int mode) {
+    switch (mode) {
+    case DW_MODE_FORCE_ITS: return "force-its";
+    case DW_MODE_FORCE_ALS: return "force-als";
+    }
+    return "?";
+}
+
+int check_opts(const dw_run_opts* o) {
+    if (!o) return fail(DW_EINVAL, "run options are NULL");
+    if (o->mode == DW_MODE_FORCE_ITS || o->mode == DW_MODE_FORCE_ALS)
+        return fail(DW_EUNSUPPORTED,
+                    "sampler mode %s is a CPU comparison baseline and is not supported by the "
+                    "GPU runtime",
+                    mode_name(o->mode));
+    if (o->mode < DW_MODE_ADAPTIVE || o->mode > DW_MODE_ERVS_NOJUMP)
+        return fail(DW_EINVAL, "unknown sampler mode %d", o->mode);
+    if (o->walk_length == 0xFFFFFFFFu) return fail(DW_EINVAL, "walk_length too large");
+    return DW_OK;
+}
+
+uint32_t target_steps(const dw_model_desc* m, const dw_run_opts* o) {
+    const uint32_t ms = m->kind == DW_MODEL_METAPATH ? m->schema_len : 0xFFFFFFFFu;
+    return std::min(o->walk_length, ms);
+}
+
+dwb::WalkParams make_params(Replica& r, const dw_model_desc* m, const dw_run_opts* o) {
+    dwb::WalkParams p;
+    std::memset(&p, 0, sizeof p);
+    p.g = dwb::DevGraph{r.g.nodes, r.g.edges, r.g.labels, r.g.nv, r.g.ne};
+    p.stride = o->walk_length + 1;
+    p.target = target_steps(m, o);
+    p.seed_lo = (uint32_t)o->seed;
+    p.seed_hi = (uint32_t)(o->seed >> 32);
+    p.cap_per_degree = o->erjs_cap_per_degree;
+    p.ratio = o->edge_cost_ratio;
+    p.counters = r.counters;
+    p.error = r.error;
+    p.error_info = r.error_info;
+    p.mp = model_params(m);
+    return p;
+}
+
+int reset_run_state(Replica& r) {
+    CU(cudaMemsetAsync(r.counters, 0, dwb::kCNum * sizeof(ull), r.stream), "memset");
+    CU(cudaMemsetAsync(r.queues, 0, kMaxBatches * sizeof(ull), r.stream), "memset");
+    CU(cudaMemsetAsync(r.error, 0, sizeof(int), r.stream), "memset");
+    return DW_OK;
+}
+
+void add_counters(dw_run_stats* st, const ull* c) {
+    st->queries += c[dwb::kCQueries];
+    st->query_errors += c[dwb::kCQueryErrors];
+    st->dead_ends += c[dwb::kCDeadEnds];
+    st->trials += c[dwb::kCTrials];
+    st->weight_reads += c[dwb::kCWeightReads];
+    st->rng_draws += c[dwb::kCRngDraws];
+    st->erjs_fallbacks += c[dwb::kCFallbacks];
+    st->algorithmic_bytes += c[dwb::kCAlgBytes];
+    for (int b = 0; b < 33; ++b)
+        for (int k = 0; k < 2; ++k) {
+            const ull v = c[dwb::kCHist + 2 * b + k];
+            st->selection_by_degree[b][k] += v;
+            st->steps += v;
+            (k ? st->select_erjs : st->select_ervs) += v;
+        }
+}
+
+// Reads back error + counters of one replica after its streams drained.
+int collect(Replica& r, dw_run_stats* st, ull qbase) {
+    int err = 0;
+    ull info = 0;
+    ull c[dwb::kCNum];
+    CU(cudaMemcpy(&err, r.error, sizeof(int), cudaMemcpyDeviceToHost), "D2H error");
+    if (err) {
+        CU(cudaMemcpy(&info, r.error_info, sizeof(ull), cudaMemcpyDeviceToHost), "D2H error");
+        switch (err) {
+        case dwb::kDevBadWeight:
+            return fail(DW_EMODEL, "model returned a negative or non-finite weight (query %llu)",
+                        info);
+        case dwb::kDevBadBound:
+            return fail(DW_EMODEL, "rejection bound must be positive and finite (query %llu)",
+                        info);
+        default:
+            return fail(DW_EMODEL, "walk kernel error %d (query %llu)", err, info);
+        }
+    }
+    (void)qbase;
+    if (st) {
+        CU(cudaMemcpy(c, r.counters, sizeof c, cudaMemcpyDeviceToHost), "D2H counters");
+        add_counters(st, c);
+    }
+    return DW_OK;
+}
+
+int ensure_scratch(Replica& r, ull nq, ull stride, bool paths) {
+    if (nq > r.cap_q) {
+        cudaFree(r.d_queries);
+        cudaFree(r.d_lengths);
+        r.d_queries = nullptr;
+        r.d_lengths = nullptr;
+        CU(cudaMalloc(&r.d_queries, nq * sizeof(uint32_t)), "cudaMalloc queries");
+        CU(cudaMalloc(&r.d_lengths, nq * sizeof(uint32_t)), "cudaMalloc lengths");
+        r.cap_q = nq;
+    }
+    if (paths && nq * stride > r.cap_paths) {
+        cudaFree(r.d_paths);
+        r.d_paths = nullptr;
+        CU(cudaMalloc(&r.d_paths, nq * stride * sizeof(uint32_t)), "cudaMalloc paths");
+        r.cap_paths = nq * stride;
+    }
+    return DW_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dw_abi_version(void) { return DW_ABI_VERSION; }
+
+const char* dw_last_error(void) { return t_error.c_str(); }
+
+int dw_device_count(int* n) {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) c = 0;
+    if (n) *n = c;
+    return DW_OK;
+}
+
+int dw_graph_create(const dw_graph_desc* desc, const int* devices, int ndev, dw_graph_t* out) {
+    if (!out) return fail(DW_EINVAL, "output handle pointer is NULL");
+    *out = nullptr;
+    std::vector<int> devs;
+    int rc = resolve_devices(devices, ndev, devs);
+    if (rc) return rc;
+    if ((rc = validate_desc(desc))) return rc;
+    auto* g = new dw_graph_s;
+    g->nv = desc->num_vertices;
+    g->ne = desc->num_edges;
+    g->has_labels = desc->edge_labels != nullptr;
+    g->reps.resize(devs.size());
+    for (size_t i = 0; i < devs.size(); ++i) {
+        if ((rc = init_replica(g->reps[i], devs[i])) || (rc = upload_replica(g->reps[i], desc))) {
+            dw_graph_destroy(g);
+            return rc;
+        }
+    }
+    g->max_degree = g->reps[0].g.max_degree;
+    *out = g;
+    return DW_OK;
+}
+
+int dw_graph_generate_rmat(const dw_rmat_desc* d, const int* devices, int ndev, dw_graph_t* out) {
+    if (!out || !d) return fail(DW_EINVAL, "NULL argument");
+    *out = nullptr;
+    if (d->scale > 30 || d->edge_factor < 2 || (2ull * (d->edge_factor / 2) << d->scale) > 0x7FFFFFFFull)
+        return fail(DW_EINVAL, "rmat: scale %u / edge factor %u out of range", d->scale,
+                    d->edge_factor);
+    if (d->weights == 0 && !(d->low > 0.0 && d->low < d->high))
+        return fail(DW_EINVAL, "uniform weight spec requires 0 < low < high");
+    if (d->weights == 2 && !(d->alpha > 0.0))
+        return fail(DW_EINVAL, "pareto weight spec requires alpha > 0");
+    if (d->weights != 0 && d->weights != 2 && d->weights != -1)
+        return fail(DW_EINVAL, "unknown weight kind %d", d->weights);
+    if (d->labels && !(d->label_low <= d->label_high && d->label_high <= 65535))
+        return fail(DW_EINVAL, "label spec requires 0 <= low <= high <= 65535");
+    std::vector<int> devs;
+    int rc = resolve_devices(devices, ndev, devs);
+    if (rc) return rc;
+    dwb::RmatSpec spec{d->scale, d->edge_factor, d->seed, d->weights, d->low, d->high, d->alpha,
+                       d->weight_seed, d->labels, d->label_low, d->label_high, d->label_seed};
+    auto* g = new dw_graph_s;
+    g->reps.resize(devs.size());
+    for (size_t i = 0; i < devs.size(); ++i) {
+        Replica& r = g->reps[i];
+        if ((rc = init_replica(r, devs[i]))) {
+            dw_graph_destroy(g);
+            return rc;
+        }
+        cudaError_t e = dwb::build_rmat(spec, r.g, r.stream);
+        if (e != cudaSuccess) {
+            dw_graph_destroy(g);
+            return cuda_fail(e, "build_rmat");
+        }
+    }
+    g->nv = g->reps[0].g.nv;
+    g->ne = g->reps[0].g.ne;
+    g->has_labels = d->labels != 0;
+    g->max_degree = g->reps[0].g.max_degree;
+    *out = g;
+    return DW_OK;
+}
+
+int dw_graph_destroy(dw_graph_t g) {
+    if (!g) return DW_OK;
+    for (auto& r : g->reps) free_replica(r);
+    delete g;
+    return DW_OK;
+}
+
+int dw_graph_info(dw_graph_t g, uint32_t* nv, uint64_t* ne, int* has_labels, uint32_t* max_degree) {
+    if (!g) return fail(DW_EINVAL, "graph handle is NULL");
+    if (nv) *nv = g->nv;
+    if (ne) *ne = g->ne;
+    if (has_labels) *has_labels = g->has_labels ? 1 : 0;
+    if (max_degree) *max_degree = g->max_degree;
+    return DW_OK;
+}
+
+int dw_graph_download(dw_graph_t g, uint64_t* row, uint32_t* col, float* prop, uint16_t* label,
+                      double* nmax, double* nsum) {
+    if (!g) return fail(DW_EINVAL, "graph handle is NULL");
+    Replica& r = g->reps[0];
+    CU(cudaSetDevice(r.device), "cudaSetDevice");
+    const ull nv = g->nv, ne = g->ne;
+    ull* d_row = nullptr;
+    uint32_t* d_col = nullptr;
+    float* d_prop = nullptr;
+    double *d_nmax = nullptr, *d_nsum = nullptr;
+    if (row) CU(cudaMalloc(&d_row, (nv + 1) * sizeof(ull)), "cudaMalloc");
+    if (col) CU(cudaMalloc(&d_col, std::max<ull>(ne, 1) * sizeof(uint32_t)), "cudaMalloc");
+    if (prop) CU(cudaMalloc(&d_prop, std::max<ull>(ne, 1) * sizeof(float)), "cudaMalloc");
+    if (nmax) CU(cudaMalloc(&d_nmax, std::max<ull>(nv, 1) * sizeof(double)), "cudaMalloc");
+    if (nsum) CU(cudaMalloc(&d_nsum, std::max<ull>(nv, 1) * sizeof(double)), "cudaMalloc");
+    CU(dwb::unpack_graph(r.g, d_row, d_col, d_prop, d_nmax, d_nsum, r.stream), "unpack");
+    CU(cudaStreamSynchronize(r.stream), "unpack");
+    if (row) CU(cudaMemcpy(row, d_row, (nv + 1) * sizeof(ull), cudaMemcpyDeviceToHost), "D2H");
+    if (col && ne) CU(cudaMemcpy(col, d_col, ne * sizeof(uint32_t), cudaMemcpyDeviceToHost), "D2H");
+    if (prop && ne) CU(cudaMemcpy(prop, d_prop, ne * sizeof(float), cudaMemcpyDeviceToHost), "D2H");
+    if (nmax && nv) CU(cudaMemcpy(nmax, d_nmax, nv * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    if (nsum && nv) CU(cudaMemcpy(nsum, d_nsum, nv * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    if (label && r.g.labels && ne)
+        CU(cudaMemcpy(label, r.g.labels, ne * sizeof(uint16_t), cudaMemcpyDeviceToHost), "D2H");
+    cudaFree(d_row);
+    cudaFree(d_col);
+    cudaFree(d_prop);
+    cudaFree(d_nmax);
+    cudaFree(d_nsum);
+    return DW_OK;
+}
+
+int dw_calibrate(dw_graph_t g, const dw_model_desc* model, uint64_t seed, double* ratio) {
+    if (!g || !ratio) return fail(DW_EINVAL, "NULL argument");
+    int rc = check_model(model);
+    if (rc) return rc;
+    Replica& r = g->reps[0];
+    CU(cudaSetDevice(r.device), "cudaSetDevice");
+    const dwb::ModelParams mp = model_params(model);
+    cudaError_t e = dwb::calibrate_ratio(r.g, model->kind, model->weighted != 0, mp, seed,
+                                         r.num_sms, r.stream, ratio);
+    if (e == cudaErrorInvalidValue) return fail(DW_EINVAL, "profiling found no node with out-edges");
+    if (e != cudaSuccess) return cuda_fail(e, "calibrate");
+    if (!(*ratio > 0.0) || !std::isfinite(*ratio))
+        return fail(DW_EINVAL, "profiled edge cost ratio is not positive and finite");
+    return DW_OK;
+}
+
+int dw_run_device(dw_graph_t g, int replica, const dw_model_desc* model, const uint32_t* d_queries,
+                  uint64_t nq, const dw_run_opts* opts, uint32_t* d_paths, uint32_t* d_lengths,
+                  void* stream) {
+    if (!g) return fail(DW_EINVAL, "graph handle is NULL");
+    if (replica < 0 || replica >= (int)g->reps.size())
+        return fail(DW_EINVAL, "replica %d out of range", replica);
+    int rc;
+    if ((rc = check_model(model)) || (rc = check_opts(opts))) return rc;
+    Replica& r = g->reps[replica];
+    CU(cudaSetDevice(r.device), "cudaSetDevice");
+    cudaStream_t s = stream ? (cudaStream_t)stream : r.stream;
+    if ((rc = reset_run_state(r))) return rc;
+    if (s != r.stream) {  // order the resets before work on the caller's stream
+        CU(cudaEventRecord(r.ev_walk[0], r.stream), "event");
+        CU(cudaStreamWaitEvent(s, r.ev_walk[0], 0), "event");
+    }
+    dwb::WalkParams p = make_params(r, model, opts);
+    p.queries = d_queries;
+    p.nq = nq;
+    p.qid_base = opts->qid_base;
+    p.paths = d_paths;
+    p.lengths = d_lengths;
+    p.next_walker = r.queues;
+    if (d_paths && nq)
+        CU(cudaMemsetAsync(d_paths, 0xFF, nq * (ull)p.stride * sizeof(uint32_t), s), "memset paths");
+    CU(cudaEventRecord(r.ev_start, s), "event");
+    CU(dwb::launch_walk(model->kind, model->weighted != 0, opts->mode, p, r.num_sms, s), "walk");
+    CU(cudaEventRecord(r.ev_stop, s), "event");
+    r.pending = true;
+    r.pending_launches = 1;
+    r.pending_qbase = opts->qid_base;
+    return DW_OK;
+}
+
+int dw_run_device_sync(dw_graph_t g, int replica, dw_run_stats* st) {
+    if (!g) return fail(DW_EINVAL, "graph handle is NULL");
+    if (replica < 0 || replica >= (int)g->reps.size())
+        return fail(DW_EINVAL, "replica %d out of range", replica);
+    Replica& r = g->reps[replica];
+    CU(cudaSetDevice(r.device), "cudaSetDevice");
+    CU(cudaEventSynchronize(r.ev_stop), "walk");
+    if (st) std::memset(st, 0, sizeof *st);
+    int rc = collect(r, st, r.pending_qbase);
+    if (st) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.ev_start, r.ev_stop);
+        st->kernel_ms = ms;
+        st->total_ms = ms;
+        st->kernel_launches = r.pending_launches;
+    }
+    r.pending = false;
+    return rc;
+}
+
+int dw_run(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries, uint64_t nq,
+           const dw_run_opts* opts, uint32_t* paths, uint32_t* lengths, dw_run_stats* st) {
+    if (!g) return fail(DW_EINVAL, "graph handle is NULL");
+    int rc;
+    if ((rc = check_model(model)) || (rc = check_opts(opts))) return rc;
+    if (nq && !queries) return fail(DW_EINVAL, "queries is NULL");
+    if (st) std::memset(st, 0, sizeof *st);
+    const int nd = (int)g->reps.size();
+    const ull stride = (ull)opts->walk_length + 1;
+    cudaEvent_t wall0 = nullptr, wall1 = nullptr;
+    CU(cudaSetDevice(g->reps[0].device), "cudaSetDevice");
+    CU(cudaEventCreate(&wall0), "event");
+    CU(cudaEventCreate(&wall1), "event");
+    CU(cudaEventRecord(wall0, g->reps[0].copy), "event");
+    ull launches = 0;
+    // contiguous walker blocks per device; batches per device overlap D2H of
+    // batch b with the walk of batch b+1
+    for (int di = 0; di < nd; ++di) {
+        Replica& r = g->reps[di];
+        const ull lo = nq * di / nd, hi = nq * (di + 1) / nd, n = hi - lo;
+        CU(cudaSetDevice(r.device), "cudaSetDevice");
+        if ((rc = ensure_scratch(r, std::max<ull>(n, 1), stride, paths != nullptr))) return rc;
+        if ((rc = reset_run_state(r))) return rc;
+        CU(cudaEventRecord(r.ev_walk[0], r.stream), "event");
+        CU(cudaStreamWaitEvent(r.copy, r.ev_walk[0], 0), "event");
+        const ull min_batch = 1ull << 20;
+        int nb = (int)std::min<ull>(8, std::max<ull>(1, n / min_batch));
+        if (n == 0) nb = 0;
+        bool started = false;
+        for (int b = 0; b < nb; ++b) {
+            const ull blo = n * b / nb, bhi = n * (b + 1) / nb, bn = bhi - blo;
+            CU(cudaMemcpyAsync(r.d_queries + blo, queries + lo + blo, bn * sizeof(uint32_t),
+                               cudaMemcpyHostToDevice, r.copy),
+               "H2D queries");
+            CU(cudaEventRecord(r.ev_h2d[b], r.copy), "event");
+            CU(cudaStreamWaitEvent(r.stream, r.ev_h2d[b], 0), "event");
+            dwb::WalkParams p = make_params(r, model, opts);
+            p.queries = r.d_queries + blo;
+            p.nq = bn;
+            p.qid_base = opts->qid_base + lo + blo;
+            p.paths = paths ? r.d_paths + blo * stride : nullptr;
+            p.lengths = r.d_lengths + blo;
+            p.next_walker = r.queues + b;
+            if (paths)
+                CU(cudaMemsetAsync(p.paths, 0xFF, bn * stride * sizeof(uint32_t), r.stream),
+                   "memset paths");
+            if (!started) {
+                CU(cudaEventRecord(r.ev_start, r.stream), "event");
+                started = true;
+            }
+            CU(dwb::launch_walk(model->kind, model->weighted != 0, opts->mode, p, r.num_sms,
+                                r.stream),
+               "walk");
+            ++launches;
+            CU(cudaEventRecord(r.ev_walk[b], r.stream), "event");
+            CU(cudaStreamWaitEvent(r.copy, r.ev_walk[b], 0), "event");
+            if (paths)
+                CU(cudaMemcpyAsync(paths + (lo + blo) * stride, p.paths,
+                                   bn * stride * sizeof(uint32_t), cudaMemcpyDeviceToHost, r.copy),
+                   "D2H paths");
+            if (lengths)
+                CU(cudaMemcpyAsync(lengths + lo + blo, p.lengths, bn * sizeof(uint32_t),
+                                   cudaMemcpyDeviceToHost, r.copy),
+                   "D2H lengths");
+        }
+        if (!started) CU(cudaEventRecord(r.ev_start, r.stream), "event");
+        CU(cudaEventRecord(r.ev_stop, r.stream), "event");
+    }
+    double kmax = 0.0;
+    for (int di = 0; di < nd; ++di) {
+        Replica& r = g->reps[di];
+        CU(cudaSetDevice(r.device), "cudaSetDevice");
+        CU(cudaStreamSynchronize(r.stream), "walk");
+        CU(cudaStreamSynchronize(r.copy), "copy");
+        if ((rc = collect(r, st, 0))) return rc;
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.ev_start, r.ev_stop);
+        kmax = std::max(kmax, (double)ms);
+    }
+    CU(cudaSetDevice(g->reps[0].device), "cudaSetDevice");
+    CU(cudaEventRecord(wall1, g->reps[0].copy), "event");
+    CU(cudaEventSynchronize(wall1), "event");
+    float wall = 0.f;
+    cudaEventElapsedTime(&wall, wall0, wall1);
+    cudaEventDestroy(wall0);
+    cudaEventDestroy(wall1);
+    if (st) {
+        st->kernel_ms = kmax;
+        st->total_ms = wall;
+        st->kernel_launches = launches;
+    }
+    return DW_OK;
+}
+
+int dw_host_alloc(size_t bytes, void** out) {
+    if (!out) return fail(DW_EINVAL, "NULL argument");
+    CU(cudaMallocHost(out, bytes), "cudaMallocHost");
+    return DW_OK;
+}
+
+int dw_host_free(void* p) {
+    CU(cudaFreeHost(p), "cudaFreeHost");
+    return DW_OK;
+}
+
+}  // extern "C"

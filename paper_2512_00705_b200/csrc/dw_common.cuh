@@ -1,0 +1,145 @@
+// dw_common.cuh -- device data layout, Philox walker streams, bit maps.
+//
+// HBM layout:
+//   NodeRec[nv]  32 B, one sector: {row begin u64, degree u32, -, max h f64,
+//                sum h f64}.  One random sector per step serves degree(cur),
+//                out_edge_begin(cur) and the cost-model aggregates
+//                (graph.hpp:209-231; decide_sampler, cost_model.hpp:46-56).
+//   EdgeRec[ne]   8 B: {target u32, prop f32}.  One random sector per
+//                rejection trial serves edge_target(e) and edge_prop(e).
+//   labels[ne]   u16, only for labelled graphs (MetaPath).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dwb {
+
+constexpr uint32_t kInvalid = 0xFFFFFFFFu;
+
+struct alignas(32) NodeRec {
+    unsigned long long begin;
+    uint32_t degree;
+    uint32_t pad;
+    double hmax;
+    double hsum;
+};
+static_assert(sizeof(NodeRec) == 32, "NodeRec must be one sector");
+
+struct alignas(8) EdgeRec {
+    uint32_t col;
+    float h;
+};
+static_assert(sizeof(EdgeRec) == 8, "EdgeRec must be 8 bytes");
+
+struct DevGraph {
+    const NodeRec* __restrict__ nodes;
+    const EdgeRec* __restrict__ edges;
+    const uint16_t* __restrict__ labels;  // may be null
+    uint32_t nv;
+    unsigned long long ne;
+};
+
+// Error codes raised from inside kernels (first one wins).
+enum DevError : int {
+    kDevOk = 0,
+    kDevBadWeight = 1,   // samplers.hpp:50-53
+    kDevBadBound = 2,    // samplers.hpp:152-154
+    kDevSchema = 3,      // models.hpp:100-101
+};
+
+__device__ __forceinline__ NodeRec load_node(const NodeRec* __restrict__ p) {
+    // one 32 B sector as two 16 B non-coherent loads
+    const uint4* q = reinterpret_cast<const uint4*>(p);
+    const uint4 a = __ldg(q);
+    const uint4 b = __ldg(q + 1);
+    NodeRec r;
+    r.begin = (unsigned long long)a.x | ((unsigned long long)a.y << 32);
+    r.degree = a.z;
+    r.pad = a.w;
+    r.hmax = __hiloint2double((int)b.y, (int)b.x);
+    r.hsum = __hiloint2double((int)b.w, (int)b.z);
+    return r;
+}
+
+__device__ __forceinline__ EdgeRec load_edge(const EdgeRec* __restrict__ p) {
+    const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+    EdgeRec e;
+    e.col = v.x;
+    e.h = __uint_as_float(v.y);
+    return e;
+}
+
+__device__ __forceinline__ uint32_t load_col(const EdgeRec* __restrict__ p) {
+    return __ldg(reinterpret_cast<const uint32_t*>(p));
+}
+
+// Philox4x32-10 (Salmon et al. 2011; constants as curand_philox4x32_x.h:88-91).
+struct U4 {
+    uint32_t x, y, z, w;
+};
+
+__host__ __device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r) {
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+#ifdef __CUDA_ARCH__
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+#else
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c.x, p1 = (uint64_t)0xCD9E8D57u * c.z;
+        const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+#endif
+        c = U4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
+    }
+    return c;
+}
+
+// Walker stream: key = seed, counter = (draw >> 1, step, qid lo, qid hi).
+// Draw 2k = words (y:x) of block k, draw 2k+1 = words (w:z).  Same map as
+// the oracle (oracle.c orc_walker_draw); one block serves one rejection trial
+// (bounded(d) then uniform01, samplers.hpp:160-161).
+struct WalkerKey {
+    uint32_t k0, k1;      // seed
+    uint32_t q0, q1;      // global walker id
+    uint32_t step;
+};
+
+__device__ __forceinline__ U4 walker_block(const WalkerKey& w, uint32_t block) {
+    return philox4x32_10(U4{block, w.step, w.q0, w.q1}, w.k0, w.k1);
+}
+
+__device__ __forceinline__ unsigned long long lo64(const U4& b) {
+    return (unsigned long long)b.x | ((unsigned long long)b.y << 32);
+}
+__device__ __forceinline__ unsigned long long hi64(const U4& b) {
+    return (unsigned long long)b.z | ((unsigned long long)b.w << 32);
+}
+
+__device__ __forceinline__ unsigned long long walker_draw(const WalkerKey& w,
+                                                          unsigned long long idx) {
+    const U4 b = walker_block(w, (uint32_t)(idx >> 1));
+    return (idx & 1) ? hi64(b) : lo64(b);
+}
+
+// Reference bit maps (rng.hpp:40-50).  Exact in IEEE double.
+__device__ __forceinline__ double uniform01(unsigned long long r) {
+    return __dmul_rn(__ull2double_rn(r >> 11), 0x1.0p-53);
+}
+__device__ __forceinline__ double open01(unsigned long long r) {
+    return __dmul_rn(__dadd_rn(__ull2double_rn(r >> 11), 0.5), 0x1.0p-53);
+}
+__device__ __forceinline__ unsigned long long bounded(unsigned long long r,
+                                                      unsigned long long n) {
+    return __umul64hi(r, n);
+}
+
+// floor(log2 d) capped at 31 (runtime.cpp:42-46).
+__device__ __forceinline__ int degree_bucket(uint32_t d) {
+    return d ? 31 - __clz(d) : 0;
+}
+
+}  // namespace dwb

@@ -1,0 +1,463 @@
+// dw_graph.cu -- device graph construction and K4 calibration.
+//
+// build_rmat: R-MAT sampling, mirroring, CSR by one 64-bit radix sort of
+// (src, dst) keys, Philox weights keyed by edge index, left-to-right
+// aggregates.  The CSR equals Graph::build(mirror=true) on the same samples
+// (graph.cpp:15-81): the reference stable-sorts each slice by target and
+// equal targets are indistinguishable before weights are synthesized per
+// edge, so a full key sort yields the identical arrays.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_reduce.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "dw_graph.cuh"
+
+namespace dwb {
+
+typedef unsigned long long ull;
+
+#define DW_TRY(x)                              \
+    do {                                       \
+        cudaError_t e_ = (x);                  \
+        if (e_ != cudaSuccess) return e_;      \
+    } while (0)
+
+static inline unsigned grid_for(ull n, int threads) {
+    ull b = (n + threads - 1) / threads;
+    if (b > 65535ull * 64) b = 65535ull * 64;
+    return (unsigned)(b ? b : 1);
+}
+
+// ---- SplitMix64 / derive_seed (rng.hpp:10-25) -------------------------------
+ull host_derive_seed(ull seed, ull stream) {
+    ull st = seed ^ (stream * 0x9e3779b97f4a7c15ULL + 0x2545f4914f6cdd1dULL);
+    auto next = [&]() {
+        ull z = (st += 0x9e3779b97f4a7c15ULL);
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+        return z ^ (z >> 31);
+    };
+    next();
+    return next();
+}
+
+// ---- packing ---------------------------------------------------------------
+__global__ void pack_edges_kernel(const uint32_t* __restrict__ col, const float* __restrict__ prop,
+                                  EdgeRec* __restrict__ out, ull ne) {
+    for (ull e = blockIdx.x * (ull)blockDim.x + threadIdx.x; e < ne;
+         e += (ull)gridDim.x * blockDim.x)
+        out[e] = EdgeRec{col[e], prop[e]};
+}
+
+// one thread per node; sequential ascending-order max/sum (graph.cpp:87-97)
+__global__ void pack_nodes_kernel(const ull* __restrict__ row, const float* __restrict__ prop,
+                                  const double* __restrict__ nmax, const double* __restrict__ nsum,
+                                  NodeRec* __restrict__ out, uint32_t nv,
+                                  unsigned* __restrict__ max_degree) {
+    for (ull v = blockIdx.x * (ull)blockDim.x + threadIdx.x; v < nv;
+         v += (ull)gridDim.x * blockDim.x) {
+        const ull b = row[v], e = row[v + 1];
+        double mx = 0.0, sum = 0.0;
+        if (nmax && nsum) {
+            mx = nmax[v];
+            sum = nsum[v];
+        } else {
+            for (ull i = b; i < e; ++i) {
+                const double p = prop[i];
+                if (p > mx) mx = p;
+                sum += p;
+            }
+        }
+        NodeRec r;
+        r.begin = b;
+        r.degree = (uint32_t)(e - b);
+        r.pad = 0;
+        r.hmax = mx;
+        r.hsum = sum;
+        out[v] = r;
+        atomicMax(max_degree, r.degree);
+    }
+}
+
+cudaError_t pack_graph(const ull* d_row, const uint32_t* d_col, const float* d_prop,
+                       const double* d_nmax, const double* d_nsum, DeviceGraphBuffers& g,
+                       cudaStream_t s) {
+    unsigned* d_maxd = nullptr;
+    DW_TRY(cudaMallocAsync(&d_maxd, sizeof(unsigned), s));
+    DW_TRY(cudaMemsetAsync(d_maxd, 0, sizeof(unsigned), s));
+    if (g.ne) pack_edges_kernel<<<grid_for(g.ne, 256), 256, 0, s>>>(d_col, d_prop, g.edges, g.ne);
+    pack_nodes_kernel<<<grid_for(g.nv, 128), 128, 0, s>>>(d_row, d_prop, d_nmax, d_nsum, g.nodes,
+                                                          g.nv, d_maxd);
+    DW_TRY(cudaGetLastError());
+    unsigned h = 0;
+    DW_TRY(cudaMemcpyAsync(&h, d_maxd, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    DW_TRY(cudaStreamSynchronize(s));
+    g.max_degree = h;
+    return cudaFreeAsync(d_maxd, s);
+}
+
+__global__ void unpack_kernel(const NodeRec* __restrict__ nodes, const EdgeRec* __restrict__ edges,
+                              uint32_t nv, ull ne, ull* row, uint32_t* col, float* prop,
+                              double* nmax, double* nsum) {
+    const ull stride = (ull)gridDim.x * blockDim.x;
+    for (ull i = blockIdx.x * (ull)blockDim.x + threadIdx.x; i < ne; i += stride) {
+        if (col) col[i] = edges[i].col;
+        if (prop) prop[i] = edges[i].h;
+    }
+    for (ull v = blockIdx.x * (ull)blockDim.x + threadIdx.x; v < nv; v += stride) {
+        if (row) row[v] = nodes[v].begin;
+        if (nmax) nmax[v] = nodes[v].hmax;
+        if (nsum) nsum[v] = nodes[v].hsum;
+    }
+    if (row && blockIdx.x == 0 && threadIdx.x == 0) row[nv] = ne;
+}
+
+cudaError_t unpack_graph(const DeviceGraphBuffers& g, ull* d_row, uint32_t* d_col, float* d_prop,
+                         double* d_nmax, double* d_nsum, cudaStream_t s) {
+    unpack_kernel<<<grid_for(std::max<ull>(g.ne, g.nv), 256), 256, 0, s>>>(
+        g.nodes, g.edges, g.nv, g.ne, d_row, d_col, d_prop, d_nmax, d_nsum);
+    return cudaGetLastError();
+}
+
+// ---- R-MAT (definition shared with oracle.c orc_rmat_samples) --------------
+#define RMAT_TA 2448131358u   /* floor(0.57 * 2^32) */
+#define RMAT_TAB 3264175144u  /* floor(0.76 * 2^32) */
+#define RMAT_TABC 4080218931u /* floor(0.95 * 2^32) */
+
+__device__ __forceinline__ uint32_t rmat_perm(uint32_t x, uint32_t scale, ull pk) {
+    if (scale == 0) return 0;
+    const uint32_t mask = scale >= 32 ? 0xFFFFFFFFu : ((1u << scale) - 1u);
+    const uint32_t sh = scale / 2 + 1;
+    const uint32_t m1 = ((uint32_t)pk | 1u), a1 = (uint32_t)(pk >> 32);
+    const uint32_t m2 = ((uint32_t)(pk >> 17) | 1u), a2 = (uint32_t)(pk >> 7);
+    x = (x * m1 + a1) & mask;
+    x ^= x >> sh;
+    x = (x * m2 + a2) & mask;
+    x ^= x >> sh;
+    return x & mask;
+}
+
+// keys[i] = (src<<32|dst); keys[ns+i] = twin, or the sentinel (nv<<32) for a
+// self-loop (Graph::build mirrors only non-self-loops, graph.cpp:17-25)
+__global__ void rmat_keys_kernel(uint32_t scale, ull ns, ull ks, ull pk, ull* __restrict__ keys,
+                                 ull* __restrict__ self_loops) {
+    const uint32_t k0 = (uint32_t)ks, k1 = (uint32_t)(ks >> 32);
+    ull loops = 0;
+    for (ull i = blockIdx.x * (ull)blockDim.x + threadIdx.x; i < ns;
+         i += (ull)gridDim.x * blockDim.x) {
+        uint32_t u = 0, v = 0;
+        U4 rnd{0, 0, 0, 0};
+        for (uint32_t lvl = 0; lvl < scale; ++lvl) {
+            if ((lvl & 3) == 0)
+                rnd = philox4x32_10(U4{lvl >> 2, (uint32_t)i, (uint32_t)(i >> 32), 0x524d4154u},
+                                    k0, k1);
+            const uint32_t q = lvl & 3;
+            const uint32_t r = q == 0 ? rnd.x : q == 1 ? rnd.y : q == 2 ? rnd.z : rnd.w;
+            const uint32_t bu = r >= RMAT_TAB;
+            const uint32_t bv = (r >= RMAT_TA && r < RMAT_TAB) || r >= RMAT_TABC;
+            u = (u << 1) | bu;
+            v = (v << 1) | bv;
+        }
+        u = rmat_perm(u, scale, pk);
+        v = rmat_perm(v, scale, pk);
+        keys[i] = ((ull)u << 32) | v;
+        if (u != v) {
+            keys[ns + i] = ((ull)v << 32) | u;
+        } else {
+            keys[ns + i] = (ull)(1ull << scale) << 32;
+            ++loops;
+        }
+    }
+    if (loops) atomicAdd(self_loops, loops);
+}
+
+__global__ void keys_to_col_kernel(const ull* __restrict__ keys, uint32_t* __restrict__ col,
+                                   ull ne) {
+    for (ull e = blockIdx.x * (ull)blockDim.x + threadIdx.x; e < ne;
+         e += (ull)gridDim.x * blockDim.x)
+        col[e] = (uint32_t)keys[e];
+}
+
+// row[v] = first e with key >= v<<32 (keys sorted)
+__global__ void row_offsets_kernel(const ull* __restrict__ keys, ull ne, uint32_t nv,
+                                   ull* __restrict__ row) {
+    for (ull v = blockIdx.x * (ull)blockDim.x + threadIdx.x; v <= nv;
+         v += (ull)gridDim.x * blockDim.x) {
+        if (v == nv) {
+            row[v] = ne;
+            continue;
+        }
+        const ull target = v << 32;
+        ull lo = 0, hi = ne;
+        while (lo < hi) {
+            const ull mid = lo + ((hi - lo) >> 1);
+            if (keys[mid] < target)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        row[v] = lo;
+    }
+}
+
+__device__ __forceinline__ ull edge_draw(ull seed, ull e, uint32_t tag) {
+    const U4 o = philox4x32_10(U4{(uint32_t)e, (uint32_t)(e >> 32), 0u, tag}, (uint32_t)seed,
+                               (uint32_t)(seed >> 32));
+    return (ull)o.x | ((ull)o.y << 32);
+}
+
+// same maps as synthesize_weights (graph.cpp:308-341), Philox keyed by edge
+__global__ void synth_props_kernel(float* __restrict__ prop, ull ne, int kind, double low,
+                                   double high, double alpha, ull seed) {
+    for (ull e = blockIdx.x * (ull)blockDim.x + threadIdx.x; e < ne;
+         e += (ull)gridDim.x * blockDim.x) {
+        if (kind == 0) {
+            const double u = uniform01(edge_draw(seed, e, 0x57474854u));
+            prop[e] = (float)(low + u * (high - low));
+        } else if (kind == 2) {
+            const double u = open01(edge_draw(seed, e, 0x50415245u));
+            prop[e] = alpha == 1.0 ? (float)(1.0 / u) : (float)pow(u, -(1.0 / alpha));
+        } else {
+            prop[e] = 1.0f;
+        }
+    }
+}
+
+__global__ void synth_labels_kernel(uint16_t* __restrict__ label, ull ne, uint32_t lo, ull span,
+                                    ull seed) {
+    for (ull e = blockIdx.x * (ull)blockDim.x + threadIdx.x; e < ne;
+         e += (ull)gridDim.x * blockDim.x)
+        label[e] = (uint16_t)(lo + __umul64hi(edge_draw(seed, e, 0x4c41424cu), span));
+}
+
+cudaError_t build_rmat(const RmatSpec& spec, DeviceGraphBuffers& g, cudaStream_t s) {
+    if (spec.scale > 30 || spec.edge_factor < 2) return cudaErrorInvalidValue;
+    const uint32_t nv = 1u << spec.scale;
+    const ull ns = (ull)(spec.edge_factor / 2) * nv;
+    const ull nkeys = 2 * ns;
+    if (nkeys > 0x7FFFFFFFull) return cudaErrorInvalidValue;  // cub int item counts
+    const ull ks = host_derive_seed(spec.seed, 0x726d6174ULL);
+    const ull pk = host_derive_seed(spec.seed, 0x7065726dULL);
+
+    ull *keys = nullptr, *keys_alt = nullptr, *d_loops = nullptr, *row = nullptr;
+    DW_TRY(cudaMallocAsync(&keys, nkeys * sizeof(ull), s));
+    DW_TRY(cudaMallocAsync(&keys_alt, nkeys * sizeof(ull), s));
+    DW_TRY(cudaMallocAsync(&d_loops, sizeof(ull), s));
+    DW_TRY(cudaMemsetAsync(d_loops, 0, sizeof(ull), s));
+    rmat_keys_kernel<<<grid_for(ns, 256), 256, 0, s>>>(spec.scale, ns, ks, pk, keys, d_loops);
+    DW_TRY(cudaGetLastError());
+
+    cub::DoubleBuffer<ull> db(keys, keys_alt);
+    size_t tmp_bytes = 0;
+    DW_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, db, (int)nkeys, 0,
+                                          32 + spec.scale + 1, s));
+    void* tmp = nullptr;
+    DW_TRY(cudaMallocAsync(&tmp, tmp_bytes, s));
+    DW_TRY(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, db, (int)nkeys, 0, 32 + spec.scale + 1,
+                                          s));
+    DW_TRY(cudaFreeAsync(tmp, s));
+    ull loops = 0;
+    DW_TRY(cudaMemcpyAsync(&loops, d_loops, sizeof(ull), cudaMemcpyDeviceToHost, s));
+    DW_TRY(cudaStreamSynchronize(s));
+    const ull ne = nkeys - loops;
+    const ull* sorted = db.Current();
+    ull* spare = db.Alternate();
+
+    g.nv = nv;
+    g.ne = ne;
+    DW_TRY(cudaMallocAsync(&row, (nv + 1ull) * sizeof(ull), s));
+    row_offsets_kernel<<<grid_for(nv + 1ull, 256), 256, 0, s>>>(sorted, ne, nv, row);
+    // col and prop live in the spare sort buffer (2*ne*4 bytes <= nkeys*8)
+    uint32_t* col = reinterpret_cast<uint32_t*>(spare);
+    float* prop = reinterpret_cast<float*>(col + ne);
+    keys_to_col_kernel<<<grid_for(ne, 256), 256, 0, s>>>(sorted, col, ne);
+    synth_props_kernel<<<grid_for(ne, 256), 256, 0, s>>>(prop, ne, spec.weights, spec.low,
+                                                         spec.high, spec.alpha, spec.weight_seed);
+    DW_TRY(cudaGetLastError());
+    DW_TRY(cudaMallocAsync(&g.edges, std::max<ull>(ne, 1) * sizeof(EdgeRec), s));
+    DW_TRY(cudaMallocAsync(&g.nodes, std::max<uint32_t>(nv, 1) * sizeof(NodeRec), s));
+    if (spec.labels) {
+        DW_TRY(cudaMallocAsync(&g.labels, std::max<ull>(ne, 1) * sizeof(uint16_t), s));
+        synth_labels_kernel<<<grid_for(ne, 256), 256, 0, s>>>(
+            g.labels, ne, spec.label_low, (ull)spec.label_high - spec.label_low + 1,
+            spec.label_seed);
+        DW_TRY(cudaGetLastError());
+    }
+    DW_TRY(pack_graph(row, col, prop, nullptr, nullptr, g, s));
+    DW_TRY(cudaFreeAsync(keys, s));
+    DW_TRY(cudaFreeAsync(keys_alt, s));
+    DW_TRY(cudaFreeAsync(d_loops, s));
+    DW_TRY(cudaFreeAsync(row, s));
+    return cudaStreamSynchronize(s);
+}
+
+// ---- K4: calibration (cost_model.cpp:37-126) -------------------------------
+template <class M>
+__device__ __forceinline__ double eval_weight(const M& m, const Step& S, const DevGraph& g, ull e) {
+    const EdgeRec er = load_edge(g.edges + e);
+    const uint16_t lab = (M::kUsesLabels && g.labels) ? g.labels[e] : (uint16_t)0;
+    const WeightCase wc = m.weight(S, er.col, er.h, lab);
+    if (!M::kSecondOrder || !wc.needs_member) return wc.w;
+    // Graph::has_edge
+    ull base = S.prev_begin;
+    uint32_t n = S.prev_degree;
+    if (n == 0) return wc.w_out;
+    while (n > 1) {
+        const uint32_t half = n >> 1;
+        if (load_col(g.edges + base + half) <= er.col) base += half;
+        n -= half;
+    }
+    return load_col(g.edges + base) == er.col ? wc.w_in : wc.w_out;
+}
+
+// probe_state (cost_model.cpp:20-33): step 1 with the first neighbour as prev
+__device__ __forceinline__ Step probe_state(const DevGraph& g, uint32_t v) {
+    Step S;
+    const NodeRec nr = load_node(g.nodes + v);
+    S.cur = v;
+    S.degree = nr.degree;
+    S.begin = nr.begin;
+    S.hmax = nr.hmax;
+    S.hsum = nr.hsum;
+    S.prev = kInvalid;
+    S.prev_degree = 0;
+    S.prev_begin = 0;
+    S.step = 0;
+    if (nr.degree) {
+        const uint32_t pv = load_col(g.edges + nr.begin);
+        const NodeRec pr = load_node(g.nodes + pv);
+        if (pr.degree) {
+            S.prev = pv;
+            S.prev_degree = pr.degree;
+            S.prev_begin = pr.begin;
+            S.step = 1;
+        }
+    }
+    return S;
+}
+
+__global__ void sample_nodes_kernel(DevGraph g, ull seed, ull tries, uint32_t want,
+                                    uint32_t* nodes, unsigned* count) {
+    for (ull i = blockIdx.x * (ull)blockDim.x + threadIdx.x; i < tries;
+         i += (ull)gridDim.x * blockDim.x) {
+        const U4 b = philox4x32_10(U4{(uint32_t)i, (uint32_t)(i >> 32), 0u, 0x70726f66u},
+                                   (uint32_t)seed, (uint32_t)(seed >> 32));
+        const uint32_t v = (uint32_t)bounded(lo64(b), g.nv);
+        if (g.nodes[v].degree == 0) continue;
+        const unsigned slot = atomicAdd(count, 1u);
+        if (slot < want) nodes[slot] = v;
+    }
+}
+
+// one warp per probed node, lane k < min(d, 32) evaluates one weight per round
+template <class M, bool RANDOM>
+__global__ void probe_pass_kernel(DevGraph g, __grid_constant__ const ModelParams mp,
+                                  const uint32_t* __restrict__ nodes, uint32_t n, int rounds,
+                                  ull seed, double* sink) {
+    const M m(mp);
+    const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    if (w >= n) return;
+    const Step S = probe_state(g, nodes[w]);
+    const uint32_t k = S.degree < 32 ? S.degree : 32;
+    double acc = 0.0;
+    if (lane < k) {
+        for (int r = 0; r < rounds; ++r) {
+            ull e;
+            if (RANDOM) {
+                const U4 b = philox4x32_10(U4{lane, (uint32_t)r, w, 0x72616e64u}, (uint32_t)seed,
+                                           (uint32_t)(seed >> 32));
+                e = S.begin + bounded(lo64(b), S.degree);
+            } else {
+                e = S.begin + lane;
+            }
+            acc += eval_weight(m, S, g, e);
+        }
+    }
+    if (acc == -1.0) *sink = acc;  // keeps the loads alive
+}
+
+template <class M>
+static cudaError_t calibrate_t(const DeviceGraphBuffers& gb, const ModelParams& mp, ull seed,
+                               cudaStream_t s, double* ratio) {
+    DevGraph g{gb.nodes, gb.edges, gb.labels, gb.nv, gb.ne};
+    // ProfileConfig defaults: 1% of nodes, >= 64, <= 32 neighbours, 5 reps
+    uint32_t want = (uint32_t)std::max<ull>((ull)std::ceil(0.01 * gb.nv), 64);
+    const ull tries = (ull)want * 8;
+    uint32_t* nodes = nullptr;
+    unsigned* count = nullptr;
+    double* sink = nullptr;
+    DW_TRY(cudaMallocAsync(&nodes, want * sizeof(uint32_t), s));
+    DW_TRY(cudaMallocAsync(&count, sizeof(unsigned), s));
+    DW_TRY(cudaMallocAsync(&sink, sizeof(double), s));
+    DW_TRY(cudaMemsetAsync(count, 0, sizeof(unsigned), s));
+    const ull kseed = host_derive_seed(seed, 0x70726f66ULL);
+    sample_nodes_kernel<<<grid_for(tries, 256), 256, 0, s>>>(g, kseed, tries, want, nodes, count);
+    unsigned got = 0;
+    DW_TRY(cudaMemcpyAsync(&got, count, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    DW_TRY(cudaStreamSynchronize(s));
+    const uint32_t n = std::min<uint32_t>(got, want);
+    if (n == 0) {
+        cudaFreeAsync(nodes, s);
+        cudaFreeAsync(count, s);
+        cudaFreeAsync(sink, s);
+        return cudaErrorInvalidValue;  // "profiling found no node with out-edges"
+    }
+    cudaEvent_t e0, e1, e2;
+    DW_TRY(cudaEventCreate(&e0));
+    DW_TRY(cudaEventCreate(&e1));
+    DW_TRY(cudaEventCreate(&e2));
+    const unsigned blocks = (n * 32 + 255) / 256;
+    auto pass = [&](int rounds, float& t_rand, float& t_seq) -> cudaError_t {
+        cudaEventRecord(e0, s);
+        probe_pass_kernel<M, true><<<blocks, 256, 0, s>>>(g, mp, nodes, n, rounds, kseed, sink);
+        cudaEventRecord(e1, s);
+        probe_pass_kernel<M, false><<<blocks, 256, 0, s>>>(g, mp, nodes, n, rounds, kseed, sink);
+        cudaEventRecord(e2, s);
+        DW_TRY(cudaEventSynchronize(e2));
+        cudaEventElapsedTime(&t_rand, e0, e1);
+        cudaEventElapsedTime(&t_seq, e1, e2);
+        return cudaGetLastError();
+    };
+    float tr = 0, ts = 0;
+    DW_TRY(pass(1, tr, ts));  // warm-up
+    int rounds = 1;
+    while (rounds < (1 << 20)) {  // grow until both passes are well above event resolution
+        DW_TRY(pass(rounds, tr, ts));
+        if (tr > 0.2f && ts > 0.2f) break;
+        rounds *= 2;
+    }
+    std::vector<double> ratios;
+    for (int rep = 0; rep < 5; ++rep) {
+        DW_TRY(pass(rounds, tr, ts));
+        ratios.push_back((double)tr / (double)ts);
+    }
+    std::sort(ratios.begin(), ratios.end());
+    *ratio = ratios[ratios.size() / 2];
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+    cudaFreeAsync(nodes, s);
+    cudaFreeAsync(count, s);
+    cudaFreeAsync(sink, s);
+    return cudaStreamSynchronize(s);
+}
+
+cudaError_t calibrate_ratio(const DeviceGraphBuffers& g, int kind, bool weighted,
+                            const ModelParams& mp, ull seed, int, cudaStream_t s, double* ratio) {
+    switch (kind) {
+    case 0: return weighted ? calibrate_t<StaticModel<true>>(g, mp, seed, s, ratio)
+                            : calibrate_t<StaticModel<false>>(g, mp, seed, s, ratio);
+    case 1: return weighted ? calibrate_t<Node2VecModel<true>>(g, mp, seed, s, ratio)
+                            : calibrate_t<Node2VecModel<false>>(g, mp, seed, s, ratio);
+    case 2: return weighted ? calibrate_t<MetaPathModel<true>>(g, mp, seed, s, ratio)
+                            : calibrate_t<MetaPathModel<false>>(g, mp, seed, s, ratio);
+    case 3: return weighted ? calibrate_t<Pr2Model<true>>(g, mp, seed, s, ratio)
+                            : calibrate_t<Pr2Model<false>>(g, mp, seed, s, ratio);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace dwb

@@ -1,0 +1,49 @@
+// dw_graph.cuh -- device graph construction and calibration (host-callable).
+#pragma once
+#include "dw_models.cuh"
+
+namespace dwb {
+
+struct DeviceGraphBuffers {
+    NodeRec* nodes = nullptr;
+    EdgeRec* edges = nullptr;
+    uint16_t* labels = nullptr;
+    uint32_t nv = 0;
+    unsigned long long ne = 0;
+    uint32_t max_degree = 0;
+};
+
+// Packs CSR arrays already on the device into NodeRec/EdgeRec.  nmax/nsum may
+// be null: they are then recomputed per node in ascending edge order
+// (graph.cpp:83-98), bit-identical to the host.
+cudaError_t pack_graph(const unsigned long long* d_row, const uint32_t* d_col, const float* d_prop,
+                       const double* d_nmax, const double* d_nsum, DeviceGraphBuffers& out,
+                       cudaStream_t s);
+
+// R-MAT topology + mirrored CSR + Philox weights/labels on the device.
+// Definition identical to oracle.c orc_gen_rmat / orc_synth_philox.
+struct RmatSpec {
+    uint32_t scale, edge_factor;
+    unsigned long long seed;       // derive_seed(seed, "rmat") / "perm" applied inside
+    int weights;                   // 0 uniform, 2 pareto, -1 none
+    double low, high, alpha;
+    unsigned long long weight_seed;
+    int labels;
+    uint32_t label_low, label_high;
+    unsigned long long label_seed;
+};
+cudaError_t build_rmat(const RmatSpec& spec, DeviceGraphBuffers& out, cudaStream_t s);
+
+// Unpacks the device graph into separate device arrays (for downloads).
+cudaError_t unpack_graph(const DeviceGraphBuffers& g, unsigned long long* d_row, uint32_t* d_col,
+                         float* d_prop, double* d_nmax, double* d_nsum, cudaStream_t s);
+
+// K4: the two profiling micro-passes of profile_edge_cost_ratio
+// (cost_model.cpp:37-126) on the device; returns the median ratio.
+cudaError_t calibrate_ratio(const DeviceGraphBuffers& g, int model_kind, bool weighted,
+                            const ModelParams& mp, unsigned long long seed, int num_sms,
+                            cudaStream_t s, double* ratio);
+
+unsigned long long host_derive_seed(unsigned long long seed, unsigned long long stream);
+
+}  // namespace dwb

@@ -1,0 +1,46 @@
+// dw_walk.cuh -- walk-path kernel interface shared by dw_walk.cu and dw_capi.cu.
+#pragma once
+#include "dw_models.cuh"
+
+namespace dwb {
+
+// Counter slots of the per-run device accumulator (RunStats, runtime.hpp:53-73).
+enum Counter : int {
+    kCQueries = 0,
+    kCQueryErrors,
+    kCDeadEnds,
+    kCTrials,
+    kCWeightReads,
+    kCRngDraws,
+    kCFallbacks,
+    kCAlgBytes,           // SURVEY §8(d) minimal-sector bytes (roofline numerator)
+    kCHist,               // [33][2] selection_by_degree
+    kCNum = kCHist + 66
+};
+
+struct WalkParams {
+    DevGraph g;
+    const uint32_t* queries;
+    unsigned long long nq;
+    unsigned long long qid_base;
+    uint32_t* paths;        // [nq][stride] or null
+    uint32_t* lengths;      // [nq] or null
+    uint32_t stride;        // walk_length + 1
+    uint32_t target;        // min(walk_length, max_steps)
+    uint32_t seed_lo, seed_hi;
+    unsigned long long cap_per_degree;
+    double ratio;
+    unsigned long long* counters;     // [kCNum]
+    unsigned long long* next_walker;  // queue head
+    int* error;                       // first DevError
+    unsigned long long* error_info;   // offending query index
+    ModelParams mp;
+};
+
+enum Mode : int { kAdaptive = 0, kForceErvs = 1, kForceErjs = 2, kErvsNoJump = 3 };
+
+// Launches the walk over p.nq walkers on `stream`; returns the CUDA error.
+cudaError_t launch_walk(int model_kind, bool weighted, int mode, const WalkParams& p,
+                        int num_sms, cudaStream_t stream);
+
+}  // namespace dwb

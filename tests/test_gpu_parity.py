@@ -1,0 +1,214 @@
+"""GPU parity suite: the CUDA path (through the C ABI) against the oracle and the
+reference goldens.  Bit-exact paths, lengths and RunStats counters wherever
+both sides consume the same Philox walker stream; chi-square p > 0.01 of
+transition frequencies against the exact probabilities otherwise."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from tests.golden.make_golden import CASES, GRAPHS, MODES, build_oracle_graph, case_id, digest, \
+    stats_core
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def to_device(dw, og):
+    a = og.arrays()
+    return dw.DeviceGraph.from_csr(a["row"], a["col"], a["prop"], a["label"])
+
+
+def run_both(dw, orc, og, dg, mk, queries, mode, L, ratio, seed=7, cap=64, qid_base=0):
+    r_dev = dw.run_queries(dg, dw.Model(**mk), queries,
+                           dw.RunOptions(mode=mode, walk_length=L, seed=seed, edge_cost_ratio=ratio,
+                                         erjs_cap_per_degree=cap, qid_base=qid_base))
+    r_orc = orc.run(og, orc.Model(**mk), queries, mode=mode, walk_length=L, seed=seed,
+                    ratio=ratio, cap_per_degree=cap, rng="philox", threads=4, qid_base=qid_base)
+    return r_dev, r_orc
+
+
+def assert_same(r_dev, r_orc, tag=""):
+    assert stats_core(r_dev.stats) == stats_core(r_orc.stats), tag
+    assert np.array_equal(r_dev.lengths, r_orc.lengths), tag
+    assert np.array_equal(r_dev.paths, r_orc.paths), tag
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: c[0] + ":" + c[1]["kind"])
+def test_reference_goldens_on_gpu(dw, orc, case):
+    """GPU == the reference's own sampler templates (tests/golden/ref_walks.json)."""
+    gold = {c["id"]: c for c in json.load(open(os.path.join(GOLDEN, "ref_walks.json")))["cases"]}
+    gname, mk, L, ratio = case
+    og = build_oracle_graph(GRAPHS[gname])
+    dg = to_device(dw, og)
+    q = np.arange(og.nv, dtype=np.uint32)
+    for mode in MODES:
+        r = dw.run_queries(dg, dw.Model(**mk), q,
+                           dw.RunOptions(mode=mode, walk_length=L, seed=7, edge_cost_ratio=ratio))
+        c = gold[case_id(gname, mk, mode, L)]
+        assert stats_core(r.stats) == c["stats"], mode
+        assert digest(r.paths, r.lengths) == c["digest"], mode
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("mk", [dict(kind="node2vec", a=2.0, b=0.5),
+                                dict(kind="node2vec", a=0.5, b=2.0),
+                                dict(kind="pr2", gamma=0.2),
+                                dict(kind="static", weighted=False)])
+def test_rmat_bit_exact(dw, orc, mk, mode):
+    """R-MAT s12 (hubs well above the warp-cooperative threshold)."""
+    og = orc.Graph.rmat(12, 16, 5).synth_philox("uniform", 1.0, 5.0, seed=6)
+    dg = to_device(dw, og)
+    q = np.arange(og.nv, dtype=np.uint32)
+    r_dev, r_orc = run_both(dw, orc, og, dg, mk, q, mode, 40, 1.2)
+    assert_same(r_dev, r_orc, (mk, mode))
+
+
+def test_metapath_labels_and_dead_ends(dw, orc):
+    og = orc.Graph.rmat(11, 16, 8).synth_philox("uniform", 1.0, 5.0, seed=9)
+    og.synth_philox("labels", 0, 3, seed=10)
+    dg = to_device(dw, og)
+    q = np.arange(og.nv, dtype=np.uint32)
+    mk = dict(kind="metapath", schema=(0, 1, 2, 3) * 20)
+    for mode in MODES:
+        r_dev, r_orc = run_both(dw, orc, og, dg, mk, q, mode, 80, 1.2)
+        assert_same(r_dev, r_orc, mode)
+        assert r_dev.stats["dead_ends"] > 0
+
+
+def test_device_rmat_builder_matches_oracle(dw, orc):
+    for scale, seed in ((10, 1), (13, 77)):
+        dg = dw.DeviceGraph.rmat(scale, 16, seed=seed, weights="uniform", weight_seed=seed + 1,
+                                 labels=(0, 3), label_seed=seed + 2)
+        og = orc.Graph.rmat(scale, 16, seed).synth_philox("uniform", 1.0, 5.0, seed=seed + 1)
+        og.synth_philox("labels", 0, 3, seed=seed + 2)
+        a, b = dg.download(), og.arrays()
+        for k in ("row", "col", "prop", "nmax", "nsum", "label"):
+            assert np.array_equal(a[k], b[k]), (scale, k)
+    dg = dw.DeviceGraph.rmat(11, 16, seed=3, weights="pareto", alpha=1.0, weight_seed=4)
+    og = orc.Graph.rmat(11, 16, 3).synth_philox("pareto", alpha=1.0, seed=4)
+    a, b = dg.download(), og.arrays()
+    for k in ("row", "col", "prop", "nmax", "nsum"):
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_upload_roundtrip_and_aggregates(dw, orc):
+    og = build_oracle_graph(GRAPHS["ba300_labels"])
+    a = og.arrays()
+    # aggregates recomputed on the device (left-to-right) equal the host's
+    dg = dw.DeviceGraph.from_csr(a["row"], a["col"], a["prop"], a["label"])
+    b = dg.download()
+    for k in ("row", "col", "prop", "nmax", "nsum", "label"):
+        assert np.array_equal(a[k], b[k]), k
+    info = dg.info()
+    assert info["num_vertices"] == og.nv and info["num_edges"] == og.ne and info["has_labels"]
+    assert info["max_degree"] == int(np.diff(a["row"]).max())
+
+
+def test_edge_cases(dw, orc):
+    """Isolated starts, out-of-range starts, walk_length 0, cap fallback, duplicates."""
+    og = orc.Graph.build([0, 0, 0, 1, 1, 2], [1, 1, 2, 0, 2, 0], [1, 2, 3, 1, 4, 2], nv_hint=6)
+    dg = to_device(dw, og)
+    q = np.array([0, 3, 99, 1, 2, 5, 0, 0], np.uint32)
+    for mode in MODES:
+        for L in (0, 1, 7):
+            r_dev, r_orc = run_both(dw, orc, og, dg, dict(kind="node2vec", a=0.5, b=2.0), q,
+                                    mode, L, 1.0)
+            assert_same(r_dev, r_orc, (mode, L))
+            assert r_dev.lengths[2] == 0 and r_dev.stats["query_errors"] == 1
+    # tiny cap: every eRJS step falls back to the reservoir
+    r_dev, r_orc = run_both(dw, orc, og, dg, dict(kind="static"), q, "force-erjs", 9, 1.0, cap=0)
+    assert_same(r_dev, r_orc, "cap0")
+    assert r_dev.stats["erjs_fallbacks"] == r_dev.stats["steps"]
+    # empty query list
+    r = dw.run_queries(dg, dw.Model(), np.zeros(0, np.uint32), dw.RunOptions(walk_length=5))
+    assert r.stats["queries"] == 0
+
+
+def test_sharding_is_output_invariant(dw, orc):
+    """Device-count analogue of worker-count invariance (test_runtime.cpp:118-138):
+    walkers split by qid_base give the paths of one unsplit run."""
+    og = orc.Graph.rmat(11, 16, 21).synth_philox("uniform", 1.0, 5.0, seed=22)
+    dg = to_device(dw, og)
+    q = np.arange(og.nv, dtype=np.uint32)
+    opts = dict(mode="adaptive", walk_length=30, seed=3, edge_cost_ratio=1.2)
+    full = dw.run_queries(dg, dw.Model(a=0.5, b=2.0), q, dw.RunOptions(**opts))
+    parts = [dw.run_queries(dg, dw.Model(a=0.5, b=2.0), q[lo:hi],
+                            dw.RunOptions(qid_base=lo, **opts))
+             for lo, hi in ((0, 700), (700, 1500), (1500, og.nv))]
+    assert np.array_equal(full.paths, np.concatenate([p.paths for p in parts]))
+    assert full.stats["steps"] == sum(p.stats["steps"] for p in parts)
+
+
+def test_large_batched_run_matches_oracle(dw, orc):
+    """> 1M walkers: dw_run splits into overlapped batches; output unchanged."""
+    og = orc.Graph.rmat(14, 16, 31).synth_philox("uniform", 1.0, 5.0, seed=32)
+    dg = to_device(dw, og)
+    rs = np.random.default_rng(0)
+    q = rs.integers(0, og.nv, size=2_500_000, dtype=np.uint32)
+    r_dev, r_orc = run_both(dw, orc, og, dg, dict(kind="node2vec", a=0.5, b=2.0), q, "adaptive",
+                            10, 1.2)
+    assert_same(r_dev, r_orc, "batched")
+    assert r_dev.stats["kernel_launches"] > 1
+
+
+def test_run_device_entry_point(dw, orc):
+    import ctypes as C
+    import torch
+    og = orc.Graph.rmat(11, 16, 41).synth_philox("uniform", 1.0, 5.0, seed=42)
+    dg = to_device(dw, og)
+    q = np.arange(og.nv, dtype=np.uint32)
+    L = 20
+    dq = torch.from_numpy(q.view(np.int32)).cuda()
+    dp = torch.empty((len(q), L + 1), dtype=torch.int32, device="cuda")
+    dl = torch.empty(len(q), dtype=torch.int32, device="cuda")
+    lib = dw.load_library()
+    m = dw.Model(a=0.5, b=2.0).c()
+    o = dw.RunOptions(walk_length=L, seed=4, edge_cost_ratio=1.2).c()
+    torch.cuda.synchronize()
+    assert lib.dw_run_device(dg.h, 0, C.byref(m), C.c_void_p(dq.data_ptr()), len(q), C.byref(o),
+                             C.c_void_p(dp.data_ptr()), C.c_void_p(dl.data_ptr()), None) == 0
+    st = dw.RunStatsC()
+    assert lib.dw_run_device_sync(dg.h, 0, C.byref(st)) == 0
+    r_orc = orc.run(og, orc.Model(a=0.5, b=2.0), q, walk_length=L, seed=4, ratio=1.2,
+                    rng="philox", threads=4)
+    assert np.array_equal(dp.cpu().numpy().view(np.uint32), r_orc.paths)
+    assert np.array_equal(dl.cpu().numpy().view(np.uint32), r_orc.lengths)
+    assert st.steps == r_orc.stats["steps"] and st.kernel_ms > 0
+
+
+def test_chi_square_transition_frequencies(dw, orc):
+    """Per-(prev,cur) transition counts vs oracle_enumerate (samplers.hpp:272-288), p > 0.01."""
+    from scipy.stats import chisquare
+    # second-order fixture (test_util.hpp:22-36) reached from prev=0 -> cur=1
+    og = orc.Graph.build([0, 0, 1, 1, 1, 1], [1, 2, 0, 2, 3, 4], [1, 1, 1, 1, 3, 1], nv_hint=5)
+    dg = to_device(dw, og)
+    n = 400_000
+    for mk in (dict(kind="node2vec", a=2.0, b=0.5), dict(kind="pr2", gamma=0.2)):
+        probs = orc.transition_probs(og, orc.Model(**mk), 1, 0, 1)
+        for mode in MODES:
+            r = dw.run_queries(dg, dw.Model(**mk), np.zeros(n, np.uint32),
+                               dw.RunOptions(mode=mode, walk_length=2, seed=11,
+                                             edge_cost_ratio=0.5))
+            sel = r.paths[:, 1] == 1  # walks that went 0 -> 1
+            nxt = r.paths[sel, 2]
+            counts = np.array([(nxt == t).sum() for t in (0, 2, 3, 4)])
+            assert chisquare(counts, probs * counts.sum()).pvalue > 0.01, (mk, mode)
+
+
+def test_calibration(dw, orc):
+    dg = dw.DeviceGraph.rmat(14, 16, seed=5)
+    for mk in (dict(kind="node2vec", a=0.5, b=2.0), dict(kind="static")):
+        r = dw.profile_edge_cost_ratio(dg, dw.Model(**mk), seed=1)
+        assert np.isfinite(r) and r > 0
+
+
+def test_errors(dw):
+    with pytest.raises(dw.DynwalkError, match="not supported"):
+        dg = dw.DeviceGraph.rmat(8, 16, seed=1)
+        dw.run_queries(dg, dw.Model(), [0], dw.RunOptions(mode="force-its"))
+    with pytest.raises(dw.DynwalkError, match="strictly positive"):
+        dw.DeviceGraph.from_csr([0, 1, 1], [1], [0.0])
+    with pytest.raises(dw.DynwalkError, match="not sorted"):
+        dw.DeviceGraph.from_csr([0, 2, 2, 2], [2, 1], [1.0, 1.0])
