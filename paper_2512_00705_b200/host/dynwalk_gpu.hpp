@@ -1,0 +1,211 @@
+// dynwalk_gpu.hpp -- header-only C++ shim: the reference's host API for the
+// walk path, executed by the B200 engine through the C ABI (dynwalk_b200.h).
+//
+// Drop-in for the reference (compile inside its tree, link libdynwalk_b200.so):
+//
+//   dynwalk::run_queries(g, model, params, queries, opts)          runtime.hpp:85-86
+//     -> dynwalk::gpu::run_queries(g, model, params, queries, opts)  (same signature)
+//   dynwalk::profile_edge_cost_ratio(g, model, cfg)                cost_model.hpp:39-40
+//     -> dynwalk::gpu::profile_edge_cost_ratio(g, model, cfg)
+//
+// Semantics kept: query order, path[0] = start, length
+// <= min(L, max_steps) + 1, empty path + query_errors++ for an out-of-range
+// start, RunStats counters exactly as runtime.cpp:141-149, output independent
+// of the device count.  Errors surface as dynwalk::Error with the reference's
+// wording.  Options the GPU runtime does not implement (ForceIts, ForceAls,
+// check_bounds, bound_scale != 1, collect_cv, DslWalk models) throw
+// dynwalk::Error naming the option; the CPU run_queries still serves them.
+// Walker randomness is the Philox (seed, walker, step) stream, so paths equal
+// the reference samplers driven by that stream (tests/golden/ref_walks.json),
+// not the mt19937 stream of the CPU run_queries.
+#pragma once
+
+#include <map>
+#include <memory>
+#include <mutex>
+#include <span>
+#include <string>
+#include <tuple>
+#include <type_traits>
+#include <variant>
+#include <vector>
+
+#include "dynwalk/cost_model.hpp"
+#include "dynwalk/runtime.hpp"
+#include "dynwalk_b200.h"
+
+namespace dynwalk::gpu {
+
+inline void check(int rc) {
+    if (rc != DW_OK) throw Error(dw_last_error());
+}
+
+// Device replicas of one immutable Graph (graph.hpp:47).
+class DeviceGraph {
+public:
+    explicit DeviceGraph(const Graph& g, std::vector<int> devices = {0}) {
+        const std::uint32_t nv = g.num_vertices();
+        std::vector<double> nmax(nv), nsum(nv);
+        for (std::uint32_t v = 0; v < nv; ++v) {
+            nmax[v] = g.node_prop_max(v);
+            nsum[v] = g.node_prop_sum(v);
+        }
+        dw_graph_desc d{};
+        d.num_vertices = nv;
+        d.num_edges = g.num_edges();
+        d.row_offsets = g.row_offsets().data();
+        d.col_indices = g.col_indices().data();
+        d.edge_props = g.edge_props().data();
+        d.edge_labels = g.has_labels() ? g.edge_labels().data() : nullptr;
+        d.node_prop_max = nmax.data();
+        d.node_prop_sum = nsum.data();
+        check(dw_graph_create(&d, devices.data(), static_cast<int>(devices.size()), &h_));
+    }
+    ~DeviceGraph() { dw_graph_destroy(h_); }
+    DeviceGraph(const DeviceGraph&) = delete;
+    DeviceGraph& operator=(const DeviceGraph&) = delete;
+    dw_graph_t handle() const { return h_; }
+
+private:
+    dw_graph_t h_ = nullptr;
+};
+
+namespace detail {
+
+// AnyModel (models.hpp:200) -> dw_model_desc; the device functor is picked by
+// kind inside the library (compile-time specialised kernels).
+struct ModelDesc {
+    dw_model_desc d{};
+    std::vector<std::uint16_t> schema;
+};
+
+inline ModelDesc to_desc(const AnyModel& model) {
+    ModelDesc m;
+    std::visit(
+        [&](const auto& v) {
+            using T = std::decay_t<decltype(v)>;
+            if constexpr (!std::is_same_v<T, DslWalk>) m.d.weighted = v.weighted ? 1 : 0;
+            if constexpr (std::is_same_v<T, StaticWalk>) {
+                m.d.kind = DW_MODEL_STATIC;
+            } else if constexpr (std::is_same_v<T, Node2Vec>) {
+                m.d.kind = DW_MODEL_NODE2VEC;
+                m.d.a = v.a;
+                m.d.b = v.b;
+            } else if constexpr (std::is_same_v<T, MetaPath>) {
+                m.d.kind = DW_MODEL_METAPATH;
+                m.schema.assign(v.schema.begin(), v.schema.end());
+            } else if constexpr (std::is_same_v<T, SecondOrderPr>) {
+                m.d.kind = DW_MODEL_PR2;
+                m.d.gamma = v.gamma;
+            }
+        },
+        model);
+    if (std::holds_alternative<DslWalk>(model))
+        throw Error("model '" + model_name(model) +
+                    "' is a DSL model; the GPU runtime needs it compiled to a device functor");
+    m.d.schema = m.schema.empty() ? nullptr : m.schema.data();
+    m.d.schema_len = static_cast<std::uint32_t>(m.schema.size());
+    return m;
+}
+
+inline int to_mode(SamplerMode mode) {
+    switch (mode) {
+    case SamplerMode::Adaptive: return DW_MODE_ADAPTIVE;
+    case SamplerMode::ForceErvs: return DW_MODE_FORCE_ERVS;
+    case SamplerMode::ForceErjs: return DW_MODE_FORCE_ERJS;
+    case SamplerMode::ErvsNoJump: return DW_MODE_ERVS_NOJUMP;
+    case SamplerMode::ForceIts: return DW_MODE_FORCE_ITS;
+    case SamplerMode::ForceAls: return DW_MODE_FORCE_ALS;
+    }
+    return -1;
+}
+
+// Cached replicas keyed by graph identity (arrays are never mutated in place:
+// set_edge_props replaces the vector, which changes the data pointer).
+inline std::shared_ptr<DeviceGraph> cached(const Graph& g) {
+    using Key = std::tuple<const Graph*, const void*, const void*, const void*, std::uint64_t>;
+    static std::mutex mu;
+    static std::map<Key, std::shared_ptr<DeviceGraph>> cache;
+    const Key k{&g, g.col_indices().data(), g.edge_props().data(),
+                g.has_labels() ? static_cast<const void*>(g.edge_labels().data()) : nullptr,
+                g.num_edges()};
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(k);
+    if (it != cache.end()) return it->second;
+    if (cache.size() >= 4) cache.clear();
+    auto dg = std::make_shared<DeviceGraph>(g);
+    cache.emplace(k, dg);
+    return dg;
+}
+
+}  // namespace detail
+
+inline RunResult run_queries(const DeviceGraph& dg, const AnyModel& model,
+                             const CostModelParams& params, std::span<const VertexId> queries,
+                             const RunOptions& opts) {
+    if (opts.workers < 1) throw Error("worker count must be >= 1");  // runtime.cpp:194
+    if (opts.check_bounds) throw Error("RunOptions.check_bounds is not supported by the GPU runtime");
+    if (opts.bound_scale != 1.0)
+        throw Error("RunOptions.bound_scale is not supported by the GPU runtime");
+    if (opts.collect_cv) throw Error("RunOptions.collect_cv is not supported by the GPU runtime");
+    const detail::ModelDesc m = detail::to_desc(model);
+    dw_run_opts o{};
+    o.mode = detail::to_mode(opts.mode);
+    o.walk_length = opts.walk_length;
+    o.seed = opts.seed;
+    o.erjs_cap_per_degree = opts.erjs_cap_per_degree;
+    o.edge_cost_ratio = params.edge_cost_ratio;
+    o.qid_base = 0;
+    const std::size_t nq = queries.size();
+    const std::size_t stride = static_cast<std::size_t>(opts.walk_length) + 1;
+    std::vector<VertexId> flat(nq * stride);
+    std::vector<std::uint32_t> lengths(nq);
+    dw_run_stats st{};
+    check(dw_run(dg.handle(), &m.d, queries.data(), nq, &o, flat.data(), lengths.data(), &st));
+
+    RunResult rr;
+    rr.paths.resize(nq);
+    for (std::size_t i = 0; i < nq; ++i)
+        rr.paths[i].assign(flat.begin() + i * stride, flat.begin() + i * stride + lengths[i]);
+    RunStats& s = rr.stats;
+    s.queries = st.queries;
+    s.query_errors = st.query_errors;
+    s.dead_ends = st.dead_ends;
+    s.steps = st.steps;
+    s.select_ervs = st.select_ervs;
+    s.select_erjs = st.select_erjs;
+    s.trials = st.trials;
+    s.weight_reads = st.weight_reads;
+    s.rng_draws = st.rng_draws;
+    s.erjs_fallbacks = st.erjs_fallbacks;
+    for (std::size_t b = 0; b < s.selection_by_degree.size(); ++b) {
+        s.selection_by_degree[b][0] = st.selection_by_degree[b][0];
+        s.selection_by_degree[b][1] = st.selection_by_degree[b][1];
+    }
+    s.path_lengths = std::move(lengths);
+    s.wall_ms = st.total_ms;
+    return rr;
+}
+
+// Same signature as dynwalk::run_queries (runtime.hpp:85-86).
+inline RunResult run_queries(const Graph& g, const AnyModel& model, const CostModelParams& params,
+                             std::span<const VertexId> queries, const RunOptions& opts) {
+    return run_queries(*detail::cached(g), model, params, queries, opts);
+}
+
+// Same signature as dynwalk::profile_edge_cost_ratio (cost_model.hpp:39-40);
+// the random / sequential micro-passes run on device 0.
+inline CostModelParams profile_edge_cost_ratio(const Graph& g, const AnyModel& model,
+                                               const ProfileConfig& cfg) {
+    if (!(cfg.node_fraction > 0.0) || cfg.node_fraction > 1.0)
+        throw Error("profile node_fraction must be in (0, 1]");
+    if (cfg.neighbors_per_node == 0 || cfg.repetitions == 0)
+        throw Error("profile neighbors_per_node and repetitions must be >= 1");
+    const detail::ModelDesc m = detail::to_desc(model);
+    CostModelParams p;
+    check(dw_calibrate(detail::cached(g)->handle(), &m.d, cfg.seed, &p.edge_cost_ratio));
+    p.profiled = true;
+    return p;
+}
+
+}  // namespace dynwalk::gpu

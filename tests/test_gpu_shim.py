@@ -1,0 +1,54 @@
+"""The product C++ shim (host/dynwalk_gpu.hpp) with the reference's own
+signature dynwalk::gpu::run_queries, driven from reference types
+(oracle/_ref/shim_check), must reproduce the reference goldens exactly."""
+import json
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from tests.golden.make_golden import CASES, GRAPHS, case_id, digest, stats_core
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SHIM = os.path.join(ROOT, "oracle", "_ref", "shim_check")
+GOLDEN = os.path.join(ROOT, "tests", "golden", "ref_walks.json")
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: c[0] + ":" + c[1]["kind"])
+def test_shim_reproduces_reference_goldens(case, tmp_path):
+    if not os.path.exists(SHIM):
+        pytest.skip("oracle/_ref/shim_check not built (needs /root/reference at build time)")
+    gold = {c["id"]: c for c in json.load(open(GOLDEN))["cases"]}
+    gname, mk, L, ratio = case
+    spec = GRAPHS[gname]
+    args = [SHIM, f"graph={spec['kind']}", f"n={spec['n']}", f"deg={spec['deg']}",
+            f"gseed={spec['seed']}", f"weights={spec['weights'][0]}",
+            f"low={spec['weights'][1]}", f"high={spec['weights'][2]}",
+            f"alpha={spec['weights'][3]}", f"model={mk['kind']}",
+            f"weighted={int(mk.get('weighted', True))}", f"a={mk.get('a', 2.0)}",
+            f"b={mk.get('b', 0.5)}", f"gamma={mk.get('gamma', 0.2)}",
+            "schema=" + ",".join(map(str, mk.get("schema", (0, 1, 2, 3, 4)))),
+            f"L={L}", f"ratio={ratio}", "seed=7"]
+    if spec["labels"]:
+        args.append(f"labels={spec['labels'][0]},{spec['labels'][1]}")
+    for mode in ("adaptive", "force-erjs", "force-ervs", "ervs-nojump"):
+        out = str(tmp_path / mode)
+        p = subprocess.run(args + [f"mode={mode}", f"out={out}"], capture_output=True, text=True,
+                           timeout=300)
+        assert p.returncode == 0, p.stderr
+        stats = json.loads(p.stdout.strip().splitlines()[-1])
+        paths = np.fromfile(out + ".paths", dtype=np.uint32).reshape(-1, L + 1)
+        lengths = np.fromfile(out + ".lengths", dtype=np.uint32)
+        c = gold[case_id(gname, mk, mode, L)]
+        assert stats_core(stats) == c["stats"], mode
+        assert digest(paths, lengths) == c["digest"], mode
+
+
+def test_shim_rejects_unsupported_options(tmp_path):
+    if not os.path.exists(SHIM):
+        pytest.skip("oracle/_ref/shim_check not built")
+    p = subprocess.run([SHIM, "mode=force-its", f"out={tmp_path}/x"], capture_output=True,
+                       text=True, timeout=120)
+    assert p.returncode == 2 and "not supported" in p.stderr
