@@ -28,7 +28,8 @@ __all__ = ["DeviceGraph", "Model", "RunOptions", "RunResult", "DynwalkError", "r
            "INVALID_VERTEX"]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB = os.path.join(HERE, "lib", "libdynwalk_b200.so")
+# DYNWALK_B200_LIB selects a locally built variant (performance experiments)
+LIB = os.environ.get("DYNWALK_B200_LIB", os.path.join(HERE, "lib", "libdynwalk_b200.so"))
 INVALID_VERTEX = 0xFFFFFFFF
 
 EXPORTED_SYMBOLS = (

@@ -110,6 +110,7 @@ void free_replica(Replica& r) {
     cudaFree(r.g.nodes);
     cudaFree(r.g.edges);
     cudaFree(r.g.labels);
+    cudaFree(r.g.hslots);
     cudaFree(r.counters);
     cudaFree(r.queues);
     cudaFree(r.error);
@@ -272,7 +273,7 @@ uint32_t target_steps(const dw_model_desc* m, const dw_run_opts* o) {
 dwb::WalkParams make_params(Replica& r, const dw_model_desc* m, const dw_run_opts* o) {
     dwb::WalkParams p;
     std::memset(&p, 0, sizeof p);
-    p.g = dwb::DevGraph{r.g.nodes, r.g.edges, r.g.labels, r.g.nv, r.g.ne};
+    p.g = dwb::DevGraph{r.g.nodes, r.g.edges, r.g.labels, r.g.hslots, r.g.nv, r.g.ne};
     p.stride = o->walk_length + 1;
     p.target = target_steps(m, o);
     p.seed_lo = (uint32_t)o->seed;

@@ -8,6 +8,7 @@
 //   EdgeRec[ne]   8 B: {target u32, prop f32}.  One random sector per
 //                rejection trial serves edge_target(e) and edge_prop(e).
 //   labels[ne]   u16, only for labelled graphs (MetaPath).
+//   hslots[]     per-row membership hash sets (dw_member.cuh), 32 B buckets.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -19,7 +20,7 @@ constexpr uint32_t kInvalid = 0xFFFFFFFFu;
 struct alignas(32) NodeRec {
     unsigned long long begin;
     uint32_t degree;
-    uint32_t pad;
+    uint32_t hoff;  // first bucket of the row's membership hash set (dw_member.cuh)
     double hmax;
     double hsum;
 };
@@ -35,6 +36,7 @@ struct DevGraph {
     const NodeRec* __restrict__ nodes;
     const EdgeRec* __restrict__ edges;
     const uint16_t* __restrict__ labels;  // may be null
+    const uint32_t* __restrict__ hslots;  // membership hash sets, 8 slots per bucket
     uint32_t nv;
     unsigned long long ne;
 };
@@ -55,7 +57,7 @@ __device__ __forceinline__ NodeRec load_node(const NodeRec* __restrict__ p) {
     NodeRec r;
     r.begin = (unsigned long long)a.x | ((unsigned long long)a.y << 32);
     r.degree = a.z;
-    r.pad = a.w;
+    r.hoff = a.w;
     r.hmax = __hiloint2double((int)b.y, (int)b.x);
     r.hsum = __hiloint2double((int)b.w, (int)b.z);
     return r;

@@ -8,6 +8,7 @@
 // edge, so a full key sort yields the identical arrays.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_reduce.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <vector>
@@ -73,12 +74,95 @@ __global__ void pack_nodes_kernel(const ull* __restrict__ row, const float* __re
         NodeRec r;
         r.begin = b;
         r.degree = (uint32_t)(e - b);
-        r.pad = 0;
+        r.hoff = 0;
         r.hmax = mx;
         r.hsum = sum;
         out[v] = r;
         atomicMax(max_degree, r.degree);
     }
+}
+
+// ---- membership hash sets (dw_member.cuh) ----------------------------------
+__global__ void bucket_count_kernel(const NodeRec* __restrict__ nodes, uint32_t nv,
+                                    uint32_t* __restrict__ counts) {
+    for (ull v = blockIdx.x * (ull)blockDim.x + threadIdx.x; v < nv;
+         v += (ull)gridDim.x * blockDim.x)
+        counts[v] = hash_buckets(nodes[v].degree);
+}
+
+__global__ void set_hoff_kernel(NodeRec* __restrict__ nodes, uint32_t nv,
+                                const uint32_t* __restrict__ offs) {
+    for (ull v = blockIdx.x * (ull)blockDim.x + threadIdx.x; v < nv;
+         v += (ull)gridDim.x * blockDim.x)
+        nodes[v].hoff = offs[v];
+}
+
+// one warp per row: lanes insert the row's targets (coalesced reads)
+__global__ void hash_insert_kernel(const NodeRec* __restrict__ nodes, uint32_t nv,
+                                   const EdgeRec* __restrict__ edges, uint32_t* __restrict__ hslots) {
+    const ull warp = (blockIdx.x * (ull)blockDim.x + threadIdx.x) >> 5;
+    const ull nwarps = ((ull)gridDim.x * blockDim.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    for (ull v = warp; v < nv; v += nwarps) {
+        const NodeRec nr = nodes[v];
+        if (nr.degree <= kScanMax) continue;
+        const uint32_t lg = hash_log2_buckets(nr.degree);
+        const uint32_t mask = (1u << lg) - 1u;
+        for (ull i = lane; i < nr.degree; i += 32) {
+            const uint32_t u = edges[nr.begin + i].col;
+            uint32_t b = hash_bucket(u, lg);
+            for (bool done = false; !done;) {
+                uint32_t* slot = hslots + 8ull * (nr.hoff + b);
+                for (int k = 0; k < 8; ++k) {
+                    const uint32_t old = atomicCAS(slot + k, kHashEmpty, u);
+                    if (old == kHashEmpty || old == u) {
+                        done = true;
+                        break;
+                    }
+                }
+                b = (b + 1) & mask;
+            }
+        }
+    }
+}
+
+static cudaError_t build_member_index(DeviceGraphBuffers& g, cudaStream_t s) {
+    uint32_t* counts = nullptr;
+    uint32_t* offs = nullptr;
+    const ull n = std::max<ull>(g.nv, 1);
+    DW_TRY(cudaMallocAsync(&counts, (n + 1) * sizeof(uint32_t), s));
+    DW_TRY(cudaMallocAsync(&offs, (n + 1) * sizeof(uint32_t), s));
+    DW_TRY(cudaMemsetAsync(counts, 0, (n + 1) * sizeof(uint32_t), s));
+    bucket_count_kernel<<<grid_for(g.nv, 256), 256, 0, s>>>(g.nodes, g.nv, counts);
+    // total fits u32 unless sum(next_pow2(2d))/8 >= 2^32 (E >~ 8e9); checked below in u64
+    ull* total64 = nullptr;
+    DW_TRY(cudaMallocAsync(&total64, sizeof(ull), s));
+    size_t tb = 0;
+    DW_TRY(cub::DeviceReduce::Sum(nullptr, tb, counts, total64, (int)(g.nv + 1), s));
+    void* tmp = nullptr;
+    DW_TRY(cudaMallocAsync(&tmp, tb, s));
+    DW_TRY(cub::DeviceReduce::Sum(tmp, tb, counts, total64, (int)(g.nv + 1), s));
+    DW_TRY(cudaFreeAsync(tmp, s));
+    ull total = 0;
+    DW_TRY(cudaMemcpyAsync(&total, total64, sizeof(ull), cudaMemcpyDeviceToHost, s));
+    DW_TRY(cudaStreamSynchronize(s));
+    DW_TRY(cudaFreeAsync(total64, s));
+    if (total >= 0xFFFFFFFFull) return cudaErrorInvalidValue;
+    tb = 0;
+    DW_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, counts, offs, (int)(g.nv + 1), s));
+    DW_TRY(cudaMallocAsync(&tmp, tb, s));
+    DW_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, counts, offs, (int)(g.nv + 1), s));
+    DW_TRY(cudaFreeAsync(tmp, s));
+    set_hoff_kernel<<<grid_for(g.nv, 256), 256, 0, s>>>(g.nodes, g.nv, offs);
+    g.nbuckets = total;
+    DW_TRY(cudaMallocAsync(&g.hslots, std::max<ull>(total, 1) * 32, s));
+    DW_TRY(cudaMemsetAsync(g.hslots, 0xFF, std::max<ull>(total, 1) * 32, s));
+    hash_insert_kernel<<<grid_for((ull)g.nv * 32, 256), 256, 0, s>>>(g.nodes, g.nv, g.edges,
+                                                                      g.hslots);
+    DW_TRY(cudaGetLastError());
+    DW_TRY(cudaFreeAsync(counts, s));
+    DW_TRY(cudaFreeAsync(offs, s));
+    return cudaStreamSynchronize(s);
 }
 
 cudaError_t pack_graph(const ull* d_row, const uint32_t* d_col, const float* d_prop,
@@ -95,7 +179,8 @@ cudaError_t pack_graph(const ull* d_row, const uint32_t* d_col, const float* d_p
     DW_TRY(cudaMemcpyAsync(&h, d_maxd, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
     DW_TRY(cudaStreamSynchronize(s));
     g.max_degree = h;
-    return cudaFreeAsync(d_maxd, s);
+    DW_TRY(cudaFreeAsync(d_maxd, s));
+    return build_member_index(g, s);
 }
 
 __global__ void unpack_kernel(const NodeRec* __restrict__ nodes, const EdgeRec* __restrict__ edges,
@@ -300,16 +385,7 @@ __device__ __forceinline__ double eval_weight(const M& m, const Step& S, const D
     const uint16_t lab = (M::kUsesLabels && g.labels) ? g.labels[e] : (uint16_t)0;
     const WeightCase wc = m.weight(S, er.col, er.h, lab);
     if (!M::kSecondOrder || !wc.needs_member) return wc.w;
-    // Graph::has_edge
-    ull base = S.prev_begin;
-    uint32_t n = S.prev_degree;
-    if (n == 0) return wc.w_out;
-    while (n > 1) {
-        const uint32_t half = n >> 1;
-        if (load_col(g.edges + base + half) <= er.col) base += half;
-        n -= half;
-    }
-    return load_col(g.edges + base) == er.col ? wc.w_in : wc.w_out;
+    return member(g, S.prev_begin, S.prev_degree, S.prev_hoff, er.col) ? wc.w_in : wc.w_out;
 }
 
 // probe_state (cost_model.cpp:20-33): step 1 with the first neighbour as prev
@@ -319,11 +395,13 @@ __device__ __forceinline__ Step probe_state(const DevGraph& g, uint32_t v) {
     S.cur = v;
     S.degree = nr.degree;
     S.begin = nr.begin;
+    S.hoff = nr.hoff;
     S.hmax = nr.hmax;
     S.hsum = nr.hsum;
     S.prev = kInvalid;
     S.prev_degree = 0;
     S.prev_begin = 0;
+    S.prev_hoff = 0;
     S.step = 0;
     if (nr.degree) {
         const uint32_t pv = load_col(g.edges + nr.begin);
@@ -332,6 +410,7 @@ __device__ __forceinline__ Step probe_state(const DevGraph& g, uint32_t v) {
             S.prev = pv;
             S.prev_degree = pr.degree;
             S.prev_begin = pr.begin;
+            S.prev_hoff = pr.hoff;
             S.step = 1;
         }
     }
@@ -382,7 +461,7 @@ __global__ void probe_pass_kernel(DevGraph g, __grid_constant__ const ModelParam
 template <class M>
 static cudaError_t calibrate_t(const DeviceGraphBuffers& gb, const ModelParams& mp, ull seed,
                                cudaStream_t s, double* ratio) {
-    DevGraph g{gb.nodes, gb.edges, gb.labels, gb.nv, gb.ne};
+    DevGraph g{gb.nodes, gb.edges, gb.labels, gb.hslots, gb.nv, gb.ne};
     // ProfileConfig defaults: 1% of nodes, >= 64, <= 32 neighbours, 5 reps
     uint32_t want = (uint32_t)std::max<ull>((ull)std::ceil(0.01 * gb.nv), 64);
     const ull tries = (ull)want * 8;

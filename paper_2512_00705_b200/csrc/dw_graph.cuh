@@ -8,6 +8,8 @@ struct DeviceGraphBuffers {
     NodeRec* nodes = nullptr;
     EdgeRec* edges = nullptr;
     uint16_t* labels = nullptr;
+    uint32_t* hslots = nullptr;  // membership hash sets (dw_member.cuh)
+    unsigned long long nbuckets = 0;
     uint32_t nv = 0;
     unsigned long long ne = 0;
     uint32_t max_degree = 0;

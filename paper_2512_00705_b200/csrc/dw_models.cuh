@@ -18,7 +18,7 @@
 // interpretation.  Arithmetic follows the reference operation order; the
 // library builds with --fmad=false so no multiply-add is ever contracted.
 #pragma once
-#include "dw_common.cuh"
+#include "dw_member.cuh"
 
 namespace dwb {
 
@@ -27,9 +27,11 @@ namespace dwb {
 struct Step {
     uint32_t cur, prev;  // prev == kInvalid: first step
     uint32_t prev_degree;
+    uint32_t prev_hoff;  // prev's membership hash set (dw_member.cuh)
     unsigned long long prev_begin;
     uint32_t step;
     uint32_t degree;  // d(cur)
+    uint32_t hoff;
     unsigned long long begin;
     double hmax, hsum;
     __device__ __forceinline__ bool has_prev() const { return prev != kInvalid; }
