@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -86,6 +87,19 @@ int init_replica(Replica& r, int device) {
     CU(cudaSetDevice(device), "cudaSetDevice");
     CU(cudaDeviceGetAttribute(&r.num_sms, cudaDevAttrMultiProcessorCount, device),
        "cudaDeviceGetAttribute");
+    // Every gather on the walk path is one random 32 B sector; an L2 that
+    // promotes misses to 64/128 B fetches would multiply DRAM traffic.
+    // DW_L2_FETCH overrides the granularity (bytes) for experiments.
+    {
+        size_t fetch = 32;
+        if (const char* s = std::getenv("DW_L2_FETCH")) fetch = (size_t)std::atoi(s);
+        if (fetch) CU(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, fetch), "L2 fetch limit");
+        if (std::getenv("DW_VERBOSE")) {
+            size_t v = 0;
+            cudaDeviceGetLimit(&v, cudaLimitMaxL2FetchGranularity);
+            std::fprintf(stderr, "dynwalk: device %d L2 fetch granularity %zu B\n", device, v);
+        }
+    }
     CU(cudaStreamCreateWithFlags(&r.stream, cudaStreamNonBlocking), "cudaStreamCreate");
     CU(cudaStreamCreateWithFlags(&r.copy, cudaStreamNonBlocking), "cudaStreamCreate");
     CU(cudaMalloc(&r.counters, dwb::kCNum * sizeof(ull)), "cudaMalloc counters");
@@ -111,6 +125,7 @@ void free_replica(Replica& r) {
     cudaFree(r.g.edges);
     cudaFree(r.g.labels);
     cudaFree(r.g.hslots);
+    cudaFree(r.g.fat);
     cudaFree(r.counters);
     cudaFree(r.queues);
     cudaFree(r.error);
@@ -223,6 +238,17 @@ int check_model(const dw_model_desc* m) {
                     "unknown model kind %d (expected static, node2vec, metapath, pr2; DSL models "
                     "need code generation)",
                     m->kind);
+    if (m->kind == DW_MODEL_NODE2VEC) {
+        // the device divides by a and b with a correctly rounded reciprocal
+        // (dw_models.cuh ddiv), exact for every quotient in this range
+        const double lo = 0x1p-500, hi = 0x1p500;
+        const double aa = std::fabs(m->a), bb = std::fabs(m->b);
+        if (!(aa >= lo && aa <= hi && bb >= lo && bb <= hi))
+            return fail(DW_EUNSUPPORTED,
+                        "node2vec parameters |a|, |b| must lie in [2^-500, 2^500] on the GPU "
+                        "runtime (a=%g, b=%g)",
+                        m->a, m->b);
+    }
     if (m->kind == DW_MODEL_METAPATH) {
         if (m->schema_len > DW_MAX_SCHEMA)
             return fail(DW_EINVAL, "metapath schema longer than %d labels", DW_MAX_SCHEMA);
@@ -237,6 +263,24 @@ dwb::ModelParams model_params(const dw_model_desc* m) {
     mp.a = m->a;
     mp.b = m->b;
     mp.gamma = m->gamma;
+    // correctly rounded reciprocals for the device's Markstein division
+    // (dw_models.cuh ddiv); only within a range where every quotient the
+    // models form stays a normal double
+    auto in_range = [](double x) { return x >= 0x1p-500 && x <= 0x1p500; };
+    mp.fast_div = (in_range(m->a) && in_range(m->b)) ? 1u : 0u;
+    mp.inv_a = 1.0 / m->a;
+    mp.inv_b = 1.0 / m->b;
+    mp.inv_3 = 1.0 / 3.0;
+    // free rejections need weights that are valid by construction
+    switch (m->kind) {
+    case DW_MODEL_NODE2VEC:
+        mp.shortcut = (m->a > 0.0 && m->b > 0.0 && std::isfinite(m->a) && std::isfinite(m->b)) ? 1u : 0u;
+        break;
+    case DW_MODEL_PR2: mp.shortcut = (m->gamma >= 0.0 && m->gamma <= 1.0) ? 1u : 0u; break;
+    default: mp.shortcut = 0u;
+    }
+    if (const char* env = std::getenv("DW_SHORTCUT"))
+        if (env[0] == '0') mp.shortcut = 0u;
     if (m->kind == DW_MODEL_METAPATH) {
         mp.schema_len = m->schema_len;
         for (uint32_t i = 0; i < m->schema_len; ++i) mp.schema[i] = m->schema[i];
@@ -273,7 +317,7 @@ uint32_t target_steps(const dw_model_desc* m, const dw_run_opts* o) {
 dwb::WalkParams make_params(Replica& r, const dw_model_desc* m, const dw_run_opts* o) {
     dwb::WalkParams p;
     std::memset(&p, 0, sizeof p);
-    p.g = dwb::DevGraph{r.g.nodes, r.g.edges, r.g.labels, r.g.hslots, r.g.nv, r.g.ne};
+    p.g = dwb::DevGraph{r.g.nodes, r.g.edges, r.g.labels, r.g.hslots, r.g.fat, r.g.nv, r.g.ne};
     p.stride = o->walk_length + 1;
     p.target = target_steps(m, o);
     p.seed_lo = (uint32_t)o->seed;

@@ -9,6 +9,13 @@
 //                rejection trial serves edge_target(e) and edge_prop(e).
 //   labels[ne]   u16, only for labelled graphs (MetaPath).
 //   hslots[]     per-row membership hash sets (dw_member.cuh), 32 B buckets.
+//   FatRec[ne]   48 B used of a 64 B stride (optional, "fat" layout): the edge
+//                plus everything the walk needs about its target, so an
+//                accepted rejection trial starts the next step with no further
+//                gather.  On B200 every random miss moves a whole 128 B L2
+//                line from HBM (tools/gather_probe.cu), so a record up to 64 B
+//                costs the same DRAM traffic as a 16 B one; what counts is the
+//                number of random requests per walker-step.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -32,11 +39,35 @@ struct alignas(8) EdgeRec {
 };
 static_assert(sizeof(EdgeRec) == 8, "EdgeRec must be 8 bytes");
 
+// Fat edge record for edge e = (v -> u), 64 B stride (one L2 line half):
+//   w0 col = u          w1 h = edge_prop(e)     w2,w3 begin(u) (48 bits) | label(e) << 48
+//   w4 degree(u)        w5 hoff(u)              w6 twin_lo: first index of v in N(u)
+//   w7 twin_cnt: multiplicity of v in N(u) (0 for a directed edge without twin)
+//   w8..11 node_prop_max(u), node_prop_sum(u) (f64, exact)
+// The twin range lets eRJS reject trials without a gather: every edge of N(u)
+// outside [twin_lo, twin_lo + twin_cnt) has target != v, so its weight is
+// bounded by the model's non-return maximum (dw_models.cuh nonreturn_max).
+struct alignas(64) FatRec {
+    uint32_t col;
+    float h;
+    unsigned long long tbegin_label;
+    uint32_t tdeg;
+    uint32_t thoff;
+    uint32_t twin_lo;
+    uint32_t twin_cnt;
+    double thmax;
+    double thsum;
+    uint32_t aux[4];  // reserved
+};
+static_assert(sizeof(FatRec) == 64, "FatRec stride must be 64 bytes");
+constexpr unsigned long long kBeginMask = (1ull << 48) - 1;
+
 struct DevGraph {
     const NodeRec* __restrict__ nodes;
     const EdgeRec* __restrict__ edges;
     const uint16_t* __restrict__ labels;  // may be null
     const uint32_t* __restrict__ hslots;  // membership hash sets, 8 slots per bucket
+    const FatRec* __restrict__ fat;       // may be null (slim layout)
     uint32_t nv;
     unsigned long long ne;
 };

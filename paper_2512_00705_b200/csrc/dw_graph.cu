@@ -11,6 +11,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "dw_graph.cuh"
@@ -105,7 +106,7 @@ __global__ void hash_insert_kernel(const NodeRec* __restrict__ nodes, uint32_t n
     const uint32_t lane = threadIdx.x & 31;
     for (ull v = warp; v < nv; v += nwarps) {
         const NodeRec nr = nodes[v];
-        if (nr.degree <= kScanMax) continue;
+        if (nr.degree == 0) continue;
         const uint32_t lg = hash_log2_buckets(nr.degree);
         const uint32_t mask = (1u << lg) - 1u;
         for (ull i = lane; i < nr.degree; i += 32) {
@@ -124,6 +125,73 @@ __global__ void hash_insert_kernel(const NodeRec* __restrict__ nodes, uint32_t n
             }
         }
     }
+}
+
+// ---- fat edge records (dw_common.cuh FatRec) --------------------------------
+// first index i in [0, d) with col[b + i] >= key (the row is sorted by target)
+__device__ __forceinline__ uint32_t row_lower_bound(const EdgeRec* __restrict__ edges, ull b,
+                                                    uint32_t d, uint32_t key) {
+    uint32_t lo = 0, hi = d;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (load_col(edges + b + mid) < key)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// one warp per row v: record e = (v -> u) gets u's node data and the range of
+// v in N(u) (its return edges when a walker stands on u having come from v)
+__global__ void fat_build_kernel(const NodeRec* __restrict__ nodes, uint32_t nv,
+                                 const EdgeRec* __restrict__ edges,
+                                 const uint16_t* __restrict__ labels, FatRec* __restrict__ fat) {
+    const ull warp = (blockIdx.x * (ull)blockDim.x + threadIdx.x) >> 5;
+    const ull nwarps = ((ull)gridDim.x * blockDim.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    for (ull v = warp; v < nv; v += nwarps) {
+        const NodeRec nr = nodes[v];
+        for (ull i = lane; i < nr.degree; i += 32) {
+            const ull e = nr.begin + i;
+            const EdgeRec er = edges[e];
+            const NodeRec nu = nodes[er.col];
+            const uint32_t lo = row_lower_bound(edges, nu.begin, nu.degree, (uint32_t)v);
+            const uint32_t hi = v == 0xFFFFFFFFull
+                                    ? nu.degree
+                                    : row_lower_bound(edges, nu.begin, nu.degree, (uint32_t)v + 1);
+            FatRec f;
+            f.col = er.col;
+            f.h = er.h;
+            f.tbegin_label = (nu.begin & kBeginMask) |
+                             ((ull)(labels ? labels[e] : (uint16_t)0) << 48);
+            f.tdeg = nu.degree;
+            f.thoff = nu.hoff;
+            f.twin_lo = lo;
+            f.twin_cnt = hi - lo;
+            f.thmax = nu.hmax;
+            f.thsum = nu.hsum;
+            f.aux[0] = f.aux[1] = f.aux[2] = f.aux[3] = 0;
+            fat[e] = f;
+        }
+    }
+}
+
+static cudaError_t build_fat(DeviceGraphBuffers& g, cudaStream_t s) {
+    g.fat = nullptr;
+    if (const char* env = getenv("DW_FAT"))
+        if (env[0] == '0') return cudaSuccess;
+    if (g.ne == 0 || g.ne > kBeginMask) return cudaSuccess;
+    // the fat layout is an accelerator: skip it when it would crowd HBM
+    size_t free_b = 0, total_b = 0;
+    DW_TRY(cudaMemGetInfo(&free_b, &total_b));
+    const ull need = g.ne * sizeof(FatRec);
+    if (need + (4ull << 30) > free_b) return cudaSuccess;
+    DW_TRY(cudaMallocAsync(&g.fat, need, s));
+    fat_build_kernel<<<grid_for((ull)g.nv * 32, 256), 256, 0, s>>>(g.nodes, g.nv, g.edges,
+                                                                   g.labels, g.fat);
+    DW_TRY(cudaGetLastError());
+    return cudaStreamSynchronize(s);
 }
 
 static cudaError_t build_member_index(DeviceGraphBuffers& g, cudaStream_t s) {
@@ -180,7 +248,8 @@ cudaError_t pack_graph(const ull* d_row, const uint32_t* d_col, const float* d_p
     DW_TRY(cudaStreamSynchronize(s));
     g.max_degree = h;
     DW_TRY(cudaFreeAsync(d_maxd, s));
-    return build_member_index(g, s);
+    DW_TRY(build_member_index(g, s));
+    return build_fat(g, s);
 }
 
 __global__ void unpack_kernel(const NodeRec* __restrict__ nodes, const EdgeRec* __restrict__ edges,
@@ -379,42 +448,47 @@ cudaError_t build_rmat(const RmatSpec& spec, DeviceGraphBuffers& g, cudaStream_t
 }
 
 // ---- K4: calibration (cost_model.cpp:37-126) -------------------------------
+struct ProbeState {
+    Step S;
+    ull begin;      // row of cur
+    uint32_t phoff; // hash set of prev
+};
+
 template <class M>
-__device__ __forceinline__ double eval_weight(const M& m, const Step& S, const DevGraph& g, ull e) {
+__device__ __forceinline__ double eval_weight(const M& m, const ProbeState& P, const DevGraph& g,
+                                              ull e) {
     const EdgeRec er = load_edge(g.edges + e);
     const uint16_t lab = (M::kUsesLabels && g.labels) ? g.labels[e] : (uint16_t)0;
-    const WeightCase wc = m.weight(S, er.col, er.h, lab);
+    const WeightCase wc = m.weight(P.S, er.col, er.h, lab);
     if (!M::kSecondOrder || !wc.needs_member) return wc.w;
-    return member(g, S.prev_begin, S.prev_degree, S.prev_hoff, er.col) ? wc.w_in : wc.w_out;
+    return member(g, P.S.prev_degree, P.phoff, er.col) ? wc.w_in : wc.w_out;
 }
 
 // probe_state (cost_model.cpp:20-33): step 1 with the first neighbour as prev
-__device__ __forceinline__ Step probe_state(const DevGraph& g, uint32_t v) {
-    Step S;
+__device__ __forceinline__ ProbeState probe_state(const DevGraph& g, uint32_t v) {
+    ProbeState P;
+    Step& S = P.S;
     const NodeRec nr = load_node(g.nodes + v);
     S.cur = v;
     S.degree = nr.degree;
-    S.begin = nr.begin;
-    S.hoff = nr.hoff;
     S.hmax = nr.hmax;
     S.hsum = nr.hsum;
     S.prev = kInvalid;
     S.prev_degree = 0;
-    S.prev_begin = 0;
-    S.prev_hoff = 0;
     S.step = 0;
+    P.begin = nr.begin;
+    P.phoff = 0;
     if (nr.degree) {
         const uint32_t pv = load_col(g.edges + nr.begin);
         const NodeRec pr = load_node(g.nodes + pv);
         if (pr.degree) {
             S.prev = pv;
             S.prev_degree = pr.degree;
-            S.prev_begin = pr.begin;
-            S.prev_hoff = pr.hoff;
+            P.phoff = pr.hoff;
             S.step = 1;
         }
     }
-    return S;
+    return P;
 }
 
 __global__ void sample_nodes_kernel(DevGraph g, ull seed, ull tries, uint32_t want,
@@ -435,11 +509,13 @@ template <class M, bool RANDOM>
 __global__ void probe_pass_kernel(DevGraph g, __grid_constant__ const ModelParams mp,
                                   const uint32_t* __restrict__ nodes, uint32_t n, int rounds,
                                   ull seed, double* sink) {
-    const M m(mp);
+    M m(mp);
     const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t lane = threadIdx.x & 31;
     if (w >= n) return;
-    const Step S = probe_state(g, nodes[w]);
+    const ProbeState P = probe_state(g, nodes[w]);
+    const Step& S = P.S;
+    m.prepare(S);
     const uint32_t k = S.degree < 32 ? S.degree : 32;
     double acc = 0.0;
     if (lane < k) {
@@ -448,11 +524,11 @@ __global__ void probe_pass_kernel(DevGraph g, __grid_constant__ const ModelParam
             if (RANDOM) {
                 const U4 b = philox4x32_10(U4{lane, (uint32_t)r, w, 0x72616e64u}, (uint32_t)seed,
                                            (uint32_t)(seed >> 32));
-                e = S.begin + bounded(lo64(b), S.degree);
+                e = P.begin + bounded(lo64(b), S.degree);
             } else {
-                e = S.begin + lane;
+                e = P.begin + lane;
             }
-            acc += eval_weight(m, S, g, e);
+            acc += eval_weight(m, P, g, e);
         }
     }
     if (acc == -1.0) *sink = acc;  // keeps the loads alive
@@ -461,7 +537,7 @@ __global__ void probe_pass_kernel(DevGraph g, __grid_constant__ const ModelParam
 template <class M>
 static cudaError_t calibrate_t(const DeviceGraphBuffers& gb, const ModelParams& mp, ull seed,
                                cudaStream_t s, double* ratio) {
-    DevGraph g{gb.nodes, gb.edges, gb.labels, gb.hslots, gb.nv, gb.ne};
+    DevGraph g{gb.nodes, gb.edges, gb.labels, gb.hslots, gb.fat, gb.nv, gb.ne};
     // ProfileConfig defaults: 1% of nodes, >= 64, <= 32 neighbours, 5 reps
     uint32_t want = (uint32_t)std::max<ull>((ull)std::ceil(0.01 * gb.nv), 64);
     const ull tries = (ull)want * 8;

@@ -9,6 +9,7 @@ struct DeviceGraphBuffers {
     EdgeRec* edges = nullptr;
     uint16_t* labels = nullptr;
     uint32_t* hslots = nullptr;  // membership hash sets (dw_member.cuh)
+    FatRec* fat = nullptr;       // fat edge records (optional accelerator)
     unsigned long long nbuckets = 0;
     uint32_t nv = 0;
     unsigned long long ne = 0;

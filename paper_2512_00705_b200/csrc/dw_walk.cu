@@ -5,29 +5,38 @@
 // lanes claim walkers from a global queue with one warp-aggregated atomic
 // (the run_queries scheduler, runtime.cpp:209-211).
 //
-// Latency structure.  A walk step is a chain of dependent random loads (node
-// record -> rejection trials -> membership probe -> ...), and lanes of a warp
-// need different numbers of them.  So the walker loop is a per-lane state
-// machine in which every lane advances exactly ONE memory phase per
+// Cost model.  Every random gather on B200 moves a whole 128 B L2 line from
+// HBM, whatever its size (tools/gather_probe.cu: ~3.7e10 random lines/s at
+// ~4.7 TB/s of DRAM traffic).  The kernel is therefore designed around the
+// NUMBER of random requests per walker-step, not their bytes:
+//   * fat edge records (dw_common.cuh FatRec): an accepted trial's record
+//     carries its target's row begin, degree, hash-set base, aggregates and
+//     the return-edge range, so a step needs no node-record gather;
+//   * free rejections: a trial whose y is >= the model's non-return maximum
+//     and whose index lies outside the return-edge range is rejected without
+//     gathering its edge -- about half of node2vec (0.5, 2) trials;
+//   * no speculative waste beyond a ring of kRing outstanding trials.
+//
+// Latency structure.  A walk step is a chain of dependent random loads and
+// lanes of a warp need different numbers of them, so the walker loop is a
+// per-lane state machine in which every lane advances one memory phase per
 // iteration:
-//     A  each lane issues the 16 B gathers its phase needs as cp.async
-//        (LDGSTS) into its own shared-memory landing slots -- no registers
-//        are tied up by loads in flight, so many gathers overlap per lane
+//     A  each lane issues the gathers its phase needs as cp.async (LDGSTS)
+//        into its own shared-memory landing slots
 //     B  cp.async.wait_all
 //     C  each lane consumes its slots and picks its next phase
-// so a warp iteration costs one memory latency no matter how the lanes are
-// spread over phases, and no lane waits for another lane's chain.
 // Phases:
-//   NODE   one 32 B node record: degree, row begin, hash-set base, max/sum
-//          aggregates; cost-model decision (decide_sampler,
+//   NODE   one 32 B node record (the walker's first step, or every step on
+//          the slim layout); cost-model decision (decide_sampler,
 //          cost_model.hpp:46-56).
-//   TRIAL  eRJS (samplers.hpp:145-178): kSlots trials issued at once --
-//          Philox is a counter RNG, so trial t's (x, y) is known without
-//          running the trials before it -- then judged in order.  A trial
-//          whose outcome hinges on the node2vec/PR2 membership test (y between
-//          the two candidate weights) parks in MEMB.
-//   MEMB   one 32 B hash-bucket probe (Graph::has_edge, dw_member.cuh), or a
-//          scan of a <= 6-record row.
+//   TRIAL  eRJS (samplers.hpp:145-178).  Philox is a counter RNG, so trial t's
+//          (x, y) is known without running the trials before it: the lane
+//          generates trials, rejects the free ones on the spot and queues
+//          the others (edge record gathers) in a ring; queued trials are
+//          judged in trial order.  A trial whose outcome hinges on the
+//          node2vec/PR2 membership test (y between the two candidate weights)
+//          parks at the ring head while one hash bucket is probed.
+//   FETCH  the fat record of the edge an eRVS step chose.
 //   VREC / VMEMB   eRVS on short rows (samplers.hpp:65-137), one neighbour per
 //          iteration, exactly the reference's sequential jump logic.
 //   COOP   rows >= kCoopMinDegree are handed to the whole warp through a
@@ -43,21 +52,25 @@
 namespace dwb {
 
 #ifndef DW_MIN_BLOCKS
-#define DW_MIN_BLOCKS 3
+#define DW_MIN_BLOCKS 4
 #endif
-#ifndef DW_SLOTS
-#define DW_SLOTS 4
+#ifndef DW_RING
+#define DW_RING 2
+#endif
+#ifndef DW_GEN
+#define DW_GEN 4
 #endif
 constexpr int kThreads = 256;
-constexpr int kSlots = DW_SLOTS;          // 16 B gathers per lane per iteration
+constexpr uint32_t kRing = DW_RING;  // queued trials per lane (power of two)
+constexpr uint32_t kGen = DW_GEN;    // Philox blocks per lane per iteration
+static_assert((kRing & (kRing - 1)) == 0, "kRing must be a power of two");
 constexpr uint32_t kCoopMinDegree = 64;
 constexpr unsigned kFull = 0xFFFFFFFFu;
 typedef unsigned long long ull;
 
-enum Phase : uint32_t { P_IDLE = 0, P_NODE, P_TRIAL, P_MEMB, P_VREC, P_VMEMB, P_COOP };
-// per-lane counters kept in shared memory (runtime.cpp:141-145)
-enum LaneCounter : int { LC_QUERIES = 0, LC_QERR, LC_DEAD, LC_TRIALS, LC_READS, LC_DRAWS, LC_FB,
-                         LC_ALG, LC_NUM };
+enum Phase : uint32_t { P_IDLE = 0, P_NODE, P_TRIAL, P_FETCH, P_VREC, P_VMEMB, P_COOP };
+// per-lane counters kept in shared memory, updated once per step
+enum LaneCounter : int { LC_TRIALS = 0, LC_READS, LC_DRAWS, LC_ALG, LC_NUM };
 
 __device__ __forceinline__ bool valid_w(double w) { return !(w < 0.0) && isfinite(w); }
 
@@ -87,27 +100,29 @@ __device__ __forceinline__ void cp_wait_all() {
 __device__ __forceinline__ const EdgeRec* pair_of(const EdgeRec* edges, ull e) {
     return edges + (e & ~1ull);  // 16 B aligned pair holding record e
 }
-__device__ __forceinline__ bool has8(const uint4& a, const uint4& b, uint32_t u) {
-    return a.x == u || a.y == u || a.z == u || a.w == u || b.x == u || b.y == u || b.z == u ||
-           b.w == u;
-}
+
+__device__ __forceinline__ void cnt_add(ull* c, ull v) { atomicAdd(c, v); }
 
 // ---- K2 (warp form): one row, 32 lanes; all lanes call with equal args ----
+// Returns the chosen target and its relative edge index (for the fat record).
 template <class M, bool NOJUMP>
-__device__ __noinline__ int ervs_warp(const M& m, const Step& S, const WalkerKey& key,
-                                      const DevGraph& g, ull idx0, uint32_t& next, ull& draws) {
+__device__ __noinline__ int ervs_warp(const ModelParams& mp, Step S, const WalkerKey key,
+                                      const DevGraph& g, ull begin, uint32_t phoff, ull idx0,
+                                      uint32_t* next, uint32_t* nidx, ull* draws) {
+    M m(mp);
+    m.prepare(S);
     const int lane = threadIdx.x & 31;
     ull idx = idx0;
     double best_log_key = -DBL_MAX;
-    uint32_t best = kInvalid;
+    uint32_t best = kInvalid, bi = 0;
     double skip = 0.0;
     bool have = false;
     // software pipeline: chunk c+1's records load while chunk c is judged
     EdgeRec nxt{kInvalid, 0.f};
     uint16_t nlab = 0;
     if ((uint32_t)lane < S.degree) {
-        nxt = load_edge(g.edges + S.begin + lane);
-        nlab = edge_label<M>(g, S.begin + lane);
+        nxt = load_edge(g.edges + begin + lane);
+        nlab = edge_label<M>(g, begin + lane);
     }
     for (uint32_t base = 0; base < S.degree; base += 32) {
         const uint32_t i = base + lane;
@@ -115,16 +130,15 @@ __device__ __noinline__ int ervs_warp(const M& m, const Step& S, const WalkerKey
         const EdgeRec er = nxt;
         const uint16_t lab = nlab;
         if (i + 32 < S.degree) {
-            nxt = load_edge(g.edges + S.begin + i + 32);
-            nlab = edge_label<M>(g, S.begin + i + 32);
+            nxt = load_edge(g.edges + begin + i + 32);
+            nlab = edge_label<M>(g, begin + i + 32);
         }
         double w = 0.0;
         if (in) {
             const WeightCase wc = m.weight(S, er.col, er.h, lab);
             w = (!M::kSecondOrder || !wc.needs_member)
                     ? wc.w
-                    : (member(g, S.prev_begin, S.prev_degree, S.prev_hoff, er.col) ? wc.w_in
-                                                                                  : wc.w_out);
+                    : (member(g, S.prev_degree, phoff, er.col) ? wc.w_in : wc.w_out);
         }
         if (__any_sync(kFull, in && !valid_w(w))) return -kDevBadWeight;
         if (NOJUMP) {
@@ -155,6 +169,7 @@ __device__ __noinline__ int ervs_warp(const M& m, const Step& S, const WalkerKey
             if (has && (best == kInvalid || lk > best_log_key)) {
                 best_log_key = lk;
                 best = cand;
+                bi = base + src;
             }
         } else {
             const uint32_t n = S.degree - base < 32u ? S.degree - base : 32u;
@@ -165,6 +180,7 @@ __device__ __noinline__ int ervs_warp(const M& m, const Step& S, const WalkerKey
                 if (best == kInvalid) {
                     best_log_key = log(open01(walker_draw(key, idx++))) / wj;
                     best = uj;
+                    bi = base + j;
                     continue;
                 }
                 if (!have) {
@@ -179,14 +195,16 @@ __device__ __noinline__ int ervs_warp(const M& m, const Step& S, const WalkerKey
                     if (lk > best_log_key) {
                         best_log_key = lk;
                         best = uj;
+                        bi = base + j;
                     }
                     have = false;
                 }
             }
         }
     }
-    next = best;
-    draws = NOJUMP ? (ull)S.degree : idx - idx0;
+    *next = best;
+    *nidx = bi;
+    *draws = NOJUMP ? (ull)S.degree : idx - idx0;
     return 0;
 }
 
@@ -195,24 +213,23 @@ __device__ __noinline__ int ervs_warp(const M& m, const Step& S, const WalkerKey
 // the log/exp code, which the hot eRJS loop never needs.
 struct ErvsState {
     double best_key, skip;
-    ull didx;       // next draw index of this step's stream
+    ull didx;        // next draw index of this step's stream
     uint32_t best;
-    uint32_t have;  // threshold drawn
-    uint32_t draws; // draws made by this call
+    uint32_t bidx;   // relative edge index of best (bits 0-30) | threshold drawn (bit 31)
 };
+constexpr uint32_t kHave = 0x80000000u;
 
 template <bool NOJUMP>
 __device__ __noinline__ ErvsState ervs_visit(ErvsState s, const WalkerKey key, uint32_t vi,
                                              uint32_t u, double w) {
-    s.draws = 0;
     if (NOJUMP) {
         const double r = open01(walker_draw(key, s.didx + vi));
-        s.draws = 1;
         if (w != 0.0) {
             const double lk = log(r) / w;
             if (s.best == kInvalid || lk > s.best_key) {
                 s.best_key = lk;
                 s.best = u;
+                s.bidx = vi;
             }
         }
         return s;
@@ -220,26 +237,25 @@ __device__ __noinline__ ErvsState ervs_visit(ErvsState s, const WalkerKey key, u
     if (w == 0.0) return s;
     if (s.best == kInvalid) {
         s.best_key = log(open01(walker_draw(key, s.didx++))) / w;
-        s.draws = 1;
         s.best = u;
+        s.bidx = vi;
         return s;
     }
-    if (!s.have) {
+    if (!(s.bidx & kHave)) {
         s.skip = log(open01(walker_draw(key, s.didx++))) / s.best_key;
-        s.draws = 1;
-        s.have = 1;
+        s.bidx |= kHave;
     }
     s.skip -= w;
     if (s.skip <= 0.0) {
         const double floor_u = exp(w * s.best_key);
         const double uu = floor_u + open01(walker_draw(key, s.didx++)) * (1.0 - floor_u);
-        ++s.draws;
         const double lk = log(uu) / w;
+        s.bidx &= ~kHave;
         if (lk > s.best_key) {
             s.best_key = lk;
             s.best = u;
+            s.bidx = vi;
         }
-        s.have = 0;
     }
     return s;
 }
@@ -251,101 +267,199 @@ __device__ __forceinline__ ull warp_sum(ull v) {
 }
 
 // ---- K3: adaptive walker loop (runtime.cpp:59-153 + 192-247) --------------
-template <class M, int MODE>
+template <class M, int MODE, bool FAT>
 __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
     walk_kernel(const __grid_constant__ WalkParams p) {
     constexpr bool kNoJump = MODE == kErvsNoJump;
-    __shared__ uint4 s_slot[kSlots][kThreads];   // cp.async landing zone, [slot][lane]
-    __shared__ double s_y[kSlots][kThreads];     // y of the trials in flight
-    __shared__ uint32_t s_lab[kSlots][kThreads]; // label words (MetaPath)
-    __shared__ ull s_lc[LC_NUM][kThreads];       // per-lane RunStats counters
+    constexpr bool kSO = M::kSecondOrder;
+    __shared__ uint4 s_rec[kRing][3][kThreads];  // landing: fat record / slim pair in [0]
+    __shared__ double s_y[kRing][kThreads];      // y of the queued trials
+    __shared__ uint32_t s_t[kRing][kThreads];    // trial index of the queued trials
+    __shared__ uint4 s_mb[2][kThreads];          // node record / hash bucket / eRVS pair
+    __shared__ uint32_t s_lab[kRing + 1][kThreads];  // label words (slim MetaPath)
+    __shared__ uint32_t s_lc[LC_NUM][kThreads];  // per-lane RunStats counters (spill at 2^31)
     __shared__ ull s_cnt[kCNum];
     const int tid = threadIdx.x;
     for (int i = tid; i < kCNum; i += blockDim.x) s_cnt[i] = 0;
 #pragma unroll
     for (int c = 0; c < LC_NUM; ++c) s_lc[c][tid] = 0;
     __syncthreads();
-#define LC(c) s_lc[c][tid]
+    constexpr int lc_slot[LC_NUM] = {kCTrials, kCWeightReads, kCRngDraws, kCAlgBytes};
+    auto lc_add = [&](int c, ull v) {
+        const ull t = (ull)s_lc[c][tid] + v;
+        if (t >= 0x80000000ull) {
+            atomicAdd(&s_cnt[lc_slot[c]], t);
+            s_lc[c][tid] = 0;
+        } else {
+            s_lc[c][tid] = (uint32_t)t;
+        }
+    };
 
-    const M model(p.mp);
+    M model(p.mp);
     const int lane = tid & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     const DevGraph& g = p.g;
+    const bool shortcut = p.mp.shortcut != 0;
 
     uint32_t phase = P_IDLE;
     bool drained = false;  // warp-uniform
     ull qi = 0;
-    Step S;
-    S.cur = S.prev = kInvalid;
-    S.prev_degree = S.prev_hoff = S.step = S.degree = S.hoff = 0;
-    S.prev_begin = S.begin = 0;
-    S.hmax = S.hsum = 0.0;
-    // TRIAL/MEMB: t trials judged, bound, parked y.  VREC/VMEMB: eRVS state.
-    ull t = 0;
-    double bound = 0.0, py = 0.0;
-    ErvsState ev{0.0, 0.0, 0, kInvalid, 0, 0};
-    uint32_t vi = 0;
-    // parked membership test (TRIAL->MEMB, VREC->VMEMB)
-    uint32_t pu = 0, mb = 0;
-    float ph = 0.f;
-    uint32_t kk = 0, sel = 0;
-
-    // outcome of one walk step (runtime.cpp:141-150 + walk_state.hpp:33-39)
-    auto finish_step = [&](uint32_t next) {
-        if (next == kInvalid) {
-            ++LC(LC_DEAD);
-            if (p.lengths) p.lengths[qi] = S.step + 1;
-            phase = P_IDLE;
-            return;
-        }
-        S.prev = S.cur;
-        S.prev_degree = S.degree;
-        S.prev_begin = S.begin;
-        S.prev_hoff = S.hoff;
-        S.cur = next;
-        ++S.step;
-        if (p.paths) p.paths[qi * p.stride + S.step] = next;
-        if (S.step >= p.target) {
-            if (p.lengths) p.lengths[qi] = S.step + 1;
-            phase = P_IDLE;
-        } else {
-            phase = P_NODE;
-        }
+    // walker state
+    uint32_t cur = kInvalid, prev = kInvalid, pdeg = 0, phoff = 0, step = 0, deg = 0, hoff = 0;
+    ull begin = 0;
+    // eRJS state
+    double bound = 0.0, mnr = 0.0;       // bound, non-return maximum
+    uint32_t tn = 0, rh = 0, rc = 0;     // next trial, ring head, ring count
+    uint32_t tw_lo = 0, tw_cnt = 0;      // return-edge range in N(cur)
+    uint32_t mb = 0, nret = 0, sel = 0;  // parked bucket (bit 31: parked), return trials, pair bits
+    // eRVS state lives in the lane's spare ring slot (the ring is idle while a
+    // lane runs eRVS), keeping the hot eRJS loop's register set small:
+    //   s_rec[kRing-1][0] = {parked neighbour u, its h}   (VMEMB)
+    //   s_rec[kRing-1][1..2] = ErvsState
+    // tn doubles as the eRVS neighbour cursor.
+    constexpr uint32_t kParked = 0x80000000u;
+    static_assert(sizeof(ErvsState) == 32, "ErvsState must fill two uint4");
+    auto ev_load = [&]() {
+        ErvsState e;
+        *reinterpret_cast<uint4*>(&e) = s_rec[kRing - 1][1][tid];
+        *(reinterpret_cast<uint4*>(&e) + 1) = s_rec[kRing - 1][2][tid];
+        return e;
     };
-    auto start_ervs = [&](ull draw_base) {
-        vi = 0;
-        ev.best = kInvalid;
-        ev.best_key = -DBL_MAX;
-        ev.skip = 0.0;
-        ev.have = 0;
-        ev.didx = draw_base;
-        // §8(d): σ(8d) + 32·min(d, ⌈d'/8⌉) when membership is needed
-        ull alg = ((8ull * S.degree + 31) / 32) * 32;
-        if (M::kSecondOrder && S.has_prev())
-            alg += 32ull * min((ull)S.degree, ((ull)S.prev_degree + 7) / 8);
-        LC(LC_ALG) += alg;
-        phase = S.degree >= kCoopMinDegree ? P_COOP : P_VREC;
+    auto ev_store = [&](const ErvsState& e) {
+        s_rec[kRing - 1][1][tid] = *reinterpret_cast<const uint4*>(&e);
+        s_rec[kRing - 1][2][tid] = *(reinterpret_cast<const uint4*>(&e) + 1);
+    };
+
+    auto mkstep = [&](double hmax, double hsum) {
+        Step S;
+        S.cur = cur;
+        S.prev = prev;
+        S.prev_degree = pdeg;
+        S.step = step;
+        S.degree = deg;
+        S.hmax = hmax;
+        S.hsum = hsum;
+        return S;
     };
     auto key_of = [&]() {
         const ull q = p.qid_base + qi;
-        return WalkerKey{p.seed_lo, p.seed_hi, (uint32_t)q, (uint32_t)(q >> 32), S.step};
+        return WalkerKey{p.seed_lo, p.seed_hi, (uint32_t)q, (uint32_t)(q >> 32), step};
     };
-    auto visit = [&](uint32_t u, double w) {
-        ev = ervs_visit<kNoJump>(ev, key_of(), vi, u, w);
-        LC(LC_DRAWS) += ev.draws;
-        ++LC(LC_READS);
-        if (++vi == S.degree) finish_step(ev.best);
-    };
-    auto park = [&](uint32_t u, float h, double y, uint32_t next_phase) {
-        pu = u;
-        ph = h;
-        py = y;
-        mb = S.prev_degree > kScanMax ? hash_bucket(u, hash_log2_buckets(S.prev_degree)) : 0;
-        phase = next_phase;
+    auto cap_of = [&]() -> uint32_t {
+        const ull c = p.cap_per_degree * (ull)deg;
+        return c > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)c;
     };
     auto fail = [&](int code) {
         raise_error(p, code, p.qid_base + qi);
         phase = P_IDLE;
+    };
+    auto end_walk = [&]() {
+        if (p.lengths) p.lengths[qi] = step + 1;
+        phase = P_IDLE;
+    };
+    auto start_ervs = [&](ull draw_base) {
+        tn = 0;
+        ev_store(ErvsState{-DBL_MAX, 0.0, draw_base, kInvalid, 0});
+        // §8(d): σ(8d) + 32·min(d, ⌈d'/8⌉) when membership is needed
+        ull alg = ((8ull * deg + 31) / 32) * 32;
+        if (kSO && prev != kInvalid) alg += 32ull * min((ull)deg, ((ull)pdeg + 7) / 8);
+        lc_add(LC_ALG, alg);
+        phase = deg >= kCoopMinDegree ? P_COOP : P_VREC;
+    };
+    // decide_sampler (cost_model.hpp:46-56) for the step at cur
+    auto begin_step = [&](double hmax, double hsum) {
+        if (deg == 0) {  // runtime.cpp:70-71: stop without counting a step
+            end_walk();
+            return;
+        }
+        Step S = mkstep(hmax, hsum);
+        model.prepare(S);
+        bool erjs = false;
+        if (MODE == kAdaptive) {
+            if (M::kBoundable) {
+                bound = model.bound(S);
+                erjs = p.ratio * bound < model.wsum(S);
+            }
+        } else if (MODE == kForceErjs) {  // runtime.cpp:109-129
+            erjs = M::kBoundable;
+            if (erjs) bound = model.bound(S);
+        }
+        atomicAdd(&s_cnt[kCHist + 2 * degree_bucket(deg) + (erjs ? 1 : 0)], 1ull);
+        // §8(d): 32 B offsets + 4 B path write (+ 32 B aggregates)
+        lc_add(LC_ALG, 36 + ((MODE == kAdaptive || MODE == kForceErjs) && M::kAggregates ? 32 : 0));
+        if (erjs) {
+            if (!(bound > 0.0) || !isfinite(bound)) {  // samplers.hpp:152-154
+                fail(kDevBadBound);
+                return;
+            }
+            mnr = shortcut ? model.nonreturn_max(S) : __longlong_as_double(0x7ff0000000000000ll);
+            tn = rh = rc = 0;
+            mb = nret = sel = 0;
+            phase = P_TRIAL;
+            if (p.cap_per_degree == 0) {  // immediate cap overrun
+                cnt_add(&s_cnt[kCFallbacks], 1);
+                start_ervs(0);
+            }
+        } else {
+            lc_add(LC_TRIALS, 1);  // single-shot kernels report one trial (samplers.hpp:22)
+            start_ervs(0);
+        }
+    };
+    // WalkerState::advance (walk_state.hpp:33-39); false when the walk ends
+    auto advance = [&](uint32_t next) {
+        prev = cur;
+        pdeg = deg;
+        phoff = hoff;
+        cur = next;
+        ++step;
+        if (p.paths) p.paths[qi * p.stride + step] = next;
+        if (step >= p.target) {
+            end_walk();
+            return false;
+        }
+        return true;
+    };
+    // take the fat record in slot k as the step's outcome
+    auto take_fat = [&](uint32_t k) {
+        const uint4 v0 = s_rec[k][0][tid], v1 = s_rec[k][1][tid], v2 = s_rec[k][2][tid];
+        if (!advance(v0.x)) return;
+        begin = ((ull)v0.z | ((ull)v0.w << 32)) & kBeginMask;
+        deg = v1.x;
+        hoff = v1.y;
+        tw_lo = v1.z;
+        tw_cnt = v1.w;
+        begin_step(__hiloint2double((int)v2.y, (int)v2.x), __hiloint2double((int)v2.w, (int)v2.z));
+    };
+    auto ervs_done = [&](uint32_t best, uint32_t bidx) {
+        if (best == kInvalid) {  // all weights zero: dead end (runtime.cpp:146-149)
+            cnt_add(&s_cnt[kCDeadEnds], 1);
+            end_walk();
+            return;
+        }
+        if (FAT) {
+            ErvsState e = ev_load();
+            e.didx = begin + (bidx & ~kHave);  // edge whose fat record starts the next step
+            ev_store(e);
+            phase = P_FETCH;
+        } else if (advance(best)) {
+            phase = P_NODE;
+        }
+    };
+    auto visit = [&](uint32_t u, double w) {
+        const ErvsState e0 = ev_load();
+        const ErvsState ev = ervs_visit<kNoJump>(e0, key_of(), tn, u, w);
+        ev_store(ev);
+        lc_add(LC_DRAWS, kNoJump ? 1ull : ev.didx - e0.didx);
+        lc_add(LC_READS, 1);
+        if (++tn == deg) ervs_done(ev.best, ev.bidx & ~kHave);
+    };
+    // eRJS bookkeeping for T judged trials, nret of them return edges
+    auto count_erjs = [&](uint32_t T) {
+        lc_add(LC_TRIALS, T);
+        lc_add(LC_READS, T);
+        lc_add(LC_DRAWS, 2ull * T);
+        const bool so = kSO && prev != kInvalid;
+        lc_add(LC_ALG, (so ? 64ull : 32ull) * T - (so ? 32ull * nret : 0ull));
     };
 
     for (;;) {
@@ -364,10 +478,10 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                 if (phase == P_IDLE) {
                     const ull i = base + (ull)__popc(need & lt_mask);
                     if (i < p.nq) {
-                        ++LC(LC_QUERIES);
+                        cnt_add(&s_cnt[kCQueries], 1);
                         const uint32_t start = p.queries[i];
                         if (start >= g.nv) {  // runtime.cpp:213-217
-                            ++LC(LC_QERR);
+                            cnt_add(&s_cnt[kCQueryErrors], 1);
                             if (p.lengths) p.lengths[i] = 0;
                         } else {
                             if (p.paths) p.paths[i * p.stride] = start;
@@ -376,11 +490,10 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                             } else {
                                 phase = P_NODE;
                                 qi = i;
-                                S.cur = start;
-                                S.prev = kInvalid;
-                                S.prev_degree = S.prev_hoff = 0;
-                                S.prev_begin = 0;
-                                S.step = 0;
+                                cur = start;
+                                prev = kInvalid;
+                                pdeg = phoff = 0;
+                                step = 0;
                             }
                         }
                     }
@@ -391,107 +504,106 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
         if (__ballot_sync(kFull, phase != P_IDLE) == 0) break;
 
         // ---- A: issue this iteration's gathers
-        if (phase == P_NODE) {
-            const char* nr = reinterpret_cast<const char*>(g.nodes + S.cur);
-            cp16(&s_slot[0][tid], nr);
-            cp16(&s_slot[1][tid], nr + 16);
-        } else if (phase == P_TRIAL) {
+        if (phase == P_TRIAL) {
+            if (mb & kParked) {
+                const uint32_t* b = g.hslots + 8ull * (phoff + (mb & ~kParked));
+                cp16(&s_mb[0][tid], b);
+                cp16(&s_mb[1][tid], b + 4);
+            }
             const WalkerKey key = key_of();
-            const ull cap = p.cap_per_degree * S.degree;
-            kk = (cap - t) < (ull)kSlots ? (uint32_t)(cap - t) : (uint32_t)kSlots;
-            sel = 0;
+            const uint32_t cap = cap_of();
 #pragma unroll 1
-            for (uint32_t k = 0; k < kk; ++k) {
-                const U4 b = walker_block(key, (uint32_t)(t + k));
-                const ull e = S.begin + bounded(lo64(b), S.degree);  // draw 2t:   bounded(d)
-                s_y[k][tid] = uniform01(hi64(b)) * bound;             // draw 2t+1: uniform01()*c
-                sel |= (uint32_t)(e & 1) << k;
-                cp16(&s_slot[k][tid], pair_of(g.edges, e));
-                if (M::kUsesLabels && g.labels) cp4(&s_lab[k][tid], g.labels + (e & ~1ull));
+            for (uint32_t gen = 0; gen < kGen && rc < kRing && tn < cap; ++gen, ++tn) {
+                const U4 b = walker_block(key, tn);
+                const uint32_t x = (uint32_t)bounded(lo64(b), deg);  // draw 2t:   bounded(d)
+                const double y = uniform01(hi64(b)) * bound;          // draw 2t+1: uniform01()*c
+                if (y >= mnr && x - tw_lo >= tw_cnt) continue;        // rejected, no gather
+                const uint32_t k = (rh + rc) & (kRing - 1);
+                s_y[k][tid] = y;
+                s_t[k][tid] = tn;
+                const ull e = begin + x;
+                if (FAT) {
+                    const uint4* r = reinterpret_cast<const uint4*>(g.fat + e);
+                    cp16(&s_rec[k][0][tid], r);
+                    cp16(&s_rec[k][1][tid], r + 1);
+                    cp16(&s_rec[k][2][tid], r + 2);
+                } else {
+                    sel = (sel & ~(1u << k)) | ((uint32_t)(e & 1) << k);
+                    cp16(&s_rec[k][0][tid], pair_of(g.edges, e));
+                    if (M::kUsesLabels && g.labels) cp4(&s_lab[k][tid], g.labels + (e & ~1ull));
+                }
+                ++rc;
             }
-        } else if (phase == P_MEMB || phase == P_VMEMB) {
-            if (S.prev_degree <= kScanMax) {
-                const ull e0 = S.prev_begin & ~1ull;
-                const ull n = S.prev_begin + S.prev_degree - e0;
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if ((ull)(2 * k) < n) cp16(&s_slot[k][tid], g.edges + e0 + 2 * k);
-            } else {
-                const uint32_t* b = g.hslots + 8ull * (S.prev_hoff + mb);
-                cp16(&s_slot[0][tid], b);
-                cp16(&s_slot[1][tid], b + 4);
-            }
+        } else if (phase == P_NODE) {
+            const char* nr = reinterpret_cast<const char*>(g.nodes + cur);
+            cp16(&s_mb[0][tid], nr);
+            cp16(&s_mb[1][tid], nr + 16);
+        } else if (phase == P_FETCH) {
+            const ull fe = ev_load().didx;
+            const uint4* r = reinterpret_cast<const uint4*>(g.fat + fe);
+            cp16(&s_rec[0][0][tid], r);
+            cp16(&s_rec[0][1][tid], r + 1);
+            cp16(&s_rec[0][2][tid], r + 2);
+        } else if (phase == P_VMEMB) {
+            const uint32_t* b = g.hslots + 8ull * (phoff + mb);
+            cp16(&s_mb[0][tid], b);
+            cp16(&s_mb[1][tid], b + 4);
         } else if (phase == P_VREC) {
-            const ull e = S.begin + vi;
+            const ull e = begin + tn;
             sel = (uint32_t)(e & 1);
-            cp16(&s_slot[0][tid], pair_of(g.edges, e));
-            if (M::kUsesLabels && g.labels) cp4(&s_lab[0][tid], g.labels + (e & ~1ull));
+            cp16(&s_mb[0][tid], pair_of(g.edges, e));
+            if (M::kUsesLabels && g.labels) cp4(&s_lab[kRing][tid], g.labels + (e & ~1ull));
         }
         // ---- B
         cp_wait_all();
 
         // ---- C: consume
-        if (phase == P_NODE) {
-            const uint4 v0 = s_slot[0][tid], v1 = s_slot[1][tid];
-            S.begin = (ull)v0.x | ((ull)v0.y << 32);
-            S.degree = v0.z;
-            S.hoff = v0.w;
-            S.hmax = __hiloint2double((int)v1.y, (int)v1.x);
-            S.hsum = __hiloint2double((int)v1.w, (int)v1.z);
-            if (S.degree == 0) {  // runtime.cpp:70-71
-                if (p.lengths) p.lengths[qi] = S.step + 1;
-                phase = P_IDLE;
-            } else {
-                bool erjs = false;
-                if (MODE == kAdaptive) {  // decide_sampler, cost_model.hpp:46-56
-                    if (M::kBoundable) {
-                        bound = model.bound(S);
-                        erjs = p.ratio * bound < model.wsum(S);
-                    }
-                } else if (MODE == kForceErjs) {  // runtime.cpp:109-129
-                    erjs = M::kBoundable;
-                    if (erjs) bound = model.bound(S);
-                }
-                atomicAdd(&s_cnt[kCHist + 2 * degree_bucket(S.degree) + (erjs ? 1 : 0)], 1ull);
-                // §8(d): 32 B offsets + 4 B path write (+ 32 B aggregates)
-                LC(LC_ALG) +=
-                    36 + ((MODE == kAdaptive || MODE == kForceErjs) && M::kAggregates ? 32 : 0);
-                if (erjs) {
-                    if (!(bound > 0.0) || !isfinite(bound)) {  // samplers.hpp:152-154
-                        fail(kDevBadBound);
-                    } else {
-                        t = 0;
-                        phase = P_TRIAL;
-                        if (p.cap_per_degree == 0) {  // immediate cap overrun
-                            ++LC(LC_FB);
-                            start_ervs(0);
-                        }
-                    }
+        if (phase == P_TRIAL) {
+            int acc = -1;
+            const Step S = mkstep(0.0, 0.0);
+            if (mb & kParked) {  // resolve the head's membership probe
+                const uint4 v0 = s_rec[rh][0][tid];
+                const uint32_t u = FAT ? v0.x : (((sel >> rh) & 1) ? v0.z : v0.x);
+                const int r = bucket_lookup(s_mb[0][tid], s_mb[1][tid], u);
+                if (r < 0) {
+                    mb = kParked | ((mb + 1) & ((1u << hash_log2_buckets(pdeg)) - 1u));
                 } else {
-                    ++LC(LC_TRIALS);  // single-shot kernels report one trial (samplers.hpp:22)
-                    start_ervs(0);
+                    const float h = __uint_as_float(FAT ? v0.y : (((sel >> rh) & 1) ? v0.w : v0.y));
+                    const WeightCase wc = model.weight(S, u, h, 0);
+                    const double w = r ? wc.w_in : wc.w_out;
+                    mb = 0;
+                    if (!valid_w(w)) {
+                        fail(kDevBadWeight);
+                    } else if (s_y[rh][tid] < w) {
+                        acc = (int)rh;
+                    } else {
+                        rh = (rh + 1) & (kRing - 1);
+                        --rc;
+                    }
                 }
             }
-        } else if (phase == P_TRIAL) {
-            uint32_t k = 0;
-            for (; k < kk; ++k) {
-                const uint4 v = s_slot[k][tid];
-                const bool odd = (sel >> k) & 1;
-                const uint32_t u = odd ? v.z : v.x;
-                const float h = __uint_as_float(odd ? v.w : v.y);
-                const uint16_t lab =
-                    M::kUsesLabels ? (uint16_t)(odd ? (s_lab[k][tid] >> 16) : s_lab[k][tid]) : 0;
-                const double y = s_y[k][tid];
+            while (phase == P_TRIAL && acc < 0 && !(mb & kParked) && rc) {
+                const uint4 v0 = s_rec[rh][0][tid];
+                const bool odd = !FAT && ((sel >> rh) & 1);
+                const uint32_t u = odd ? v0.z : v0.x;
+                const float h = __uint_as_float(odd ? v0.w : v0.y);
+                uint16_t lab = 0;
+                if (M::kUsesLabels) {
+                    if (FAT)
+                        lab = (uint16_t)(v0.w >> 16);
+                    else
+                        lab = (uint16_t)(odd ? (s_lab[rh][tid] >> 16) : s_lab[rh][tid]);
+                }
+                const double y = s_y[rh][tid];
                 const WeightCase wc = model.weight(S, u, h, lab);
-                // 32 B edge record + 32 B membership sector when u != prev (§8(d))
-                LC(LC_ALG) += (M::kSecondOrder && S.has_prev() && u != S.prev) ? 64 : 32;
+                if (kSO && u == prev) ++nret;
                 if (!wc.needs_member) {
                     if (!valid_w(wc.w)) {
                         fail(kDevBadWeight);
                         break;
                     }
                     if (y < wc.w) {
-                        finish_step(u);
+                        acc = (int)rh;
                         break;
                     }
                 } else {
@@ -499,74 +611,71 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                     const double hi = wc.w_in < wc.w_out ? wc.w_out : wc.w_in;
                     const bool ok = valid_w(wc.w_in) && valid_w(wc.w_out);
                     if (ok && y < lo) {
-                        finish_step(u);
+                        acc = (int)rh;
                         break;
                     }
                     if (!ok || y < hi) {  // outcome hinges on u in N(prev)
-                        park(u, h, y, P_MEMB);
+                        mb = kParked | hash_bucket(u, hash_log2_buckets(pdeg));
                         break;
                     }
                 }
+                rh = (rh + 1) & (kRing - 1);
+                --rc;
             }
-            const uint32_t judged = k < kk ? k + 1 : kk;
-            t += judged;
-            LC(LC_TRIALS) += judged;
-            LC(LC_READS) += judged;
-            LC(LC_DRAWS) += 2 * judged;
-            if (phase == P_TRIAL && t >= p.cap_per_degree * S.degree) {
-                ++LC(LC_FB);  // cap overrun -> reservoir with the same stream
-                start_ervs(2 * t);
-            }
-        } else if (phase == P_MEMB || phase == P_VMEMB) {
-            int hit = -1;  // -1: probe the next bucket
-            if (S.prev_degree <= kScanMax) {
-                const uint32_t off = (uint32_t)(S.prev_begin & 1ull);
-                bool f = false;
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const uint4 v = s_slot[k][tid];
-                    const uint32_t j0 = 2 * k, j1 = 2 * k + 1;
-                    f |= (j0 >= off && j0 < off + S.prev_degree && v.x == pu);
-                    f |= (j1 >= off && j1 < off + S.prev_degree && v.z == pu);
+            if (phase == P_TRIAL) {
+                if (acc >= 0) {
+                    count_erjs(s_t[acc][tid] + 1);
+                    if (FAT) {
+                        take_fat((uint32_t)acc);
+                    } else {
+                        const uint4 v0 = s_rec[acc][0][tid];
+                        const uint32_t u = ((sel >> acc) & 1) ? v0.z : v0.x;
+                        if (advance(u)) phase = P_NODE;
+                    }
+                } else if (!(mb & kParked) && rc == 0 && tn >= cap_of()) {
+                    count_erjs(tn);
+                    cnt_add(&s_cnt[kCFallbacks], 1);  // cap overrun -> reservoir, same stream
+                    start_ervs(2ull * tn);
                 }
-                hit = f ? 1 : 0;
-            } else {
-                const uint4 v0 = s_slot[0][tid], v1 = s_slot[1][tid];
-                if (has8(v0, v1, pu))
-                    hit = 1;
-                else if (v1.w == kHashEmpty)
-                    hit = 0;
-                else
-                    mb = (mb + 1) & ((1u << hash_log2_buckets(S.prev_degree)) - 1u);
             }
-            if (hit >= 0) {
-                const WeightCase wc = model.weight(S, pu, ph, 0);
-                const double w = hit ? wc.w_in : wc.w_out;
+        } else if (phase == P_NODE) {
+            const uint4 v0 = s_mb[0][tid], v1 = s_mb[1][tid];
+            begin = (ull)v0.x | ((ull)v0.y << 32);
+            deg = v0.z;
+            hoff = v0.w;
+            // first step: no return edge; later (slim layout) the range is unknown
+            tw_lo = 0;
+            tw_cnt = prev == kInvalid ? 0u : 0xFFFFFFFFu;
+            begin_step(__hiloint2double((int)v1.y, (int)v1.x), __hiloint2double((int)v1.w, (int)v1.z));
+        } else if (phase == P_FETCH) {
+            take_fat(0);
+        } else if (phase == P_VMEMB) {
+            const uint4 pk = s_rec[kRing - 1][0][tid];
+            const uint32_t pu = pk.x;
+            const int r = bucket_lookup(s_mb[0][tid], s_mb[1][tid], pu);
+            if (r < 0) {
+                mb = (mb + 1) & ((1u << hash_log2_buckets(pdeg)) - 1u);
+            } else {
+                const WeightCase wc = model.weight(mkstep(0.0, 0.0), pu, __uint_as_float(pk.y), 0);
+                const double w = r ? wc.w_in : wc.w_out;
                 if (!valid_w(w)) {
                     fail(kDevBadWeight);
-                } else if (phase == P_MEMB) {
-                    if (py < w) {
-                        finish_step(pu);
-                    } else if (t >= p.cap_per_degree * S.degree) {
-                        ++LC(LC_FB);
-                        start_ervs(2 * t);
-                    } else {
-                        phase = P_TRIAL;
-                    }
                 } else {
                     phase = P_VREC;
                     visit(pu, w);
                 }
             }
         } else if (phase == P_VREC) {
-            const uint4 v = s_slot[0][tid];
+            const uint4 v = s_mb[0][tid];
             const uint32_t u = sel ? v.z : v.x;
             const float h = __uint_as_float(sel ? v.w : v.y);
             const uint16_t lab =
-                M::kUsesLabels ? (uint16_t)(sel ? (s_lab[0][tid] >> 16) : s_lab[0][tid]) : 0;
-            const WeightCase wc = model.weight(S, u, h, lab);
-            if (M::kSecondOrder && wc.needs_member) {
-                park(u, h, 0.0, P_VMEMB);
+                M::kUsesLabels ? (uint16_t)(sel ? (s_lab[kRing][tid] >> 16) : s_lab[kRing][tid]) : 0;
+            const WeightCase wc = model.weight(mkstep(0.0, 0.0), u, h, lab);
+            if (kSO && wc.needs_member) {
+                s_rec[kRing - 1][0][tid] = make_uint4(u, __float_as_uint(h), 0u, 0u);
+                mb = hash_bucket(u, hash_log2_buckets(pdeg));
+                phase = P_VMEMB;
             } else if (!valid_w(wc.w)) {
                 fail(kDevBadWeight);
             } else {
@@ -580,68 +689,69 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
             const int L = __ffs(coop) - 1;
             coop &= coop - 1;
             Step T;
-            T.cur = __shfl_sync(kFull, S.cur, L);
-            T.prev = __shfl_sync(kFull, S.prev, L);
-            T.prev_degree = __shfl_sync(kFull, S.prev_degree, L);
-            T.prev_begin = __shfl_sync(kFull, S.prev_begin, L);
-            T.prev_hoff = __shfl_sync(kFull, S.prev_hoff, L);
-            T.step = __shfl_sync(kFull, S.step, L);
-            T.degree = __shfl_sync(kFull, S.degree, L);
-            T.hoff = __shfl_sync(kFull, S.hoff, L);
-            T.begin = __shfl_sync(kFull, S.begin, L);
-            T.hmax = __shfl_sync(kFull, S.hmax, L);
-            T.hsum = __shfl_sync(kFull, S.hsum, L);
+            T.cur = __shfl_sync(kFull, cur, L);
+            T.prev = __shfl_sync(kFull, prev, L);
+            T.prev_degree = __shfl_sync(kFull, pdeg, L);
+            T.step = __shfl_sync(kFull, step, L);
+            T.degree = __shfl_sync(kFull, deg, L);
+            T.hmax = T.hsum = 0.0;
+            const uint32_t tph = __shfl_sync(kFull, phoff, L);
+            const ull tb = __shfl_sync(kFull, begin, L);
             const ull q = p.qid_base + __shfl_sync(kFull, qi, L);
             const WalkerKey K{p.seed_lo, p.seed_hi, (uint32_t)q, (uint32_t)(q >> 32), T.step};
-            const ull db = __shfl_sync(kFull, ev.didx, L);
-            uint32_t nx = kInvalid;
+            const ull db = __shfl_sync(kFull, lane == L ? ev_load().didx : 0ull, L);
+            uint32_t nx = kInvalid, ni = 0;
             ull dr = 0;
-            const int st = ervs_warp<M, kNoJump>(model, T, K, g, db, nx, dr);
+            const int st = ervs_warp<M, kNoJump>(p.mp, T, K, g, tb, tph, db, &nx, &ni, &dr);
             if (lane == L) {
                 if (st < 0) {
                     fail(-st);
                 } else {
-                    LC(LC_READS) += T.degree;
-                    LC(LC_DRAWS) += dr;
-                    finish_step(nx);
+                    lc_add(LC_READS, T.degree);
+                    lc_add(LC_DRAWS, dr);
+                    ervs_done(nx, ni);
                 }
             }
         }
     }
 
-    // ---- flush counters (Counter order == LaneCounter order)
+    // ---- flush counters (LaneCounter order: trials, reads, draws, alg)
 #pragma unroll
     for (int k = 0; k < LC_NUM; ++k) {
-        const ull s = warp_sum(s_lc[k][tid]);
-        if (lane == 0 && s) atomicAdd(&s_cnt[k], s);
+        const ull s = warp_sum((ull)s_lc[k][tid]);
+        if (lane == 0 && s) atomicAdd(&s_cnt[lc_slot[k]], s);
     }
-#undef LC
     __syncthreads();
     for (int i = tid; i < kCNum; i += blockDim.x)
         if (s_cnt[i]) atomicAdd(&p.counters[i], s_cnt[i]);
 }
 
-template <class M, int MODE>
+template <class M, int MODE, bool FAT>
 static cudaError_t launch_t(const WalkParams& p, int num_sms, cudaStream_t stream) {
     int per_sm = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, walk_kernel<M, MODE>,
-                                                                  kThreads, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, walk_kernel<M, MODE, FAT>, kThreads, 0);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
     unsigned long long blocks = (unsigned long long)num_sms * per_sm;
     const unsigned long long need = (p.nq + kThreads - 1) / kThreads;
     if (need < blocks) blocks = need ? need : 1;
-    walk_kernel<M, MODE><<<(unsigned)blocks, kThreads, 0, stream>>>(p);
+    walk_kernel<M, MODE, FAT><<<(unsigned)blocks, kThreads, 0, stream>>>(p);
     return cudaGetLastError();
 }
 
 template <class M>
 static cudaError_t launch_m(int mode, const WalkParams& p, int num_sms, cudaStream_t s) {
+    const bool fat = p.g.fat != nullptr;
     switch (mode) {
-    case kAdaptive: return launch_t<M, kAdaptive>(p, num_sms, s);
-    case kForceErvs: return launch_t<M, kForceErvs>(p, num_sms, s);
-    case kForceErjs: return launch_t<M, kForceErjs>(p, num_sms, s);
-    case kErvsNoJump: return launch_t<M, kErvsNoJump>(p, num_sms, s);
+    case kAdaptive:
+        return fat ? launch_t<M, kAdaptive, true>(p, num_sms, s)
+                   : launch_t<M, kAdaptive, false>(p, num_sms, s);
+    case kForceErjs:
+        return fat ? launch_t<M, kForceErjs, true>(p, num_sms, s)
+                   : launch_t<M, kForceErjs, false>(p, num_sms, s);
+    case kForceErvs: return launch_t<M, kForceErvs, false>(p, num_sms, s);
+    case kErvsNoJump: return launch_t<M, kErvsNoJump, false>(p, num_sms, s);
     }
     return cudaErrorInvalidValue;
 }

@@ -212,3 +212,55 @@ def test_errors(dw):
         dw.DeviceGraph.from_csr([0, 1, 1], [1], [0.0])
     with pytest.raises(dw.DynwalkError, match="not sorted"):
         dw.DeviceGraph.from_csr([0, 2, 2, 2], [2, 1], [1.0, 1.0])
+
+
+def _with_env(env: dict, fn):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return fn()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("layout", ["fat", "slim"])
+@pytest.mark.parametrize("shortcut", ["1", "0"])
+@pytest.mark.parametrize("mk", [dict(kind="node2vec", a=0.5, b=2.0),
+                                dict(kind="node2vec", a=2.0, b=0.5),
+                                dict(kind="node2vec", a=0.3, b=1.7),
+                                dict(kind="pr2", gamma=0.2)])
+def test_layouts_and_free_rejections(dw, orc, mk, shortcut, layout):
+    """Fat records (dw_common.cuh FatRec) and free rejections
+    (nonreturn_max) must not change a single path or counter: the same run on
+    the slim layout, with and without the shortcut, equals the oracle."""
+    og = orc.Graph.rmat(12, 16, 11).synth_philox("uniform", 1.0, 5.0, seed=12)
+    dg = _with_env({"DW_FAT": "1" if layout == "fat" else "0"}, lambda: to_device(dw, og))
+    q = np.arange(og.nv, dtype=np.uint32)
+    for mode in ("adaptive", "force-erjs"):
+        r_dev, r_orc = _with_env({"DW_SHORTCUT": shortcut},
+                                 lambda: run_both(dw, orc, og, dg, mk, q, mode, 60, 1.2))
+        assert_same(r_dev, r_orc, (mk, mode, layout, shortcut))
+
+
+def test_directed_multigraph_without_twins(dw, orc):
+    """A directed graph with duplicate edges and self-loops: return-edge ranges
+    are empty or multi-edge, so free rejections and the fat twin range are
+    exercised on their edge cases."""
+    rng = np.random.default_rng(5)
+    n = 3000
+    src = rng.integers(0, n, 40000).astype(np.uint32)
+    dst = (src + rng.integers(-40, 40, 40000)).clip(0, n - 1).astype(np.uint32)
+    src = np.concatenate([src, src[:3000], np.arange(0, n, 7, dtype=np.uint32)])
+    dst = np.concatenate([dst, dst[:3000], np.arange(0, n, 7, dtype=np.uint32)])
+    prop = rng.uniform(1.0, 5.0, len(src)).astype(np.float32)
+    og = orc.Graph.build(src, dst, prop, mirror=False, nv_hint=n)
+    dg = to_device(dw, og)
+    q = np.arange(og.nv, dtype=np.uint32)
+    for mk in (dict(kind="node2vec", a=0.5, b=2.0), dict(kind="pr2", gamma=0.3)):
+        for mode in MODES:
+            r_dev, r_orc = run_both(dw, orc, og, dg, mk, q, mode, 50, 1.1)
+            assert_same(r_dev, r_orc, (mk, mode))
