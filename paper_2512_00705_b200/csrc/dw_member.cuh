@@ -15,9 +15,13 @@ constexpr uint32_t kHashEmpty = 0xFFFFFFFFu;  // == kInvalid, never a target id
 
 __host__ __device__ __forceinline__ uint32_t hash_log2_buckets(uint32_t d) {
     // slots = max(8, next_pow2(2d)); buckets = slots / 8
+#ifdef __CUDA_ARCH__
+    return d <= 4 ? 0u : 29u - __clz(2u * d - 1u);
+#else
     uint32_t lg = 3;
     while ((1ull << lg) < 2ull * d) ++lg;
     return lg - 3;
+#endif
 }
 
 __host__ __device__ __forceinline__ uint32_t hash_buckets(uint32_t d) {

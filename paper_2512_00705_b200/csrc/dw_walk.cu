@@ -52,7 +52,7 @@
 namespace dwb {
 
 #ifndef DW_MIN_BLOCKS
-#define DW_MIN_BLOCKS 4
+#define DW_MIN_BLOCKS 3
 #endif
 #ifndef DW_RING
 #define DW_RING 2
@@ -69,8 +69,11 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 typedef unsigned long long ull;
 
 enum Phase : uint32_t { P_IDLE = 0, P_NODE, P_TRIAL, P_FETCH, P_VREC, P_VMEMB, P_COOP };
-// per-lane counters kept in shared memory, updated once per step
-enum LaneCounter : int { LC_TRIALS = 0, LC_READS, LC_DRAWS, LC_ALG, LC_NUM };
+// per-lane counters kept in shared memory (updated per walker or per eRVS
+// neighbour): eRJS trials, single-shot eRVS trials, eRVS reads and draws,
+// algorithmic bytes / 4.  Their block totals sit in the last LC_NUM slots of
+// the shared counter array (scratch slots of Counter, dw_walk.cuh).
+enum LaneCounter : int { LC_ETRIALS = 0, LC_ETRIALS1, LC_EREADS, LC_EDRAWS, LC_ALG4, LC_NUM };
 
 __device__ __forceinline__ bool valid_w(double w) { return !(w < 0.0) && isfinite(w); }
 
@@ -279,16 +282,21 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
     __shared__ uint32_t s_lab[kRing + 1][kThreads];  // label words (slim MetaPath)
     __shared__ uint32_t s_lc[LC_NUM][kThreads];  // per-lane RunStats counters (spill at 2^31)
     __shared__ ull s_cnt[kCNum];
+    __shared__ uint32_t s_hist[66];
+    __shared__ ull s_lct[LC_NUM];  // block totals of the lane counters
     const int tid = threadIdx.x;
     for (int i = tid; i < kCNum; i += blockDim.x) s_cnt[i] = 0;
+    if (tid < LC_NUM) s_lct[tid] = 0;
+    for (int i = tid; i < 66; i += blockDim.x) s_hist[i] = 0;
 #pragma unroll
     for (int c = 0; c < LC_NUM; ++c) s_lc[c][tid] = 0;
     __syncthreads();
-    constexpr int lc_slot[LC_NUM] = {kCTrials, kCWeightReads, kCRngDraws, kCAlgBytes};
+    // lane counters: LC_* accumulate per lane in shared memory and spill into
+    // the block's 64-bit totals (s_lct) before they can overflow
     auto lc_add = [&](int c, ull v) {
         const ull t = (ull)s_lc[c][tid] + v;
         if (t >= 0x80000000ull) {
-            atomicAdd(&s_cnt[lc_slot[c]], t);
+            atomicAdd(&s_lct[c], t);
             s_lc[c][tid] = 0;
         } else {
             s_lc[c][tid] = (uint32_t)t;
@@ -305,13 +313,17 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
     bool drained = false;  // warp-uniform
     ull qi = 0;
     // walker state
-    uint32_t cur = kInvalid, prev = kInvalid, pdeg = 0, phoff = 0, step = 0, deg = 0, hoff = 0;
+    uint32_t cur = kInvalid, prev = kInvalid, pdeg = 0, phoff = 0, plg = 0, step = 0, deg = 0,
+             hoff = 0;
     ull begin = 0;
     // eRJS state
     double bound = 0.0, mnr = 0.0;       // bound, non-return maximum
+    uint32_t cap = 0;                    // trial cap of the step (samplers.hpp:157)
     uint32_t tn = 0, rh = 0, rc = 0;     // next trial, ring head, ring count
     uint32_t tw_lo = 0, tw_cnt = 0;      // return-edge range in N(cur)
     uint32_t mb = 0, nret = 0, sel = 0;  // parked bucket (bit 31: parked), return trials, pair bits
+    // per-walker register counters, folded into the lane counters at walk end
+    uint32_t c_trials = 0, c_alg4 = 0;   // eRJS trials, algorithmic bytes / 4
     // eRVS state lives in the lane's spare ring slot (the ring is idle while a
     // lane runs eRVS), keeping the hot eRJS loop's register set small:
     //   s_rec[kRing-1][0] = {parked neighbour u, its h}   (VMEMB)
@@ -329,7 +341,6 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
         s_rec[kRing - 1][1][tid] = *reinterpret_cast<const uint4*>(&e);
         s_rec[kRing - 1][2][tid] = *(reinterpret_cast<const uint4*>(&e) + 1);
     };
-
     auto mkstep = [&](double hmax, double hsum) {
         Step S;
         S.cur = cur;
@@ -345,16 +356,18 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
         const ull q = p.qid_base + qi;
         return WalkerKey{p.seed_lo, p.seed_hi, (uint32_t)q, (uint32_t)(q >> 32), step};
     };
-    auto cap_of = [&]() -> uint32_t {
-        const ull c = p.cap_per_degree * (ull)deg;
-        return c > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)c;
-    };
     auto fail = [&](int code) {
         raise_error(p, code, p.qid_base + qi);
         phase = P_IDLE;
     };
+    auto flush_walker = [&]() {
+        lc_add(LC_ETRIALS, c_trials);
+        lc_add(LC_ALG4, c_alg4);
+        c_trials = c_alg4 = 0;
+    };
     auto end_walk = [&]() {
         if (p.lengths) p.lengths[qi] = step + 1;
+        flush_walker();
         phase = P_IDLE;
     };
     auto start_ervs = [&](ull draw_base) {
@@ -363,103 +376,15 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
         // §8(d): σ(8d) + 32·min(d, ⌈d'/8⌉) when membership is needed
         ull alg = ((8ull * deg + 31) / 32) * 32;
         if (kSO && prev != kInvalid) alg += 32ull * min((ull)deg, ((ull)pdeg + 7) / 8);
-        lc_add(LC_ALG, alg);
+        c_alg4 += (uint32_t)(alg >> 2);
         phase = deg >= kCoopMinDegree ? P_COOP : P_VREC;
-    };
-    // decide_sampler (cost_model.hpp:46-56) for the step at cur
-    auto begin_step = [&](double hmax, double hsum) {
-        if (deg == 0) {  // runtime.cpp:70-71: stop without counting a step
-            end_walk();
-            return;
-        }
-        Step S = mkstep(hmax, hsum);
-        model.prepare(S);
-        bool erjs = false;
-        if (MODE == kAdaptive) {
-            if (M::kBoundable) {
-                bound = model.bound(S);
-                erjs = p.ratio * bound < model.wsum(S);
-            }
-        } else if (MODE == kForceErjs) {  // runtime.cpp:109-129
-            erjs = M::kBoundable;
-            if (erjs) bound = model.bound(S);
-        }
-        atomicAdd(&s_cnt[kCHist + 2 * degree_bucket(deg) + (erjs ? 1 : 0)], 1ull);
-        // §8(d): 32 B offsets + 4 B path write (+ 32 B aggregates)
-        lc_add(LC_ALG, 36 + ((MODE == kAdaptive || MODE == kForceErjs) && M::kAggregates ? 32 : 0));
-        if (erjs) {
-            if (!(bound > 0.0) || !isfinite(bound)) {  // samplers.hpp:152-154
-                fail(kDevBadBound);
-                return;
-            }
-            mnr = shortcut ? model.nonreturn_max(S) : __longlong_as_double(0x7ff0000000000000ll);
-            tn = rh = rc = 0;
-            mb = nret = sel = 0;
-            phase = P_TRIAL;
-            if (p.cap_per_degree == 0) {  // immediate cap overrun
-                cnt_add(&s_cnt[kCFallbacks], 1);
-                start_ervs(0);
-            }
-        } else {
-            lc_add(LC_TRIALS, 1);  // single-shot kernels report one trial (samplers.hpp:22)
-            start_ervs(0);
-        }
-    };
-    // WalkerState::advance (walk_state.hpp:33-39); false when the walk ends
-    auto advance = [&](uint32_t next) {
-        prev = cur;
-        pdeg = deg;
-        phoff = hoff;
-        cur = next;
-        ++step;
-        if (p.paths) p.paths[qi * p.stride + step] = next;
-        if (step >= p.target) {
-            end_walk();
-            return false;
-        }
-        return true;
-    };
-    // take the fat record in slot k as the step's outcome
-    auto take_fat = [&](uint32_t k) {
-        const uint4 v0 = s_rec[k][0][tid], v1 = s_rec[k][1][tid], v2 = s_rec[k][2][tid];
-        if (!advance(v0.x)) return;
-        begin = ((ull)v0.z | ((ull)v0.w << 32)) & kBeginMask;
-        deg = v1.x;
-        hoff = v1.y;
-        tw_lo = v1.z;
-        tw_cnt = v1.w;
-        begin_step(__hiloint2double((int)v2.y, (int)v2.x), __hiloint2double((int)v2.w, (int)v2.z));
-    };
-    auto ervs_done = [&](uint32_t best, uint32_t bidx) {
-        if (best == kInvalid) {  // all weights zero: dead end (runtime.cpp:146-149)
-            cnt_add(&s_cnt[kCDeadEnds], 1);
-            end_walk();
-            return;
-        }
-        if (FAT) {
-            ErvsState e = ev_load();
-            e.didx = begin + (bidx & ~kHave);  // edge whose fat record starts the next step
-            ev_store(e);
-            phase = P_FETCH;
-        } else if (advance(best)) {
-            phase = P_NODE;
-        }
-    };
-    auto visit = [&](uint32_t u, double w) {
-        const ErvsState e0 = ev_load();
-        const ErvsState ev = ervs_visit<kNoJump>(e0, key_of(), tn, u, w);
-        ev_store(ev);
-        lc_add(LC_DRAWS, kNoJump ? 1ull : ev.didx - e0.didx);
-        lc_add(LC_READS, 1);
-        if (++tn == deg) ervs_done(ev.best, ev.bidx & ~kHave);
     };
     // eRJS bookkeeping for T judged trials, nret of them return edges
     auto count_erjs = [&](uint32_t T) {
-        lc_add(LC_TRIALS, T);
-        lc_add(LC_READS, T);
-        lc_add(LC_DRAWS, 2ull * T);
+        c_trials += T;
         const bool so = kSO && prev != kInvalid;
-        lc_add(LC_ALG, (so ? 64ull : 32ull) * T - (so ? 32ull * nret : 0ull));
+        c_alg4 += (so ? 16u : 8u) * T - (so ? 8u * nret : 0u);
+        if ((c_trials | c_alg4) & 0xC0000000u) flush_walker();
     };
 
     for (;;) {
@@ -492,7 +417,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                                 qi = i;
                                 cur = start;
                                 prev = kInvalid;
-                                pdeg = phoff = 0;
+                                pdeg = phoff = plg = 0;
                                 step = 0;
                             }
                         }
@@ -511,7 +436,6 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                 cp16(&s_mb[1][tid], b + 4);
             }
             const WalkerKey key = key_of();
-            const uint32_t cap = cap_of();
 #pragma unroll 1
             for (uint32_t gen = 0; gen < kGen && rc < kRing && tn < cap; ++gen, ++tn) {
                 const U4 b = walker_block(key, tn);
@@ -557,7 +481,9 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
         // ---- B
         cp_wait_all();
 
-        // ---- C: consume
+        // ---- C: consume; a finished step leaves its outcome in `next_ev`
+        enum : uint32_t { E_NONE = 0, E_FAT, E_ADV, E_NODE };
+        uint32_t next_ev = E_NONE, next_slot = 0, next_u = 0;
         if (phase == P_TRIAL) {
             int acc = -1;
             const Step S = mkstep(0.0, 0.0);
@@ -566,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                 const uint32_t u = FAT ? v0.x : (((sel >> rh) & 1) ? v0.z : v0.x);
                 const int r = bucket_lookup(s_mb[0][tid], s_mb[1][tid], u);
                 if (r < 0) {
-                    mb = kParked | ((mb + 1) & ((1u << hash_log2_buckets(pdeg)) - 1u));
+                    mb = kParked | ((mb + 1) & ((1u << plg) - 1u));
                 } else {
                     const float h = __uint_as_float(FAT ? v0.y : (((sel >> rh) & 1) ? v0.w : v0.y));
                     const WeightCase wc = model.weight(S, u, h, 0);
@@ -615,7 +541,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                         break;
                     }
                     if (!ok || y < hi) {  // outcome hinges on u in N(prev)
-                        mb = kParked | hash_bucket(u, hash_log2_buckets(pdeg));
+                        mb = kParked | hash_bucket(u, plg);
                         break;
                     }
                 }
@@ -626,60 +552,163 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                 if (acc >= 0) {
                     count_erjs(s_t[acc][tid] + 1);
                     if (FAT) {
-                        take_fat((uint32_t)acc);
+                        next_ev = E_FAT;
+                        next_slot = (uint32_t)acc;
                     } else {
                         const uint4 v0 = s_rec[acc][0][tid];
-                        const uint32_t u = ((sel >> acc) & 1) ? v0.z : v0.x;
-                        if (advance(u)) phase = P_NODE;
+                        next_ev = E_ADV;
+                        next_u = ((sel >> acc) & 1) ? v0.z : v0.x;
                     }
-                } else if (!(mb & kParked) && rc == 0 && tn >= cap_of()) {
+                } else if (!(mb & kParked) && rc == 0 && tn >= cap) {
                     count_erjs(tn);
                     cnt_add(&s_cnt[kCFallbacks], 1);  // cap overrun -> reservoir, same stream
                     start_ervs(2ull * tn);
                 }
             }
         } else if (phase == P_NODE) {
+            next_ev = E_NODE;
+        } else if (phase == P_FETCH) {
+            next_ev = E_FAT;
+        } else if (phase == P_VMEMB || phase == P_VREC) {
+            uint32_t u;
+            float h;
+            int r = 2;  // 2: no membership needed
+            if (phase == P_VMEMB) {
+                const uint4 pk = s_rec[kRing - 1][0][tid];
+                u = pk.x;
+                h = __uint_as_float(pk.y);
+                r = bucket_lookup(s_mb[0][tid], s_mb[1][tid], u);
+                if (r < 0) mb = (mb + 1) & ((1u << plg) - 1u);
+            } else {
+                const uint4 v = s_mb[0][tid];
+                u = sel ? v.z : v.x;
+                h = __uint_as_float(sel ? v.w : v.y);
+            }
+            if (r >= 0) {
+                const uint16_t lab = (M::kUsesLabels && phase == P_VREC)
+                                         ? (uint16_t)(sel ? (s_lab[kRing][tid] >> 16)
+                                                          : s_lab[kRing][tid])
+                                         : 0;
+                const WeightCase wc = model.weight(mkstep(0.0, 0.0), u, h, lab);
+                if (kSO && r == 2 && wc.needs_member) {
+                    s_rec[kRing - 1][0][tid] = make_uint4(u, __float_as_uint(h), 0u, 0u);
+                    mb = hash_bucket(u, plg);
+                    phase = P_VMEMB;
+                } else {
+                    const double w = r == 2 ? wc.w : (r ? wc.w_in : wc.w_out);
+                    if (!valid_w(w)) {
+                        fail(kDevBadWeight);
+                    } else {
+                        phase = P_VREC;
+                        const ErvsState e0 = ev_load();
+                        const ErvsState ev = ervs_visit<kNoJump>(e0, key_of(), tn, u, w);
+                        ev_store(ev);
+                        lc_add(LC_EDRAWS, kNoJump ? 1ull : ev.didx - e0.didx);
+                        lc_add(LC_EREADS, 1);
+                        if (++tn == deg) {  // the scan is complete
+                            if (ev.best == kInvalid) {  // all weights zero: dead end
+                                cnt_add(&s_cnt[kCDeadEnds], 1);
+                                end_walk();
+                            } else if (FAT) {
+                                ErvsState e = ev;
+                                e.didx = begin + (ev.bidx & ~kHave);  // its fat record starts the next step
+                                ev_store(e);
+                                phase = P_FETCH;
+                            } else {
+                                next_ev = E_ADV;
+                                next_u = ev.best;
+                            }
+                        }
+                    }
+                }
+            }
+        }
+
+        // ---- D: step transitions, one code site for every phase
+        double hmax = 0.0, hsum = 0.0;
+        if (next_ev == E_FAT || next_ev == E_ADV) {
+            // WalkerState::advance (walk_state.hpp:33-39)
+            const uint4 v0 = s_rec[next_slot][0][tid];
+            const uint32_t nx = next_ev == E_FAT ? v0.x : next_u;
+            prev = cur;
+            pdeg = deg;
+            phoff = hoff;
+            plg = hash_log2_buckets(deg);
+            cur = nx;
+            ++step;
+            if (p.paths) p.paths[qi * p.stride + step] = nx;
+            if (step >= p.target) {
+                end_walk();
+                next_ev = E_NONE;
+            } else if (next_ev == E_FAT) {
+                const uint4 v1 = s_rec[next_slot][1][tid], v2 = s_rec[next_slot][2][tid];
+                begin = ((ull)v0.z | ((ull)v0.w << 32)) & kBeginMask;
+                deg = v1.x;
+                hoff = v1.y;
+                tw_lo = v1.z;
+                tw_cnt = v1.w;
+                hmax = __hiloint2double((int)v2.y, (int)v2.x);
+                hsum = __hiloint2double((int)v2.w, (int)v2.z);
+            } else {
+                phase = P_NODE;  // slim layout: the node record comes next iteration
+                next_ev = E_NONE;
+            }
+        } else if (next_ev == E_NODE) {
             const uint4 v0 = s_mb[0][tid], v1 = s_mb[1][tid];
             begin = (ull)v0.x | ((ull)v0.y << 32);
             deg = v0.z;
             hoff = v0.w;
+            hmax = __hiloint2double((int)v1.y, (int)v1.x);
+            hsum = __hiloint2double((int)v1.w, (int)v1.z);
             // first step: no return edge; later (slim layout) the range is unknown
             tw_lo = 0;
             tw_cnt = prev == kInvalid ? 0u : 0xFFFFFFFFu;
-            begin_step(__hiloint2double((int)v1.y, (int)v1.x), __hiloint2double((int)v1.w, (int)v1.z));
-        } else if (phase == P_FETCH) {
-            take_fat(0);
-        } else if (phase == P_VMEMB) {
-            const uint4 pk = s_rec[kRing - 1][0][tid];
-            const uint32_t pu = pk.x;
-            const int r = bucket_lookup(s_mb[0][tid], s_mb[1][tid], pu);
-            if (r < 0) {
-                mb = (mb + 1) & ((1u << hash_log2_buckets(pdeg)) - 1u);
+        }
+        if (next_ev != E_NONE) {
+            // decide_sampler (cost_model.hpp:46-56) for the step at cur
+            if (deg == 0) {  // runtime.cpp:70-71: stop without counting a step
+                end_walk();
             } else {
-                const WeightCase wc = model.weight(mkstep(0.0, 0.0), pu, __uint_as_float(pk.y), 0);
-                const double w = r ? wc.w_in : wc.w_out;
-                if (!valid_w(w)) {
-                    fail(kDevBadWeight);
-                } else {
-                    phase = P_VREC;
-                    visit(pu, w);
+                Step S = mkstep(hmax, hsum);
+                model.prepare(S);
+                bool erjs = false;
+                if (MODE == kAdaptive) {
+                    if (M::kBoundable) {
+                        bound = model.bound(S);
+                        erjs = p.ratio * bound < model.wsum(S);
+                    }
+                } else if (MODE == kForceErjs) {  // runtime.cpp:109-129
+                    erjs = M::kBoundable;
+                    if (erjs) bound = model.bound(S);
                 }
-            }
-        } else if (phase == P_VREC) {
-            const uint4 v = s_mb[0][tid];
-            const uint32_t u = sel ? v.z : v.x;
-            const float h = __uint_as_float(sel ? v.w : v.y);
-            const uint16_t lab =
-                M::kUsesLabels ? (uint16_t)(sel ? (s_lab[kRing][tid] >> 16) : s_lab[kRing][tid]) : 0;
-            const WeightCase wc = model.weight(mkstep(0.0, 0.0), u, h, lab);
-            if (kSO && wc.needs_member) {
-                s_rec[kRing - 1][0][tid] = make_uint4(u, __float_as_uint(h), 0u, 0u);
-                mb = hash_bucket(u, hash_log2_buckets(pdeg));
-                phase = P_VMEMB;
-            } else if (!valid_w(wc.w)) {
-                fail(kDevBadWeight);
-            } else {
-                visit(u, wc.w);
+                {
+                    const uint32_t hb = 2 * degree_bucket(deg) + (erjs ? 1 : 0);
+                    if (atomicAdd(&s_hist[hb], 1u) == 0x7FFFFFFFu) {  // spill before overflow
+                        atomicSub(&s_hist[hb], 0x80000000u);
+                        atomicAdd(&s_cnt[kCHist + hb], 0x80000000ull);
+                    }
+                }
+                // §8(d): 32 B offsets + 4 B path write (+ 32 B aggregates)
+                c_alg4 += (36 + ((MODE == kAdaptive || MODE == kForceErjs) && M::kAggregates ? 32 : 0)) / 4;
+                if (erjs) {
+                    if (!(bound > 0.0) || !isfinite(bound)) {  // samplers.hpp:152-154
+                        fail(kDevBadBound);
+                    } else {
+                        mnr = shortcut ? model.nonreturn_max(S) : __longlong_as_double(0x7ff0000000000000ll);
+                        const ull c = p.cap_per_degree * (ull)deg;
+                        cap = c > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)c;
+                        tn = rh = rc = 0;
+                        mb = nret = sel = 0;
+                        phase = P_TRIAL;
+                        if (cap == 0) {  // immediate cap overrun
+                            cnt_add(&s_cnt[kCFallbacks], 1);
+                            start_ervs(0);
+                        }
+                    }
+                } else {
+                    lc_add(LC_ETRIALS1, 1);  // single-shot kernels report one trial (samplers.hpp:22)
+                    start_ervs(0);
+                }
             }
         }
 
@@ -707,19 +736,55 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                 if (st < 0) {
                     fail(-st);
                 } else {
-                    lc_add(LC_READS, T.degree);
-                    lc_add(LC_DRAWS, dr);
-                    ervs_done(nx, ni);
+                    lc_add(LC_EREADS, T.degree);
+                    lc_add(LC_EDRAWS, dr);
+                    if (nx == kInvalid) {
+                        cnt_add(&s_cnt[kCDeadEnds], 1);
+                        end_walk();
+                    } else if (FAT) {
+                        ErvsState e = ev_load();
+                        e.didx = tb + ni;
+                        ev_store(e);
+                        phase = P_FETCH;
+                    } else {
+                        // advance here (rare path); the node record comes next iteration
+                        prev = cur;
+                        pdeg = deg;
+                        phoff = hoff;
+                        plg = hash_log2_buckets(deg);
+                        cur = nx;
+                        ++step;
+                        if (p.paths) p.paths[qi * p.stride + step] = nx;
+                        if (step >= p.target)
+                            end_walk();
+                        else
+                            phase = P_NODE;
+                    }
                 }
             }
         }
     }
 
-    // ---- flush counters (LaneCounter order: trials, reads, draws, alg)
-#pragma unroll
-    for (int k = 0; k < LC_NUM; ++k) {
-        const ull s = warp_sum((ull)s_lc[k][tid]);
-        if (lane == 0 && s) atomicAdd(&s_cnt[lc_slot[k]], s);
+    // ---- flush counters: eRJS trials count as trials, reads and 2 draws each
+    __syncthreads();
+    if (tid < 66 && s_hist[tid]) s_cnt[kCHist + tid] += s_hist[tid];
+    const ull et = warp_sum((ull)s_lc[LC_ETRIALS][tid]), e1 = warp_sum((ull)s_lc[LC_ETRIALS1][tid]);
+    const ull er = warp_sum((ull)s_lc[LC_EREADS][tid]), ed = warp_sum((ull)s_lc[LC_EDRAWS][tid]);
+    const ull ea = warp_sum((ull)s_lc[LC_ALG4][tid]);
+    if (lane == 0) {
+        atomicAdd(&s_lct[LC_ETRIALS], et);
+        atomicAdd(&s_lct[LC_ETRIALS1], e1);
+        atomicAdd(&s_lct[LC_EREADS], er);
+        atomicAdd(&s_lct[LC_EDRAWS], ed);
+        atomicAdd(&s_lct[LC_ALG4], ea);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const ull t = s_lct[LC_ETRIALS];
+        s_cnt[kCTrials] = t + s_lct[LC_ETRIALS1];
+        s_cnt[kCWeightReads] = t + s_lct[LC_EREADS];
+        s_cnt[kCRngDraws] = 2 * t + s_lct[LC_EDRAWS];
+        s_cnt[kCAlgBytes] = 4 * s_lct[LC_ALG4];
     }
     __syncthreads();
     for (int i = tid; i < kCNum; i += blockDim.x)
