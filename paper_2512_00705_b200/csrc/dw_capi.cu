@@ -279,8 +279,24 @@ dwb::ModelParams model_params(const dw_model_desc* m) {
     case DW_MODEL_PR2: mp.shortcut = (m->gamma >= 0.0 && m->gamma <= 1.0) ? 1u : 0u; break;
     default: mp.shortcut = 0u;
     }
+    auto pow2 = [](double x) {
+        int e = 0;
+        return std::isfinite(x) && x != 0.0 && std::fabs(std::frexp(x, &e)) == 0.5;
+    };
+    mp.pow2_a = pow2(m->a) ? 1u : 0u;
+    mp.pow2_b = pow2(m->b) ? 1u : 0u;
+    switch (m->kind) {
+    case DW_MODEL_NODE2VEC: mp.pos_weights = (m->a > 0.0 && m->b > 0.0) ? 1u : 0u; break;
+    case DW_MODEL_PR2: mp.pos_weights = (m->gamma >= 0.0 && m->gamma < 1.0) ? 1u : 0u; break;
+    case DW_MODEL_STATIC: mp.pos_weights = 1u; break;  // props are validated > 0
+    default: mp.pos_weights = 0u;
+    }
+    if (const char* env = std::getenv("DW_POW2"))
+        if (env[0] == '0') mp.pow2_a = mp.pow2_b = 0u;
+    if (const char* env = std::getenv("DW_D1"))
+        if (env[0] == '0') mp.pos_weights = 0u;
     if (const char* env = std::getenv("DW_SHORTCUT"))
-        if (env[0] == '0') mp.shortcut = 0u;
+        if (env[0] == '0') mp.shortcut = mp.pos_weights = 0u;
     if (m->kind == DW_MODEL_METAPATH) {
         mp.schema_len = m->schema_len;
         for (uint32_t i = 0; i < m->schema_len; ++i) mp.schema[i] = m->schema[i];
@@ -322,6 +338,7 @@ dwb::WalkParams make_params(Replica& r, const dw_model_desc* m, const dw_run_opt
     p.target = target_steps(m, o);
     p.seed_lo = (uint32_t)o->seed;
     p.seed_hi = (uint32_t)(o->seed >> 32);
+    p.rk = dwb::philox_keys(p.seed_lo, p.seed_hi);
     p.cap_per_degree = o->erjs_cap_per_degree;
     p.ratio = o->edge_cost_ratio;
     p.counters = r.counters;

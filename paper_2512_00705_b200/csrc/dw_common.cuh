@@ -141,6 +141,30 @@ struct WalkerKey {
     uint32_t step;
 };
 
+// Same Philox with the round keys precomputed (rk[0][r] = k0 + r*0x9E3779B9,
+// rk[1][r] = k1 + r*0xBB67AE85), read straight from the kernel's constant
+// parameter bank: no key-schedule registers or adds in the hot loop.
+struct PhiloxKeys {
+    uint32_t k[2][10];
+};
+__host__ __device__ __forceinline__ PhiloxKeys philox_keys(uint32_t k0, uint32_t k1) {
+    PhiloxKeys r;
+    for (int i = 0; i < 10; ++i) {
+        r.k[0][i] = k0 + (uint32_t)i * 0x9E3779B9u;
+        r.k[1][i] = k1 + (uint32_t)i * 0xBB67AE85u;
+    }
+    return r;
+}
+__device__ __forceinline__ U4 philox4x32_10_rk(U4 c, const PhiloxKeys& rk) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+        c = U4{hi1 ^ c.y ^ rk.k[0][r], lo1, hi0 ^ c.w ^ rk.k[1][r], lo0};
+    }
+    return c;
+}
+
 __device__ __forceinline__ U4 walker_block(const WalkerKey& w, uint32_t block) {
     return philox4x32_10(U4{block, w.step, w.q0, w.q1}, w.k0, w.k1);
 }

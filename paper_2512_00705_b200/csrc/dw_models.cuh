@@ -60,6 +60,8 @@ struct ModelParams {
     double a, b, gamma;
     double inv_a, inv_b, inv_3;
     uint32_t fast_div, shortcut;
+    uint32_t pow2_a, pow2_b;  // a / b is a power of two: x / a == x * inv_a exactly
+    uint32_t pos_weights;     // every weight is > 0 and finite by construction
     uint32_t schema_len;
     uint16_t schema[128];
 };
@@ -108,10 +110,12 @@ struct Node2VecModel {
     static constexpr bool kBoundable = true;
     static constexpr bool kAggregates = W;  // PER_STEP bound reads node max/sum
     double a, b, ia, ib, i3;
+    bool pa, pb;
     __device__ explicit Node2VecModel(const ModelParams& p)
-        : a(p.a), b(p.b), ia(p.inv_a), ib(p.inv_b), i3(p.inv_3) {}
-    __device__ double da(double x) const { return ddiv(x, a, ia); }
-    __device__ double db(double x) const { return ddiv(x, b, ib); }
+        : a(p.a), b(p.b), ia(p.inv_a), ib(p.inv_b), i3(p.inv_3), pa(p.pow2_a != 0),
+          pb(p.pow2_b != 0) {}
+    __device__ double da(double x) const { return pa ? __dmul_rn(x, ia) : ddiv(x, a, ia); }
+    __device__ double db(double x) const { return pb ? __dmul_rn(x, ib) : ddiv(x, b, ib); }
     __device__ uint32_t max_steps() const { return 0xFFFFFFFFu; }
     __device__ double bound(const Step& s) const {  // models.hpp:74-79
         const double hmax = W ? s.hmax : 1.0;

@@ -372,11 +372,22 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
     };
     auto start_ervs = [&](ull draw_base) {
         tn = 0;
-        ev_store(ErvsState{-DBL_MAX, 0.0, draw_base, kInvalid, 0});
         // §8(d): σ(8d) + 32·min(d, ⌈d'/8⌉) when membership is needed
         ull alg = ((8ull * deg + 31) / 32) * 32;
         if (kSO && prev != kInvalid) alg += 32ull * min((ull)deg, ((ull)pdeg + 7) / 8);
         c_alg4 += (uint32_t)(alg >> 2);
+        if (FAT && (MODE == kAdaptive || MODE == kForceErjs) && deg == 1 && p.mp.pos_weights &&
+            bound > 0.0 && isfinite(bound)) {
+            // one neighbour whose weight is positive and finite by construction
+            // (its h is the row's finite hmax): the reservoir keeps it after
+            // its single key draw (samplers.hpp:82-85)
+            lc_add(LC_EREADS, 1);
+            lc_add(LC_EDRAWS, 1);
+            ev_store(ErvsState{0.0, 0.0, begin, kInvalid, 0});
+            phase = P_FETCH;
+            return;
+        }
+        ev_store(ErvsState{-DBL_MAX, 0.0, draw_base, kInvalid, 0});
         phase = deg >= kCoopMinDegree ? P_COOP : P_VREC;
     };
     // eRJS bookkeeping for T judged trials, nret of them return edges
@@ -435,29 +446,33 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                 cp16(&s_mb[0][tid], b);
                 cp16(&s_mb[1][tid], b + 4);
             }
-            const WalkerKey key = key_of();
-#pragma unroll 1
-            for (uint32_t gen = 0; gen < kGen && rc < kRing && tn < cap; ++gen, ++tn) {
-                const U4 b = walker_block(key, tn);
+            const ull q = p.qid_base + qi;
+            // one trial: free rejection, or queue its record gather in the ring
+            auto trial = [&](const U4& b) {
                 const uint32_t x = (uint32_t)bounded(lo64(b), deg);  // draw 2t:   bounded(d)
                 const double y = uniform01(hi64(b)) * bound;          // draw 2t+1: uniform01()*c
-                if (y >= mnr && x - tw_lo >= tw_cnt) continue;        // rejected, no gather
-                const uint32_t k = (rh + rc) & (kRing - 1);
-                s_y[k][tid] = y;
-                s_t[k][tid] = tn;
-                const ull e = begin + x;
-                if (FAT) {
-                    const uint4* r = reinterpret_cast<const uint4*>(g.fat + e);
-                    cp16(&s_rec[k][0][tid], r);
-                    cp16(&s_rec[k][1][tid], r + 1);
-                    cp16(&s_rec[k][2][tid], r + 2);
-                } else {
-                    sel = (sel & ~(1u << k)) | ((uint32_t)(e & 1) << k);
-                    cp16(&s_rec[k][0][tid], pair_of(g.edges, e));
-                    if (M::kUsesLabels && g.labels) cp4(&s_lab[k][tid], g.labels + (e & ~1ull));
+                if (!(y >= mnr && x - tw_lo >= tw_cnt)) {             // else rejected, no gather
+                    const uint32_t k = (rh + rc) & (kRing - 1);
+                    s_y[k][tid] = y;
+                    s_t[k][tid] = tn;
+                    const ull e = begin + x;
+                    if (FAT) {
+                        const uint4* r = reinterpret_cast<const uint4*>(g.fat + e);
+                        cp16(&s_rec[k][0][tid], r);
+                        cp16(&s_rec[k][1][tid], r + 1);
+                        cp16(&s_rec[k][2][tid], r + 2);
+                    } else {
+                        sel = (sel & ~(1u << k)) | ((uint32_t)(e & 1) << k);
+                        cp16(&s_rec[k][0][tid], pair_of(g.edges, e));
+                        if (M::kUsesLabels && g.labels) cp4(&s_lab[k][tid], g.labels + (e & ~1ull));
+                    }
+                    ++rc;
                 }
-                ++rc;
-            }
+                ++tn;
+            };
+#pragma unroll 1
+            for (uint32_t gen = 0; gen < kGen && rc < kRing && tn < cap; ++gen)
+                trial(philox4x32_10_rk(U4{tn, step, (uint32_t)q, (uint32_t)(q >> 32)}, p.rk));
         } else if (phase == P_NODE) {
             const char* nr = reinterpret_cast<const char*>(g.nodes + cur);
             cp16(&s_mb[0][tid], nr);

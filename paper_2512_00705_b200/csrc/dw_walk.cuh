@@ -28,6 +28,7 @@ struct WalkParams {
     uint32_t stride;        // walk_length + 1
     uint32_t target;        // min(walk_length, max_steps)
     uint32_t seed_lo, seed_hi;
+    PhiloxKeys rk;          // round keys of seed (dw_common.cuh philox_keys)
     unsigned long long cap_per_degree;
     double ratio;
     unsigned long long* counters;     // [kCNum]

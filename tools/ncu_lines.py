@@ -47,7 +47,7 @@ def main():
             return float(x.replace(",", ""))
         except ValueError:
             return 0.0
-    agg = collections.defaultdict(lambda: [0.0, 0.0, 0.0, 0.0])
+    agg = collections.defaultdict(lambda: [0.0, 0.0, 0.0, 0.0, 0.0, 0.0])
     for r in data:
         a = int(r[ix["Address"]], 16) - base
         key = m.get(a, ("?", 0))
@@ -56,6 +56,8 @@ def main():
         v[1] += num(r[ix["Thread Instructions Executed"]])
         v[2] += num(r[ix["Warp Stall Sampling (All Samples)"]])
         v[3] += num(r[ix["stall_no_inst"]])
+        v[4] += num(r[ix["stall_wait"]])
+        v[5] += num(r[ix["stall_long_sb"]])
     ti = sum(v[0] for v in agg.values()) or 1
     ts = sum(v[2] for v in agg.values()) or 1
     src = {}
@@ -65,12 +67,15 @@ def main():
                 src[key[0]] = open(subprocess.run(["bash", "-c", f"ls paper_2512_00705_b200/csrc/{key[0]} 2>/dev/null"], capture_output=True, text=True).stdout.strip()).read().splitlines()
             except Exception:
                 src[key[0]] = []
-    print(f"{'file:line':22s} {'inst%':>6s} {'simt':>5s} {'samp%':>6s} {'noinst%':>7s}  source")
-    for key, v in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
+    order = 0
+    if len(sys.argv) > 5:
+        order = {"inst": 0, "samp": 2, "wait": 4, "lsb": 5}[sys.argv[5]]
+    print(f"{'file:line':22s} {'inst%':>6s} {'simt':>5s} {'samp%':>6s} {'noinst%':>7s} {'wait%':>6s} {'lsb%':>6s}  source")
+    for key, v in sorted(agg.items(), key=lambda kv: -kv[1][order])[:top]:
         s = src.get(key[0], [])
         text = s[key[1] - 1].strip()[:60] if 0 < key[1] <= len(s) else ""
         print(f"{key[0] + ':' + str(key[1]):22s} {100 * v[0] / ti:6.2f} {v[1] / max(v[0], 1):5.1f} "
-              f"{100 * v[2] / ts:6.2f} {100 * v[3] / ts:7.2f}  {text}")
+              f"{100 * v[2] / ts:6.2f} {100 * v[3] / ts:7.2f} {100 * v[4] / ts:6.2f} {100 * v[5] / ts:6.2f}  {text}")
 
 
 if __name__ == "__main__":
