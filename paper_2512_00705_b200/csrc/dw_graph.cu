@@ -579,13 +579,16 @@ static cudaError_t calibrate_t(const DeviceGraphBuffers& gb, const ModelParams& 
     float tr = 0, ts = 0;
     DW_TRY(pass(1, tr, ts));  // warm-up
     int rounds = 1;
-    while (rounds < (1 << 20)) {  // grow until both passes are well above event resolution
+    // grow until both passes take milliseconds: sub-millisecond passes on a
+    // 148-SM part are dominated by launch and tail effects, and the ratio
+    // then swings by +-30% between runs
+    while (rounds < (1 << 20)) {
         DW_TRY(pass(rounds, tr, ts));
-        if (tr > 0.2f && ts > 0.2f) break;
+        if (tr > 2.0f && ts > 2.0f) break;
         rounds *= 2;
     }
     std::vector<double> ratios;
-    for (int rep = 0; rep < 5; ++rep) {
+    for (int rep = 0; rep < 5; ++rep) {  // ProfileConfig::repetitions
         DW_TRY(pass(rounds, tr, ts));
         ratios.push_back((double)tr / (double)ts);
     }
