@@ -261,23 +261,28 @@ def run_ours(args):
     kernel_ms = reduce_max(float(np.mean(kms)), dist, dev)
     alg_bytes = reduce_sum(int(stats.algorithmic_bytes), dist, dev)
 
-    # ---- e2e through the C ABI with pinned host buffers (H2D + D2H timed)
+    # ---- e2e through the C ABI with pinned host buffers (H2D + D2H timed):
+    # dw_run_compact returns RunResult.paths flattened (offsets + ids), so only
+    # ids that exist cross PCIe
     e2e = None
     if args.e2e_steps > 0 and n > 0:
         hq = C.c_void_p()
-        hp = C.c_void_p()
-        hl = C.c_void_p()
-        for buf, nbytes in ((hq, n * 4), (hp, n * (L + 1) * 4), (hl, n * 4)):
+        ho = C.c_void_p()
+        hf = C.c_void_p()
+        cap = n * (L + 1)
+        for buf, nbytes in ((hq, n * 4), (ho, (n + 1) * 8), (hf, cap * 4)):
             rc = lib.dw_host_alloc(nbytes, C.byref(buf))
             if rc:
                 raise dw.DynwalkError(rc, lib.dw_last_error().decode())
         qa = np.ctypeslib.as_array(C.cast(hq, dw.u32p), (n,))
         qa[:] = np.arange(lo, hi, dtype=np.uint32)
+        oa = np.ctypeslib.as_array(C.cast(ho, dw.u64p), (n + 1,))
         st = dw.RunStatsC()
 
         def e2e_step():
-            rc = lib.dw_run(dg.h, C.byref(mdesc), C.cast(hq, dw.u32p), n, C.byref(odesc),
-                            C.cast(hp, dw.u32p), C.cast(hl, dw.u32p), C.byref(st))
+            rc = lib.dw_run_compact(dg.h, C.byref(mdesc), C.cast(hq, dw.u32p), n,
+                                    C.byref(odesc), C.cast(ho, dw.u64p), C.cast(hf, dw.u32p),
+                                    cap, C.byref(st))
             if rc:
                 raise dw.DynwalkError(rc, lib.dw_last_error().decode())
 
@@ -290,12 +295,13 @@ def run_ours(args):
             e2e_step()
             ts.append(time.perf_counter() - t0)
         t_e2e = reduce_max(float(np.mean(ts)), dist, dev)
+        ids = int(oa[n])
         e2e = {"value": walker_steps / t_e2e, "unit": UNIT,
                "h2d_bytes_per_step": reduce_sum(n * 4, dist, dev),
-               "d2h_bytes_per_step": reduce_sum(n * (L + 2) * 4, dist, dev),
+               "d2h_bytes_per_step": reduce_sum((n + 1) * 8 + ids * 4, dist, dev),
                "ms_per_step": t_e2e * 1e3,
-               "api": "dw_run (C ABI), pinned host queries/paths/lengths"}
-        for buf in (hq, hp, hl):
+               "api": "dw_run_compact (C ABI): pinned host queries in, offsets + path ids out"}
+        for buf in (hq, ho, hf):
             lib.dw_host_free(buf)
 
     # ---- CPU baseline (oracle port, host cores), rank 0 at N=1 only

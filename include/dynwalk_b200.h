@@ -142,6 +142,15 @@ int dw_calibrate(dw_graph_t g, const dw_model_desc* model, uint64_t seed, double
 int dw_run(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries, uint64_t nq,
            const dw_run_opts* opts, uint32_t* paths, uint32_t* lengths, dw_run_stats* stats);
 
+/* run_queries with compact output, the layout of RunResult.paths
+ * (vector<vector<VertexId>>, runtime.hpp:75-78) flattened: path i is
+ * flat[offsets[i] .. offsets[i+1]), empty on a query error.  offsets: host
+ * [nq + 1]; flat: host, flat_capacity ids (nq * (walk_length + 1) always
+ * suffices).  Only the ids that exist cross PCIe, not the padding. */
+int dw_run_compact(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries,
+                   uint64_t nq, const dw_run_opts* opts, uint64_t* offsets, uint32_t* flat,
+                   uint64_t flat_capacity, dw_run_stats* stats);
+
 /* Device-resident variant on replica `replica`: d_queries / d_paths /
  * d_lengths are device pointers on that device (d_paths, d_lengths may be
  * NULL), `stream` a cudaStream_t (NULL = the replica's stream).  Enqueues and

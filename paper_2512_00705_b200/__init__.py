@@ -35,7 +35,8 @@ INVALID_VERTEX = 0xFFFFFFFF
 EXPORTED_SYMBOLS = (
     "dw_abi_version", "dw_last_error", "dw_device_count", "dw_graph_create",
     "dw_graph_generate_rmat", "dw_graph_destroy", "dw_graph_info", "dw_graph_download",
-    "dw_calibrate", "dw_run", "dw_run_device", "dw_run_device_sync", "dw_host_alloc",
+    "dw_calibrate", "dw_run", "dw_run_compact", "dw_run_device", "dw_run_device_sync",
+    "dw_host_alloc",
     "dw_host_free",
 )
 
@@ -129,6 +130,9 @@ def load_library() -> C.CDLL:
     L.dw_calibrate.argtypes = [vp, C.POINTER(ModelDesc), C.c_uint64, f64p]
     L.dw_run.argtypes = [vp, C.POINTER(ModelDesc), u32p, C.c_uint64, C.POINTER(RunOptsC), u32p,
                          u32p, C.POINTER(RunStatsC)]
+    L.dw_run_compact.argtypes = [vp, C.POINTER(ModelDesc), u32p, C.c_uint64,
+                                 C.POINTER(RunOptsC), u64p, u32p, C.c_uint64,
+                                 C.POINTER(RunStatsC)]
     L.dw_run_device.argtypes = [vp, C.c_int, C.POINTER(ModelDesc), vp, C.c_uint64,
                                 C.POINTER(RunOptsC), vp, vp, vp]
     L.dw_run_device_sync.argtypes = [vp, C.c_int, C.POINTER(RunStatsC)]
@@ -287,3 +291,20 @@ def run_queries(g: DeviceGraph, model: Model, queries, opts: RunOptions,
     _check(L.dw_run(g.h, C.byref(m), _p(q, u32p), len(q), C.byref(o), _p(paths, u32p),
                     _p(lengths, u32p), C.byref(st)))
     return RunResult(paths, lengths, st.as_dict())
+
+
+def run_queries_compact(g: DeviceGraph, model: Model, queries, opts: RunOptions):
+    """run_queries with the RunResult.paths layout flattened (dw_run_compact):
+    returns (offsets[nq+1] u64, flat u32, stats); path i is
+    flat[offsets[i]:offsets[i+1]]."""
+    L = load_library()
+    q = np.ascontiguousarray(queries, np.uint32)
+    offsets = np.empty(len(q) + 1, np.uint64)
+    cap = len(q) * (opts.walk_length + 1)
+    flat = np.empty(max(cap, 1), np.uint32)
+    st = RunStatsC()
+    m = model.c()
+    o = opts.c()
+    _check(L.dw_run_compact(g.h, C.byref(m), _p(q, u32p), len(q), C.byref(o),
+                            _p(offsets, u64p), _p(flat, u32p), cap, C.byref(st)))
+    return offsets, flat[:int(offsets[-1])], st.as_dict()

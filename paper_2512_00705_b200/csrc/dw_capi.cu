@@ -52,6 +52,8 @@ struct Replica {
     int num_sms = 0;
     cudaStream_t stream = nullptr;  // walk kernels
     cudaStream_t copy = nullptr;    // H2D/D2H
+    cudaStream_t ends = nullptr;    // dw_run_compact: batch end offsets (D2H)
+    cudaStream_t d2h = nullptr;     // dw_run_compact: compacted paths and offsets (D2H)
     DeviceGraphBuffers g;
     ull* counters = nullptr;   // [kCNum]
     ull* queues = nullptr;     // [kMaxBatches]
@@ -62,6 +64,15 @@ struct Replica {
     uint32_t* d_paths = nullptr;
     uint32_t* d_lengths = nullptr;
     ull cap_q = 0, cap_paths = 0;
+    // dw_run_compact scratch
+    ull* d_offs = nullptr;      // [cap_q + kMaxBatches] global (per device) path offsets
+    uint32_t* d_flat = nullptr; // [cap_paths] compacted paths
+    ull* d_base = nullptr;      // running offset of the batches already compacted
+    void* d_scan = nullptr;
+    size_t scan_bytes = 0;
+    ull cap_offs = 0, cap_flat = 0;
+    ull* h_ends = nullptr;      // pinned [kMaxBatches] batch end offsets
+    std::vector<cudaEvent_t> ev_end;
     cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
     std::vector<cudaEvent_t> ev_h2d, ev_walk;
     // dw_run_device bookkeeping
@@ -102,6 +113,8 @@ int init_replica(Replica& r, int device) {
     }
     CU(cudaStreamCreateWithFlags(&r.stream, cudaStreamNonBlocking), "cudaStreamCreate");
     CU(cudaStreamCreateWithFlags(&r.copy, cudaStreamNonBlocking), "cudaStreamCreate");
+    CU(cudaStreamCreateWithFlags(&r.ends, cudaStreamNonBlocking), "cudaStreamCreate");
+    CU(cudaStreamCreateWithFlags(&r.d2h, cudaStreamNonBlocking), "cudaStreamCreate");
     CU(cudaMalloc(&r.counters, dwb::kCNum * sizeof(ull)), "cudaMalloc counters");
     CU(cudaMalloc(&r.queues, kMaxBatches * sizeof(ull)), "cudaMalloc queues");
     CU(cudaMalloc(&r.error, sizeof(int)), "cudaMalloc error");
@@ -110,10 +123,14 @@ int init_replica(Replica& r, int device) {
     CU(cudaEventCreate(&r.ev_stop), "cudaEventCreate");
     r.ev_h2d.resize(kMaxBatches);
     r.ev_walk.resize(kMaxBatches);
+    r.ev_end.resize(kMaxBatches);
     for (int i = 0; i < kMaxBatches; ++i) {
         CU(cudaEventCreateWithFlags(&r.ev_h2d[i], cudaEventDisableTiming), "cudaEventCreate");
         CU(cudaEventCreateWithFlags(&r.ev_walk[i], cudaEventDisableTiming), "cudaEventCreate");
+        CU(cudaEventCreateWithFlags(&r.ev_end[i], cudaEventDisableTiming), "cudaEventCreate");
     }
+    CU(cudaMallocHost(&r.h_ends, kMaxBatches * sizeof(ull)), "cudaMallocHost");
+    CU(cudaMalloc(&r.d_base, sizeof(ull)), "cudaMalloc");
     return DW_OK;
 }
 
@@ -121,6 +138,8 @@ void free_replica(Replica& r) {
     if (cudaSetDevice(r.device) != cudaSuccess) return;
     if (r.stream) cudaStreamSynchronize(r.stream);
     if (r.copy) cudaStreamSynchronize(r.copy);
+    if (r.ends) cudaStreamSynchronize(r.ends);
+    if (r.d2h) cudaStreamSynchronize(r.d2h);
     cudaFree(r.g.nodes);
     cudaFree(r.g.edges);
     cudaFree(r.g.labels);
@@ -137,8 +156,16 @@ void free_replica(Replica& r) {
     if (r.ev_stop) cudaEventDestroy(r.ev_stop);
     for (auto e : r.ev_h2d) if (e) cudaEventDestroy(e);
     for (auto e : r.ev_walk) if (e) cudaEventDestroy(e);
+    for (auto e : r.ev_end) if (e) cudaEventDestroy(e);
+    cudaFree(r.d_offs);
+    cudaFree(r.d_flat);
+    cudaFree(r.d_base);
+    cudaFree(r.d_scan);
+    if (r.h_ends) cudaFreeHost(r.h_ends);
     if (r.stream) cudaStreamDestroy(r.stream);
     if (r.copy) cudaStreamDestroy(r.copy);
+    if (r.ends) cudaStreamDestroy(r.ends);
+    if (r.d2h) cudaStreamDestroy(r.d2h);
 }
 
 int resolve_devices(const int* devices, int ndev, std::vector<int>& out) {
@@ -419,6 +446,30 @@ int ensure_scratch(Replica& r, ull nq, ull stride, bool paths) {
     return DW_OK;
 }
 
+int ensure_compact_scratch(Replica& r, ull nq, ull stride) {
+    if (nq + kMaxBatches > r.cap_offs) {
+        cudaFree(r.d_offs);
+        r.d_offs = nullptr;
+        CU(cudaMalloc(&r.d_offs, (nq + kMaxBatches) * sizeof(ull)), "cudaMalloc offsets");
+        r.cap_offs = nq + kMaxBatches;
+    }
+    if (nq * stride > r.cap_flat) {
+        cudaFree(r.d_flat);
+        r.d_flat = nullptr;
+        CU(cudaMalloc(&r.d_flat, nq * stride * sizeof(uint32_t)), "cudaMalloc flat paths");
+        r.cap_flat = nq * stride;
+    }
+    size_t need = 0;
+    CU(dwb::path_offsets(nullptr, nq, nullptr, nullptr, nullptr, need, r.stream), "scan size");
+    if (need > r.scan_bytes) {
+        cudaFree(r.d_scan);
+        r.d_scan = nullptr;
+        CU(cudaMalloc(&r.d_scan, need), "cudaMalloc scan");
+        r.scan_bytes = need;
+    }
+    return DW_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -671,15 +722,17 @@ int dw_run(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries, ui
                                 r.stream),
                "walk");
             ++launches;
+            // D2H on its own stream, so the next batch's H2D (r.copy) never
+            // queues behind this batch's walk
             CU(cudaEventRecord(r.ev_walk[b], r.stream), "event");
-            CU(cudaStreamWaitEvent(r.copy, r.ev_walk[b], 0), "event");
+            CU(cudaStreamWaitEvent(r.d2h, r.ev_walk[b], 0), "event");
             if (paths)
                 CU(cudaMemcpyAsync(paths + (lo + blo) * stride, p.paths,
-                                   bn * stride * sizeof(uint32_t), cudaMemcpyDeviceToHost, r.copy),
+                                   bn * stride * sizeof(uint32_t), cudaMemcpyDeviceToHost, r.d2h),
                    "D2H paths");
             if (lengths)
                 CU(cudaMemcpyAsync(lengths + lo + blo, p.lengths, bn * sizeof(uint32_t),
-                                   cudaMemcpyDeviceToHost, r.copy),
+                                   cudaMemcpyDeviceToHost, r.d2h),
                    "D2H lengths");
         }
         if (!started) CU(cudaEventRecord(r.ev_start, r.stream), "event");
@@ -691,7 +744,139 @@ int dw_run(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries, ui
         CU(cudaSetDevice(r.device), "cudaSetDevice");
         CU(cudaStreamSynchronize(r.stream), "walk");
         CU(cudaStreamSynchronize(r.copy), "copy");
+        CU(cudaStreamSynchronize(r.d2h), "copy");
         if ((rc = collect(r, st, 0))) return rc;
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.ev_start, r.ev_stop);
+        kmax = std::max(kmax, (double)ms);
+    }
+    CU(cudaSetDevice(g->reps[0].device), "cudaSetDevice");
+    CU(cudaEventRecord(wall1, g->reps[0].d2h), "event");
+    CU(cudaEventSynchronize(wall1), "event");
+    float wall = 0.f;
+    cudaEventElapsedTime(&wall, wall0, wall1);
+    cudaEventDestroy(wall0);
+    cudaEventDestroy(wall1);
+    if (st) {
+        st->kernel_ms = kmax;
+        st->total_ms = wall;
+        st->kernel_launches = launches;
+    }
+    return DW_OK;
+}
+
+int dw_run_compact(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries,
+                   uint64_t nq, const dw_run_opts* opts, uint64_t* offsets, uint32_t* flat,
+                   uint64_t flat_capacity, dw_run_stats* st) {
+    if (!g) return fail(DW_EINVAL, "graph handle is NULL");
+    int rc;
+    if ((rc = check_model(model)) || (rc = check_opts(opts))) return rc;
+    if (nq && !queries) return fail(DW_EINVAL, "queries is NULL");
+    if (!offsets) return fail(DW_EINVAL, "offsets is NULL");
+    if (st) std::memset(st, 0, sizeof *st);
+    const int nd = (int)g->reps.size();
+    const ull stride = (ull)opts->walk_length + 1;
+    cudaEvent_t wall0 = nullptr, wall1 = nullptr;
+    CU(cudaSetDevice(g->reps[0].device), "cudaSetDevice");
+    CU(cudaEventCreate(&wall0), "event");
+    CU(cudaEventCreate(&wall1), "event");
+    CU(cudaEventRecord(wall0, g->reps[0].copy), "event");
+    ull launches = 0;
+    std::vector<int> nbs(nd, 0);
+    // phase 1: every batch's H2D, walk, offsets, compaction and end-offset read
+    // back are enqueued up front, so the devices never wait for the host
+    for (int di = 0; di < nd; ++di) {
+        Replica& r = g->reps[di];
+        const ull lo = nq * di / nd, hi = nq * (di + 1) / nd, n = hi - lo;
+        CU(cudaSetDevice(r.device), "cudaSetDevice");
+        if ((rc = ensure_scratch(r, std::max<ull>(n, 1), stride, true))) return rc;
+        if ((rc = ensure_compact_scratch(r, std::max<ull>(n, 1), stride))) return rc;
+        if ((rc = reset_run_state(r))) return rc;
+        CU(cudaMemsetAsync(r.d_base, 0, sizeof(ull), r.stream), "memset");
+        CU(cudaEventRecord(r.ev_walk[0], r.stream), "event");
+        CU(cudaStreamWaitEvent(r.copy, r.ev_walk[0], 0), "event");
+        const ull min_batch = 1ull << 20;
+        int nb = (int)std::min<ull>(8, std::max<ull>(1, n / min_batch));
+        if (n == 0) nb = 0;
+        nbs[di] = nb;
+        CU(cudaEventRecord(r.ev_start, r.stream), "event");
+        for (int b = 0; b < nb; ++b) {
+            const ull blo = n * b / nb, bhi = n * (b + 1) / nb, bn = bhi - blo;
+            CU(cudaMemcpyAsync(r.d_queries + blo, queries + lo + blo, bn * sizeof(uint32_t),
+                               cudaMemcpyHostToDevice, r.copy),
+               "H2D queries");
+            CU(cudaEventRecord(r.ev_h2d[b], r.copy), "event");
+            CU(cudaStreamWaitEvent(r.stream, r.ev_h2d[b], 0), "event");
+            dwb::WalkParams p = make_params(r, model, opts);
+            p.queries = r.d_queries + blo;
+            p.nq = bn;
+            p.qid_base = opts->qid_base + lo + blo;
+            p.paths = r.d_paths + blo * stride;  // no padding needed: only lengths are read
+            p.lengths = r.d_lengths + blo;
+            p.next_walker = r.queues + b;
+            CU(dwb::launch_walk(model->kind, model->weighted != 0, opts->mode, p, r.num_sms,
+                                r.stream),
+               "walk");
+            ++launches;
+            ull* offs = r.d_offs + blo + b;  // bn + 1 entries
+            size_t tb = r.scan_bytes;
+            CU(dwb::path_offsets(p.lengths, bn, offs, r.d_base, r.d_scan, tb, r.stream), "scan");
+            CU(dwb::compact_paths(p.paths, p.lengths, bn, stride, offs, 0, r.d_flat, r.stream),
+               "compact");
+            launches += 5;
+            CU(cudaEventRecord(r.ev_walk[b], r.stream), "event");
+            CU(cudaStreamWaitEvent(r.ends, r.ev_walk[b], 0), "event");
+            CU(cudaMemcpyAsync(r.h_ends + b, offs + bn, sizeof(ull), cudaMemcpyDeviceToHost,
+                               r.ends),
+               "D2H end");
+            CU(cudaEventRecord(r.ev_end[b], r.ends), "event");
+        }
+        CU(cudaEventRecord(r.ev_stop, r.stream), "event");
+    }
+    // phase 2: as each batch's end offset arrives, its compacted paths follow
+    // (overlapping the walks of the later batches)
+    ull gbase = 0;  // host offset of the current device's first path
+    for (int di = 0; di < nd; ++di) {
+        Replica& r = g->reps[di];
+        const ull lo = nq * di / nd, hi = nq * (di + 1) / nd, n = hi - lo;
+        CU(cudaSetDevice(r.device), "cudaSetDevice");
+        ull start = 0;
+        for (int b = 0; b < nbs[di]; ++b) {
+            const ull blo = n * b / nbs[di], bhi = n * (b + 1) / nbs[di], bn = bhi - blo;
+            CU(cudaEventSynchronize(r.ev_end[b]), "walk");
+            const ull end = r.h_ends[b];
+            if (gbase + end > flat_capacity) {
+                cudaStreamSynchronize(r.stream);
+                cudaStreamSynchronize(r.d2h);
+                return fail(DW_EINVAL, "flat path buffer too small: need more than %llu ids",
+                            (unsigned long long)(gbase + end));
+            }
+            if (end > start) {
+                if (!flat) return fail(DW_EINVAL, "flat is NULL");
+                CU(cudaMemcpyAsync(flat + gbase + start, r.d_flat + start,
+                                   (end - start) * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                                   r.d2h),
+                   "D2H paths");
+            }
+            CU(cudaMemcpyAsync(offsets + lo + blo, r.d_offs + blo + b, bn * sizeof(ull),
+                               cudaMemcpyDeviceToHost, r.d2h),
+               "D2H offsets");
+            start = end;
+        }
+        CU(cudaStreamSynchronize(r.stream), "walk");
+        CU(cudaStreamSynchronize(r.copy), "copy");
+        CU(cudaStreamSynchronize(r.ends), "copy");
+        CU(cudaStreamSynchronize(r.d2h), "copy");
+        if ((rc = collect(r, st, 0))) return rc;
+        if (gbase)
+            for (ull i = lo; i < hi; ++i) offsets[i] += gbase;
+        gbase += start;
+        (void)n;
+    }
+    offsets[nq] = gbase;
+    double kmax = 0.0;
+    for (int di = 0; di < nd; ++di) {
+        Replica& r = g->reps[di];
         float ms = 0.f;
         cudaEventElapsedTime(&ms, r.ev_start, r.ev_stop);
         kmax = std::max(kmax, (double)ms);

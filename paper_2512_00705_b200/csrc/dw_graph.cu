@@ -618,4 +618,60 @@ cudaError_t calibrate_ratio(const DeviceGraphBuffers& g, int kind, bool weighted
     return cudaErrorInvalidValue;
 }
 
+// ---- path compaction (dw_run_compact) ---------------------------------------
+__global__ void widen_lengths_kernel(const uint32_t* __restrict__ len, ull n,
+                                     ull* __restrict__ out) {
+    for (ull i = blockIdx.x * (ull)blockDim.x + threadIdx.x; i <= n;
+         i += (ull)gridDim.x * blockDim.x)
+        out[i] = i < n ? len[i] : 0ull;
+}
+
+__global__ void add_base_kernel(ull* __restrict__ offs, ull n, ull* __restrict__ d_base) {
+    const ull base = *d_base;  // read by every thread before the last block advances it
+    for (ull i = blockIdx.x * (ull)blockDim.x + threadIdx.x; i <= n;
+         i += (ull)gridDim.x * blockDim.x)
+        offs[i] += base;
+}
+
+__global__ void advance_base_kernel(const ull* __restrict__ offs, ull n, ull* __restrict__ d_base) {
+    *d_base = offs[n];
+}
+
+cudaError_t path_offsets(const uint32_t* lengths, ull n, ull* offs, ull* d_base, void* tmp,
+                         size_t& tmp_bytes, cudaStream_t s) {
+    if (!tmp) {
+        return cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, offs, offs, (int)(n + 1), s);
+    }
+    widen_lengths_kernel<<<grid_for(n + 1, 256), 256, 0, s>>>(lengths, n, offs);
+    DW_TRY(cudaGetLastError());
+    DW_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, offs, offs, (int)(n + 1), s));
+    add_base_kernel<<<grid_for(n + 1, 256), 256, 0, s>>>(offs, n, d_base);
+    DW_TRY(cudaGetLastError());
+    advance_base_kernel<<<1, 1, 0, s>>>(offs, n, d_base);
+    return cudaGetLastError();
+}
+
+__global__ void compact_paths_kernel(const uint32_t* __restrict__ paths,
+                                     const uint32_t* __restrict__ len, ull n, ull stride,
+                                     const ull* __restrict__ offs, ull flat_base,
+                                     uint32_t* __restrict__ flat) {
+    const ull warp = (blockIdx.x * (ull)blockDim.x + threadIdx.x) >> 5;
+    const ull nwarps = ((ull)gridDim.x * blockDim.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    for (ull i = warp; i < n; i += nwarps) {
+        const uint32_t l = len[i];
+        const uint32_t* src = paths + i * stride;
+        uint32_t* dst = flat + (offs[i] - flat_base);
+        for (uint32_t j = lane; j < l; j += 32) dst[j] = src[j];
+    }
+}
+
+cudaError_t compact_paths(const uint32_t* paths, const uint32_t* lengths, ull n, ull stride,
+                          const ull* offs, ull flat_base, uint32_t* flat, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    compact_paths_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(paths, lengths, n, stride, offs,
+                                                               flat_base, flat);
+    return cudaGetLastError();
+}
+
 }  // namespace dwb

@@ -49,4 +49,17 @@ cudaError_t calibrate_ratio(const DeviceGraphBuffers& g, int model_kind, bool we
 
 unsigned long long host_derive_seed(unsigned long long seed, unsigned long long stream);
 
+// ---- path compaction (dw_run_compact) ----------------------------------------
+// offs[0..n] = base + exclusive prefix sum of lengths[0..n) (offs[n] = base +
+// total); base is read from *d_base (device scalar) and *d_base is advanced by
+// the batch total, so consecutive batches on one stream produce global
+// offsets.  tmp/tmp_bytes: CUB scratch, query with tmp = nullptr.
+cudaError_t path_offsets(const uint32_t* lengths, unsigned long long n, unsigned long long* offs,
+                         unsigned long long* d_base, void* tmp, size_t& tmp_bytes,
+                         cudaStream_t s);
+// flat[offs[i] - flat_base ..) = paths[i * stride .. + lengths[i]), one warp per walker
+cudaError_t compact_paths(const uint32_t* paths, const uint32_t* lengths, unsigned long long n,
+                          unsigned long long stride, const unsigned long long* offs,
+                          unsigned long long flat_base, uint32_t* flat, cudaStream_t s);
+
 }  // namespace dwb

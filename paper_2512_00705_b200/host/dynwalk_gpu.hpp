@@ -20,6 +20,7 @@
 // not the mt19937 stream of the CPU run_queries.
 #pragma once
 
+#include <algorithm>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -158,15 +159,20 @@ inline RunResult run_queries(const DeviceGraph& dg, const AnyModel& model,
     o.qid_base = 0;
     const std::size_t nq = queries.size();
     const std::size_t stride = static_cast<std::size_t>(opts.walk_length) + 1;
-    std::vector<VertexId> flat(nq * stride);
-    std::vector<std::uint32_t> lengths(nq);
+    // compact transfer: offsets + the ids that exist (dw_run_compact)
+    std::vector<VertexId> flat(std::max<std::size_t>(nq * stride, 1));
+    std::vector<std::uint64_t> offsets(nq + 1);
     dw_run_stats st{};
-    check(dw_run(dg.handle(), &m.d, queries.data(), nq, &o, flat.data(), lengths.data(), &st));
+    check(dw_run_compact(dg.handle(), &m.d, queries.data(), nq, &o, offsets.data(), flat.data(),
+                         flat.size(), &st));
 
     RunResult rr;
     rr.paths.resize(nq);
-    for (std::size_t i = 0; i < nq; ++i)
-        rr.paths[i].assign(flat.begin() + i * stride, flat.begin() + i * stride + lengths[i]);
+    std::vector<std::uint32_t> lengths(nq);
+    for (std::size_t i = 0; i < nq; ++i) {
+        rr.paths[i].assign(flat.begin() + offsets[i], flat.begin() + offsets[i + 1]);
+        lengths[i] = static_cast<std::uint32_t>(offsets[i + 1] - offsets[i]);
+    }
     RunStats& s = rr.stats;
     s.queries = st.queries;
     s.query_errors = st.query_errors;

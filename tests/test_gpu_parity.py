@@ -264,3 +264,22 @@ def test_directed_multigraph_without_twins(dw, orc):
         for mode in MODES:
             r_dev, r_orc = run_both(dw, orc, og, dg, mk, q, mode, 50, 1.1)
             assert_same(r_dev, r_orc, (mk, mode))
+
+
+def test_compact_output_matches_padded(dw, orc):
+    """dw_run_compact (flattened RunResult.paths) carries exactly the padded
+    run's paths, including empty paths for query errors, over several batches."""
+    og = orc.Graph.rmat(13, 16, 21).synth_philox("uniform", 1.0, 5.0, seed=22)
+    dg = to_device(dw, og)
+    rng = np.random.default_rng(3)
+    q = rng.integers(0, og.nv + 50, 2_300_000).astype(np.uint32)  # > 2 batches, some invalid
+    opts = dw.RunOptions(mode="adaptive", walk_length=30, seed=5, edge_cost_ratio=1.3)
+    model = dw.Model(a=0.5, b=2.0)
+    r = dw.run_queries(dg, model, q, opts)
+    offs, flat, st = dw.run_queries_compact(dg, model, q, opts)
+    lens = np.diff(offs.astype(np.int64))
+    assert np.array_equal(lens, r.lengths.astype(np.int64))
+    mask = np.arange(r.paths.shape[1])[None, :] < r.lengths[:, None]
+    assert np.array_equal(flat, r.paths[mask])
+    for k in ("steps", "trials", "rng_draws", "dead_ends", "query_errors"):
+        assert st[k] == r.stats[k], k
