@@ -65,10 +65,21 @@ constexpr uint32_t kRing = DW_RING;  // queued trials per lane (power of two)
 constexpr uint32_t kGen = DW_GEN;    // Philox blocks per lane per iteration
 static_assert((kRing & (kRing - 1)) == 0, "kRing must be a power of two");
 constexpr uint32_t kCoopMinDegree = 64;
+#ifndef DW_EBATCH
+#define DW_EBATCH 8
+#endif
+#ifndef DW_EWAIT
+#define DW_EWAIT 10
+#endif
+// short-row eRVS: rows of <= kEBatchMaxDeg neighbours collect their weights in
+// the lane's first ring slot (6 doubles) and scan in batches of kEBatch lanes
+constexpr uint32_t kEBatchMaxDeg = 6;
+constexpr uint32_t kEBatch = DW_EBATCH;
+constexpr uint32_t kEWait = DW_EWAIT;
 constexpr unsigned kFull = 0xFFFFFFFFu;
 typedef unsigned long long ull;
 
-enum Phase : uint32_t { P_IDLE = 0, P_NODE, P_TRIAL, P_FETCH, P_VREC, P_VMEMB, P_COOP };
+enum Phase : uint32_t { P_IDLE = 0, P_NODE, P_TRIAL, P_FETCH, P_VREC, P_VMEMB, P_COOP, P_EMATH };
 // per-lane counters kept in shared memory (updated per walker or per eRVS
 // neighbour): eRJS trials, single-shot eRVS trials, eRVS reads and draws,
 // algorithmic bytes / 4.  Their block totals sit in the last LC_NUM slots of
@@ -223,8 +234,8 @@ struct ErvsState {
 constexpr uint32_t kHave = 0x80000000u;
 
 template <bool NOJUMP>
-__device__ __noinline__ ErvsState ervs_visit(ErvsState s, const WalkerKey key, uint32_t vi,
-                                             uint32_t u, double w) {
+__device__ __forceinline__ ErvsState ervs_visit_impl(ErvsState s, const WalkerKey& key, uint32_t vi,
+                                                     uint32_t u, double w) {
     if (NOJUMP) {
         const double r = open01(walker_draw(key, s.didx + vi));
         if (w != 0.0) {
@@ -261,6 +272,25 @@ __device__ __noinline__ ErvsState ervs_visit(ErvsState s, const WalkerKey key, u
         }
     }
     return s;
+}
+
+template <bool NOJUMP>
+__device__ __noinline__ ErvsState ervs_visit(ErvsState s, const WalkerKey key, uint32_t vi,
+                                             uint32_t u, double w) {
+    return ervs_visit_impl<NOJUMP>(s, key, vi, u, w);
+}
+
+// The whole jump scan (samplers.hpp:65-107) over d <= kEBatchMaxDeg weights in
+// the lane's landing slot (weight j at w[(j/2) * 2 * kThreads + j%2], i.e.
+// half j%2 of uint4 j/2 of the lane); returns the draw index after the scan
+// and the kept neighbour's index (kInvalid when every weight is zero).
+__device__ __noinline__ ull ervs_scan_short(const double* w, uint32_t d, const WalkerKey key,
+                                            ull didx, uint32_t* bidx) {
+    ErvsState s{-DBL_MAX, 0.0, didx, kInvalid, 0};
+    for (uint32_t j = 0; j < d; ++j)
+        s = ervs_visit_impl<false>(s, key, j, 0u, w[(j >> 1) * 2 * kThreads + (j & 1)]);
+    *bidx = s.best == kInvalid ? kInvalid : (s.bidx & ~kHave);
+    return s.didx;
 }
 
 __device__ __forceinline__ ull warp_sum(ull v) {
@@ -613,6 +643,16 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                     const double w = r == 2 ? wc.w : (r ? wc.w_in : wc.w_out);
                     if (!valid_w(w)) {
                         fail(kDevBadWeight);
+                    } else if (FAT && deg <= kEBatchMaxDeg) {
+                        // short row: collect the weights, run the reservoir
+                        // scan later together with other lanes (P_EMATH)
+                        // weight j in the lane's own slot-0 words: s_rec[0][j/2][tid], half j%2
+                        reinterpret_cast<double*>(&s_rec[0][tn >> 1][tid])[tn & 1] = w;
+                        phase = P_VREC;
+                        if (++tn == deg) {
+                            tn = 0;  // now counts the iterations spent waiting
+                            phase = P_EMATH;
+                        }
                     } else {
                         phase = P_VREC;
                         const ErvsState e0 = ev_load();
@@ -723,6 +763,39 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                 } else {
                     lc_add(LC_ETRIALS1, 1);  // single-shot kernels report one trial (samplers.hpp:22)
                     start_ervs(0);
+                }
+            }
+        }
+
+        // ---- batched reservoir scans of short rows: lanes whose weights are
+        // all collected wait until kEBatch of them (or one that waited
+        // kEWait iterations) can run the scan in the same instruction stream
+        if (FAT) {
+            const unsigned ready = __ballot_sync(kFull, phase == P_EMATH);
+            if (ready) {
+                const bool go = __popc(ready) >= kEBatch ||
+                                __any_sync(kFull, phase == P_EMATH && tn >= kEWait);
+                if (phase == P_EMATH) {
+                    if (go) {
+                        const ull d0 = ev_load().didx;
+                        uint32_t bidx = 0;
+                        const ull d1 = ervs_scan_short(
+                            reinterpret_cast<const double*>(&s_rec[0][0][tid]), deg, key_of(), d0,
+                            &bidx);
+                        lc_add(LC_EREADS, deg);
+                        lc_add(LC_EDRAWS, d1 - d0);
+                        if (bidx == kInvalid) {  // all weights zero: dead end
+                            cnt_add(&s_cnt[kCDeadEnds], 1);
+                            end_walk();
+                        } else {
+                            ErvsState e = ev_load();
+                            e.didx = begin + bidx;  // its fat record starts the next step
+                            ev_store(e);
+                            phase = P_FETCH;
+                        }
+                    } else {
+                        ++tn;
+                    }
                 }
             }
         }
