@@ -120,7 +120,7 @@ __device__ __forceinline__ void cnt_add(ull* c, ull v) { atomicAdd(c, v); }
 // ---- K2 (warp form): one row, 32 lanes; all lanes call with equal args ----
 // Returns the chosen target and its relative edge index (for the fat record).
 template <class M, bool NOJUMP>
-__device__ __noinline__ int ervs_warp(const ModelParams& mp, Step S, const WalkerKey key,
+__device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const WalkerKey key,
                                       const DevGraph& g, ull begin, uint32_t phoff, ull idx0,
                                       uint32_t* next, uint32_t* nidx, ull* draws) {
     M m(mp);
@@ -275,7 +275,7 @@ __device__ __forceinline__ ErvsState ervs_visit_impl(ErvsState s, const WalkerKe
 }
 
 template <bool NOJUMP>
-__device__ __noinline__ ErvsState ervs_visit(ErvsState s, const WalkerKey key, uint32_t vi,
+__device__ __forceinline__ ErvsState ervs_visit(ErvsState s, const WalkerKey key, uint32_t vi,
                                              uint32_t u, double w) {
     return ervs_visit_impl<NOJUMP>(s, key, vi, u, w);
 }
@@ -284,7 +284,7 @@ __device__ __noinline__ ErvsState ervs_visit(ErvsState s, const WalkerKey key, u
 // the lane's landing slot (weight j at w[(j/2) * 2 * kThreads + j%2], i.e.
 // half j%2 of uint4 j/2 of the lane); returns the draw index after the scan
 // and the kept neighbour's index (kInvalid when every weight is zero).
-__device__ __noinline__ ull ervs_scan_short(const double* w, uint32_t d, const WalkerKey key,
+__device__ __forceinline__ ull ervs_scan_short(const double* w, uint32_t d, const WalkerKey key,
                                             ull didx, uint32_t* bidx) {
     ErvsState s{-DBL_MAX, 0.0, didx, kInvalid, 0};
     for (uint32_t j = 0; j < d; ++j)
