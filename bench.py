@@ -1,7 +1,10 @@
 #!/usr/bin/env python
 """Benchmark: walker-steps/sec for node2vec on R-MAT scale-24 (BASELINE.json configs[1]).
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--config C]
+
+--config selects another BASELINE.json config (1: s16 node2vec (2, 0.5); 3:
+MetaPath s22; 4: PR2 on Pareto-weighted s25); the default is the headline, 2.
 
 One step = one full walk batch: every vertex of the R-MAT s24 ef16 graph
 (uniform [1,5) weights) starts one node2vec walker (a=p=0.5, b=q=2, 80
@@ -35,7 +38,23 @@ sys.path.insert(0, ROOT)
 
 METRIC = "walker-steps/sec (node2vec, R-MAT s24) at 1/2/4/8 B200; % of HBM roofline"
 UNIT = "walker-steps/s"
-TOPO_SEED, WEIGHT_SEED, WALK_SEED, PROFILE_SEED = 1, 2, 7, 5
+# BASELINE.json configs (1-based, as listed there).  The driver runs the
+# default, configs[1] = 2; the others are for DESIGN.md's per-config table.
+CONFIGS = {
+    1: dict(scale=16, model="node2vec", a=2.0, b=0.5, weights="uniform", labels=None,
+            desc="node2vec p=2 q=0.5, length 80, one walker per node, weighted R-MAT s16 ef16"),
+    2: dict(scale=24, model="node2vec", a=0.5, b=2.0, weights="uniform", labels=None,
+            desc="node2vec p=0.5 q=2, walk length 80, one walker per vertex, weighted R-MAT "
+                 "scale-24 ef16 (BASELINE configs[1])"),
+    3: dict(scale=22, model="metapath", schema=(0, 1, 2, 3) * 20, weights="uniform",
+            labels=(0, 3),
+            desc="MetaPath schema (0,1,2,3) repeated to length 80, R-MAT s22 ef16, labels "
+                 "uniform [0,3], uniform [1,5) weights"),
+    4: dict(scale=25, model="pr2", gamma=0.15, weights="pareto", labels=None,
+            desc="second-order PR gamma=0.15 (no restart in the reference, SURVEY 7.3), "
+                 "R-MAT/Kronecker s25 ef16, Pareto alpha=1 weights"),
+}
+TOPO_SEED, WEIGHT_SEED, WALK_SEED, PROFILE_SEED, LABEL_SEED = 1, 2, 7, 5, 3
 
 
 def parse():
@@ -44,10 +63,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--scale", type=int, default=24)
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS),
+                    help="BASELINE.json config (2 = the headline)")
+    ap.add_argument("--scale", type=int, default=0, help="override the config's R-MAT scale")
     ap.add_argument("--walk-length", type=int, default=80)
-    ap.add_argument("--a", type=float, default=0.5)
-    ap.add_argument("--b", type=float, default=2.0)
+
     ap.add_argument("--mode", default="adaptive")
     ap.add_argument("--ratio", type=float, default=0.0, help="override the calibrated ratio")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -55,18 +75,40 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true",
                     help="build + 1 warm walk + 1 walk, for ncu (no JSON line)")
-    return ap.parse_args()
+    a = ap.parse_args()
+    a.cfg = dict(CONFIGS[a.config])
+    if a.scale:
+        a.cfg["scale"] = a.scale
+    a.scale = a.cfg["scale"]
+    return a
+
+
+def metric(args) -> str:
+    if args.config == 2 and args.scale == 24:
+        return METRIC
+    c = args.cfg
+    return f"walker-steps/sec ({c['model']}, R-MAT s{args.scale}, BASELINE config {args.config})"
+
+
+def model_kw(cfg) -> dict:
+    if cfg["model"] == "node2vec":
+        return dict(a=cfg["a"], b=cfg["b"])
+    if cfg["model"] == "metapath":
+        return dict(schema=tuple(cfg["schema"]))
+    return dict(gamma=cfg["gamma"])
 
 
 def workload(args) -> dict:
-    return {"workload": f"node2vec p={args.a:g} q={args.b:g}, walk length {args.walk_length}, "
-                        f"one walker per vertex, weighted R-MAT scale-{args.scale} ef16 "
-                        "(BASELINE configs[1])",
-            "graph": f"rmat s{args.scale} ef16 (A,B,C,D)=(.57,.19,.19,.05), mirrored, "
-                     "uniform[1,5) f32 weights",
-            "model": "node2vec", "a": args.a, "b": args.b, "walk_length": args.walk_length,
-            "mode": args.mode, "walkers": 2 ** args.scale,
-            "l2": "inputs larger than L2 (graph 2.7 GB vs 126 MB L2), no flush"}
+    c = args.cfg
+    w = "uniform[1,5) f32 weights" if c["weights"] == "uniform" else "Pareto alpha=1 f32 weights"
+    if c["labels"]:
+        w += f", labels uniform [{c['labels'][0]},{c['labels'][1]}]"
+    return {"workload": c["desc"] if args.scale == CONFIGS[args.config]["scale"]
+            else c["desc"] + f" (run at scale {args.scale})",
+            "graph": f"rmat s{args.scale} ef16 (A,B,C,D)=(.57,.19,.19,.05), mirrored, {w}",
+            "model": c["model"], **{k: v for k, v in model_kw(c).items() if k != "schema"},
+            "walk_length": args.walk_length, "mode": args.mode, "walkers": 2 ** args.scale,
+            "l2": "inputs larger than L2 (graph >= 2 GB vs 126 MB L2), no flush"}
 
 
 # ---------------------------------------------------------------- distributed
@@ -188,11 +230,13 @@ def run_ours(args):
     import paper_2512_00705_b200 as dw
 
     t0 = time.perf_counter()
-    dg = dw.DeviceGraph.rmat(args.scale, 16, seed=TOPO_SEED, weights="uniform", low=1.0,
-                             high=5.0, weight_seed=WEIGHT_SEED, devices=[local])
+    cfg = args.cfg
+    dg = dw.DeviceGraph.rmat(args.scale, 16, seed=TOPO_SEED, weights=cfg["weights"], low=1.0,
+                             high=5.0, alpha=1.0, weight_seed=WEIGHT_SEED, labels=cfg["labels"],
+                             label_seed=LABEL_SEED, devices=[local])
     info = dg.info()
     build_s = time.perf_counter() - t0
-    model = dw.Model("node2vec", a=args.a, b=args.b)
+    model = dw.Model(cfg["model"], **model_kw(cfg))
     # one calibration (rank 0), broadcast so every shard makes the same decisions
     ratio = args.ratio
     t0 = time.perf_counter()
@@ -315,7 +359,7 @@ def run_ours(args):
     achieved = alg_bytes / (kernel_ms / 1e3) / 1e9
     traffic = ncu_traffic(args.scale)
     out = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": metric(args), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
         "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64 (bit-exact reference arithmetic), u32 ids",
@@ -326,7 +370,8 @@ def run_ours(args):
                            "override" if args.ratio > 0 else "device-calibrated (K4)")),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"],
                      "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
-                     "peak_source": pk["source"], "kernel": "walk_kernel<Node2VecModel<true>,0>",
+                     "peak_source": pk["source"],
+                     "kernel": f"walk_kernel<{cfg['model']} model, adaptive, fat records>",
                      "kernel_ms_per_launch": kernel_ms,
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "algorithmic_bytes_per_walker_step": alg_bytes / max(walker_steps, 1),
@@ -351,10 +396,10 @@ def cpu_baseline_port(dg, args, ratio, nv) -> dict:
     cores) on a bounded walker sample of the same graph and ratio."""
     import oracle
     a = dg.download()
-    og = oracle.Graph.from_csr(a["row"], a["col"], a["prop"])
+    og = oracle.Graph.from_csr(a["row"], a["col"], a["prop"], a["label"])
     del a
     cores = os.cpu_count() or 1
-    m = oracle.Model("node2vec", a=args.a, b=args.b)
+    m = oracle.Model(args.cfg["model"], **model_kw(args.cfg))
     n = 1 << 14
     rate = None
     while True:
@@ -383,14 +428,19 @@ def run_reference(args):
     cores = os.cpu_count() or 1
     t0 = time.perf_counter()
     # identical graph to the GPU arm, built on the CPU (oracle generator)
+    cfg = args.cfg
     og = oracle.Graph.rmat_par(args.scale, 16, TOPO_SEED, 1.0, 5.0, WEIGHT_SEED, cores)
+    if cfg["weights"] == "pareto":
+        og.synth_philox("pareto", alpha=1.0, seed=WEIGHT_SEED)
+    if cfg["labels"]:
+        og.synth_philox("labels", cfg["labels"][0], cfg["labels"][1], seed=LABEL_SEED)
     a = og.arrays()
     del og
     kind = "reference" if oracle.ref_available() else "port"
-    m = oracle.Model("node2vec", a=args.a, b=args.b)
+    m = oracle.Model(cfg["model"], **model_kw(cfg))
     nv = len(a["row"]) - 1
     if kind == "reference":
-        g = oracle.RefGraph.from_csr(a["row"], a["col"], a["prop"])
+        g = oracle.RefGraph.from_csr(a["row"], a["col"], a["prop"], a["label"])
         del a
         # the reference's own cost-model profile (cost_model.cpp:37-126), CLI seed
         ratio = oracle.ref_profile_ratio(g, m, oracle.derive_seed(WALK_SEED, PROFILE_SEED))
@@ -401,7 +451,7 @@ def run_reference(args):
                                keep_paths=False)
             return r.stats["steps"] - r.stats["dead_ends"], r.wall_ms / 1e3
     else:
-        g = oracle.Graph.from_csr(a["row"], a["col"], a["prop"])
+        g = oracle.Graph.from_csr(a["row"], a["col"], a["prop"], a["label"])
         ratio = args.ratio if args.ratio > 0 else 1.2
 
         def walk(q):
@@ -432,7 +482,7 @@ def run_reference(args):
     value = tot_ws / tot_t
     sample = (f"{len(q)} walkers per step (every {stride}th vertex), {tot_ws // args.steps} "
               f"walker-steps per step; time = RunStats.wall_ms")
-    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+    out = {"metric": metric(args), "value": value, "unit": UNIT, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_t / args.steps * 1e3,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
            "dtype": "f64", "data": "synthetic R-MAT (same graph as the GPU arm, CPU-built)",

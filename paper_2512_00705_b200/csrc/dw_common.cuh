@@ -40,7 +40,9 @@ struct alignas(8) EdgeRec {
 static_assert(sizeof(EdgeRec) == 8, "EdgeRec must be 8 bytes");
 
 // Fat edge record for edge e = (v -> u), 64 B stride (one L2 line half):
-//   w0 col = u          w1 h = edge_prop(e)     w2,w3 begin(u) (48 bits) | label(e) << 48
+//   w0 col = u          w1 h = edge_prop(e)
+//   w2,w3 begin(u) (bits 0-39) | label(e) (bits 40-55) | label mask of u (bits 56-63:
+//         bit l < 7 set iff N(u) has an edge labelled l; bit 7: N(u) has a label >= 7)
 //   w4 degree(u)        w5 hoff(u)              w6 twin_lo: first index of v in N(u)
 //   w7 twin_cnt: multiplicity of v in N(u) (0 for a directed edge without twin)
 //   w8..11 node_prop_max(u), node_prop_sum(u) (f64, exact)
@@ -60,7 +62,8 @@ struct alignas(64) FatRec {
     uint32_t aux[4];  // reserved
 };
 static_assert(sizeof(FatRec) == 64, "FatRec stride must be 64 bytes");
-constexpr unsigned long long kBeginMask = (1ull << 48) - 1;
+constexpr unsigned long long kBeginMask = (1ull << 40) - 1;
+constexpr uint32_t kMaskLabels = 7;  // labels with an exact bit in the fat record's mask
 
 struct DevGraph {
     const NodeRec* __restrict__ nodes;

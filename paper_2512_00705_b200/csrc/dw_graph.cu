@@ -144,9 +144,29 @@ __device__ __forceinline__ uint32_t row_lower_bound(const EdgeRec* __restrict__ 
 
 // one warp per row v: record e = (v -> u) gets u's node data and the range of
 // v in N(u) (its return edges when a walker stands on u having come from v)
+// per node: bit l (l < kMaskLabels) iff the row has an edge labelled l, bit
+// kMaskLabels iff it has a label >= kMaskLabels (MetaPath dead-row detection)
+__global__ void label_mask_kernel(const NodeRec* __restrict__ nodes, uint32_t nv,
+                                  const uint16_t* __restrict__ labels, uint8_t* __restrict__ mask) {
+    const ull warp = (blockIdx.x * (ull)blockDim.x + threadIdx.x) >> 5;
+    const ull nwarps = ((ull)gridDim.x * blockDim.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    for (ull v = warp; v < nv; v += nwarps) {
+        const NodeRec nr = nodes[v];
+        uint32_t m = 0;
+        for (ull i = lane; i < nr.degree; i += 32) {
+            const uint32_t l = labels[nr.begin + i];
+            m |= l < kMaskLabels ? (1u << l) : (1u << kMaskLabels);
+        }
+        m = __reduce_or_sync(0xFFFFFFFFu, m);
+        if (lane == 0) mask[v] = (uint8_t)m;
+    }
+}
+
 __global__ void fat_build_kernel(const NodeRec* __restrict__ nodes, uint32_t nv,
                                  const EdgeRec* __restrict__ edges,
-                                 const uint16_t* __restrict__ labels, FatRec* __restrict__ fat) {
+                                 const uint16_t* __restrict__ labels,
+                                 const uint8_t* __restrict__ lmask, FatRec* __restrict__ fat) {
     const ull warp = (blockIdx.x * (ull)blockDim.x + threadIdx.x) >> 5;
     const ull nwarps = ((ull)gridDim.x * blockDim.x) >> 5;
     const uint32_t lane = threadIdx.x & 31;
@@ -164,7 +184,8 @@ __global__ void fat_build_kernel(const NodeRec* __restrict__ nodes, uint32_t nv,
             f.col = er.col;
             f.h = er.h;
             f.tbegin_label = (nu.begin & kBeginMask) |
-                             ((ull)(labels ? labels[e] : (uint16_t)0) << 48);
+                             ((ull)(labels ? labels[e] : (uint16_t)0) << 40) |
+                             ((ull)(lmask ? lmask[er.col] : 1u) << 56);
             f.tdeg = nu.degree;
             f.thoff = nu.hoff;
             f.twin_lo = lo;
@@ -188,9 +209,17 @@ static cudaError_t build_fat(DeviceGraphBuffers& g, cudaStream_t s) {
     const ull need = g.ne * sizeof(FatRec);
     if (need + (4ull << 30) > free_b) return cudaSuccess;
     DW_TRY(cudaMallocAsync(&g.fat, need, s));
+    uint8_t* lmask = nullptr;
+    if (g.labels) {
+        DW_TRY(cudaMallocAsync(&lmask, std::max<ull>(g.nv, 1), s));
+        label_mask_kernel<<<grid_for((ull)g.nv * 32, 256), 256, 0, s>>>(g.nodes, g.nv, g.labels,
+                                                                        lmask);
+        DW_TRY(cudaGetLastError());
+    }
     fat_build_kernel<<<grid_for((ull)g.nv * 32, 256), 256, 0, s>>>(g.nodes, g.nv, g.edges,
-                                                                   g.labels, g.fat);
+                                                                   g.labels, lmask, g.fat);
     DW_TRY(cudaGetLastError());
+    if (lmask) DW_TRY(cudaFreeAsync(lmask, s));
     return cudaStreamSynchronize(s);
 }
 

@@ -561,7 +561,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                 uint16_t lab = 0;
                 if (M::kUsesLabels) {
                     if (FAT)
-                        lab = (uint16_t)(v0.w >> 16);
+                        lab = (uint16_t)(v0.w >> 8);
                     else
                         lab = (uint16_t)(odd ? (s_lab[rh][tid] >> 16) : s_lab[rh][tid]);
                 }
@@ -681,6 +681,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
 
         // ---- D: step transitions, one code site for every phase
         double hmax = 0.0, hsum = 0.0;
+        uint32_t lmask = 0xFFu;  // labels present in N(cur) (fat record), all = unknown
         if (next_ev == E_FAT || next_ev == E_ADV) {
             // WalkerState::advance (walk_state.hpp:33-39)
             const uint4 v0 = s_rec[next_slot][0][tid];
@@ -704,6 +705,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                 tw_cnt = v1.w;
                 hmax = __hiloint2double((int)v2.y, (int)v2.x);
                 hsum = __hiloint2double((int)v2.w, (int)v2.z);
+                lmask = v0.w >> 24;
             } else {
                 phase = P_NODE;  // slim layout: the node record comes next iteration
                 next_ev = E_NONE;
@@ -745,7 +747,31 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                 }
                 // §8(d): 32 B offsets + 4 B path write (+ 32 B aggregates)
                 c_alg4 += (36 + ((MODE == kAdaptive || MODE == kForceErjs) && M::kAggregates ? 32 : 0)) / 4;
-                if (erjs) {
+                bool dead_row = false;
+                if (M::kUsesLabels && FAT) {
+                    // MetaPath row without an edge of label schema[step]: every
+                    // weight is 0 (models.hpp:99-104).  The reference burns the
+                    // 64·d trial cap, falls back to eRVS and finds no candidate;
+                    // the counters of that sequence are known in closed form
+                    // (samplers.hpp:156-177), so the walk ends here.
+                    const uint32_t want = p.mp.schema[step];
+                    dead_row = want < kMaskLabels && !(lmask & (1u << want)) &&
+                               (!erjs || (bound > 0.0 && isfinite(bound)));
+                }
+                if (dead_row) {
+                    if (erjs) {
+                        const ull c = p.cap_per_degree * (ull)deg;
+                        nret = 0;
+                        count_erjs(c > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)c);
+                        cnt_add(&s_cnt[kCFallbacks], 1);
+                    } else {
+                        lc_add(LC_ETRIALS1, 1);  // single-shot eRVS
+                    }
+                    lc_add(LC_EREADS, deg);  // the reservoir pass reads every weight, draws none
+                    c_alg4 += (uint32_t)(((8ull * deg + 31) / 32) * 8);
+                    cnt_add(&s_cnt[kCDeadEnds], 1);
+                    end_walk();
+                } else if (erjs) {
                     if (!(bound > 0.0) || !isfinite(bound)) {  // samplers.hpp:152-154
                         fail(kDevBadBound);
                     } else {
