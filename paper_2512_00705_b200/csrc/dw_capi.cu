@@ -46,6 +46,7 @@ int cuda_fail(cudaError_t e, const char* what) {
     } while (0)
 
 constexpr int kMaxBatches = 64;
+constexpr int kRingSlots = 3;
 
 struct Replica {
     int device = 0;
@@ -59,22 +60,25 @@ struct Replica {
     ull* queues = nullptr;     // [kMaxBatches]
     int* error = nullptr;
     ull* error_info = nullptr;
-    // dw_run scratch
-    uint32_t* d_queries = nullptr;
-    uint32_t* d_paths = nullptr;
-    uint32_t* d_lengths = nullptr;
-    ull cap_q = 0, cap_paths = 0;
-    // dw_run_compact scratch
-    ull* d_offs = nullptr;      // [cap_q + kMaxBatches] global (per device) path offsets
-    uint32_t* d_flat = nullptr; // [cap_paths] compacted paths
+    // dw_run / dw_run_compact: a ring of batch slots, so device memory stays
+    // bounded whatever nq is (BASELINE config 5 streams 435 GB of paths)
+    struct Slot {
+        uint32_t* q = nullptr;      // [cap] queries
+        uint32_t* len = nullptr;    // [cap] path lengths
+        uint32_t* paths = nullptr;  // [cap][stride] padded paths
+        uint32_t* flat = nullptr;   // [cap * stride] compacted paths (compact runs)
+        ull* offs = nullptr;        // [cap + 1] global path offsets (compact runs)
+        cudaEvent_t h2d = nullptr, walk = nullptr, end = nullptr, d2h = nullptr;
+    };
+    Slot slots[kRingSlots];
+    ull slot_cap = 0, slot_stride = 0;
+    bool slot_flat = false;
     ull* d_base = nullptr;      // running offset of the batches already compacted
     void* d_scan = nullptr;
     size_t scan_bytes = 0;
-    ull cap_offs = 0, cap_flat = 0;
-    ull* h_ends = nullptr;      // pinned [kMaxBatches] batch end offsets
-    std::vector<cudaEvent_t> ev_end;
+    ull* h_ends = nullptr;      // pinned [kRingSlots] batch end offsets
     cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
-    std::vector<cudaEvent_t> ev_h2d, ev_walk;
+    cudaEvent_t ev_reset = nullptr;
     // dw_run_device bookkeeping
     bool pending = false;
     ull pending_launches = 0;
@@ -121,15 +125,11 @@ int init_replica(Replica& r, int device) {
     CU(cudaMalloc(&r.error_info, sizeof(ull)), "cudaMalloc error");
     CU(cudaEventCreate(&r.ev_start), "cudaEventCreate");
     CU(cudaEventCreate(&r.ev_stop), "cudaEventCreate");
-    r.ev_h2d.resize(kMaxBatches);
-    r.ev_walk.resize(kMaxBatches);
-    r.ev_end.resize(kMaxBatches);
-    for (int i = 0; i < kMaxBatches; ++i) {
-        CU(cudaEventCreateWithFlags(&r.ev_h2d[i], cudaEventDisableTiming), "cudaEventCreate");
-        CU(cudaEventCreateWithFlags(&r.ev_walk[i], cudaEventDisableTiming), "cudaEventCreate");
-        CU(cudaEventCreateWithFlags(&r.ev_end[i], cudaEventDisableTiming), "cudaEventCreate");
-    }
-    CU(cudaMallocHost(&r.h_ends, kMaxBatches * sizeof(ull)), "cudaMallocHost");
+    CU(cudaEventCreateWithFlags(&r.ev_reset, cudaEventDisableTiming), "cudaEventCreate");
+    for (auto& sl : r.slots)
+        for (cudaEvent_t* e : {&sl.h2d, &sl.walk, &sl.end, &sl.d2h})
+            CU(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "cudaEventCreate");
+    CU(cudaMallocHost(&r.h_ends, kRingSlots * sizeof(ull)), "cudaMallocHost");
     CU(cudaMalloc(&r.d_base, sizeof(ull)), "cudaMalloc");
     return DW_OK;
 }
@@ -149,19 +149,21 @@ void free_replica(Replica& r) {
     cudaFree(r.queues);
     cudaFree(r.error);
     cudaFree(r.error_info);
-    cudaFree(r.d_queries);
-    cudaFree(r.d_paths);
-    cudaFree(r.d_lengths);
-    if (r.ev_start) cudaEventDestroy(r.ev_start);
-    if (r.ev_stop) cudaEventDestroy(r.ev_stop);
-    for (auto e : r.ev_h2d) if (e) cudaEventDestroy(e);
-    for (auto e : r.ev_walk) if (e) cudaEventDestroy(e);
-    for (auto e : r.ev_end) if (e) cudaEventDestroy(e);
-    cudaFree(r.d_offs);
-    cudaFree(r.d_flat);
+    for (auto& sl : r.slots) {
+        cudaFree(sl.q);
+        cudaFree(sl.len);
+        cudaFree(sl.paths);
+        cudaFree(sl.flat);
+        cudaFree(sl.offs);
+        for (cudaEvent_t e : {sl.h2d, sl.walk, sl.end, sl.d2h})
+            if (e) cudaEventDestroy(e);
+    }
     cudaFree(r.d_base);
     cudaFree(r.d_scan);
     if (r.h_ends) cudaFreeHost(r.h_ends);
+    if (r.ev_start) cudaEventDestroy(r.ev_start);
+    if (r.ev_stop) cudaEventDestroy(r.ev_stop);
+    if (r.ev_reset) cudaEventDestroy(r.ev_reset);
     if (r.stream) cudaStreamDestroy(r.stream);
     if (r.copy) cudaStreamDestroy(r.copy);
     if (r.ends) cudaStreamDestroy(r.ends);
@@ -427,45 +429,247 @@ int collect(Replica& r, dw_run_stats* st, ull qbase) {
     return DW_OK;
 }
 
-int ensure_scratch(Replica& r, ull nq, ull stride, bool paths) {
-    if (nq > r.cap_q) {
-        cudaFree(r.d_queries);
-        cudaFree(r.d_lengths);
-        r.d_queries = nullptr;
-        r.d_lengths = nullptr;
-        CU(cudaMalloc(&r.d_queries, nq * sizeof(uint32_t)), "cudaMalloc queries");
-        CU(cudaMalloc(&r.d_lengths, nq * sizeof(uint32_t)), "cudaMalloc lengths");
-        r.cap_q = nq;
+int ensure_ring(Replica& r, ull cap, ull stride, bool flat) {
+    if (cap <= r.slot_cap && stride <= r.slot_stride && (!flat || r.slot_flat)) return DW_OK;
+    CU(cudaDeviceSynchronize(), "ring");
+    cap = std::max(cap, r.slot_cap);
+    stride = std::max(stride, r.slot_stride);
+    flat = flat || r.slot_flat;
+    for (auto& sl : r.slots) {
+        cudaFree(sl.q);
+        cudaFree(sl.len);
+        cudaFree(sl.paths);
+        cudaFree(sl.flat);
+        cudaFree(sl.offs);
+        sl.q = sl.len = sl.paths = sl.flat = nullptr;
+        sl.offs = nullptr;
+        CU(cudaMalloc(&sl.q, cap * sizeof(uint32_t)), "cudaMalloc queries");
+        CU(cudaMalloc(&sl.len, cap * sizeof(uint32_t)), "cudaMalloc lengths");
+        CU(cudaMalloc(&sl.paths, cap * stride * sizeof(uint32_t)), "cudaMalloc paths");
+        if (flat) {
+            CU(cudaMalloc(&sl.flat, cap * stride * sizeof(uint32_t)), "cudaMalloc flat paths");
+            CU(cudaMalloc(&sl.offs, (cap + 1) * sizeof(ull)), "cudaMalloc offsets");
+        }
     }
-    if (paths && nq * stride > r.cap_paths) {
-        cudaFree(r.d_paths);
-        r.d_paths = nullptr;
-        CU(cudaMalloc(&r.d_paths, nq * stride * sizeof(uint32_t)), "cudaMalloc paths");
-        r.cap_paths = nq * stride;
+    if (flat) {
+        size_t need = 0;
+        CU(dwb::path_offsets(nullptr, cap, nullptr, nullptr, nullptr, need, r.stream), "scan size");
+        if (need > r.scan_bytes) {
+            cudaFree(r.d_scan);
+            r.d_scan = nullptr;
+            CU(cudaMalloc(&r.d_scan, need), "cudaMalloc scan");
+            r.scan_bytes = need;
+        }
     }
+    r.slot_cap = cap;
+    r.slot_stride = stride;
+    r.slot_flat = flat;
     return DW_OK;
 }
 
-int ensure_compact_scratch(Replica& r, ull nq, ull stride) {
-    if (nq + kMaxBatches > r.cap_offs) {
-        cudaFree(r.d_offs);
-        r.d_offs = nullptr;
-        CU(cudaMalloc(&r.d_offs, (nq + kMaxBatches) * sizeof(ull)), "cudaMalloc offsets");
-        r.cap_offs = nq + kMaxBatches;
+// Output of a host-buffer run: padded paths + lengths (dw_run), or the
+// flattened RunResult.paths layout (dw_run_compact).
+struct RunOut {
+    bool compact = false;
+    uint32_t* paths = nullptr;
+    uint32_t* lengths = nullptr;
+    ull* offsets = nullptr;
+    uint32_t* flat = nullptr;
+    ull flat_cap = 0;
+};
+
+// Walkers per batch: ~8 batches per device so H2D/D2H overlap the walks, at
+// least 256K walkers per launch, at most 4M (1.3 GB of padded paths at L=80)
+ull batch_size(ull n) {
+    const ull want = (n + 7) / 8;
+    return std::max<ull>(1, std::min<ull>(n, std::max<ull>(1ull << 18, std::min<ull>(want, 1ull << 22))));
+}
+
+// The batched H2D -> walk -> (compaction) -> D2H pipeline behind dw_run and
+// dw_run_compact.  Each device walks a contiguous block of the queries in
+// batches that cycle through kRingSlots buffer slots; stream events order slot
+// reuse, so the host only blocks to learn a compact batch's size.
+int run_engine(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries, ull nq,
+               const dw_run_opts* opts, const RunOut& out, dw_run_stats* st) {
+    if (st) std::memset(st, 0, sizeof *st);
+    const int nd = (int)g->reps.size();
+    const ull stride = (ull)opts->walk_length + 1;
+    struct Dev {
+        ull lo = 0, n = 0, bs = 1, nb = 0, eb = 0, db = 0, end = 0;
+    };
+    std::vector<Dev> dv(nd);
+    cudaEvent_t wall0 = nullptr, wall1 = nullptr;
+    CU(cudaSetDevice(g->reps[0].device), "cudaSetDevice");
+    CU(cudaEventCreate(&wall0), "event");
+    CU(cudaEventCreate(&wall1), "event");
+    CU(cudaEventRecord(wall0, g->reps[0].copy), "event");
+    ull launches = 0;
+    int rc;
+    for (int di = 0; di < nd; ++di) {
+        Replica& r = g->reps[di];
+        Dev& d = dv[di];
+        d.lo = nq * di / nd;
+        d.n = nq * (di + 1) / nd - d.lo;
+        d.bs = batch_size(d.n);
+        d.nb = d.n ? (d.n + d.bs - 1) / d.bs : 0;
+        CU(cudaSetDevice(r.device), "cudaSetDevice");
+        if ((rc = ensure_ring(r, d.bs, stride, out.compact))) return rc;
+        if ((rc = reset_run_state(r))) return rc;
+        CU(cudaMemsetAsync(r.d_base, 0, sizeof(ull), r.stream), "memset");
+        CU(cudaEventRecord(r.ev_reset, r.stream), "event");
+        CU(cudaStreamWaitEvent(r.copy, r.ev_reset, 0), "event");
+        CU(cudaEventRecord(r.ev_start, r.stream), "event");
     }
-    if (nq * stride > r.cap_flat) {
-        cudaFree(r.d_flat);
-        r.d_flat = nullptr;
-        CU(cudaMalloc(&r.d_flat, nq * stride * sizeof(uint32_t)), "cudaMalloc flat paths");
-        r.cap_flat = nq * stride;
+    auto enqueue = [&](int di, ull b) -> int {
+        Replica& r = g->reps[di];
+        Dev& d = dv[di];
+        Replica::Slot& sl = r.slots[b % kRingSlots];
+        const ull blo = b * d.bs, bn = std::min(d.bs, d.n - blo);
+        CU(cudaSetDevice(r.device), "cudaSetDevice");
+        if (b >= (ull)kRingSlots) {  // the slot's previous batch must be walked and drained
+            CU(cudaStreamWaitEvent(r.copy, sl.walk, 0), "event");
+            CU(cudaStreamWaitEvent(r.stream, sl.d2h, 0), "event");
+        }
+        CU(cudaMemcpyAsync(sl.q, queries + d.lo + blo, bn * sizeof(uint32_t),
+                           cudaMemcpyHostToDevice, r.copy),
+           "H2D queries");
+        CU(cudaEventRecord(sl.h2d, r.copy), "event");
+        CU(cudaStreamWaitEvent(r.stream, sl.h2d, 0), "event");
+        dwb::WalkParams p = make_params(r, model, opts);
+        p.queries = sl.q;
+        p.nq = bn;
+        p.qid_base = opts->qid_base + d.lo + blo;
+        p.paths = (out.compact || out.paths) ? sl.paths : nullptr;
+        p.lengths = sl.len;
+        p.next_walker = r.queues + (b % kRingSlots);
+        CU(cudaMemsetAsync(p.next_walker, 0, sizeof(ull), r.stream), "memset");
+        if (p.paths && !out.compact)  // compaction copies only the written ids
+            CU(cudaMemsetAsync(p.paths, 0xFF, bn * stride * sizeof(uint32_t), r.stream),
+               "memset paths");
+        CU(dwb::launch_walk(model->kind, model->weighted != 0, opts->mode, p, r.num_sms,
+                            r.stream),
+           "walk");
+        ++launches;
+        if (out.compact) {
+            size_t tb = r.scan_bytes;
+            CU(dwb::path_offsets(sl.len, bn, sl.offs, r.d_base, r.d_scan, tb, r.stream), "scan");
+            CU(dwb::compact_paths(sl.paths, sl.len, bn, stride, sl.offs, sl.flat, r.stream),
+               "compact");
+            launches += 5;
+        }
+        CU(cudaEventRecord(sl.walk, r.stream), "event");
+        if (out.compact) {
+            CU(cudaStreamWaitEvent(r.ends, sl.walk, 0), "event");
+            CU(cudaMemcpyAsync(r.h_ends + (b % kRingSlots), sl.offs + bn, sizeof(ull),
+                               cudaMemcpyDeviceToHost, r.ends),
+               "D2H end");
+            CU(cudaEventRecord(sl.end, r.ends), "event");
+        } else {
+            CU(cudaStreamWaitEvent(r.d2h, sl.walk, 0), "event");
+            if (out.paths)
+                CU(cudaMemcpyAsync(out.paths + (d.lo + blo) * stride, sl.paths,
+                                   bn * stride * sizeof(uint32_t), cudaMemcpyDeviceToHost, r.d2h),
+                   "D2H paths");
+            if (out.lengths)
+                CU(cudaMemcpyAsync(out.lengths + d.lo + blo, sl.len, bn * sizeof(uint32_t),
+                                   cudaMemcpyDeviceToHost, r.d2h),
+                   "D2H lengths");
+            CU(cudaEventRecord(sl.d2h, r.d2h), "event");
+        }
+        return DW_OK;
+    };
+    ull gbase = 0;     // compact: host offset of the device being drained
+    int drain_dev = 0;  // compact: devices drain in order (their host offsets chain)
+    auto drain = [&](int di, ull b) -> int {
+        Replica& r = g->reps[di];
+        Dev& d = dv[di];
+        Replica::Slot& sl = r.slots[b % kRingSlots];
+        if (!out.compact) return DW_OK;  // the D2H was enqueued with the walk
+        const ull blo = b * d.bs, bn = std::min(d.bs, d.n - blo);
+        CU(cudaSetDevice(r.device), "cudaSetDevice");
+        CU(cudaEventSynchronize(sl.end), "walk");
+        const ull end = r.h_ends[b % kRingSlots];
+        if (gbase + end > out.flat_cap) {
+            cudaDeviceSynchronize();
+            return fail(DW_EINVAL, "flat path buffer too small: need more than %llu ids",
+                        (unsigned long long)(gbase + end));
+        }
+        if (end > d.end) {
+            if (!out.flat) return fail(DW_EINVAL, "flat is NULL");
+            CU(cudaMemcpyAsync(out.flat + gbase + d.end, sl.flat, (end - d.end) * sizeof(uint32_t),
+                               cudaMemcpyDeviceToHost, r.d2h),
+               "D2H paths");
+        }
+        CU(cudaMemcpyAsync(out.offsets + d.lo + blo, sl.offs, bn * sizeof(ull),
+                           cudaMemcpyDeviceToHost, r.d2h),
+           "D2H offsets");
+        CU(cudaEventRecord(sl.d2h, r.d2h), "event");
+        d.end = end;
+        return DW_OK;
+    };
+    for (;;) {
+        bool busy = false;
+        for (int di = 0; di < nd; ++di) {
+            Dev& d = dv[di];
+            while (d.eb < d.nb && d.eb - d.db < (ull)kRingSlots) {
+                if ((rc = enqueue(di, d.eb))) return rc;
+                ++d.eb;
+                busy = true;
+            }
+            const bool may_drain = !out.compact || di == drain_dev;
+            if (d.db < d.eb && may_drain) {
+                if ((rc = drain(di, d.db))) return rc;
+                ++d.db;
+                busy = true;
+            }
+            if (out.compact && di == drain_dev && d.db == d.nb) {
+                // device finished: its offsets become global, the next device drains
+                Replica& r = g->reps[di];
+                CU(cudaSetDevice(r.device), "cudaSetDevice");
+                if (gbase) {
+                    CU(cudaStreamSynchronize(r.d2h), "copy");
+                    for (ull i = d.lo; i < d.lo + d.n; ++i) out.offsets[i] += gbase;
+                }
+                gbase += d.end;
+                ++drain_dev;
+                busy = true;
+            }
+            if (!out.compact && d.db < d.eb) {
+                d.db = d.eb;  // padded runs need no host step per batch
+                busy = true;
+            }
+        }
+        bool done = true;
+        for (const Dev& d : dv) done = done && d.db == d.nb;
+        if (done && (!out.compact || drain_dev == nd)) break;
+        if (!busy) return fail(DW_ECUDA, "run pipeline stalled");
     }
-    size_t need = 0;
-    CU(dwb::path_offsets(nullptr, nq, nullptr, nullptr, nullptr, need, r.stream), "scan size");
-    if (need > r.scan_bytes) {
-        cudaFree(r.d_scan);
-        r.d_scan = nullptr;
-        CU(cudaMalloc(&r.d_scan, need), "cudaMalloc scan");
-        r.scan_bytes = need;
+    if (out.compact) out.offsets[nq] = gbase;
+    double kmax = 0.0;
+    for (int di = 0; di < nd; ++di) {
+        Replica& r = g->reps[di];
+        CU(cudaSetDevice(r.device), "cudaSetDevice");
+        CU(cudaEventRecord(r.ev_stop, r.stream), "event");
+        CU(cudaStreamSynchronize(r.stream), "walk");
+        CU(cudaStreamSynchronize(r.copy), "copy");
+        CU(cudaStreamSynchronize(r.ends), "copy");
+        CU(cudaStreamSynchronize(r.d2h), "copy");
+        if ((rc = collect(r, st, 0))) return rc;
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.ev_start, r.ev_stop);
+        kmax = std::max(kmax, (double)ms);
+    }
+    CU(cudaSetDevice(g->reps[0].device), "cudaSetDevice");
+    CU(cudaEventRecord(wall1, g->reps[0].d2h), "event");
+    CU(cudaEventSynchronize(wall1), "event");
+    float wall = 0.f;
+    cudaEventElapsedTime(&wall, wall0, wall1);
+    cudaEventDestroy(wall0);
+    cudaEventDestroy(wall1);
+    if (st) {
+        st->kernel_ms = kmax;
+        st->total_ms = wall;
+        st->kernel_launches = launches;
     }
     return DW_OK;
 }
@@ -627,8 +831,8 @@ int dw_run_device(dw_graph_t g, int replica, const dw_model_desc* model, const u
     cudaStream_t s = stream ? (cudaStream_t)stream : r.stream;
     if ((rc = reset_run_state(r))) return rc;
     if (s != r.stream) {  // order the resets before work on the caller's stream
-        CU(cudaEventRecord(r.ev_walk[0], r.stream), "event");
-        CU(cudaStreamWaitEvent(s, r.ev_walk[0], 0), "event");
+        CU(cudaEventRecord(r.ev_reset, r.stream), "event");
+        CU(cudaStreamWaitEvent(s, r.ev_reset, 0), "event");
     }
     dwb::WalkParams p = make_params(r, model, opts);
     p.queries = d_queries;
@@ -674,95 +878,10 @@ int dw_run(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries, ui
     int rc;
     if ((rc = check_model(model)) || (rc = check_opts(opts))) return rc;
     if (nq && !queries) return fail(DW_EINVAL, "queries is NULL");
-    if (st) std::memset(st, 0, sizeof *st);
-    const int nd = (int)g->reps.size();
-    const ull stride = (ull)opts->walk_length + 1;
-    cudaEvent_t wall0 = nullptr, wall1 = nullptr;
-    CU(cudaSetDevice(g->reps[0].device), "cudaSetDevice");
-    CU(cudaEventCreate(&wall0), "event");
-    CU(cudaEventCreate(&wall1), "event");
-    CU(cudaEventRecord(wall0, g->reps[0].copy), "event");
-    ull launches = 0;
-    // contiguous walker blocks per device; batches per device overlap D2H of
-    // batch b with the walk of batch b+1
-    for (int di = 0; di < nd; ++di) {
-        Replica& r = g->reps[di];
-        const ull lo = nq * di / nd, hi = nq * (di + 1) / nd, n = hi - lo;
-        CU(cudaSetDevice(r.device), "cudaSetDevice");
-        if ((rc = ensure_scratch(r, std::max<ull>(n, 1), stride, paths != nullptr))) return rc;
-        if ((rc = reset_run_state(r))) return rc;
-        CU(cudaEventRecord(r.ev_walk[0], r.stream), "event");
-        CU(cudaStreamWaitEvent(r.copy, r.ev_walk[0], 0), "event");
-        const ull min_batch = 1ull << 20;
-        int nb = (int)std::min<ull>(8, std::max<ull>(1, n / min_batch));
-        if (n == 0) nb = 0;
-        bool started = false;
-        for (int b = 0; b < nb; ++b) {
-            const ull blo = n * b / nb, bhi = n * (b + 1) / nb, bn = bhi - blo;
-            CU(cudaMemcpyAsync(r.d_queries + blo, queries + lo + blo, bn * sizeof(uint32_t),
-                               cudaMemcpyHostToDevice, r.copy),
-               "H2D queries");
-            CU(cudaEventRecord(r.ev_h2d[b], r.copy), "event");
-            CU(cudaStreamWaitEvent(r.stream, r.ev_h2d[b], 0), "event");
-            dwb::WalkParams p = make_params(r, model, opts);
-            p.queries = r.d_queries + blo;
-            p.nq = bn;
-            p.qid_base = opts->qid_base + lo + blo;
-            p.paths = paths ? r.d_paths + blo * stride : nullptr;
-            p.lengths = r.d_lengths + blo;
-            p.next_walker = r.queues + b;
-            if (paths)
-                CU(cudaMemsetAsync(p.paths, 0xFF, bn * stride * sizeof(uint32_t), r.stream),
-                   "memset paths");
-            if (!started) {
-                CU(cudaEventRecord(r.ev_start, r.stream), "event");
-                started = true;
-            }
-            CU(dwb::launch_walk(model->kind, model->weighted != 0, opts->mode, p, r.num_sms,
-                                r.stream),
-               "walk");
-            ++launches;
-            // D2H on its own stream, so the next batch's H2D (r.copy) never
-            // queues behind this batch's walk
-            CU(cudaEventRecord(r.ev_walk[b], r.stream), "event");
-            CU(cudaStreamWaitEvent(r.d2h, r.ev_walk[b], 0), "event");
-            if (paths)
-                CU(cudaMemcpyAsync(paths + (lo + blo) * stride, p.paths,
-                                   bn * stride * sizeof(uint32_t), cudaMemcpyDeviceToHost, r.d2h),
-                   "D2H paths");
-            if (lengths)
-                CU(cudaMemcpyAsync(lengths + lo + blo, p.lengths, bn * sizeof(uint32_t),
-                                   cudaMemcpyDeviceToHost, r.d2h),
-                   "D2H lengths");
-        }
-        if (!started) CU(cudaEventRecord(r.ev_start, r.stream), "event");
-        CU(cudaEventRecord(r.ev_stop, r.stream), "event");
-    }
-    double kmax = 0.0;
-    for (int di = 0; di < nd; ++di) {
-        Replica& r = g->reps[di];
-        CU(cudaSetDevice(r.device), "cudaSetDevice");
-        CU(cudaStreamSynchronize(r.stream), "walk");
-        CU(cudaStreamSynchronize(r.copy), "copy");
-        CU(cudaStreamSynchronize(r.d2h), "copy");
-        if ((rc = collect(r, st, 0))) return rc;
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, r.ev_start, r.ev_stop);
-        kmax = std::max(kmax, (double)ms);
-    }
-    CU(cudaSetDevice(g->reps[0].device), "cudaSetDevice");
-    CU(cudaEventRecord(wall1, g->reps[0].d2h), "event");
-    CU(cudaEventSynchronize(wall1), "event");
-    float wall = 0.f;
-    cudaEventElapsedTime(&wall, wall0, wall1);
-    cudaEventDestroy(wall0);
-    cudaEventDestroy(wall1);
-    if (st) {
-        st->kernel_ms = kmax;
-        st->total_ms = wall;
-        st->kernel_launches = launches;
-    }
-    return DW_OK;
+    RunOut out;
+    out.paths = paths;
+    out.lengths = lengths;
+    return run_engine(g, model, queries, nq, opts, out, st);
 }
 
 int dw_run_compact(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries,
@@ -773,127 +892,12 @@ int dw_run_compact(dw_graph_t g, const dw_model_desc* model, const uint32_t* que
     if ((rc = check_model(model)) || (rc = check_opts(opts))) return rc;
     if (nq && !queries) return fail(DW_EINVAL, "queries is NULL");
     if (!offsets) return fail(DW_EINVAL, "offsets is NULL");
-    if (st) std::memset(st, 0, sizeof *st);
-    const int nd = (int)g->reps.size();
-    const ull stride = (ull)opts->walk_length + 1;
-    cudaEvent_t wall0 = nullptr, wall1 = nullptr;
-    CU(cudaSetDevice(g->reps[0].device), "cudaSetDevice");
-    CU(cudaEventCreate(&wall0), "event");
-    CU(cudaEventCreate(&wall1), "event");
-    CU(cudaEventRecord(wall0, g->reps[0].copy), "event");
-    ull launches = 0;
-    std::vector<int> nbs(nd, 0);
-    // phase 1: every batch's H2D, walk, offsets, compaction and end-offset read
-    // back are enqueued up front, so the devices never wait for the host
-    for (int di = 0; di < nd; ++di) {
-        Replica& r = g->reps[di];
-        const ull lo = nq * di / nd, hi = nq * (di + 1) / nd, n = hi - lo;
-        CU(cudaSetDevice(r.device), "cudaSetDevice");
-        if ((rc = ensure_scratch(r, std::max<ull>(n, 1), stride, true))) return rc;
-        if ((rc = ensure_compact_scratch(r, std::max<ull>(n, 1), stride))) return rc;
-        if ((rc = reset_run_state(r))) return rc;
-        CU(cudaMemsetAsync(r.d_base, 0, sizeof(ull), r.stream), "memset");
-        CU(cudaEventRecord(r.ev_walk[0], r.stream), "event");
-        CU(cudaStreamWaitEvent(r.copy, r.ev_walk[0], 0), "event");
-        const ull min_batch = 1ull << 20;
-        int nb = (int)std::min<ull>(8, std::max<ull>(1, n / min_batch));
-        if (n == 0) nb = 0;
-        nbs[di] = nb;
-        CU(cudaEventRecord(r.ev_start, r.stream), "event");
-        for (int b = 0; b < nb; ++b) {
-            const ull blo = n * b / nb, bhi = n * (b + 1) / nb, bn = bhi - blo;
-            CU(cudaMemcpyAsync(r.d_queries + blo, queries + lo + blo, bn * sizeof(uint32_t),
-                               cudaMemcpyHostToDevice, r.copy),
-               "H2D queries");
-            CU(cudaEventRecord(r.ev_h2d[b], r.copy), "event");
-            CU(cudaStreamWaitEvent(r.stream, r.ev_h2d[b], 0), "event");
-            dwb::WalkParams p = make_params(r, model, opts);
-            p.queries = r.d_queries + blo;
-            p.nq = bn;
-            p.qid_base = opts->qid_base + lo + blo;
-            p.paths = r.d_paths + blo * stride;  // no padding needed: only lengths are read
-            p.lengths = r.d_lengths + blo;
-            p.next_walker = r.queues + b;
-            CU(dwb::launch_walk(model->kind, model->weighted != 0, opts->mode, p, r.num_sms,
-                                r.stream),
-               "walk");
-            ++launches;
-            ull* offs = r.d_offs + blo + b;  // bn + 1 entries
-            size_t tb = r.scan_bytes;
-            CU(dwb::path_offsets(p.lengths, bn, offs, r.d_base, r.d_scan, tb, r.stream), "scan");
-            CU(dwb::compact_paths(p.paths, p.lengths, bn, stride, offs, 0, r.d_flat, r.stream),
-               "compact");
-            launches += 5;
-            CU(cudaEventRecord(r.ev_walk[b], r.stream), "event");
-            CU(cudaStreamWaitEvent(r.ends, r.ev_walk[b], 0), "event");
-            CU(cudaMemcpyAsync(r.h_ends + b, offs + bn, sizeof(ull), cudaMemcpyDeviceToHost,
-                               r.ends),
-               "D2H end");
-            CU(cudaEventRecord(r.ev_end[b], r.ends), "event");
-        }
-        CU(cudaEventRecord(r.ev_stop, r.stream), "event");
-    }
-    // phase 2: as each batch's end offset arrives, its compacted paths follow
-    // (overlapping the walks of the later batches)
-    ull gbase = 0;  // host offset of the current device's first path
-    for (int di = 0; di < nd; ++di) {
-        Replica& r = g->reps[di];
-        const ull lo = nq * di / nd, hi = nq * (di + 1) / nd, n = hi - lo;
-        CU(cudaSetDevice(r.device), "cudaSetDevice");
-        ull start = 0;
-        for (int b = 0; b < nbs[di]; ++b) {
-            const ull blo = n * b / nbs[di], bhi = n * (b + 1) / nbs[di], bn = bhi - blo;
-            CU(cudaEventSynchronize(r.ev_end[b]), "walk");
-            const ull end = r.h_ends[b];
-            if (gbase + end > flat_capacity) {
-                cudaStreamSynchronize(r.stream);
-                cudaStreamSynchronize(r.d2h);
-                return fail(DW_EINVAL, "flat path buffer too small: need more than %llu ids",
-                            (unsigned long long)(gbase + end));
-            }
-            if (end > start) {
-                if (!flat) return fail(DW_EINVAL, "flat is NULL");
-                CU(cudaMemcpyAsync(flat + gbase + start, r.d_flat + start,
-                                   (end - start) * sizeof(uint32_t), cudaMemcpyDeviceToHost,
-                                   r.d2h),
-                   "D2H paths");
-            }
-            CU(cudaMemcpyAsync(offsets + lo + blo, r.d_offs + blo + b, bn * sizeof(ull),
-                               cudaMemcpyDeviceToHost, r.d2h),
-               "D2H offsets");
-            start = end;
-        }
-        CU(cudaStreamSynchronize(r.stream), "walk");
-        CU(cudaStreamSynchronize(r.copy), "copy");
-        CU(cudaStreamSynchronize(r.ends), "copy");
-        CU(cudaStreamSynchronize(r.d2h), "copy");
-        if ((rc = collect(r, st, 0))) return rc;
-        if (gbase)
-            for (ull i = lo; i < hi; ++i) offsets[i] += gbase;
-        gbase += start;
-        (void)n;
-    }
-    offsets[nq] = gbase;
-    double kmax = 0.0;
-    for (int di = 0; di < nd; ++di) {
-        Replica& r = g->reps[di];
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, r.ev_start, r.ev_stop);
-        kmax = std::max(kmax, (double)ms);
-    }
-    CU(cudaSetDevice(g->reps[0].device), "cudaSetDevice");
-    CU(cudaEventRecord(wall1, g->reps[0].copy), "event");
-    CU(cudaEventSynchronize(wall1), "event");
-    float wall = 0.f;
-    cudaEventElapsedTime(&wall, wall0, wall1);
-    cudaEventDestroy(wall0);
-    cudaEventDestroy(wall1);
-    if (st) {
-        st->kernel_ms = kmax;
-        st->total_ms = wall;
-        st->kernel_launches = launches;
-    }
-    return DW_OK;
+    RunOut out;
+    out.compact = true;
+    out.offsets = reinterpret_cast<ull*>(offsets);
+    out.flat = flat;
+    out.flat_cap = flat_capacity;
+    return run_engine(g, model, queries, nq, opts, out, st);
 }
 
 int dw_host_alloc(size_t bytes, void** out) {

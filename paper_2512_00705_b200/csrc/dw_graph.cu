@@ -682,8 +682,8 @@ cudaError_t path_offsets(const uint32_t* lengths, ull n, ull* offs, ull* d_base,
 
 __global__ void compact_paths_kernel(const uint32_t* __restrict__ paths,
                                      const uint32_t* __restrict__ len, ull n, ull stride,
-                                     const ull* __restrict__ offs, ull flat_base,
-                                     uint32_t* __restrict__ flat) {
+                                     const ull* __restrict__ offs, uint32_t* __restrict__ flat) {
+    const ull flat_base = offs[0];
     const ull warp = (blockIdx.x * (ull)blockDim.x + threadIdx.x) >> 5;
     const ull nwarps = ((ull)gridDim.x * blockDim.x) >> 5;
     const uint32_t lane = threadIdx.x & 31;
@@ -696,10 +696,10 @@ __global__ void compact_paths_kernel(const uint32_t* __restrict__ paths,
 }
 
 cudaError_t compact_paths(const uint32_t* paths, const uint32_t* lengths, ull n, ull stride,
-                          const ull* offs, ull flat_base, uint32_t* flat, cudaStream_t s) {
+                          const ull* offs, uint32_t* flat, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     compact_paths_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(paths, lengths, n, stride, offs,
-                                                               flat_base, flat);
+                                                               flat);
     return cudaGetLastError();
 }
 

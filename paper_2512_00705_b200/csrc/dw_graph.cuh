@@ -57,9 +57,10 @@ unsigned long long host_derive_seed(unsigned long long seed, unsigned long long 
 cudaError_t path_offsets(const uint32_t* lengths, unsigned long long n, unsigned long long* offs,
                          unsigned long long* d_base, void* tmp, size_t& tmp_bytes,
                          cudaStream_t s);
-// flat[offs[i] - flat_base ..) = paths[i * stride .. + lengths[i]), one warp per walker
+// flat[offs[i] - offs[0] ..) = paths[i * stride .. + lengths[i]], one warp per
+// walker (flat holds one batch, offs its global offsets)
 cudaError_t compact_paths(const uint32_t* paths, const uint32_t* lengths, unsigned long long n,
                           unsigned long long stride, const unsigned long long* offs,
-                          unsigned long long flat_base, uint32_t* flat, cudaStream_t s);
+                          uint32_t* flat, cudaStream_t s);
 
 }  // namespace dwb
