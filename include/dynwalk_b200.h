@@ -123,6 +123,13 @@ int dw_device_count(int* n);
 int dw_graph_create(const dw_graph_desc* desc, const int* devices, int ndev, dw_graph_t* out);
 int dw_graph_generate_rmat(const dw_rmat_desc* desc, const int* devices, int ndev,
                            dw_graph_t* out);
+/* Loads a DWG1 binary CSR cache (dynwalk::save_binary, graph.cpp:243-256)
+ * straight onto the devices: the file streams through pinned staging buffers
+ * into device arrays, and Graph::build's invariants (graph.cpp:15-81: slices
+ * stable-sorted by target, referenced ids extend the vertex count) are
+ * re-established on the device instead of the host round-trip that
+ * load_binary makes (graph.cpp:258-291).  Error messages follow load_binary. */
+int dw_graph_load_dwg1(const char* path, const int* devices, int ndev, dw_graph_t* out);
 int dw_graph_destroy(dw_graph_t g);
 int dw_graph_info(dw_graph_t g, uint32_t* num_vertices, uint64_t* num_edges, int* has_labels,
                   uint32_t* max_degree);

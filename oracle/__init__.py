@@ -150,6 +150,9 @@ def ref() -> C.CDLL:
         R.ref_run_philox.argtypes = run_args
         R.ref_profile_ratio.restype = C.c_double
         R.ref_profile_ratio.argtypes = [vp, C.POINTER(OrcModel), C.c_uint64]
+        R.ref_save_binary.argtypes = [vp, C.c_char_p]
+        R.ref_load_binary.restype = vp
+        R.ref_load_binary.argtypes = [C.c_char_p]
         _ref = R
     return _ref
 
@@ -346,6 +349,16 @@ class RefGraph:
         if ref().ref_synth(self.ptr, k, low, high, alpha, seed) != 0:
             raise RuntimeError(ref().ref_last_error().decode())
         return self
+
+    def save_binary(self, path: str) -> None:
+        """dynwalk::save_binary (graph.cpp:243-256): the DWG1 CSR cache."""
+        if ref().ref_save_binary(self.ptr, path.encode()) != 0:
+            raise RuntimeError(ref().ref_last_error().decode())
+
+    @staticmethod
+    def load_binary(path: str) -> "RefGraph":
+        """dynwalk::load_binary (graph.cpp:258-291)."""
+        return RefGraph(ref().ref_load_binary(path.encode()))
 
     def arrays(self) -> dict:
         nv, ne, hl = C.c_uint32(), C.c_uint64(), C.c_int()

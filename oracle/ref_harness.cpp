@@ -242,6 +242,26 @@ int ref_synth(void* gp, int kind, double low, double high, double alpha, std::ui
     }
 }
 
+// DWG1 binary CSR cache (graph.cpp:217-300), for the device loader's tests
+int ref_save_binary(const void* gp, const char* path) {
+    try {
+        dw::save_binary(*static_cast<const dw::Graph*>(gp), path);
+        return 0;
+    } catch (const std::exception& ex) {
+        tl_error = ex.what();
+        return -1;
+    }
+}
+
+void* ref_load_binary(const char* path) {
+    try {
+        return new dw::Graph(dw::load_binary(path));
+    } catch (const std::exception& ex) {
+        tl_error = ex.what();
+        return nullptr;
+    }
+}
+
 void ref_graph_free(void* g) { delete static_cast<dw::Graph*>(g); }
 
 void ref_graph_dims(const void* gp, std::uint32_t* nv, std::uint64_t* ne, int* has_labels) {

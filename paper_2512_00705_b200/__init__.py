@@ -33,7 +33,7 @@ LIB = os.environ.get("DYNWALK_B200_LIB", os.path.join(HERE, "lib", "libdynwalk_b
 INVALID_VERTEX = 0xFFFFFFFF
 
 EXPORTED_SYMBOLS = (
-    "dw_abi_version", "dw_last_error", "dw_device_count", "dw_graph_create",
+    "dw_abi_version", "dw_last_error", "dw_device_count", "dw_graph_create", "dw_graph_load_dwg1",
     "dw_graph_generate_rmat", "dw_graph_destroy", "dw_graph_info", "dw_graph_download",
     "dw_calibrate", "dw_run", "dw_run_compact", "dw_run_device", "dw_run_device_sync",
     "dw_host_alloc",
@@ -124,6 +124,7 @@ def load_library() -> C.CDLL:
                                   C.POINTER(vp)]
     L.dw_graph_generate_rmat.argtypes = [C.POINTER(RmatDesc), C.POINTER(C.c_int), C.c_int,
                                          C.POINTER(vp)]
+    L.dw_graph_load_dwg1.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.c_int, C.POINTER(vp)]
     L.dw_graph_destroy.argtypes = [vp]
     L.dw_graph_info.argtypes = [vp, u32p, u64p, C.POINTER(C.c_int), u32p]
     L.dw_graph_download.argtypes = [vp, u64p, u32p, f32p, u16p, f64p, f64p]
@@ -245,6 +246,15 @@ class DeviceGraph:
         h = C.c_void_p()
         devs, nd = cls._devs(devices)
         _check(L.dw_graph_generate_rmat(C.byref(d), devs, nd, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def load_dwg1(cls, path: str, devices=None) -> "DeviceGraph":
+        """A DWG1 binary CSR cache (dynwalk::save_binary) streamed to the devices."""
+        L = load_library()
+        h = C.c_void_p()
+        devs, nd = cls._devs(devices)
+        _check(L.dw_graph_load_dwg1(os.fsencode(path), devs, nd, C.byref(h)))
         return cls(h)
 
     def info(self) -> dict:

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -675,6 +676,220 @@ int run_engine(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries
 }
 
 }  // namespace
+
+// ---- DWG1 binary CSR cache, streamed to the devices (graph.cpp:217-300) ----
+namespace {
+
+struct Dwg1Reader {
+    FILE* f = nullptr;
+    std::string path;
+    ~Dwg1Reader() {
+        if (f) std::fclose(f);
+    }
+    bool read(void* dst, size_t n) { return std::fread(dst, 1, n, f) == n; }
+};
+
+// Streams `count` elements of `elem` bytes from the file into every device
+// array in `dst` through two pinned staging buffers (file reads overlap the
+// H2D copies).  first/last receive the array's first and last 8-byte words
+// when non-null (the offsets array checks).
+int stream_array(Dwg1Reader& rd, dw_graph_s* g, const std::vector<void*>& dst, ull count,
+                 size_t elem, ull* first, ull* last) {
+    constexpr size_t kChunk = 64u << 20;
+    void* stage[2] = {nullptr, nullptr};
+    cudaEvent_t done[2][8] = {};
+    const int nd = (int)g->reps.size();
+    CU(cudaSetDevice(g->reps[0].device), "cudaSetDevice");
+    CU(cudaMallocHost(&stage[0], kChunk), "cudaMallocHost");
+    CU(cudaMallocHost(&stage[1], kChunk), "cudaMallocHost");
+    int rc = DW_OK;
+    const ull bytes = count * elem;
+    ull off = 0;
+    int k = 0;
+    bool used[2] = {false, false};
+    while (off < bytes && rc == DW_OK) {
+        const size_t n = (size_t)std::min<ull>(kChunk, bytes - off);
+        if (used[k])
+            for (int di = 0; di < nd && di < 8; ++di) cudaEventSynchronize(done[k][di]);
+        if (!rd.read(stage[k], n)) {
+            rc = fail(DW_EINVAL, "truncated binary graph file: %s", rd.path.c_str());
+            break;
+        }
+        if (first && off == 0 && n >= 8) std::memcpy(first, stage[k], 8);
+        if (last && off + n == bytes && n >= 8) std::memcpy(last, (char*)stage[k] + n - 8, 8);
+        for (int di = 0; di < nd && rc == DW_OK; ++di) {
+            Replica& r = g->reps[di];
+            if (cudaSetDevice(r.device) != cudaSuccess ||
+                cudaMemcpyAsync((char*)dst[di] + off, stage[k], n, cudaMemcpyHostToDevice,
+                                r.copy) != cudaSuccess) {
+                rc = fail(DW_ECUDA, "H2D of %s failed", rd.path.c_str());
+                break;
+            }
+            if (!done[k][di]) cudaEventCreateWithFlags(&done[k][di], cudaEventDisableTiming);
+            cudaEventRecord(done[k][di], r.copy);
+        }
+        used[k] = true;
+        off += n;
+        k ^= 1;
+    }
+    for (int j = 0; j < 2; ++j)
+        for (int di = 0; di < nd && di < 8; ++di)
+            if (done[j][di]) {
+                cudaEventSynchronize(done[j][di]);
+                cudaEventDestroy(done[j][di]);
+            }
+    cudaFreeHost(stage[0]);
+    cudaFreeHost(stage[1]);
+    return rc;
+}
+
+int read_count(Dwg1Reader& rd, ull* n) {
+    if (!rd.read(n, sizeof *n))
+        return fail(DW_EINVAL, "truncated binary graph file: %s", rd.path.c_str());
+    return DW_OK;
+}
+
+}  // namespace
+
+extern "C" int dw_graph_load_dwg1(const char* path, const int* devices, int ndev,
+                                  dw_graph_t* out) {
+    if (!out || !path) return fail(DW_EINVAL, "NULL argument");
+    *out = nullptr;
+    Dwg1Reader rd;
+    rd.path = path;
+    rd.f = std::fopen(path, "rb");
+    if (!rd.f) return fail(DW_EINVAL, "cannot open graph file: %s", path);
+    char magic[4];
+    if (!rd.read(magic, 4) || std::memcmp(magic, "DWG1", 4) != 0)
+        return fail(DW_EINVAL, "not a binary graph file: %s", path);
+    uint32_t version = 0;
+    if (!rd.read(&version, 4) || version != 1)
+        return fail(DW_EINVAL, "unsupported binary graph version %u", version);
+    uint8_t labels = 0;
+    if (!rd.read(&labels, 1)) return fail(DW_EINVAL, "truncated binary graph file: %s", path);
+    ull n_off = 0;
+    int rc;
+    if ((rc = read_count(rd, &n_off))) return rc;
+    if (n_off == 0) return fail(DW_EINVAL, "corrupt binary graph file: %s", path);
+    if (n_off - 1 >= DW_INVALID_VERTEX)
+        return fail(DW_EINVAL, "vertex id overflow: graph needs %llu vertices",
+                    (unsigned long long)(n_off - 1));
+    std::vector<int> devs;
+    if ((rc = resolve_devices(devices, ndev, devs))) return rc;
+    auto* g = new dw_graph_s;
+    std::unique_ptr<dw_graph_s, int (*)(dw_graph_t)> guard(g, dw_graph_destroy);
+    g->reps.resize(devs.size());
+    for (size_t i = 0; i < devs.size(); ++i)
+        if ((rc = init_replica(g->reps[i], devs[i]))) return rc;
+    const int nd = (int)devs.size();
+    std::vector<ull*> row(nd, nullptr);
+    std::vector<uint32_t*> col(nd, nullptr);
+    std::vector<float*> prop(nd, nullptr);
+    std::vector<uint16_t*> lab(nd, nullptr);
+    auto free_all = [&]() {
+        for (int di = 0; di < nd; ++di) {
+            cudaSetDevice(g->reps[di].device);
+            cudaFree(row[di]);
+            cudaFree(col[di]);
+            cudaFree(prop[di]);
+            if (!g->reps[di].g.labels) cudaFree(lab[di]);
+        }
+    };
+    std::vector<void*> dst(nd);
+    // offsets
+    for (int di = 0; di < nd; ++di) {
+        CU(cudaSetDevice(g->reps[di].device), "cudaSetDevice");
+        CU(cudaMalloc(&row[di], n_off * sizeof(ull)), "cudaMalloc offsets");
+        dst[di] = row[di];
+    }
+    ull front = 0, back = 0;
+    if ((rc = stream_array(rd, g, dst, n_off, sizeof(ull), &front, &back))) {
+        free_all();
+        return rc;
+    }
+    // targets, props, labels
+    ull ne = 0;
+    if ((rc = read_count(rd, &ne))) {
+        free_all();
+        return rc;
+    }
+    if (front != 0 || back != ne) {
+        free_all();
+        return fail(DW_EINVAL, "corrupt binary graph file: %s", path);
+    }
+    for (int di = 0; di < nd; ++di) {
+        CU(cudaSetDevice(g->reps[di].device), "cudaSetDevice");
+        CU(cudaMalloc(&col[di], std::max<ull>(ne, 1) * sizeof(uint32_t)), "cudaMalloc");
+        CU(cudaMalloc(&prop[di], std::max<ull>(ne, 1) * sizeof(float)), "cudaMalloc");
+        if (labels) CU(cudaMalloc(&lab[di], std::max<ull>(ne, 1) * sizeof(uint16_t)), "cudaMalloc");
+        dst[di] = col[di];
+    }
+    if ((rc = stream_array(rd, g, dst, ne, sizeof(uint32_t), nullptr, nullptr))) {
+        free_all();
+        return rc;
+    }
+    ull n = 0;
+    if ((rc = read_count(rd, &n))) {
+        free_all();
+        return rc;
+    }
+    if (n != ne) {
+        free_all();
+        return fail(DW_EINVAL, "corrupt binary graph file: %s", path);
+    }
+    for (int di = 0; di < nd; ++di) dst[di] = prop[di];
+    if ((rc = stream_array(rd, g, dst, ne, sizeof(float), nullptr, nullptr))) {
+        free_all();
+        return rc;
+    }
+    if (labels) {
+        if ((rc = read_count(rd, &n))) {
+            free_all();
+            return rc;
+        }
+        if (n != ne) {
+            free_all();
+            return fail(DW_EINVAL, "corrupt binary graph file: %s", path);
+        }
+        for (int di = 0; di < nd; ++di) dst[di] = lab[di];
+        if ((rc = stream_array(rd, g, dst, ne, sizeof(uint16_t), nullptr, nullptr))) {
+            free_all();
+            return rc;
+        }
+    }
+    // Graph::build's invariants, then the device layout (pack_graph)
+    uint32_t nv = 0;
+    for (int di = 0; di < nd; ++di) {
+        Replica& r = g->reps[di];
+        CU(cudaSetDevice(r.device), "cudaSetDevice");
+        CU(cudaStreamSynchronize(r.copy), "H2D");
+        nv = (uint32_t)(n_off - 1);
+        int status = 0;
+        CU(dwb::prepare_loaded_csr(&row[di], &nv, ne, col[di], prop[di], lab[di], &status,
+                                   r.stream),
+           "prepare csr");
+        if (status) {
+            free_all();
+            return fail(DW_EINVAL, status == 1 ? "edge property must be strictly positive and finite"
+                                   : status == 2 ? "vertex id overflow"
+                                                 : "unsorted adjacency slices above 2^31 edges are not supported");
+        }
+        r.g.nv = nv;
+        r.g.ne = ne;
+        CU(cudaMalloc(&r.g.nodes, std::max<uint32_t>(nv, 1) * sizeof(dwb::NodeRec)), "cudaMalloc nodes");
+        CU(cudaMalloc(&r.g.edges, std::max<ull>(ne, 1) * sizeof(dwb::EdgeRec)), "cudaMalloc edges");
+        r.g.labels = lab[di];  // owned by the replica from here on
+        CU(dwb::pack_graph(row[di], col[di], prop[di], nullptr, nullptr, r.g, r.stream), "pack_graph");
+        CU(cudaStreamSynchronize(r.stream), "pack");
+    }
+    free_all();
+    g->nv = nv;
+    g->ne = ne;
+    g->has_labels = labels != 0;
+    g->max_degree = g->reps[0].g.max_degree;
+    *out = guard.release();
+    return DW_OK;
+}
 
 extern "C" {
 

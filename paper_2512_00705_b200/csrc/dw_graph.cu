@@ -9,6 +9,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 
 #include <algorithm>
 #include <cstdlib>
@@ -701,6 +702,134 @@ cudaError_t compact_paths(const uint32_t* paths, const uint32_t* lengths, ull n,
     compact_paths_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(paths, lengths, n, stride, offs,
                                                                flat);
     return cudaGetLastError();
+}
+
+// ---- DWG1 loads ----------------------------------------------------------------
+__global__ void check_props_kernel(const float* __restrict__ prop, ull ne, int* __restrict__ bad) {
+    for (ull e = blockIdx.x * (ull)blockDim.x + threadIdx.x; e < ne;
+         e += (ull)gridDim.x * blockDim.x) {
+        const float p = prop[e];
+        if (!(p > 0.0f) || !isfinite(p)) atomicOr(bad, 1);
+    }
+}
+
+// one warp per row: any descending neighbour pair marks the graph unsorted
+__global__ void check_sorted_kernel(const ull* __restrict__ row, uint32_t nv,
+                                    const uint32_t* __restrict__ col, int* __restrict__ unsorted) {
+    const ull warp = (blockIdx.x * (ull)blockDim.x + threadIdx.x) >> 5;
+    const ull nwarps = ((ull)gridDim.x * blockDim.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    for (ull v = warp; v < nv; v += nwarps) {
+        const ull b = row[v], e = row[v + 1];
+        bool bad = false;
+        for (ull i = b + 1 + lane; i < e; i += 32) bad |= col[i - 1] > col[i];
+        if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(unsorted, 1);
+    }
+}
+
+__global__ void iota_kernel(uint32_t* __restrict__ out, ull n) {
+    for (ull i = blockIdx.x * (ull)blockDim.x + threadIdx.x; i < n;
+         i += (ull)gridDim.x * blockDim.x)
+        out[i] = (uint32_t)i;
+}
+
+template <class T>
+__global__ void gather_kernel(const T* __restrict__ in, const uint32_t* __restrict__ idx, ull n,
+                              T* __restrict__ out) {
+    for (ull i = blockIdx.x * (ull)blockDim.x + threadIdx.x; i < n;
+         i += (ull)gridDim.x * blockDim.x)
+        out[i] = in[idx[i]];
+}
+
+__global__ void fill_u64_kernel(ull* __restrict__ out, ull n, ull v) {
+    for (ull i = blockIdx.x * (ull)blockDim.x + threadIdx.x; i < n;
+         i += (ull)gridDim.x * blockDim.x)
+        out[i] = v;
+}
+
+cudaError_t prepare_loaded_csr(ull** d_row, uint32_t* nv, ull ne, uint32_t* d_col, float* d_prop,
+                               uint16_t* d_label, int* status, cudaStream_t s) {
+    *status = 0;
+    int* flags = nullptr;  // [0] bad prop, [1] unsorted
+    DW_TRY(cudaMallocAsync(&flags, 2 * sizeof(int), s));
+    DW_TRY(cudaMemsetAsync(flags, 0, 2 * sizeof(int), s));
+    uint32_t vmax = 0;
+    if (ne) {
+        // Graph::build: num_vertices = max(hint, max referenced id + 1)
+        uint32_t* d_max = nullptr;
+        DW_TRY(cudaMallocAsync(&d_max, sizeof(uint32_t), s));
+        size_t tb = 0;
+        DW_TRY(cub::DeviceReduce::Max(nullptr, tb, d_col, d_max, (int64_t)ne, s));
+        void* tmp = nullptr;
+        DW_TRY(cudaMallocAsync(&tmp, tb, s));
+        DW_TRY(cub::DeviceReduce::Max(tmp, tb, d_col, d_max, (int64_t)ne, s));
+        DW_TRY(cudaMemcpyAsync(&vmax, d_max, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        DW_TRY(cudaStreamSynchronize(s));
+        DW_TRY(cudaFreeAsync(tmp, s));
+        DW_TRY(cudaFreeAsync(d_max, s));
+        if ((ull)vmax + 1 >= 0xFFFFFFFFull) {
+            *status = 2;
+            return cudaFreeAsync(flags, s);
+        }
+        if (vmax + 1 > *nv) {  // extend: the new vertices have no out-edges
+            const uint32_t nv2 = vmax + 1;
+            ull* row2 = nullptr;
+            DW_TRY(cudaMallocAsync(&row2, (nv2 + 1ull) * sizeof(ull), s));
+            DW_TRY(cudaMemcpyAsync(row2, *d_row, (*nv + 1ull) * sizeof(ull),
+                                   cudaMemcpyDeviceToDevice, s));
+            fill_u64_kernel<<<grid_for(nv2 - *nv, 256), 256, 0, s>>>(row2 + *nv + 1, nv2 - *nv, ne);
+            DW_TRY(cudaFreeAsync(*d_row, s));
+            *d_row = row2;
+            *nv = nv2;
+        }
+        check_props_kernel<<<grid_for(ne, 256), 256, 0, s>>>(d_prop, ne, flags);
+        check_sorted_kernel<<<grid_for((ull)*nv * 32, 256), 256, 0, s>>>(*d_row, *nv, d_col,
+                                                                         flags + 1);
+        DW_TRY(cudaGetLastError());
+    }
+    int h[2] = {0, 0};
+    DW_TRY(cudaMemcpyAsync(h, flags, sizeof h, cudaMemcpyDeviceToHost, s));
+    DW_TRY(cudaStreamSynchronize(s));
+    DW_TRY(cudaFreeAsync(flags, s));
+    if (h[0]) {
+        *status = 1;
+        return cudaSuccess;
+    }
+    if (h[1]) {  // Graph::build's per-slice stable sort by target
+        if (ne > 0x7FFFFFFFull) {
+            *status = 3;
+            return cudaSuccess;
+        }
+        uint32_t *idx = nullptr, *idx2 = nullptr, *col2 = nullptr;
+        DW_TRY(cudaMallocAsync(&idx, ne * sizeof(uint32_t), s));
+        DW_TRY(cudaMallocAsync(&idx2, ne * sizeof(uint32_t), s));
+        DW_TRY(cudaMallocAsync(&col2, ne * sizeof(uint32_t), s));
+        iota_kernel<<<grid_for(ne, 256), 256, 0, s>>>(idx, ne);
+        size_t tb = 0;
+        DW_TRY(cub::DeviceSegmentedSort::StableSortPairs(nullptr, tb, d_col, col2, idx, idx2,
+                                                         (int)ne, (int)*nv, *d_row, *d_row + 1,
+                                                         s));
+        void* tmp = nullptr;
+        DW_TRY(cudaMallocAsync(&tmp, tb, s));
+        DW_TRY(cub::DeviceSegmentedSort::StableSortPairs(tmp, tb, d_col, col2, idx, idx2, (int)ne,
+                                                         (int)*nv, *d_row, *d_row + 1, s));
+        DW_TRY(cudaMemcpyAsync(d_col, col2, ne * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+        float* p2 = reinterpret_cast<float*>(col2);  // reuse as the props scratch
+        gather_kernel<float><<<grid_for(ne, 256), 256, 0, s>>>(d_prop, idx2, ne, p2);
+        DW_TRY(cudaMemcpyAsync(d_prop, p2, ne * sizeof(float), cudaMemcpyDeviceToDevice, s));
+        if (d_label) {
+            uint16_t* l2 = reinterpret_cast<uint16_t*>(idx);
+            gather_kernel<uint16_t><<<grid_for(ne, 256), 256, 0, s>>>(d_label, idx2, ne, l2);
+            DW_TRY(cudaMemcpyAsync(d_label, l2, ne * sizeof(uint16_t), cudaMemcpyDeviceToDevice,
+                                   s));
+        }
+        DW_TRY(cudaGetLastError());
+        DW_TRY(cudaFreeAsync(tmp, s));
+        DW_TRY(cudaFreeAsync(idx, s));
+        DW_TRY(cudaFreeAsync(idx2, s));
+        DW_TRY(cudaFreeAsync(col2, s));
+    }
+    return cudaStreamSynchronize(s);
 }
 
 }  // namespace dwb

@@ -49,6 +49,17 @@ cudaError_t calibrate_ratio(const DeviceGraphBuffers& g, int model_kind, bool we
 
 unsigned long long host_derive_seed(unsigned long long seed, unsigned long long stream);
 
+// ---- DWG1 loads (dw_graph_load_dwg1) ----------------------------------------
+// Re-establishes Graph::build's invariants (graph.cpp:15-81) on a CSR that was
+// streamed to the device as stored in the file: vertices referenced beyond the
+// offsets array extend the vertex count (*d_row is reallocated), unsorted
+// slices are stable-sorted by target (props and labels follow), and every prop
+// must be strictly positive and finite (graph.hpp:51).  *status: 0 ok,
+// 1 bad prop, 2 vertex id overflow, 3 unsorted slices above 2^31 edges.
+cudaError_t prepare_loaded_csr(unsigned long long** d_row, uint32_t* nv, unsigned long long ne,
+                               uint32_t* d_col, float* d_prop, uint16_t* d_label, int* status,
+                               cudaStream_t s);
+
 // ---- path compaction (dw_run_compact) ----------------------------------------
 // offs[0..n] = base + exclusive prefix sum of lengths[0..n) (offs[n] = base +
 // total); base is read from *d_base (device scalar) and *d_base is advanced by

@@ -80,3 +80,22 @@ int main(void){printf("%zu %zu %zu %zu %zu %zu\n", sizeof(dw_graph_desc), sizeof
     want = [C.sizeof(dw.GraphDesc), C.sizeof(dw.RmatDesc), C.sizeof(dw.ModelDesc),
             C.sizeof(dw.RunOptsC), C.sizeof(dw.RunStatsC), C.sizeof(C.c_void_p)]
     assert sizes == want
+
+
+def test_dwg1_header_errors(dw, tmp_path):
+    """dw_graph_load_dwg1 rejects bad files with load_binary's messages
+    (graph.cpp:258-276) before touching a device."""
+    with pytest.raises(dw.DynwalkError, match="cannot open graph file"):
+        dw.DeviceGraph.load_dwg1(str(tmp_path / "missing.dwg1"))
+    bad = tmp_path / "bad.dwg1"
+    bad.write_bytes(b"XXXX" + b"\0" * 32)
+    with pytest.raises(dw.DynwalkError, match="not a binary graph file"):
+        dw.DeviceGraph.load_dwg1(str(bad))
+    v2 = tmp_path / "v2.dwg1"
+    v2.write_bytes(b"DWG1" + (2).to_bytes(4, "little") + b"\0" + b"\0" * 8)
+    with pytest.raises(dw.DynwalkError, match="unsupported binary graph version 2"):
+        dw.DeviceGraph.load_dwg1(str(v2))
+    empty = tmp_path / "empty.dwg1"
+    empty.write_bytes(b"DWG1" + (1).to_bytes(4, "little") + b"\0" + (0).to_bytes(8, "little"))
+    with pytest.raises(dw.DynwalkError, match="corrupt binary graph file"):
+        dw.DeviceGraph.load_dwg1(str(empty))

@@ -283,3 +283,56 @@ def test_compact_output_matches_padded(dw, orc):
     assert np.array_equal(flat, r.paths[mask])
     for k in ("steps", "trials", "rng_draws", "dead_ends", "query_errors"):
         assert st[k] == r.stats[k], k
+
+
+def _write_dwg1(path, row, col, prop, label=None):
+    """DWG1 as dynwalk::save_binary writes it (graph.cpp:243-256)."""
+    with open(path, "wb") as f:
+        f.write(b"DWG1" + (1).to_bytes(4, "little") + bytes([1 if label is not None else 0]))
+        for a in (np.asarray(row, np.uint64), np.asarray(col, np.uint32),
+                  np.asarray(prop, np.float32)) + (() if label is None
+                                                   else (np.asarray(label, np.uint16),)):
+            f.write(len(a).to_bytes(8, "little"))
+            f.write(a.tobytes())
+
+
+def test_dwg1_loader_matches_reference(dw, orc, tmp_path):
+    """A DWG1 file streamed to the device equals dynwalk::load_binary's graph,
+    including unsorted slices (stable-sorted on load) and targets beyond the
+    offsets array (they extend the vertex count), and walks equal the oracle."""
+    og = build_oracle_graph(GRAPHS["ba300_labels"])
+    a = og.arrays()
+    p1 = str(tmp_path / "g1.dwg1")
+    _write_dwg1(p1, a["row"], a["col"], a["prop"], a["label"])
+    dg = dw.DeviceGraph.load_dwg1(p1)
+    b = dg.download()
+    for k in ("row", "col", "prop", "label", "nmax", "nsum"):
+        assert np.array_equal(a[k], b[k]), k
+    q = np.arange(og.nv, dtype=np.uint32)
+    r_dev, r_orc = run_both(dw, orc, og, dg, dict(kind="node2vec", a=0.5, b=2.0), q, "adaptive",
+                            30, 1.2)
+    assert_same(r_dev, r_orc)
+    # unsorted slices with duplicates, and a target id past the offsets array
+    rng = np.random.default_rng(9)
+    row = np.array([0, 4, 4, 9, 12], np.uint64)
+    col = np.array([3, 1, 3, 0, 2, 7, 2, 2, 1, 0, 5, 0], np.uint32)
+    prop = rng.uniform(1.0, 5.0, len(col)).astype(np.float32)
+    lab = rng.integers(0, 4, len(col)).astype(np.uint16)
+    p2 = str(tmp_path / "g2.dwg1")
+    _write_dwg1(p2, row, col, prop, lab)
+    b = dw.DeviceGraph.load_dwg1(p2).download()
+    if orc.ref_available():
+        ref = orc.RefGraph.load_binary(p2).arrays()
+        for k in ("row", "col", "prop", "label", "nmax", "nsum"):
+            assert np.array_equal(ref[k], b[k]), k
+    assert len(b["row"]) == 9  # vertex 7 referenced: 8 vertices
+    assert list(b["col"][0:4]) == [0, 1, 3, 3] and b["prop"][2] == prop[0] and b["prop"][3] == prop[2]
+    # truncated and corrupt files
+    p3 = str(tmp_path / "trunc.dwg1")
+    open(p3, "wb").write(open(p1, "rb").read()[:-10])
+    with pytest.raises(dw.DynwalkError, match="truncated binary graph file"):
+        dw.DeviceGraph.load_dwg1(p3)
+    p4 = str(tmp_path / "corrupt.dwg1")
+    _write_dwg1(p4, np.array([0, 3], np.uint64), col[:2], prop[:2])
+    with pytest.raises(dw.DynwalkError, match="corrupt binary graph file"):
+        dw.DeviceGraph.load_dwg1(p4)
