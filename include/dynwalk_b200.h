@@ -158,6 +158,15 @@ int dw_run_compact(dw_graph_t g, const dw_model_desc* model, const uint32_t* que
                    uint64_t nq, const dw_run_opts* opts, uint64_t* offsets, uint32_t* flat,
                    uint64_t flat_capacity, dw_run_stats* stats);
 
+/* run_queries + write_paths (runtime.cpp:280-291) as one streamed sink: the
+ * paths are formatted as text on the device ("id id ... id\n" per query in
+ * query order, "\n" for an empty path) and written batch by batch while the
+ * next batches walk; device and host memory stay bounded for any nq.  The
+ * file is byte-identical to write_paths on the same paths. */
+int dw_run_write_paths(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries,
+                       uint64_t nq, const dw_run_opts* opts, const char* path,
+                       dw_run_stats* stats);
+
 /* Device-resident variant on replica `replica`: d_queries / d_paths /
  * d_lengths are device pointers on that device (d_paths, d_lengths may be
  * NULL), `stream` a cudaStream_t (NULL = the replica's stream).  Enqueues and

@@ -35,7 +35,8 @@ INVALID_VERTEX = 0xFFFFFFFF
 EXPORTED_SYMBOLS = (
     "dw_abi_version", "dw_last_error", "dw_device_count", "dw_graph_create", "dw_graph_load_dwg1",
     "dw_graph_generate_rmat", "dw_graph_destroy", "dw_graph_info", "dw_graph_download",
-    "dw_calibrate", "dw_run", "dw_run_compact", "dw_run_device", "dw_run_device_sync",
+    "dw_calibrate", "dw_run", "dw_run_compact", "dw_run_write_paths", "dw_run_device",
+    "dw_run_device_sync",
     "dw_host_alloc",
     "dw_host_free",
 )
@@ -134,6 +135,8 @@ def load_library() -> C.CDLL:
     L.dw_run_compact.argtypes = [vp, C.POINTER(ModelDesc), u32p, C.c_uint64,
                                  C.POINTER(RunOptsC), u64p, u32p, C.c_uint64,
                                  C.POINTER(RunStatsC)]
+    L.dw_run_write_paths.argtypes = [vp, C.POINTER(ModelDesc), u32p, C.c_uint64,
+                                     C.POINTER(RunOptsC), C.c_char_p, C.POINTER(RunStatsC)]
     L.dw_run_device.argtypes = [vp, C.c_int, C.POINTER(ModelDesc), vp, C.c_uint64,
                                 C.POINTER(RunOptsC), vp, vp, vp]
     L.dw_run_device_sync.argtypes = [vp, C.c_int, C.POINTER(RunStatsC)]
@@ -318,3 +321,16 @@ def run_queries_compact(g: DeviceGraph, model: Model, queries, opts: RunOptions)
     _check(L.dw_run_compact(g.h, C.byref(m), _p(q, u32p), len(q), C.byref(o),
                             _p(offsets, u64p), _p(flat, u32p), cap, C.byref(st)))
     return offsets, flat[:int(offsets[-1])], st.as_dict()
+
+
+def run_write_paths(g: DeviceGraph, model: Model, queries, opts: RunOptions, path: str) -> dict:
+    """run_queries + write_paths (runtime.cpp:280-291) streamed to `path`, the
+    text formatted on the device; returns the RunStats counters."""
+    L = load_library()
+    q = np.ascontiguousarray(queries, np.uint32)
+    st = RunStatsC()
+    m = model.c()
+    o = opts.c()
+    _check(L.dw_run_write_paths(g.h, C.byref(m), _p(q, u32p), len(q), C.byref(o),
+                                os.fsencode(path), C.byref(st)))
+    return st.as_dict()

@@ -68,12 +68,13 @@ struct Replica {
         uint32_t* len = nullptr;    // [cap] path lengths
         uint32_t* paths = nullptr;  // [cap][stride] padded paths
         uint32_t* flat = nullptr;   // [cap * stride] compacted paths (compact runs)
-        ull* offs = nullptr;        // [cap + 1] global path offsets (compact runs)
+        ull* offs = nullptr;        // [cap + 1] global path (or text byte) offsets
+        char* txt = nullptr;        // [cap * stride * 11] path text (text runs)
         cudaEvent_t h2d = nullptr, walk = nullptr, end = nullptr, d2h = nullptr;
     };
     Slot slots[kRingSlots];
     ull slot_cap = 0, slot_stride = 0;
-    bool slot_flat = false;
+    bool slot_flat = false, slot_txt = false;
     ull* d_base = nullptr;      // running offset of the batches already compacted
     void* d_scan = nullptr;
     size_t scan_bytes = 0;
@@ -156,6 +157,7 @@ void free_replica(Replica& r) {
         cudaFree(sl.paths);
         cudaFree(sl.flat);
         cudaFree(sl.offs);
+        cudaFree(sl.txt);
         for (cudaEvent_t e : {sl.h2d, sl.walk, sl.end, sl.d2h})
             if (e) cudaEventDestroy(e);
     }
@@ -430,20 +432,27 @@ int collect(Replica& r, dw_run_stats* st, ull qbase) {
     return DW_OK;
 }
 
-int ensure_ring(Replica& r, ull cap, ull stride, bool flat) {
-    if (cap <= r.slot_cap && stride <= r.slot_stride && (!flat || r.slot_flat)) return DW_OK;
+constexpr ull kTextBytesPerId = 11;  // up to 10 digits + separator
+
+int ensure_ring(Replica& r, ull cap, ull stride, bool flat, bool txt) {
+    if (cap <= r.slot_cap && stride <= r.slot_stride && (!flat || r.slot_flat) &&
+        (!txt || r.slot_txt))
+        return DW_OK;
     CU(cudaDeviceSynchronize(), "ring");
     cap = std::max(cap, r.slot_cap);
     stride = std::max(stride, r.slot_stride);
-    flat = flat || r.slot_flat;
+    flat = flat || txt || r.slot_flat;
+    txt = txt || r.slot_txt;
     for (auto& sl : r.slots) {
         cudaFree(sl.q);
         cudaFree(sl.len);
         cudaFree(sl.paths);
         cudaFree(sl.flat);
         cudaFree(sl.offs);
+        cudaFree(sl.txt);
         sl.q = sl.len = sl.paths = sl.flat = nullptr;
         sl.offs = nullptr;
+        sl.txt = nullptr;
         CU(cudaMalloc(&sl.q, cap * sizeof(uint32_t)), "cudaMalloc queries");
         CU(cudaMalloc(&sl.len, cap * sizeof(uint32_t)), "cudaMalloc lengths");
         CU(cudaMalloc(&sl.paths, cap * stride * sizeof(uint32_t)), "cudaMalloc paths");
@@ -451,6 +460,7 @@ int ensure_ring(Replica& r, ull cap, ull stride, bool flat) {
             CU(cudaMalloc(&sl.flat, cap * stride * sizeof(uint32_t)), "cudaMalloc flat paths");
             CU(cudaMalloc(&sl.offs, (cap + 1) * sizeof(ull)), "cudaMalloc offsets");
         }
+        if (txt) CU(cudaMalloc(&sl.txt, cap * stride * kTextBytesPerId), "cudaMalloc text");
     }
     if (flat) {
         size_t need = 0;
@@ -465,6 +475,7 @@ int ensure_ring(Replica& r, ull cap, ull stride, bool flat) {
     r.slot_cap = cap;
     r.slot_stride = stride;
     r.slot_flat = flat;
+    r.slot_txt = txt;
     return DW_OK;
 }
 
@@ -472,6 +483,9 @@ int ensure_ring(Replica& r, ull cap, ull stride, bool flat) {
 // flattened RunResult.paths layout (dw_run_compact).
 struct RunOut {
     bool compact = false;
+    FILE* text = nullptr;       // write_paths sink (dw_run_write_paths)
+    const char* text_path = nullptr;
+    char* h_txt = nullptr;      // pinned staging for one batch of text
     uint32_t* paths = nullptr;
     uint32_t* lengths = nullptr;
     ull* offsets = nullptr;
@@ -511,10 +525,10 @@ int run_engine(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries
         Dev& d = dv[di];
         d.lo = nq * di / nd;
         d.n = nq * (di + 1) / nd - d.lo;
-        d.bs = batch_size(d.n);
+        d.bs = out.text ? std::min<ull>(batch_size(d.n), 1ull << 20) : batch_size(d.n);
         d.nb = d.n ? (d.n + d.bs - 1) / d.bs : 0;
         CU(cudaSetDevice(r.device), "cudaSetDevice");
-        if ((rc = ensure_ring(r, d.bs, stride, out.compact))) return rc;
+        if ((rc = ensure_ring(r, d.bs, stride, out.compact, out.text != nullptr))) return rc;
         if ((rc = reset_run_state(r))) return rc;
         CU(cudaMemsetAsync(r.d_base, 0, sizeof(ull), r.stream), "memset");
         CU(cudaEventRecord(r.ev_reset, r.stream), "event");
@@ -540,11 +554,11 @@ int run_engine(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries
         p.queries = sl.q;
         p.nq = bn;
         p.qid_base = opts->qid_base + d.lo + blo;
-        p.paths = (out.compact || out.paths) ? sl.paths : nullptr;
+        p.paths = (out.compact || out.text || out.paths) ? sl.paths : nullptr;
         p.lengths = sl.len;
         p.next_walker = r.queues + (b % kRingSlots);
         CU(cudaMemsetAsync(p.next_walker, 0, sizeof(ull), r.stream), "memset");
-        if (p.paths && !out.compact)  // compaction copies only the written ids
+        if (p.paths && !out.compact && !out.text)  // compaction copies only the written ids
             CU(cudaMemsetAsync(p.paths, 0xFF, bn * stride * sizeof(uint32_t), r.stream),
                "memset paths");
         CU(dwb::launch_walk(model->kind, model->weighted != 0, opts->mode, p, r.num_sms,
@@ -557,9 +571,17 @@ int run_engine(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries
             CU(dwb::compact_paths(sl.paths, sl.len, bn, stride, sl.offs, sl.flat, r.stream),
                "compact");
             launches += 5;
+        } else if (out.text) {  // write_paths bytes, formatted on the device
+            uint32_t* bytes = sl.flat;
+            size_t tb = r.scan_bytes;
+            CU(dwb::path_text_bytes(sl.paths, sl.len, bn, stride, bytes, r.stream), "text");
+            CU(dwb::path_offsets(bytes, bn, sl.offs, r.d_base, r.d_scan, tb, r.stream), "scan");
+            CU(dwb::path_text_write(sl.paths, sl.len, bn, stride, sl.offs, sl.txt, r.stream),
+               "text");
+            launches += 6;
         }
         CU(cudaEventRecord(sl.walk, r.stream), "event");
-        if (out.compact) {
+        if (out.compact || out.text) {
             CU(cudaStreamWaitEvent(r.ends, sl.walk, 0), "event");
             CU(cudaMemcpyAsync(r.h_ends + (b % kRingSlots), sl.offs + bn, sizeof(ull),
                                cudaMemcpyDeviceToHost, r.ends),
@@ -585,11 +607,24 @@ int run_engine(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries
         Replica& r = g->reps[di];
         Dev& d = dv[di];
         Replica::Slot& sl = r.slots[b % kRingSlots];
-        if (!out.compact) return DW_OK;  // the D2H was enqueued with the walk
+        if (!out.compact && !out.text) return DW_OK;  // the D2H was enqueued with the walk
         const ull blo = b * d.bs, bn = std::min(d.bs, d.n - blo);
         CU(cudaSetDevice(r.device), "cudaSetDevice");
         CU(cudaEventSynchronize(sl.end), "walk");
         const ull end = r.h_ends[b % kRingSlots];
+        if (out.text) {  // the batch's text follows the previous batches in the file
+            const ull nb_bytes = end - d.end;
+            if (nb_bytes) {
+                CU(cudaMemcpyAsync(out.h_txt, sl.txt, nb_bytes, cudaMemcpyDeviceToHost, r.d2h),
+                   "D2H text");
+                CU(cudaStreamSynchronize(r.d2h), "D2H text");
+                if (std::fwrite(out.h_txt, 1, nb_bytes, out.text) != nb_bytes)
+                    return fail(DW_EINVAL, "write failed: %s", out.text_path);
+            }
+            CU(cudaEventRecord(sl.d2h, r.d2h), "event");
+            d.end = end;
+            return DW_OK;
+        }
         if (gbase + end > out.flat_cap) {
             cudaDeviceSynchronize();
             return fail(DW_EINVAL, "flat path buffer too small: need more than %llu ids",
@@ -617,17 +652,18 @@ int run_engine(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries
                 ++d.eb;
                 busy = true;
             }
-            const bool may_drain = !out.compact || di == drain_dev;
+            const bool ordered = out.compact || out.text;
+            const bool may_drain = !ordered || di == drain_dev;
             if (d.db < d.eb && may_drain) {
                 if ((rc = drain(di, d.db))) return rc;
                 ++d.db;
                 busy = true;
             }
-            if (out.compact && di == drain_dev && d.db == d.nb) {
+            if (ordered && di == drain_dev && d.db == d.nb) {
                 // device finished: its offsets become global, the next device drains
                 Replica& r = g->reps[di];
                 CU(cudaSetDevice(r.device), "cudaSetDevice");
-                if (gbase) {
+                if (gbase && out.compact) {
                     CU(cudaStreamSynchronize(r.d2h), "copy");
                     for (ull i = d.lo; i < d.lo + d.n; ++i) out.offsets[i] += gbase;
                 }
@@ -635,14 +671,14 @@ int run_engine(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries
                 ++drain_dev;
                 busy = true;
             }
-            if (!out.compact && d.db < d.eb) {
+            if (!ordered && d.db < d.eb) {
                 d.db = d.eb;  // padded runs need no host step per batch
                 busy = true;
             }
         }
         bool done = true;
         for (const Dev& d : dv) done = done && d.db == d.nb;
-        if (done && (!out.compact || drain_dev == nd)) break;
+        if (done && (!(out.compact || out.text) || drain_dev == nd)) break;
         if (!busy) return fail(DW_ECUDA, "run pipeline stalled");
     }
     if (out.compact) out.offsets[nq] = gbase;
@@ -1097,6 +1133,32 @@ int dw_run(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries, ui
     out.paths = paths;
     out.lengths = lengths;
     return run_engine(g, model, queries, nq, opts, out, st);
+}
+
+int dw_run_write_paths(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries,
+                       uint64_t nq, const dw_run_opts* opts, const char* path,
+                       dw_run_stats* st) {
+    if (!g) return fail(DW_EINVAL, "graph handle is NULL");
+    int rc;
+    if ((rc = check_model(model)) || (rc = check_opts(opts))) return rc;
+    if (nq && !queries) return fail(DW_EINVAL, "queries is NULL");
+    if (!path) return fail(DW_EINVAL, "path is NULL");
+    FILE* f = std::fopen(path, "wb");
+    if (!f) return fail(DW_EINVAL, "cannot open paths output file: %s", path);
+    RunOut out;
+    out.text = f;
+    out.text_path = path;
+    const ull stride = (ull)opts->walk_length + 1;
+    const ull cap = std::min<ull>(batch_size(std::max<ull>(nq, 1)), 1ull << 20);
+    CU(cudaSetDevice(g->reps[0].device), "cudaSetDevice");
+    if (cudaMallocHost(&out.h_txt, cap * stride * kTextBytesPerId) != cudaSuccess) {
+        std::fclose(f);
+        return fail(DW_ECUDA, "cudaMallocHost text staging");
+    }
+    rc = run_engine(g, model, queries, nq, opts, out, st);
+    cudaFreeHost(out.h_txt);
+    if (std::fclose(f) != 0 && rc == DW_OK) rc = fail(DW_EINVAL, "write failed: %s", path);
+    return rc;
 }
 
 int dw_run_compact(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries,

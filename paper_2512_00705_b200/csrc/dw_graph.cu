@@ -832,4 +832,84 @@ cudaError_t prepare_loaded_csr(ull** d_row, uint32_t* nv, ull ne, uint32_t* d_co
     return cudaStreamSynchronize(s);
 }
 
+// ---- text sink ------------------------------------------------------------------
+__device__ __forceinline__ uint32_t dec_digits(uint32_t x) {
+    uint32_t d = 1;
+    while (x >= 10) {
+        x /= 10;
+        ++d;
+    }
+    return d;
+}
+
+// one warp per path
+__global__ void text_bytes_kernel(const uint32_t* __restrict__ paths,
+                                  const uint32_t* __restrict__ len, ull n, ull stride,
+                                  uint32_t* __restrict__ bytes) {
+    const ull warp = (blockIdx.x * (ull)blockDim.x + threadIdx.x) >> 5;
+    const ull nwarps = ((ull)gridDim.x * blockDim.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    for (ull i = warp; i < n; i += nwarps) {
+        const uint32_t l = len[i];
+        uint32_t b = 0;
+        for (uint32_t j = lane; j < l; j += 32) b += dec_digits(paths[i * stride + j]) + 1;
+        b = __reduce_add_sync(0xFFFFFFFFu, b);
+        if (lane == 0) bytes[i] = l ? b : 1;  // separators + newline == l; "\n" when empty
+    }
+}
+
+__global__ void text_write_kernel(const uint32_t* __restrict__ paths,
+                                  const uint32_t* __restrict__ len, ull n, ull stride,
+                                  const ull* __restrict__ toffs, char* __restrict__ text) {
+    const ull warp = (blockIdx.x * (ull)blockDim.x + threadIdx.x) >> 5;
+    const ull nwarps = ((ull)gridDim.x * blockDim.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    const ull base0 = toffs[0];
+    for (ull i = warp; i < n; i += nwarps) {
+        const uint32_t l = len[i];
+        char* out = text + (toffs[i] - base0);
+        if (l == 0) {
+            if (lane == 0) out[0] = '\n';
+            continue;
+        }
+        uint32_t pos = 0;  // running byte position of the chunk's first id
+        for (uint32_t j0 = 0; j0 < l; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            const uint32_t x = j < l ? paths[i * stride + j] : 0u;
+            const uint32_t w = j < l ? dec_digits(x) + 1 : 0u;  // digits + separator
+            uint32_t incl = w;  // inclusive warp scan of widths
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (lane >= (uint32_t)o) incl += t;
+            }
+            if (j < l) {
+                char* q = out + pos + incl - w;
+                uint32_t y = x;
+                for (int k = (int)w - 2; k >= 0; --k) {
+                    q[k] = (char)('0' + y % 10);
+                    y /= 10;
+                }
+                q[w - 1] = j + 1 == l ? '\n' : ' ';
+            }
+            pos += __shfl_sync(0xFFFFFFFFu, incl, 31);
+        }
+    }
+}
+
+cudaError_t path_text_bytes(const uint32_t* paths, const uint32_t* lengths, ull n, ull stride,
+                            uint32_t* bytes, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    text_bytes_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(paths, lengths, n, stride, bytes);
+    return cudaGetLastError();
+}
+
+cudaError_t path_text_write(const uint32_t* paths, const uint32_t* lengths, ull n, ull stride,
+                            const ull* toffs, char* text, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    text_write_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(paths, lengths, n, stride, toffs,
+                                                            text);
+    return cudaGetLastError();
+}
+
 }  // namespace dwb

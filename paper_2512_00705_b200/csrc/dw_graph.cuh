@@ -49,6 +49,15 @@ cudaError_t calibrate_ratio(const DeviceGraphBuffers& g, int model_kind, bool we
 
 unsigned long long host_derive_seed(unsigned long long seed, unsigned long long stream);
 
+// ---- text sink (dw_run_write_paths): write_paths' format, runtime.cpp:280-291
+// bytes[i] = text size of path i ("id id ... id\n", "\n" when empty)
+cudaError_t path_text_bytes(const uint32_t* paths, const uint32_t* lengths, unsigned long long n,
+                            unsigned long long stride, uint32_t* bytes, cudaStream_t s);
+// text[toffs[i] - toffs[0] ..) = path i as text
+cudaError_t path_text_write(const uint32_t* paths, const uint32_t* lengths, unsigned long long n,
+                            unsigned long long stride, const unsigned long long* toffs, char* text,
+                            cudaStream_t s);
+
 // ---- DWG1 loads (dw_graph_load_dwg1) ----------------------------------------
 // Re-establishes Graph::build's invariants (graph.cpp:15-81) on a CSR that was
 // streamed to the device as stored in the file: vertices referenced beyond the

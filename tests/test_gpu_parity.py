@@ -336,3 +336,24 @@ def test_dwg1_loader_matches_reference(dw, orc, tmp_path):
     _write_dwg1(p4, np.array([0, 3], np.uint64), col[:2], prop[:2])
     with pytest.raises(dw.DynwalkError, match="corrupt binary graph file"):
         dw.DeviceGraph.load_dwg1(p4)
+
+
+def test_write_paths_text_sink(dw, orc, tmp_path):
+    """dw_run_write_paths is byte-identical to write_paths (runtime.cpp:280-291)
+    applied to the same paths, over many ring batches and with query errors."""
+    og = orc.Graph.rmat(13, 16, 31).synth_philox("uniform", 1.0, 5.0, seed=32)
+    dg = to_device(dw, og)
+    rng = np.random.default_rng(8)
+    q = rng.integers(0, og.nv + 40, 2_300_000).astype(np.uint32)
+    opts = dw.RunOptions(mode="adaptive", walk_length=12, seed=9, edge_cost_ratio=1.3)
+    model = dw.Model(a=0.5, b=2.0)
+    out = str(tmp_path / "paths.txt")
+    st = dw.run_write_paths(dg, model, q, opts, out)
+    r = dw.run_queries(dg, model, q, opts)
+    lines = [" ".join(map(str, r.paths[i, :r.lengths[i]])) for i in range(len(q))]
+    want = ("\n".join(lines) + "\n").encode()
+    got = open(out, "rb").read()
+    assert got == want
+    assert st["steps"] == r.stats["steps"] and st["query_errors"] == r.stats["query_errors"] > 0
+    with pytest.raises(dw.DynwalkError, match="cannot open paths output file"):
+        dw.run_write_paths(dg, model, q[:10], opts, str(tmp_path / "no" / "such" / "dir.txt"))
