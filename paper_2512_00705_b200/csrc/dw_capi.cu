@@ -323,6 +323,11 @@ dwb::ModelParams model_params(const dw_model_desc* m) {
     case DW_MODEL_STATIC: mp.pos_weights = 1u; break;  // props are validated > 0
     default: mp.pos_weights = 0u;
     }
+    // one-multiply weight-sum screen (dw_models.cuh wsum_approx)
+    mp.screen = (m->kind == DW_MODEL_NODE2VEC && m->a > 0.0 && m->b > 0.0) ? 1u : 0u;
+    mp.wsum_coef = (1.0 / m->a + 1.0 + 1.0 / m->b) / 3.0;
+    if (const char* env = std::getenv("DW_SCREEN"))
+        if (env[0] == '0') mp.screen = 0u;
     if (const char* env = std::getenv("DW_POW2"))
         if (env[0] == '0') mp.pow2_a = mp.pow2_b = 0u;
     if (const char* env = std::getenv("DW_D1"))

@@ -62,6 +62,8 @@ struct ModelParams {
     uint32_t fast_div, shortcut;
     uint32_t pow2_a, pow2_b;  // a / b is a power of two: x / a == x * inv_a exactly
     uint32_t pos_weights;     // every weight is > 0 and finite by construction
+    uint32_t screen;          // wsum_approx is within 1e-15 (relative) of wsum
+    double wsum_coef;         // node2vec: RN((1/a + 1 + 1/b) / 3)
     uint32_t schema_len;
     uint16_t schema[128];
 };
@@ -87,6 +89,7 @@ __device__ __forceinline__ double dmax3(double x, double y, double z) {
 // StaticWalk (models.hpp:33-51)
 template <bool W>
 struct StaticModel {
+    static constexpr bool kScreen = false;
     static constexpr bool kUsesLabels = false;
     static constexpr bool kSecondOrder = false;
     static constexpr bool kBoundable = true;
@@ -97,6 +100,7 @@ struct StaticModel {
     __device__ double wsum(const Step& s) const { return W ? s.hsum : (double)s.degree; }
     __device__ double nonreturn_max(const Step& s) const { return bound(s); }
     __device__ void prepare(const Step&) const {}
+    __device__ double wsum_approx(const Step& s) const { return wsum(s); }
     __device__ WeightCase weight(const Step&, uint32_t, float h, uint16_t) const {
         return exact(W ? (double)h : 1.0);
     }
@@ -109,11 +113,18 @@ struct Node2VecModel {
     static constexpr bool kSecondOrder = true;
     static constexpr bool kBoundable = true;
     static constexpr bool kAggregates = W;  // PER_STEP bound reads node max/sum
-    double a, b, ia, ib, i3;
+    static constexpr bool kScreen = true;
+    double a, b, ia, ib, i3, wc;
     bool pa, pb;
     __device__ explicit Node2VecModel(const ModelParams& p)
-        : a(p.a), b(p.b), ia(p.inv_a), ib(p.inv_b), i3(p.inv_3), pa(p.pow2_a != 0),
-          pb(p.pow2_b != 0) {}
+        : a(p.a), b(p.b), ia(p.inv_a), ib(p.inv_b), i3(p.inv_3), wc(p.wsum_coef),
+          pa(p.pow2_a != 0), pb(p.pow2_b != 0) {}
+    // x * (1/a + 1 + 1/b) / 3 in one multiply: relative error <= ~8 ulp
+    // against wsum() when a, b > 0 (all terms positive), so the decision
+    // ratio * bound < wsum only needs wsum() within a 1e-12 band
+    __device__ double wsum_approx(const Step& s) const {
+        return W ? s.hsum * wc : wc * (double)s.degree;
+    }
     __device__ double da(double x) const { return pa ? __dmul_rn(x, ia) : ddiv(x, a, ia); }
     __device__ double db(double x) const { return pb ? __dmul_rn(x, ib) : ddiv(x, b, ib); }
     __device__ uint32_t max_steps() const { return 0xFFFFFFFFu; }
@@ -147,6 +158,7 @@ struct Node2VecModel {
 // MetaPath (models.hpp:95-118)
 template <bool W>
 struct MetaPathModel {
+    static constexpr bool kScreen = false;
     static constexpr bool kUsesLabels = true;
     static constexpr bool kSecondOrder = false;
     static constexpr bool kBoundable = true;
@@ -161,6 +173,7 @@ struct MetaPathModel {
     }
     __device__ double nonreturn_max(const Step& s) const { return bound(s); }
     __device__ void prepare(const Step&) const {}
+    __device__ double wsum_approx(const Step& s) const { return wsum(s); }
     __device__ WeightCase weight(const Step& s, uint32_t, float hf, uint16_t label) const {
         const double h = W ? (double)hf : 1.0;
         return exact(label == p->schema[s.step] ? h : 0.0);
@@ -172,6 +185,7 @@ struct MetaPathModel {
 // (prepare) with the reference's operation order; weight() then multiplies.
 template <bool W>
 struct Pr2Model {
+    static constexpr bool kScreen = false;
     static constexpr bool kUsesLabels = false;
     static constexpr bool kSecondOrder = true;
     static constexpr bool kBoundable = true;
@@ -213,6 +227,7 @@ struct Pr2Model {
     __device__ void prepare(const Step& s) {
         if (s.has_prev()) factors(s, c_plain, c_boost, maxd);
     }
+    __device__ double wsum_approx(const Step& s) const { return wsum(s); }
     __device__ WeightCase weight(const Step& s, uint32_t u, float hf, uint16_t) const {
         const double h = W ? (double)hf : 1.0;  // models.hpp:128-138
         if (!s.has_prev()) return exact(h);

@@ -119,8 +119,16 @@ __device__ __forceinline__ void cnt_add(ull* c, ull v) { atomicAdd(c, v); }
 
 // ---- K2 (warp form): one row, 32 lanes; all lanes call with equal args ----
 // Returns the chosen target and its relative edge index (for the fat record).
+#ifndef DW_COOP_INLINE
+#define DW_COOP_INLINE 1
+#endif
+#if DW_COOP_INLINE
+#define DW_COOP_ATTR __forceinline__
+#else
+#define DW_COOP_ATTR __noinline__
+#endif
 template <class M, bool NOJUMP>
-__device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const WalkerKey key,
+__device__ DW_COOP_ATTR int ervs_warp(const ModelParams& mp, Step S, const WalkerKey key,
                                       const DevGraph& g, ull begin, uint32_t phoff, ull idx0,
                                       uint32_t* next, uint32_t* nidx, ull* draws) {
     M m(mp);
@@ -732,7 +740,17 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                 if (MODE == kAdaptive) {
                     if (M::kBoundable) {
                         bound = model.bound(S);
-                        erjs = p.ratio * bound < model.wsum(S);
+                        const double T = p.ratio * bound;
+                        if (M::kScreen && p.mp.screen) {
+                            // decide on the one-multiply estimate unless T
+                            // falls in its error band (then the exact sum)
+                            const double Wa = model.wsum_approx(S);
+                            erjs = T < Wa * (1.0 - 1e-12)
+                                       ? true
+                                       : (T > Wa * (1.0 + 1e-12) ? false : T < model.wsum(S));
+                        } else {
+                            erjs = T < model.wsum(S);
+                        }
                     }
                 } else if (MODE == kForceErjs) {  // runtime.cpp:109-129
                     erjs = M::kBoundable;
