@@ -308,20 +308,37 @@ __device__ __forceinline__ ull warp_sum(ull v) {
 }
 
 // ---- K3: adaptive walker loop (runtime.cpp:59-153 + 192-247) --------------
+// Per-lane landing slots and counters, structure-of-arrays ([.][kThreads]) so
+// a warp's 16 B accesses are conflict-free.
+struct WalkSmem {
+    uint4 rec[kRing][3][kThreads];   // landing: fat record / slim pair in [0]
+    double y[kRing][kThreads];       // y of the queued trials
+    uint32_t t[kRing][kThreads];     // trial index of the queued trials
+    uint4 mb[2][kThreads];           // node record / hash bucket / eRVS pair
+    uint32_t lab[kRing + 1][kThreads];  // label words (slim MetaPath)
+    uint32_t lc[LC_NUM][kThreads];   // per-lane RunStats counters (spill at 2^31)
+    ull cnt[kCNum];
+    uint32_t hist[66];
+    ull lct[LC_NUM];                 // block totals of the lane counters
+};
+
 template <class M, int MODE, bool FAT>
 __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
     walk_kernel(const __grid_constant__ WalkParams p) {
     constexpr bool kNoJump = MODE == kErvsNoJump;
     constexpr bool kSO = M::kSecondOrder;
-    __shared__ uint4 s_rec[kRing][3][kThreads];  // landing: fat record / slim pair in [0]
-    __shared__ double s_y[kRing][kThreads];      // y of the queued trials
-    __shared__ uint32_t s_t[kRing][kThreads];    // trial index of the queued trials
-    __shared__ uint4 s_mb[2][kThreads];          // node record / hash bucket / eRVS pair
-    __shared__ uint32_t s_lab[kRing + 1][kThreads];  // label words (slim MetaPath)
-    __shared__ uint32_t s_lc[LC_NUM][kThreads];  // per-lane RunStats counters (spill at 2^31)
-    __shared__ ull s_cnt[kCNum];
-    __shared__ uint32_t s_hist[66];
-    __shared__ ull s_lct[LC_NUM];  // block totals of the lane counters
+    // dynamic shared memory (WalkSmem): may exceed the 48 KB static limit
+    extern __shared__ __align__(16) unsigned char dsm[];
+    WalkSmem& sm = *reinterpret_cast<WalkSmem*>(dsm);
+    auto& s_rec = sm.rec;
+    auto& s_y = sm.y;
+    auto& s_t = sm.t;
+    auto& s_mb = sm.mb;
+    auto& s_lab = sm.lab;
+    auto& s_lc = sm.lc;
+    auto& s_cnt = sm.cnt;
+    auto& s_hist = sm.hist;
+    auto& s_lct = sm.lct;
     const int tid = threadIdx.x;
     for (int i = tid; i < kCNum; i += blockDim.x) s_cnt[i] = 0;
     if (tid < LC_NUM) s_lct[tid] = 0;
@@ -926,14 +943,22 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
 template <class M, int MODE, bool FAT>
 static cudaError_t launch_t(const WalkParams& p, int num_sms, cudaStream_t stream) {
     int per_sm = 0;
+    const size_t smem = sizeof(WalkSmem);
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        cudaError_t ea = cudaFuncSetAttribute(walk_kernel<M, MODE, FAT>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (ea != cudaSuccess) return ea;
+        attr_set = true;
+    }
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, walk_kernel<M, MODE, FAT>, kThreads, 0);
+        &per_sm, walk_kernel<M, MODE, FAT>, kThreads, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
     unsigned long long blocks = (unsigned long long)num_sms * per_sm;
     const unsigned long long need = (p.nq + kThreads - 1) / kThreads;
     if (need < blocks) blocks = need ? need : 1;
-    walk_kernel<M, MODE, FAT><<<(unsigned)blocks, kThreads, 0, stream>>>(p);
+    walk_kernel<M, MODE, FAT><<<(unsigned)blocks, kThreads, smem, stream>>>(p);
     return cudaGetLastError();
 }
 
