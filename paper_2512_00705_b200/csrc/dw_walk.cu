@@ -315,8 +315,12 @@ struct WalkSmem {
     double y[kRing][kThreads];       // y of the queued trials
     uint32_t t[kRing][kThreads];     // trial index of the queued trials
     uint4 mb[2][kThreads];           // node record / hash bucket / eRVS pair
-    uint32_t lab[kRing + 1][kThreads];  // label words (slim MetaPath)
     uint32_t lc[LC_NUM][kThreads];   // per-lane RunStats counters (spill at 2^31)
+    // walker state read once per step or per iteration, kept out of registers
+    // so the loop fits the register budget of 3-4 CTAs/SM without spills
+    uint32_t cur[kThreads], phoff[kThreads], plg[kThreads], hoff[kThreads], cap[kThreads],
+        twlo[kThreads], twcnt[kThreads], nret[kThreads];
+    double bound[kThreads], mnr[kThreads];
     ull cnt[kCNum];
     uint32_t hist[66];
     ull lct[LC_NUM];                 // block totals of the lane counters
@@ -334,7 +338,6 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
     auto& s_y = sm.y;
     auto& s_t = sm.t;
     auto& s_mb = sm.mb;
-    auto& s_lab = sm.lab;
     auto& s_lc = sm.lc;
     auto& s_cnt = sm.cnt;
     auto& s_hist = sm.hist;
@@ -368,15 +371,25 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
     bool drained = false;  // warp-uniform
     ull qi = 0;
     // walker state
-    uint32_t cur = kInvalid, prev = kInvalid, pdeg = 0, phoff = 0, plg = 0, step = 0, deg = 0,
-             hoff = 0;
+    uint32_t prev = kInvalid, pdeg = 0, step = 0, deg = 0;
+    uint32_t& cur = sm.cur[tid];
+    uint32_t& phoff = sm.phoff[tid];  // hash set of prev
+    uint32_t& plg = sm.plg[tid];      // log2 buckets of prev's hash set
+    uint32_t& hoff = sm.hoff[tid];    // hash set of cur
+    cur = kInvalid;
+    phoff = plg = hoff = 0;
     ull begin = 0;
     // eRJS state
-    double bound = 0.0, mnr = 0.0;       // bound, non-return maximum
-    uint32_t cap = 0;                    // trial cap of the step (samplers.hpp:157)
-    uint32_t tn = 0, rh = 0, rc = 0;     // next trial, ring head, ring count
-    uint32_t tw_lo = 0, tw_cnt = 0;      // return-edge range in N(cur)
-    uint32_t mb = 0, nret = 0, sel = 0;  // parked bucket (bit 31: parked), return trials, pair bits
+    double& bound = sm.bound[tid];    // rejection bound
+    double& mnr = sm.mnr[tid];        // non-return maximum
+    uint32_t& cap = sm.cap[tid];      // trial cap of the step (samplers.hpp:157)
+    uint32_t& tw_lo = sm.twlo[tid];   // return-edge range in N(cur)
+    uint32_t& tw_cnt = sm.twcnt[tid];
+    uint32_t& nret = sm.nret[tid];    // judged return-edge trials
+    bound = mnr = 0.0;
+    cap = tw_lo = tw_cnt = nret = 0;
+    uint32_t tn = 0, rh = 0, rc = 0;  // next trial, ring head, ring count
+    uint32_t mb = 0, sel = 0;         // parked bucket (bit 31: parked), pair bits
     // per-walker register counters, folded into the lane counters at walk end
     uint32_t c_trials = 0, c_alg4 = 0;   // eRJS trials, algorithmic bytes / 4
     // eRVS state lives in the lane's spare ring slot (the ring is idle while a
@@ -519,7 +532,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                     } else {
                         sel = (sel & ~(1u << k)) | ((uint32_t)(e & 1) << k);
                         cp16(&s_rec[k][0][tid], pair_of(g.edges, e));
-                        if (M::kUsesLabels && g.labels) cp4(&s_lab[k][tid], g.labels + (e & ~1ull));
+                        if (M::kUsesLabels && g.labels) cp4(&s_rec[k][1][tid], g.labels + (e & ~1ull));
                     }
                     ++rc;
                 }
@@ -546,7 +559,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
             const ull e = begin + tn;
             sel = (uint32_t)(e & 1);
             cp16(&s_mb[0][tid], pair_of(g.edges, e));
-            if (M::kUsesLabels && g.labels) cp4(&s_lab[kRing][tid], g.labels + (e & ~1ull));
+            if (M::kUsesLabels && g.labels) cp4(&s_mb[1][tid], g.labels + (e & ~1ull));
         }
         // ---- B
         cp_wait_all();
@@ -588,7 +601,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                     if (FAT)
                         lab = (uint16_t)(v0.w >> 8);
                     else
-                        lab = (uint16_t)(odd ? (s_lab[rh][tid] >> 16) : s_lab[rh][tid]);
+                        lab = (uint16_t)(odd ? (s_rec[rh][1][tid].x >> 16) : s_rec[rh][1][tid].x);
                 }
                 const double y = s_y[rh][tid];
                 const WeightCase wc = model.weight(S, u, h, lab);
@@ -656,8 +669,8 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
             }
             if (r >= 0) {
                 const uint16_t lab = (M::kUsesLabels && phase == P_VREC)
-                                         ? (uint16_t)(sel ? (s_lab[kRing][tid] >> 16)
-                                                          : s_lab[kRing][tid])
+                                         ? (uint16_t)(sel ? (s_mb[1][tid].x >> 16)
+                                                          : s_mb[1][tid].x)
                                          : 0;
                 const WeightCase wc = model.weight(mkstep(0.0, 0.0), u, h, lab);
                 if (kSO && r == 2 && wc.needs_member) {
