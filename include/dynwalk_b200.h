@@ -69,7 +69,16 @@ typedef struct dw_graph_s* dw_graph_t;
 
 /* Builtin models (models.hpp:33-164); a user model compiles in as a device
  * functor (paper_2512_00705_b200/csrc/dw_models.cuh). */
-enum { DW_MODEL_STATIC = 0, DW_MODEL_NODE2VEC = 1, DW_MODEL_METAPATH = 2, DW_MODEL_PR2 = 3 };
+enum {
+    DW_MODEL_STATIC = 0,
+    DW_MODEL_NODE2VEC = 1,
+    DW_MODEL_METAPATH = 2,
+    DW_MODEL_PR2 = 3,
+    DW_MODEL_CUSTOM = 4 /* a DslWalk compiled with dw_model_compile */
+};
+
+/* A DslWalk model (models.hpp:170-198) compiled into the walk kernel. */
+typedef struct dw_custom_model_s* dw_custom_model_t;
 
 typedef struct dw_model_desc {
     int kind;
@@ -78,6 +87,7 @@ typedef struct dw_model_desc {
     double gamma;             /* second-order pagerank mixing */
     const uint16_t* schema;   /* metapath label schema */
     uint32_t schema_len;      /* <= DW_MAX_SCHEMA */
+    dw_custom_model_t custom; /* DW_MODEL_CUSTOM only */
 } dw_model_desc;
 #define DW_MAX_SCHEMA 128
 
@@ -141,6 +151,20 @@ int dw_graph_download(dw_graph_t g, uint64_t* row_offsets, uint32_t* col_indices
 /* Replaces profile_edge_cost_ratio (cost_model.hpp:39-40, cost_model.cpp:37-126):
  * random-neighbour vs sequential weight evaluation timed on device 0. */
 int dw_calibrate(dw_graph_t g, const dw_model_desc* model, uint64_t seed, double* ratio);
+
+/* Compiles a DslWalk weight function into the walk kernel.
+ * `source` is the CUDA model functor that paper_2512_00705_b200/host/
+ * dsl_codegen.hpp generates from the reference's parsed program and analysis
+ * (dsl::Program, dsl::AnalysisResult); NVRTC compiles it against the kernel
+ * template this library was built from, for every sampler mode.  max_steps is
+ * DslWalk::max_steps(); flags bit 0: the estimators read per-node label
+ * MAX/SUM (built on the device at first use).  No interpretation happens on
+ * the device.  Errors: DW_EUNSUPPORTED without NVRTC, DW_EMODEL with the
+ * compiler log. */
+#define DW_CUSTOM_LABEL_AGGREGATES 1u
+int dw_model_compile(const char* source, uint32_t max_steps, uint32_t flags,
+                     dw_custom_model_t* out);
+int dw_model_free(dw_custom_model_t model);
 
 /* Replaces run_queries (runtime.hpp:85-86, runtime.cpp:192-247).
  * queries: host [nq].  paths: host [nq][walk_length+1], DW_INVALID_VERTEX

@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(HERE, "liboracle.so")
 REF_PATH = os.path.join(HERE, "_ref", "libdynwalk_ref.so")
 INVALID = 0xFFFFFFFF
 
-MODEL_KINDS = {"static": 0, "node2vec": 1, "metapath": 2, "pr2": 3}
+MODEL_KINDS = {"static": 0, "node2vec": 1, "metapath": 2, "pr2": 3, "dsl": 4}
 MODES = {"adaptive": 0, "force-ervs": 1, "force-erjs": 2, "ervs-nojump": 3}
 RNG = {"mt19937": 0, "philox": 1}
 
@@ -150,6 +150,9 @@ def ref() -> C.CDLL:
         R.ref_run_philox.argtypes = run_args
         R.ref_profile_ratio.restype = C.c_double
         R.ref_profile_ratio.argtypes = [vp, C.POINTER(OrcModel), C.c_uint64]
+        R.ref_set_dsl_source.argtypes = [C.c_char_p]
+        R.ref_dsl_codegen.restype = C.c_long
+        R.ref_dsl_codegen.argtypes = [C.c_char_p, C.c_char_p, C.c_uint64, u32p, u32p]
         R.ref_save_binary.argtypes = [vp, C.c_char_p]
         R.ref_load_binary.restype = vp
         R.ref_load_binary.argtypes = [C.c_char_p]
@@ -400,3 +403,22 @@ def ref_profile_ratio(g: RefGraph, model: Model, seed: int) -> float:
     if r < 0:
         raise RuntimeError(ref().ref_last_error().decode())
     return r
+
+
+def dsl_codegen(source: str):
+    """The product's DSL -> CUDA model codegen (paper_2512_00705_b200/host/
+    dsl_codegen.hpp) applied to the reference's parse/analysis of `source`.
+    Returns (cuda_source, max_steps, flags)."""
+    R = ref()
+    ms, fl = C.c_uint32(), C.c_uint32()
+    n = R.ref_dsl_codegen(source.encode(), None, 0, C.byref(ms), C.byref(fl))
+    if n < 0:
+        raise RuntimeError(R.ref_last_error().decode())
+    buf = C.create_string_buffer(n + 1)
+    R.ref_dsl_codegen(source.encode(), buf, n + 1, C.byref(ms), C.byref(fl))
+    return buf.value.decode(), ms.value, fl.value
+
+
+def set_dsl_source(source: str) -> None:
+    """The program ModelDesc kind 4 ("dsl") parses on the reference side."""
+    ref().ref_set_dsl_source(source.encode())

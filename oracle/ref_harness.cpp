@@ -31,6 +31,9 @@
 #include "dynwalk/models.hpp"
 #include "dynwalk/rng.hpp"
 #include "dynwalk/runtime.hpp"
+#include "dynwalk/dsl/parser.hpp"
+#include "dynwalk/dsl/analyzer.hpp"
+#include "dsl_codegen.hpp"
 #include "dynwalk/samplers.hpp"
 
 #include "oracle.h"
@@ -40,6 +43,9 @@ namespace dw = dynwalk;
 namespace {
 
 thread_local std::string tl_error;
+// DSL program for ModelDesc kind 4 (ref_set_dsl_source); parsed with the
+// reference's own parser, so the reference's DslWalk is what runs
+std::string tl_dsl_source;  // set before a run (tests are single-threaded)
 
 struct ModelDesc {
     int kind;
@@ -49,7 +55,11 @@ struct ModelDesc {
     std::uint32_t schema_len;
 };
 
-dw::AnyModel make_model(const ModelDesc& d) {
+dw::AnyModel make_model(const ModelDesc& d, const dw::Graph* g = nullptr) {
+    if (d.kind == 4) {
+        if (!g) throw dw::Error("DSL model needs the graph");
+        return dw::DslWalk(dw::dsl::parse(tl_dsl_source, "<test>"), *g);
+    }
     switch (d.kind) {
     case 0: return dw::StaticWalk{d.weighted != 0};
     case 1: return dw::Node2Vec{d.a, d.b, d.weighted != 0};
@@ -242,6 +252,35 @@ int ref_synth(void* gp, int kind, double low, double high, double alpha, std::ui
     }
 }
 
+void ref_set_dsl_source(const char* src) { tl_dsl_source = src ? src : ""; }
+
+// The product's DSL -> CUDA codegen (host/dsl_codegen.hpp) applied to the
+// reference's parse and analysis of `src`; test infrastructure for the GPU
+// DSL parity tests.  Returns the source length (or -1), writes at most cap
+// bytes.
+long ref_dsl_codegen(const char* src, char* out, std::uint64_t cap, std::uint32_t* max_steps,
+                     std::uint32_t* flags) {
+    try {
+        const dw::dsl::Program prog = dw::dsl::parse(src, "<test>");
+        const dw::dsl::AnalysisResult res = dw::dsl::analyze(prog);
+        std::uint32_t ms = 0xFFFFFFFFu;
+        for (const auto& [name, value] : prog.scalar_params)
+            if (name == "walk_length") ms = static_cast<std::uint32_t>(value);
+        const auto code = dw::gpu::detail::dsl_codegen(prog, res, ms);
+        if (max_steps) *max_steps = ms;
+        if (flags) *flags = code.label_aggregates ? 1u : 0u;
+        if (out && cap) {
+            const std::size_t n = std::min<std::size_t>(code.source.size(), cap - 1);
+            std::memcpy(out, code.source.data(), n);
+            out[n] = '\0';
+        }
+        return static_cast<long>(code.source.size());
+    } catch (const std::exception& ex) {
+        tl_error = ex.what();
+        return -1;
+    }
+}
+
 // DWG1 binary CSR cache (graph.cpp:217-300), for the device loader's tests
 int ref_save_binary(const void* gp, const char* path) {
     try {
@@ -308,7 +347,7 @@ int ref_run(const void* gp, const ModelDesc* md, int mode, std::uint32_t walk_le
         opts.erjs_cap_per_degree = cap;
         dw::CostModelParams params;
         params.edge_cost_ratio = ratio;
-        const dw::AnyModel model = make_model(*md);
+        const dw::AnyModel model = make_model(*md, g);
         const dw::RunResult rr =
             dw::run_queries(*g, model, params, std::span<const dw::VertexId>(queries, nq), opts);
         emit_paths(rr.paths, walk_length + 1, paths, lengths);
@@ -345,7 +384,7 @@ int ref_run_philox(const void* gp, const ModelDesc* md, int mode, std::uint32_t 
         const auto* g = static_cast<const dw::Graph*>(gp);
         dw::CostModelParams params;
         params.edge_cost_ratio = ratio;
-        const dw::AnyModel model = make_model(*md);
+        const dw::AnyModel model = make_model(*md, g);
         std::vector<std::vector<dw::VertexId>> out(nq);
         orc_stats total;
         std::memset(&total, 0, sizeof total);
@@ -400,8 +439,8 @@ double ref_profile_ratio(const void* gp, const ModelDesc* md, std::uint64_t seed
     try {
         dw::ProfileConfig cfg;
         cfg.seed = seed;
-        return dw::profile_edge_cost_ratio(*static_cast<const dw::Graph*>(gp), make_model(*md),
-                                           cfg)
+        const auto* g = static_cast<const dw::Graph*>(gp);
+        return dw::profile_edge_cost_ratio(*g, make_model(*md, g), cfg)
             .edge_cost_ratio;
     } catch (const std::exception& ex) {
         tl_error = ex.what();

@@ -14,6 +14,7 @@
 #include <sstream>
 #include <string>
 
+#include "dynwalk/dsl/parser.hpp"
 #include "dynwalk/gen.hpp"
 #include "dynwalk/rng.hpp"
 #include "dynwalk_gpu.hpp"
@@ -66,7 +67,10 @@ int main(int argc, char** argv) {
         for (std::string t; std::getline(ss, t, ',');) mp.schema.push_back(std::stoul(t));
         std::string name = get("model", "node2vec");
         if (get("weighted", "1") == "0") name += "-unw";
-        const dw::AnyModel model = dw::make_builtin_model(name, mp);
+        // dsl=<file>: a DslWalk parsed by the reference, compiled for the GPU by the shim
+        const dw::AnyModel model = get("dsl", "") != ""
+                                       ? dw::AnyModel(dw::DslWalk(dw::dsl::parse_file(get("dsl", "")), g))
+                                       : dw::make_builtin_model(name, mp);
 
         dw::RunOptions opts;
         opts.mode = dw::parse_sampler_mode(get("mode", "adaptive"));

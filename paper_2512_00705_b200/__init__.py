@@ -35,13 +35,14 @@ INVALID_VERTEX = 0xFFFFFFFF
 EXPORTED_SYMBOLS = (
     "dw_abi_version", "dw_last_error", "dw_device_count", "dw_graph_create", "dw_graph_load_dwg1",
     "dw_graph_generate_rmat", "dw_graph_destroy", "dw_graph_info", "dw_graph_download",
-    "dw_calibrate", "dw_run", "dw_run_compact", "dw_run_write_paths", "dw_run_device",
+    "dw_calibrate", "dw_model_compile", "dw_model_free", "dw_run", "dw_run_compact",
+    "dw_run_write_paths", "dw_run_device",
     "dw_run_device_sync",
     "dw_host_alloc",
     "dw_host_free",
 )
 
-MODEL_KINDS = {"static": 0, "node2vec": 1, "metapath": 2, "pr2": 3}
+MODEL_KINDS = {"static": 0, "node2vec": 1, "metapath": 2, "pr2": 3, "custom": 4}
 MODES = {"adaptive": 0, "force-ervs": 1, "force-erjs": 2, "ervs-nojump": 3, "force-its": 4,
          "force-als": 5}
 
@@ -77,7 +78,8 @@ class RmatDesc(C.Structure):
 
 class ModelDesc(C.Structure):
     _fields_ = [("kind", C.c_int), ("weighted", C.c_int), ("a", C.c_double), ("b", C.c_double),
-                ("gamma", C.c_double), ("schema", u16p), ("schema_len", C.c_uint32)]
+                ("gamma", C.c_double), ("schema", u16p), ("schema_len", C.c_uint32),
+                ("custom", C.c_void_p)]
 
 
 class RunOptsC(C.Structure):
@@ -130,6 +132,8 @@ def load_library() -> C.CDLL:
     L.dw_graph_info.argtypes = [vp, u32p, u64p, C.POINTER(C.c_int), u32p]
     L.dw_graph_download.argtypes = [vp, u64p, u32p, f32p, u16p, f64p, f64p]
     L.dw_calibrate.argtypes = [vp, C.POINTER(ModelDesc), C.c_uint64, f64p]
+    L.dw_model_compile.argtypes = [C.c_char_p, C.c_uint32, C.c_uint32, C.POINTER(vp)]
+    L.dw_model_free.argtypes = [vp]
     L.dw_run.argtypes = [vp, C.POINTER(ModelDesc), u32p, C.c_uint64, C.POINTER(RunOptsC), u32p,
                          u32p, C.POINTER(RunStatsC)]
     L.dw_run_compact.argtypes = [vp, C.POINTER(ModelDesc), u32p, C.c_uint64,
@@ -164,15 +168,34 @@ class Model:
     b: float = 0.5
     gamma: float = 0.2
     schema: tuple = (0, 1, 2, 3, 4)
+    custom: "CustomModel" = None  # kind "custom": a compiled DslWalk
     _arr: np.ndarray = field(default=None, repr=False)
 
     def c(self) -> ModelDesc:
         if self.kind not in MODEL_KINDS:
             raise DynwalkError(-1, f"unknown model '{self.kind}' (expected static, node2vec, "
-                                   "metapath, pr2)")
+                                   "metapath, pr2, custom)")
         self._arr = np.ascontiguousarray(self.schema, np.uint16)
         return ModelDesc(MODEL_KINDS[self.kind], int(self.weighted), self.a, self.b, self.gamma,
-                         _p(self._arr, u16p), len(self.schema))
+                         _p(self._arr, u16p), len(self.schema),
+                         self.custom.h if self.custom is not None else None)
+
+
+class CustomModel:
+    """A DslWalk weight function compiled into the walk kernel (dw_model_compile).
+
+    `source` is the CUDA model functor generated from the reference's parsed
+    program by paper_2512_00705_b200/host/dsl_codegen.hpp."""
+
+    def __init__(self, source: str, max_steps: int = 2**32 - 1, flags: int = 0):
+        L = load_library()
+        self.h = C.c_void_p()
+        _check(L.dw_model_compile(source.encode(), max_steps, flags, C.byref(self.h)))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            load_library().dw_model_free(self.h)
+            self.h = None
 
 
 @dataclass

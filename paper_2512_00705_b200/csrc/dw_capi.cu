@@ -26,6 +26,19 @@ namespace {
 
 thread_local std::string t_error;
 
+}  // namespace
+
+struct dw_custom_model_s;
+namespace dwb {
+std::string* dsl_error_slot() { return &t_error; }
+cudaError_t launch_custom(const dw_custom_model_s* cm, int mode, const WalkParams& p, int num_sms,
+                          cudaStream_t stream);
+uint32_t custom_max_steps(const dw_custom_model_s* cm);
+uint32_t custom_flags(const dw_custom_model_s* cm);
+}  // namespace dwb
+
+namespace {
+
 int fail(int code, const char* fmt, ...) {
     char buf[1024];
     va_list ap;
@@ -147,6 +160,7 @@ void free_replica(Replica& r) {
     cudaFree(r.g.labels);
     cudaFree(r.g.hslots);
     cudaFree(r.g.fat);
+    cudaFree(r.g.lagg);
     cudaFree(r.counters);
     cudaFree(r.queues);
     cudaFree(r.error);
@@ -265,6 +279,10 @@ int upload_replica(Replica& r, const dw_graph_desc* d) {
 
 int check_model(const dw_model_desc* m) {
     if (!m) return fail(DW_EINVAL, "model descriptor is NULL");
+    if (m->kind == DW_MODEL_CUSTOM) {
+        if (!m->custom) return fail(DW_EINVAL, "custom model handle is NULL");
+        return DW_OK;
+    }
     if (m->kind < DW_MODEL_STATIC || m->kind > DW_MODEL_PR2)
         return fail(DW_EINVAL,
                     "unknown model kind %d (expected static, node2vec, metapath, pr2; DSL models "
@@ -363,14 +381,16 @@ int check_opts(const dw_run_opts* o) {
 }
 
 uint32_t target_steps(const dw_model_desc* m, const dw_run_opts* o) {
-    const uint32_t ms = m->kind == DW_MODEL_METAPATH ? m->schema_len : 0xFFFFFFFFu;
+    const uint32_t ms = m->kind == DW_MODEL_METAPATH ? m->schema_len
+                        : m->kind == DW_MODEL_CUSTOM ? dwb::custom_max_steps(m->custom)
+                                                     : 0xFFFFFFFFu;
     return std::min(o->walk_length, ms);
 }
 
 dwb::WalkParams make_params(Replica& r, const dw_model_desc* m, const dw_run_opts* o) {
     dwb::WalkParams p;
     std::memset(&p, 0, sizeof p);
-    p.g = dwb::DevGraph{r.g.nodes, r.g.edges, r.g.labels, r.g.hslots, r.g.fat, r.g.nv, r.g.ne};
+    p.g = dwb::DevGraph{r.g.nodes, r.g.edges, r.g.labels, r.g.hslots, r.g.fat, r.g.lagg, r.g.nv, r.g.ne};
     p.stride = o->walk_length + 1;
     p.target = target_steps(m, o);
     p.seed_lo = (uint32_t)o->seed;
@@ -383,6 +403,23 @@ dwb::WalkParams make_params(Replica& r, const dw_model_desc* m, const dw_run_opt
     p.error_info = r.error_info;
     p.mp = model_params(m);
     return p;
+}
+
+// builtin models are template instantiations; DSL models NVRTC-compiled kernels
+cudaError_t launch_model(Replica& r, const dw_model_desc* m, int mode, const dwb::WalkParams& p,
+                         cudaStream_t s) {
+    if (m->kind == DW_MODEL_CUSTOM) return dwb::launch_custom(m->custom, mode, p, r.num_sms, s);
+    return dwb::launch_walk(m->kind, m->weighted != 0, mode, p, r.num_sms, s);
+}
+
+// per-replica preprocessing a model needs before its first walk
+int prepare_model(Replica& r, const dw_model_desc* m) {
+    if (m->kind == DW_MODEL_CUSTOM && (dwb::custom_flags(m->custom) & DW_CUSTOM_LABEL_AGGREGATES) &&
+        !r.g.lagg) {
+        CU(cudaSetDevice(r.device), "cudaSetDevice");
+        CU(dwb::build_label_aggregates(r.g, r.stream), "label aggregates");
+    }
+    return DW_OK;
 }
 
 int reset_run_state(Replica& r) {
@@ -533,6 +570,7 @@ int run_engine(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries
         d.bs = out.text ? std::min<ull>(batch_size(d.n), 1ull << 20) : batch_size(d.n);
         d.nb = d.n ? (d.n + d.bs - 1) / d.bs : 0;
         CU(cudaSetDevice(r.device), "cudaSetDevice");
+        if ((rc = prepare_model(r, model))) return rc;
         if ((rc = ensure_ring(r, d.bs, stride, out.compact, out.text != nullptr))) return rc;
         if ((rc = reset_run_state(r))) return rc;
         CU(cudaMemsetAsync(r.d_base, 0, sizeof(ull), r.stream), "memset");
@@ -566,9 +604,7 @@ int run_engine(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries
         if (p.paths && !out.compact && !out.text)  // compaction copies only the written ids
             CU(cudaMemsetAsync(p.paths, 0xFF, bn * stride * sizeof(uint32_t), r.stream),
                "memset paths");
-        CU(dwb::launch_walk(model->kind, model->weighted != 0, opts->mode, p, r.num_sms,
-                            r.stream),
-           "walk");
+        CU(launch_model(r, model, opts->mode, p, r.stream), "walk");
         ++launches;
         if (out.compact) {
             size_t tb = r.scan_bytes;
@@ -1062,6 +1098,9 @@ int dw_calibrate(dw_graph_t g, const dw_model_desc* model, uint64_t seed, double
     if (!g || !ratio) return fail(DW_EINVAL, "NULL argument");
     int rc = check_model(model);
     if (rc) return rc;
+    if (model->kind == DW_MODEL_CUSTOM)
+        return fail(DW_EUNSUPPORTED,
+                    "device calibration of DSL models is not supported; pass edge_cost_ratio");
     Replica& r = g->reps[0];
     CU(cudaSetDevice(r.device), "cudaSetDevice");
     const dwb::ModelParams mp = model_params(model);
@@ -1084,6 +1123,7 @@ int dw_run_device(dw_graph_t g, int replica, const dw_model_desc* model, const u
     if ((rc = check_model(model)) || (rc = check_opts(opts))) return rc;
     Replica& r = g->reps[replica];
     CU(cudaSetDevice(r.device), "cudaSetDevice");
+    if ((rc = prepare_model(r, model))) return rc;
     cudaStream_t s = stream ? (cudaStream_t)stream : r.stream;
     if ((rc = reset_run_state(r))) return rc;
     if (s != r.stream) {  // order the resets before work on the caller's stream
@@ -1100,7 +1140,7 @@ int dw_run_device(dw_graph_t g, int replica, const dw_model_desc* model, const u
     if (d_paths && nq)
         CU(cudaMemsetAsync(d_paths, 0xFF, nq * (ull)p.stride * sizeof(uint32_t), s), "memset paths");
     CU(cudaEventRecord(r.ev_start, s), "event");
-    CU(dwb::launch_walk(model->kind, model->weighted != 0, opts->mode, p, r.num_sms, s), "walk");
+    CU(launch_model(r, model, opts->mode, p, s), "walk");
     CU(cudaEventRecord(r.ev_stop, s), "event");
     r.pending = true;
     r.pending_launches = 1;

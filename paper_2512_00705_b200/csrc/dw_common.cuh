@@ -17,8 +17,18 @@
 //                costs the same DRAM traffic as a 16 B one; what counts is the
 //                number of random requests per walker-step.
 #pragma once
+#ifdef __CUDACC_RTC__
+// NVRTC (DSL models, dw_dsl.cu): no host headers
+typedef unsigned char uint8_t;
+typedef unsigned short uint16_t;
+typedef unsigned int uint32_t;
+typedef unsigned long long uint64_t;
+typedef long long int64_t;
+#define DBL_MAX 1.7976931348623157e+308
+#else
 #include <cstdint>
 #include <cuda_runtime.h>
+#endif
 
 namespace dwb {
 
@@ -71,6 +81,7 @@ struct DevGraph {
     const uint16_t* __restrict__ labels;  // may be null
     const uint32_t* __restrict__ hslots;  // membership hash sets, 8 slots per bucket
     const FatRec* __restrict__ fat;       // may be null (slim layout)
+    const double2* __restrict__ lagg;     // per-node {label MAX, label SUM} or null (DSL)
     uint32_t nv;
     unsigned long long ne;
 };

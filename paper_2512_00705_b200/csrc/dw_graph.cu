@@ -567,7 +567,7 @@ __global__ void probe_pass_kernel(DevGraph g, __grid_constant__ const ModelParam
 template <class M>
 static cudaError_t calibrate_t(const DeviceGraphBuffers& gb, const ModelParams& mp, ull seed,
                                cudaStream_t s, double* ratio) {
-    DevGraph g{gb.nodes, gb.edges, gb.labels, gb.hslots, gb.fat, gb.nv, gb.ne};
+    DevGraph g{gb.nodes, gb.edges, gb.labels, gb.hslots, gb.fat, gb.lagg, gb.nv, gb.ne};
     // ProfileConfig defaults: 1% of nodes, >= 64, <= 32 neighbours, 5 reps
     uint32_t want = (uint32_t)std::max<ull>((ull)std::ceil(0.01 * gb.nv), 64);
     const ull tries = (ull)want * 8;
@@ -910,6 +910,31 @@ cudaError_t path_text_write(const uint32_t* paths, const uint32_t* lengths, ull 
     text_write_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(paths, lengths, n, stride, toffs,
                                                             text);
     return cudaGetLastError();
+}
+
+// ---- DSL preprocess: label aggregates ------------------------------------------
+__global__ void label_agg_kernel(const NodeRec* __restrict__ nodes, uint32_t nv,
+                                 const uint16_t* __restrict__ labels, double2* __restrict__ out) {
+    for (ull v = blockIdx.x * (ull)blockDim.x + threadIdx.x; v < nv;
+         v += (ull)gridDim.x * blockDim.x) {
+        const NodeRec nr = nodes[v];
+        double mx = 0.0, sum = 0.0;
+        if (labels)
+            for (ull e = nr.begin; e < nr.begin + nr.degree; ++e) {
+                const double l = labels[e];
+                if (l > mx) mx = l;
+                sum += l;
+            }
+        out[v] = make_double2(mx, sum);
+    }
+}
+
+cudaError_t build_label_aggregates(DeviceGraphBuffers& g, cudaStream_t s) {
+    if (g.lagg) return cudaSuccess;
+    DW_TRY(cudaMalloc(&g.lagg, std::max<uint32_t>(g.nv, 1) * sizeof(double2)));
+    label_agg_kernel<<<grid_for(g.nv, 128), 128, 0, s>>>(g.nodes, g.nv, g.labels, g.lagg);
+    DW_TRY(cudaGetLastError());
+    return cudaStreamSynchronize(s);
 }
 
 }  // namespace dwb

@@ -10,6 +10,7 @@ struct DeviceGraphBuffers {
     uint16_t* labels = nullptr;
     uint32_t* hslots = nullptr;  // membership hash sets (dw_member.cuh)
     FatRec* fat = nullptr;       // fat edge records (optional accelerator)
+    double2* lagg = nullptr;     // per-node label MAX/SUM, built on first DSL use
     unsigned long long nbuckets = 0;
     uint32_t nv = 0;
     unsigned long long ne = 0;
@@ -48,6 +49,10 @@ cudaError_t calibrate_ratio(const DeviceGraphBuffers& g, int model_kind, bool we
                             cudaStream_t s, double* ratio);
 
 unsigned long long host_derive_seed(unsigned long long seed, unsigned long long stream);
+
+// Per-node {MAX, SUM} over the row's labels in ascending edge order, the
+// DslWalk preprocess step (models.cpp:19-35); zero rows without labels.
+cudaError_t build_label_aggregates(DeviceGraphBuffers& g, cudaStream_t s);
 
 // ---- text sink (dw_run_write_paths): write_paths' format, runtime.cpp:280-291
 // bytes[i] = text size of path i ("id id ... id\n", "\n" when empty)

@@ -38,6 +38,7 @@ struct Step {
     uint32_t step;
     uint32_t degree;  // d(cur)
     double hmax, hsum;
+    double lmax, lsum;  // per-node label MAX/SUM (DSL models whose estimators read labels)
     __device__ __forceinline__ bool has_prev() const { return prev != kInvalid; }
 };
 
@@ -90,6 +91,7 @@ __device__ __forceinline__ double dmax3(double x, double y, double z) {
 template <bool W>
 struct StaticModel {
     static constexpr bool kScreen = false;
+    static constexpr bool kLabelAgg = false;
     static constexpr bool kUsesLabels = false;
     static constexpr bool kSecondOrder = false;
     static constexpr bool kBoundable = true;
@@ -114,6 +116,7 @@ struct Node2VecModel {
     static constexpr bool kBoundable = true;
     static constexpr bool kAggregates = W;  // PER_STEP bound reads node max/sum
     static constexpr bool kScreen = true;
+    static constexpr bool kLabelAgg = false;
     double a, b, ia, ib, i3, wc;
     bool pa, pb;
     __device__ explicit Node2VecModel(const ModelParams& p)
@@ -159,6 +162,7 @@ struct Node2VecModel {
 template <bool W>
 struct MetaPathModel {
     static constexpr bool kScreen = false;
+    static constexpr bool kLabelAgg = false;
     static constexpr bool kUsesLabels = true;
     static constexpr bool kSecondOrder = false;
     static constexpr bool kBoundable = true;
@@ -186,6 +190,7 @@ struct MetaPathModel {
 template <bool W>
 struct Pr2Model {
     static constexpr bool kScreen = false;
+    static constexpr bool kLabelAgg = false;
     static constexpr bool kUsesLabels = false;
     static constexpr bool kSecondOrder = true;
     static constexpr bool kBoundable = true;

@@ -1,957 +1,8 @@
-// dw_walk.cu -- the walk hot path: K1 eRJS, K2 eRVS, K3 adaptive walker loop.
-//
-// One persistent kernel per run.  Each lane owns one walker at a time and
-// keeps its WalkerState (walk_state.hpp:13-40) in registers for all steps;
-// lanes claim walkers from a global queue with one warp-aggregated atomic
-// (the run_queries scheduler, runtime.cpp:209-211).
-//
-// Cost model.  Every random gather on B200 moves a whole 128 B L2 line from
-// HBM, whatever its size (tools/gather_probe.cu: ~3.7e10 random lines/s at
-// ~4.7 TB/s of DRAM traffic).  The kernel is therefore designed around the
-// NUMBER of random requests per walker-step, not their bytes:
-//   * fat edge records (dw_common.cuh FatRec): an accepted trial's record
-//     carries its target's row begin, degree, hash-set base, aggregates and
-//     the return-edge range, so a step needs no node-record gather;
-//   * free rejections: a trial whose y is >= the model's non-return maximum
-//     and whose index lies outside the return-edge range is rejected without
-//     gathering its edge -- about half of node2vec (0.5, 2) trials;
-//   * no speculative waste beyond a ring of kRing outstanding trials.
-//
-// Latency structure.  A walk step is a chain of dependent random loads and
-// lanes of a warp need different numbers of them, so the walker loop is a
-// per-lane state machine in which every lane advances one memory phase per
-// iteration:
-//     A  each lane issues the gathers its phase needs as cp.async (LDGSTS)
-//        into its own shared-memory landing slots
-//     B  cp.async.wait_all
-//     C  each lane consumes its slots and picks its next phase
-// Phases:
-//   NODE   one 32 B node record (the walker's first step, or every step on
-//          the slim layout); cost-model decision (decide_sampler,
-//          cost_model.hpp:46-56).
-//   TRIAL  eRJS (samplers.hpp:145-178).  Philox is a counter RNG, so trial t's
-//          (x, y) is known without running the trials before it: the lane
-//          generates trials, rejects the free ones on the spot and queues
-//          the others (edge record gathers) in a ring; queued trials are
-//          judged in trial order.  A trial whose outcome hinges on the
-//          node2vec/PR2 membership test (y between the two candidate weights)
-//          parks at the ring head while one hash bucket is probed.
-//   FETCH  the fat record of the edge an eRVS step chose.
-//   VREC / VMEMB   eRVS on short rows (samplers.hpp:65-137), one neighbour per
-//          iteration, exactly the reference's sequential jump logic.
-//   COOP   rows >= kCoopMinDegree are handed to the whole warp through a
-//          ballot (FlexiWalker's mixed mode): 32 lanes load a chunk and
-//          resolve 32 weights in parallel, then the A-ExpJ jump scan runs
-//          warp-uniformly over the chunk with shuffles.
-// Paths, counters and draw counts equal the sequential reference on the same
-// Philox stream (tests/test_gpu_parity.py).
-#include <cfloat>
-
-#include "dw_walk.cuh"
+// dw_walk.cu -- builtin-model instantiations and launch of the walk kernel
+// (dw_walk_kernel.cuh).
+#include "dw_walk_kernel.cuh"
 
 namespace dwb {
-
-#ifndef DW_MIN_BLOCKS
-#define DW_MIN_BLOCKS 3
-#endif
-#ifndef DW_RING
-#define DW_RING 2
-#endif
-#ifndef DW_GEN
-#define DW_GEN 4
-#endif
-constexpr int kThreads = 256;
-constexpr uint32_t kRing = DW_RING;  // queued trials per lane (power of two)
-constexpr uint32_t kGen = DW_GEN;    // Philox blocks per lane per iteration
-static_assert((kRing & (kRing - 1)) == 0, "kRing must be a power of two");
-constexpr uint32_t kCoopMinDegree = 64;
-#ifndef DW_EBATCH
-#define DW_EBATCH 8
-#endif
-#ifndef DW_EWAIT
-#define DW_EWAIT 10
-#endif
-// short-row eRVS: rows of <= kEBatchMaxDeg neighbours collect their weights in
-// the lane's first ring slot (6 doubles) and scan in batches of kEBatch lanes
-constexpr uint32_t kEBatchMaxDeg = 6;
-constexpr uint32_t kEBatch = DW_EBATCH;
-constexpr uint32_t kEWait = DW_EWAIT;
-constexpr unsigned kFull = 0xFFFFFFFFu;
-typedef unsigned long long ull;
-
-enum Phase : uint32_t { P_IDLE = 0, P_NODE, P_TRIAL, P_FETCH, P_VREC, P_VMEMB, P_COOP, P_EMATH };
-// per-lane counters kept in shared memory (updated per walker or per eRVS
-// neighbour): eRJS trials, single-shot eRVS trials, eRVS reads and draws,
-// algorithmic bytes / 4.  Their block totals sit in the last LC_NUM slots of
-// the shared counter array (scratch slots of Counter, dw_walk.cuh).
-enum LaneCounter : int { LC_ETRIALS = 0, LC_ETRIALS1, LC_EREADS, LC_EDRAWS, LC_ALG4, LC_NUM };
-
-__device__ __forceinline__ bool valid_w(double w) { return !(w < 0.0) && isfinite(w); }
-
-template <class M>
-__device__ __forceinline__ uint16_t edge_label(const DevGraph& g, ull e) {
-    if (!M::kUsesLabels) return 0;
-    return g.labels ? __ldg(g.labels + e) : (uint16_t)0;
-}
-
-__device__ __forceinline__ void raise_error(const WalkParams& p, int code, ull q) {
-    if (atomicCAS(p.error, 0, code) == 0) *p.error_info = q;
-}
-
-// ---- cp.async (LDGSTS) gathers into the lane's landing slots --------------
-__device__ __forceinline__ void cp16(void* smem, const void* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp4(void* smem, const void* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_wait_all() {
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
-}
-
-__device__ __forceinline__ const EdgeRec* pair_of(const EdgeRec* edges, ull e) {
-    return edges + (e & ~1ull);  // 16 B aligned pair holding record e
-}
-
-__device__ __forceinline__ void cnt_add(ull* c, ull v) { atomicAdd(c, v); }
-
-// ---- K2 (warp form): one row, 32 lanes; all lanes call with equal args ----
-// Returns the chosen target and its relative edge index (for the fat record).
-#ifndef DW_COOP_INLINE
-#define DW_COOP_INLINE 1
-#endif
-#if DW_COOP_INLINE
-#define DW_COOP_ATTR __forceinline__
-#else
-#define DW_COOP_ATTR __noinline__
-#endif
-template <class M, bool NOJUMP>
-__device__ DW_COOP_ATTR int ervs_warp(const ModelParams& mp, Step S, const WalkerKey key,
-                                      const DevGraph& g, ull begin, uint32_t phoff, ull idx0,
-                                      uint32_t* next, uint32_t* nidx, ull* draws) {
-    M m(mp);
-    m.prepare(S);
-    const int lane = threadIdx.x & 31;
-    ull idx = idx0;
-    double best_log_key = -DBL_MAX;
-    uint32_t best = kInvalid, bi = 0;
-    double skip = 0.0;
-    bool have = false;
-    // software pipeline: chunk c+1's records load while chunk c is judged
-    EdgeRec nxt{kInvalid, 0.f};
-    uint16_t nlab = 0;
-    if ((uint32_t)lane < S.degree) {
-        nxt = load_edge(g.edges + begin + lane);
-        nlab = edge_label<M>(g, begin + lane);
-    }
-    for (uint32_t base = 0; base < S.degree; base += 32) {
-        const uint32_t i = base + lane;
-        const bool in = i < S.degree;
-        const EdgeRec er = nxt;
-        const uint16_t lab = nlab;
-        if (i + 32 < S.degree) {
-            nxt = load_edge(g.edges + begin + i + 32);
-            nlab = edge_label<M>(g, begin + i + 32);
-        }
-        double w = 0.0;
-        if (in) {
-            const WeightCase wc = m.weight(S, er.col, er.h, lab);
-            w = (!M::kSecondOrder || !wc.needs_member)
-                    ? wc.w
-                    : (member(g, S.prev_degree, phoff, er.col) ? wc.w_in : wc.w_out);
-        }
-        if (__any_sync(kFull, in && !valid_w(w))) return -kDevBadWeight;
-        if (NOJUMP) {
-            // every neighbour draws its own key (draw idx0 + i), zero weights included
-            double lk = -DBL_MAX;
-            int has = 0;
-            if (in) {
-                const double u = open01(walker_draw(key, idx0 + i));
-                if (w != 0.0) {
-                    lk = log(u) / w;
-                    has = 1;
-                }
-            }
-            int src = lane;
-#pragma unroll
-            for (int off = 16; off; off >>= 1) {
-                const double olk = __shfl_xor_sync(kFull, lk, off);
-                const int ohas = __shfl_xor_sync(kFull, has, off);
-                const int osrc = __shfl_xor_sync(kFull, src, off);
-                const bool take = ohas && (!has || olk > lk || (olk == lk && osrc < src));
-                if (take) {
-                    lk = olk;
-                    has = ohas;
-                    src = osrc;
-                }
-            }
-            const uint32_t cand = __shfl_sync(kFull, er.col, src);
-            if (has && (best == kInvalid || lk > best_log_key)) {
-                best_log_key = lk;
-                best = cand;
-                bi = base + src;
-            }
-        } else {
-            const uint32_t n = S.degree - base < 32u ? S.degree - base : 32u;
-            for (uint32_t j = 0; j < n; ++j) {
-                const double wj = __shfl_sync(kFull, w, j);
-                const uint32_t uj = __shfl_sync(kFull, er.col, j);
-                if (wj == 0.0) continue;
-                if (best == kInvalid) {
-                    best_log_key = log(open01(walker_draw(key, idx++))) / wj;
-                    best = uj;
-                    bi = base + j;
-                    continue;
-                }
-                if (!have) {
-                    skip = log(open01(walker_draw(key, idx++))) / best_log_key;
-                    have = true;
-                }
-                skip -= wj;
-                if (skip <= 0.0) {
-                    const double floor_u = exp(wj * best_log_key);
-                    const double u = floor_u + open01(walker_draw(key, idx++)) * (1.0 - floor_u);
-                    const double lk = log(u) / wj;
-                    if (lk > best_log_key) {
-                        best_log_key = lk;
-                        best = uj;
-                        bi = base + j;
-                    }
-                    have = false;
-                }
-            }
-        }
-    }
-    *next = best;
-    *nidx = bi;
-    *draws = NOJUMP ? (ull)S.degree : idx - idx0;
-    return 0;
-}
-
-// ---- K2 (lane form): one neighbour of the reservoir scan ------------------
-// samplers.hpp:78-102 (jump) / 122-133 (no jump).  Kept out of line: it holds
-// the log/exp code, which the hot eRJS loop never needs.
-struct ErvsState {
-    double best_key, skip;
-    ull didx;        // next draw index of this step's stream
-    uint32_t best;
-    uint32_t bidx;   // relative edge index of best (bits 0-30) | threshold drawn (bit 31)
-};
-constexpr uint32_t kHave = 0x80000000u;
-
-template <bool NOJUMP>
-__device__ __forceinline__ ErvsState ervs_visit_impl(ErvsState s, const WalkerKey& key, uint32_t vi,
-                                                     uint32_t u, double w) {
-    if (NOJUMP) {
-        const double r = open01(walker_draw(key, s.didx + vi));
-        if (w != 0.0) {
-            const double lk = log(r) / w;
-            if (s.best == kInvalid || lk > s.best_key) {
-                s.best_key = lk;
-                s.best = u;
-                s.bidx = vi;
-            }
-        }
-        return s;
-    }
-    if (w == 0.0) return s;
-    if (s.best == kInvalid) {
-        s.best_key = log(open01(walker_draw(key, s.didx++))) / w;
-        s.best = u;
-        s.bidx = vi;
-        return s;
-    }
-    if (!(s.bidx & kHave)) {
-        s.skip = log(open01(walker_draw(key, s.didx++))) / s.best_key;
-        s.bidx |= kHave;
-    }
-    s.skip -= w;
-    if (s.skip <= 0.0) {
-        const double floor_u = exp(w * s.best_key);
-        const double uu = floor_u + open01(walker_draw(key, s.didx++)) * (1.0 - floor_u);
-        const double lk = log(uu) / w;
-        s.bidx &= ~kHave;
-        if (lk > s.best_key) {
-            s.best_key = lk;
-            s.best = u;
-            s.bidx = vi;
-        }
-    }
-    return s;
-}
-
-template <bool NOJUMP>
-__device__ __forceinline__ ErvsState ervs_visit(ErvsState s, const WalkerKey key, uint32_t vi,
-                                             uint32_t u, double w) {
-    return ervs_visit_impl<NOJUMP>(s, key, vi, u, w);
-}
-
-// The whole jump scan (samplers.hpp:65-107) over d <= kEBatchMaxDeg weights in
-// the lane's landing slot (weight j at w[(j/2) * 2 * kThreads + j%2], i.e.
-// half j%2 of uint4 j/2 of the lane); returns the draw index after the scan
-// and the kept neighbour's index (kInvalid when every weight is zero).
-__device__ __forceinline__ ull ervs_scan_short(const double* w, uint32_t d, const WalkerKey key,
-                                            ull didx, uint32_t* bidx) {
-    ErvsState s{-DBL_MAX, 0.0, didx, kInvalid, 0};
-    for (uint32_t j = 0; j < d; ++j)
-        s = ervs_visit_impl<false>(s, key, j, 0u, w[(j >> 1) * 2 * kThreads + (j & 1)]);
-    *bidx = s.best == kInvalid ? kInvalid : (s.bidx & ~kHave);
-    return s.didx;
-}
-
-__device__ __forceinline__ ull warp_sum(ull v) {
-#pragma unroll
-    for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
-    return v;
-}
-
-// ---- K3: adaptive walker loop (runtime.cpp:59-153 + 192-247) --------------
-// Per-lane landing slots and counters, structure-of-arrays ([.][kThreads]) so
-// a warp's 16 B accesses are conflict-free.
-struct WalkSmem {
-    uint4 rec[kRing][3][kThreads];   // landing: fat record / slim pair in [0]
-    double y[kRing][kThreads];       // y of the queued trials
-    uint32_t t[kRing][kThreads];     // trial index of the queued trials
-    uint4 mb[2][kThreads];           // node record / hash bucket / eRVS pair
-    uint32_t lc[LC_NUM][kThreads];   // per-lane RunStats counters (spill at 2^31)
-    // walker state read once per step or per iteration, kept out of registers
-    // so the loop fits the register budget of 3-4 CTAs/SM without spills
-    uint32_t cur[kThreads], phoff[kThreads], plg[kThreads], hoff[kThreads], cap[kThreads],
-        twlo[kThreads], twcnt[kThreads], nret[kThreads];
-    double bound[kThreads], mnr[kThreads];
-    ull cnt[kCNum];
-    uint32_t hist[66];
-    ull lct[LC_NUM];                 // block totals of the lane counters
-};
-
-template <class M, int MODE, bool FAT>
-__global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
-    walk_kernel(const __grid_constant__ WalkParams p) {
-    constexpr bool kNoJump = MODE == kErvsNoJump;
-    constexpr bool kSO = M::kSecondOrder;
-    // dynamic shared memory (WalkSmem): may exceed the 48 KB static limit
-    extern __shared__ __align__(16) unsigned char dsm[];
-    WalkSmem& sm = *reinterpret_cast<WalkSmem*>(dsm);
-    auto& s_rec = sm.rec;
-    auto& s_y = sm.y;
-    auto& s_t = sm.t;
-    auto& s_mb = sm.mb;
-    auto& s_lc = sm.lc;
-    auto& s_cnt = sm.cnt;
-    auto& s_hist = sm.hist;
-    auto& s_lct = sm.lct;
-    const int tid = threadIdx.x;
-    for (int i = tid; i < kCNum; i += blockDim.x) s_cnt[i] = 0;
-    if (tid < LC_NUM) s_lct[tid] = 0;
-    for (int i = tid; i < 66; i += blockDim.x) s_hist[i] = 0;
-#pragma unroll
-    for (int c = 0; c < LC_NUM; ++c) s_lc[c][tid] = 0;
-    __syncthreads();
-    // lane counters: LC_* accumulate per lane in shared memory and spill into
-    // the block's 64-bit totals (s_lct) before they can overflow
-    auto lc_add = [&](int c, ull v) {
-        const ull t = (ull)s_lc[c][tid] + v;
-        if (t >= 0x80000000ull) {
-            atomicAdd(&s_lct[c], t);
-            s_lc[c][tid] = 0;
-        } else {
-            s_lc[c][tid] = (uint32_t)t;
-        }
-    };
-
-    M model(p.mp);
-    const int lane = tid & 31;
-    const unsigned lt_mask = (1u << lane) - 1u;
-    const DevGraph& g = p.g;
-    const bool shortcut = p.mp.shortcut != 0;
-
-    uint32_t phase = P_IDLE;
-    bool drained = false;  // warp-uniform
-    ull qi = 0;
-    // walker state
-    uint32_t prev = kInvalid, pdeg = 0, step = 0, deg = 0;
-    uint32_t& cur = sm.cur[tid];
-    uint32_t& phoff = sm.phoff[tid];  // hash set of prev
-    uint32_t& plg = sm.plg[tid];      // log2 buckets of prev's hash set
-    uint32_t& hoff = sm.hoff[tid];    // hash set of cur
-    cur = kInvalid;
-    phoff = plg = hoff = 0;
-    ull begin = 0;
-    // eRJS state
-    double& bound = sm.bound[tid];    // rejection bound
-    double& mnr = sm.mnr[tid];        // non-return maximum
-    uint32_t& cap = sm.cap[tid];      // trial cap of the step (samplers.hpp:157)
-    uint32_t& tw_lo = sm.twlo[tid];   // return-edge range in N(cur)
-    uint32_t& tw_cnt = sm.twcnt[tid];
-    uint32_t& nret = sm.nret[tid];    // judged return-edge trials
-    bound = mnr = 0.0;
-    cap = tw_lo = tw_cnt = nret = 0;
-    uint32_t tn = 0, rh = 0, rc = 0;  // next trial, ring head, ring count
-    uint32_t mb = 0, sel = 0;         // parked bucket (bit 31: parked), pair bits
-    // per-walker register counters, folded into the lane counters at walk end
-    uint32_t c_trials = 0, c_alg4 = 0;   // eRJS trials, algorithmic bytes / 4
-    // eRVS state lives in the lane's spare ring slot (the ring is idle while a
-    // lane runs eRVS), keeping the hot eRJS loop's register set small:
-    //   s_rec[kRing-1][0] = {parked neighbour u, its h}   (VMEMB)
-    //   s_rec[kRing-1][1..2] = ErvsState
-    // tn doubles as the eRVS neighbour cursor.
-    constexpr uint32_t kParked = 0x80000000u;
-    static_assert(sizeof(ErvsState) == 32, "ErvsState must fill two uint4");
-    auto ev_load = [&]() {
-        ErvsState e;
-        *reinterpret_cast<uint4*>(&e) = s_rec[kRing - 1][1][tid];
-        *(reinterpret_cast<uint4*>(&e) + 1) = s_rec[kRing - 1][2][tid];
-        return e;
-    };
-    auto ev_store = [&](const ErvsState& e) {
-        s_rec[kRing - 1][1][tid] = *reinterpret_cast<const uint4*>(&e);
-        s_rec[kRing - 1][2][tid] = *(reinterpret_cast<const uint4*>(&e) + 1);
-    };
-    auto mkstep = [&](double hmax, double hsum) {
-        Step S;
-        S.cur = cur;
-        S.prev = prev;
-        S.prev_degree = pdeg;
-        S.step = step;
-        S.degree = deg;
-        S.hmax = hmax;
-        S.hsum = hsum;
-        return S;
-    };
-    auto key_of = [&]() {
-        const ull q = p.qid_base + qi;
-        return WalkerKey{p.seed_lo, p.seed_hi, (uint32_t)q, (uint32_t)(q >> 32), step};
-    };
-    auto fail = [&](int code) {
-        raise_error(p, code, p.qid_base + qi);
-        phase = P_IDLE;
-    };
-    auto flush_walker = [&]() {
-        lc_add(LC_ETRIALS, c_trials);
-        lc_add(LC_ALG4, c_alg4);
-        c_trials = c_alg4 = 0;
-    };
-    auto end_walk = [&]() {
-        if (p.lengths) p.lengths[qi] = step + 1;
-        flush_walker();
-        phase = P_IDLE;
-    };
-    auto start_ervs = [&](ull draw_base) {
-        tn = 0;
-        // §8(d): σ(8d) + 32·min(d, ⌈d'/8⌉) when membership is needed
-        ull alg = ((8ull * deg + 31) / 32) * 32;
-        if (kSO && prev != kInvalid) alg += 32ull * min((ull)deg, ((ull)pdeg + 7) / 8);
-        c_alg4 += (uint32_t)(alg >> 2);
-        if (FAT && (MODE == kAdaptive || MODE == kForceErjs) && deg == 1 && p.mp.pos_weights &&
-            bound > 0.0 && isfinite(bound)) {
-            // one neighbour whose weight is positive and finite by construction
-            // (its h is the row's finite hmax): the reservoir keeps it after
-            // its single key draw (samplers.hpp:82-85)
-            lc_add(LC_EREADS, 1);
-            lc_add(LC_EDRAWS, 1);
-            ev_store(ErvsState{0.0, 0.0, begin, kInvalid, 0});
-            phase = P_FETCH;
-            return;
-        }
-        ev_store(ErvsState{-DBL_MAX, 0.0, draw_base, kInvalid, 0});
-        phase = deg >= kCoopMinDegree ? P_COOP : P_VREC;
-    };
-    // eRJS bookkeeping for T judged trials, nret of them return edges
-    auto count_erjs = [&](uint32_t T) {
-        c_trials += T;
-        const bool so = kSO && prev != kInvalid;
-        c_alg4 += (so ? 16u : 8u) * T - (so ? 8u * nret : 0u);
-        if ((c_trials | c_alg4) & 0xC0000000u) flush_walker();
-    };
-
-    for (;;) {
-        // ---- refill idle lanes: one atomic per warp (runtime.cpp:209-211)
-        unsigned need = __ballot_sync(kFull, phase == P_IDLE);
-        if (need && !drained) {
-            if (*(volatile int*)p.error != 0) drained = true;  // abandon after an error
-            drained = __any_sync(kFull, drained);
-            while (need && !drained) {
-                const int leader = __ffs(need) - 1;
-                const int n = __popc(need);
-                ull base = 0;
-                if (lane == leader) base = atomicAdd(p.next_walker, (ull)n);
-                base = __shfl_sync(kFull, base, leader);
-                if (base + (ull)n >= p.nq) drained = true;
-                if (phase == P_IDLE) {
-                    const ull i = base + (ull)__popc(need & lt_mask);
-                    if (i < p.nq) {
-                        cnt_add(&s_cnt[kCQueries], 1);
-                        const uint32_t start = p.queries[i];
-                        if (start >= g.nv) {  // runtime.cpp:213-217
-                            cnt_add(&s_cnt[kCQueryErrors], 1);
-                            if (p.lengths) p.lengths[i] = 0;
-                        } else {
-                            if (p.paths) p.paths[i * p.stride] = start;
-                            if (p.target == 0) {
-                                if (p.lengths) p.lengths[i] = 1;
-                            } else {
-                                phase = P_NODE;
-                                qi = i;
-                                cur = start;
-                                prev = kInvalid;
-                                pdeg = phoff = plg = 0;
-                                step = 0;
-                            }
-                        }
-                    }
-                }
-                need = __ballot_sync(kFull, phase == P_IDLE);
-            }
-        }
-        if (__ballot_sync(kFull, phase != P_IDLE) == 0) break;
-
-        // ---- A: issue this iteration's gathers
-        if (phase == P_TRIAL) {
-            if (mb & kParked) {
-                const uint32_t* b = g.hslots + 8ull * (phoff + (mb & ~kParked));
-                cp16(&s_mb[0][tid], b);
-                cp16(&s_mb[1][tid], b + 4);
-            }
-            const ull q = p.qid_base + qi;
-            // one trial: free rejection, or queue its record gather in the ring
-            auto trial = [&](const U4& b) {
-                const uint32_t x = (uint32_t)bounded(lo64(b), deg);  // draw 2t:   bounded(d)
-                const double y = uniform01(hi64(b)) * bound;          // draw 2t+1: uniform01()*c
-                if (!(y >= mnr && x - tw_lo >= tw_cnt)) {             // else rejected, no gather
-                    const uint32_t k = (rh + rc) & (kRing - 1);
-                    s_y[k][tid] = y;
-                    s_t[k][tid] = tn;
-                    const ull e = begin + x;
-                    if (FAT) {
-                        const uint4* r = reinterpret_cast<const uint4*>(g.fat + e);
-                        cp16(&s_rec[k][0][tid], r);
-                        cp16(&s_rec[k][1][tid], r + 1);
-                        cp16(&s_rec[k][2][tid], r + 2);
-                    } else {
-                        sel = (sel & ~(1u << k)) | ((uint32_t)(e & 1) << k);
-                        cp16(&s_rec[k][0][tid], pair_of(g.edges, e));
-                        if (M::kUsesLabels && g.labels) cp4(&s_rec[k][1][tid], g.labels + (e & ~1ull));
-                    }
-                    ++rc;
-                }
-                ++tn;
-            };
-#pragma unroll 1
-            for (uint32_t gen = 0; gen < kGen && rc < kRing && tn < cap; ++gen)
-                trial(philox4x32_10_rk(U4{tn, step, (uint32_t)q, (uint32_t)(q >> 32)}, p.rk));
-        } else if (phase == P_NODE) {
-            const char* nr = reinterpret_cast<const char*>(g.nodes + cur);
-            cp16(&s_mb[0][tid], nr);
-            cp16(&s_mb[1][tid], nr + 16);
-        } else if (phase == P_FETCH) {
-            const ull fe = ev_load().didx;
-            const uint4* r = reinterpret_cast<const uint4*>(g.fat + fe);
-            cp16(&s_rec[0][0][tid], r);
-            cp16(&s_rec[0][1][tid], r + 1);
-            cp16(&s_rec[0][2][tid], r + 2);
-        } else if (phase == P_VMEMB) {
-            const uint32_t* b = g.hslots + 8ull * (phoff + mb);
-            cp16(&s_mb[0][tid], b);
-            cp16(&s_mb[1][tid], b + 4);
-        } else if (phase == P_VREC) {
-            const ull e = begin + tn;
-            sel = (uint32_t)(e & 1);
-            cp16(&s_mb[0][tid], pair_of(g.edges, e));
-            if (M::kUsesLabels && g.labels) cp4(&s_mb[1][tid], g.labels + (e & ~1ull));
-        }
-        // ---- B
-        cp_wait_all();
-
-        // ---- C: consume; a finished step leaves its outcome in `next_ev`
-        enum : uint32_t { E_NONE = 0, E_FAT, E_ADV, E_NODE };
-        uint32_t next_ev = E_NONE, next_slot = 0, next_u = 0;
-        if (phase == P_TRIAL) {
-            int acc = -1;
-            const Step S = mkstep(0.0, 0.0);
-            if (mb & kParked) {  // resolve the head's membership probe
-                const uint4 v0 = s_rec[rh][0][tid];
-                const uint32_t u = FAT ? v0.x : (((sel >> rh) & 1) ? v0.z : v0.x);
-                const int r = bucket_lookup(s_mb[0][tid], s_mb[1][tid], u);
-                if (r < 0) {
-                    mb = kParked | ((mb + 1) & ((1u << plg) - 1u));
-                } else {
-                    const float h = __uint_as_float(FAT ? v0.y : (((sel >> rh) & 1) ? v0.w : v0.y));
-                    const WeightCase wc = model.weight(S, u, h, 0);
-                    const double w = r ? wc.w_in : wc.w_out;
-                    mb = 0;
-                    if (!valid_w(w)) {
-                        fail(kDevBadWeight);
-                    } else if (s_y[rh][tid] < w) {
-                        acc = (int)rh;
-                    } else {
-                        rh = (rh + 1) & (kRing - 1);
-                        --rc;
-                    }
-                }
-            }
-            while (phase == P_TRIAL && acc < 0 && !(mb & kParked) && rc) {
-                const uint4 v0 = s_rec[rh][0][tid];
-                const bool odd = !FAT && ((sel >> rh) & 1);
-                const uint32_t u = odd ? v0.z : v0.x;
-                const float h = __uint_as_float(odd ? v0.w : v0.y);
-                uint16_t lab = 0;
-                if (M::kUsesLabels) {
-                    if (FAT)
-                        lab = (uint16_t)(v0.w >> 8);
-                    else
-                        lab = (uint16_t)(odd ? (s_rec[rh][1][tid].x >> 16) : s_rec[rh][1][tid].x);
-                }
-                const double y = s_y[rh][tid];
-                const WeightCase wc = model.weight(S, u, h, lab);
-                if (kSO && u == prev) ++nret;
-                if (!wc.needs_member) {
-                    if (!valid_w(wc.w)) {
-                        fail(kDevBadWeight);
-                        break;
-                    }
-                    if (y < wc.w) {
-                        acc = (int)rh;
-                        break;
-                    }
-                } else {
-                    const double lo = wc.w_in < wc.w_out ? wc.w_in : wc.w_out;
-                    const double hi = wc.w_in < wc.w_out ? wc.w_out : wc.w_in;
-                    const bool ok = valid_w(wc.w_in) && valid_w(wc.w_out);
-                    if (ok && y < lo) {
-                        acc = (int)rh;
-                        break;
-                    }
-                    if (!ok || y < hi) {  // outcome hinges on u in N(prev)
-                        mb = kParked | hash_bucket(u, plg);
-                        break;
-                    }
-                }
-                rh = (rh + 1) & (kRing - 1);
-                --rc;
-            }
-            if (phase == P_TRIAL) {
-                if (acc >= 0) {
-                    count_erjs(s_t[acc][tid] + 1);
-                    if (FAT) {
-                        next_ev = E_FAT;
-                        next_slot = (uint32_t)acc;
-                    } else {
-                        const uint4 v0 = s_rec[acc][0][tid];
-                        next_ev = E_ADV;
-                        next_u = ((sel >> acc) & 1) ? v0.z : v0.x;
-                    }
-                } else if (!(mb & kParked) && rc == 0 && tn >= cap) {
-                    count_erjs(tn);
-                    cnt_add(&s_cnt[kCFallbacks], 1);  // cap overrun -> reservoir, same stream
-                    start_ervs(2ull * tn);
-                }
-            }
-        } else if (phase == P_NODE) {
-            next_ev = E_NODE;
-        } else if (phase == P_FETCH) {
-            next_ev = E_FAT;
-        } else if (phase == P_VMEMB || phase == P_VREC) {
-            uint32_t u;
-            float h;
-            int r = 2;  // 2: no membership needed
-            if (phase == P_VMEMB) {
-                const uint4 pk = s_rec[kRing - 1][0][tid];
-                u = pk.x;
-                h = __uint_as_float(pk.y);
-                r = bucket_lookup(s_mb[0][tid], s_mb[1][tid], u);
-                if (r < 0) mb = (mb + 1) & ((1u << plg) - 1u);
-            } else {
-                const uint4 v = s_mb[0][tid];
-                u = sel ? v.z : v.x;
-                h = __uint_as_float(sel ? v.w : v.y);
-            }
-            if (r >= 0) {
-                const uint16_t lab = (M::kUsesLabels && phase == P_VREC)
-                                         ? (uint16_t)(sel ? (s_mb[1][tid].x >> 16)
-                                                          : s_mb[1][tid].x)
-                                         : 0;
-                const WeightCase wc = model.weight(mkstep(0.0, 0.0), u, h, lab);
-                if (kSO && r == 2 && wc.needs_member) {
-                    s_rec[kRing - 1][0][tid] = make_uint4(u, __float_as_uint(h), 0u, 0u);
-                    mb = hash_bucket(u, plg);
-                    phase = P_VMEMB;
-                } else {
-                    const double w = r == 2 ? wc.w : (r ? wc.w_in : wc.w_out);
-                    if (!valid_w(w)) {
-                        fail(kDevBadWeight);
-                    } else if (FAT && deg <= kEBatchMaxDeg) {
-                        // short row: collect the weights, run the reservoir
-                        // scan later together with other lanes (P_EMATH)
-                        // weight j in the lane's own slot-0 words: s_rec[0][j/2][tid], half j%2
-                        reinterpret_cast<double*>(&s_rec[0][tn >> 1][tid])[tn & 1] = w;
-                        phase = P_VREC;
-                        if (++tn == deg) {
-                            tn = 0;  // now counts the iterations spent waiting
-                            phase = P_EMATH;
-                        }
-                    } else {
-                        phase = P_VREC;
-                        const ErvsState e0 = ev_load();
-                        const ErvsState ev = ervs_visit<kNoJump>(e0, key_of(), tn, u, w);
-                        ev_store(ev);
-                        lc_add(LC_EDRAWS, kNoJump ? 1ull : ev.didx - e0.didx);
-                        lc_add(LC_EREADS, 1);
-                        if (++tn == deg) {  // the scan is complete
-                            if (ev.best == kInvalid) {  // all weights zero: dead end
-                                cnt_add(&s_cnt[kCDeadEnds], 1);
-                                end_walk();
-                            } else if (FAT) {
-                                ErvsState e = ev;
-                                e.didx = begin + (ev.bidx & ~kHave);  // its fat record starts the next step
-                                ev_store(e);
-                                phase = P_FETCH;
-                            } else {
-                                next_ev = E_ADV;
-                                next_u = ev.best;
-                            }
-                        }
-                    }
-                }
-            }
-        }
-
-        // ---- D: step transitions, one code site for every phase
-        double hmax = 0.0, hsum = 0.0;
-        uint32_t lmask = 0xFFu;  // labels present in N(cur) (fat record), all = unknown
-        if (next_ev == E_FAT || next_ev == E_ADV) {
-            // WalkerState::advance (walk_state.hpp:33-39)
-            const uint4 v0 = s_rec[next_slot][0][tid];
-            const uint32_t nx = next_ev == E_FAT ? v0.x : next_u;
-            prev = cur;
-            pdeg = deg;
-            phoff = hoff;
-            plg = hash_log2_buckets(deg);
-            cur = nx;
-            ++step;
-            if (p.paths) p.paths[qi * p.stride + step] = nx;
-            if (step >= p.target) {
-                end_walk();
-                next_ev = E_NONE;
-            } else if (next_ev == E_FAT) {
-                const uint4 v1 = s_rec[next_slot][1][tid], v2 = s_rec[next_slot][2][tid];
-                begin = ((ull)v0.z | ((ull)v0.w << 32)) & kBeginMask;
-                deg = v1.x;
-                hoff = v1.y;
-                tw_lo = v1.z;
-                tw_cnt = v1.w;
-                hmax = __hiloint2double((int)v2.y, (int)v2.x);
-                hsum = __hiloint2double((int)v2.w, (int)v2.z);
-                lmask = v0.w >> 24;
-            } else {
-                phase = P_NODE;  // slim layout: the node record comes next iteration
-                next_ev = E_NONE;
-            }
-        } else if (next_ev == E_NODE) {
-            const uint4 v0 = s_mb[0][tid], v1 = s_mb[1][tid];
-            begin = (ull)v0.x | ((ull)v0.y << 32);
-            deg = v0.z;
-            hoff = v0.w;
-            hmax = __hiloint2double((int)v1.y, (int)v1.x);
-            hsum = __hiloint2double((int)v1.w, (int)v1.z);
-            // first step: no return edge; later (slim layout) the range is unknown
-            tw_lo = 0;
-            tw_cnt = prev == kInvalid ? 0u : 0xFFFFFFFFu;
-        }
-        if (next_ev != E_NONE) {
-            // decide_sampler (cost_model.hpp:46-56) for the step at cur
-            if (deg == 0) {  // runtime.cpp:70-71: stop without counting a step
-                end_walk();
-            } else {
-                Step S = mkstep(hmax, hsum);
-                model.prepare(S);
-                bool erjs = false;
-                if (MODE == kAdaptive) {
-                    if (M::kBoundable) {
-                        bound = model.bound(S);
-                        const double T = p.ratio * bound;
-                        if (M::kScreen && p.mp.screen) {
-                            // decide on the one-multiply estimate unless T
-                            // falls in its error band (then the exact sum)
-                            const double Wa = model.wsum_approx(S);
-                            erjs = T < Wa * (1.0 - 1e-12)
-                                       ? true
-                                       : (T > Wa * (1.0 + 1e-12) ? false : T < model.wsum(S));
-                        } else {
-                            erjs = T < model.wsum(S);
-                        }
-                    }
-                } else if (MODE == kForceErjs) {  // runtime.cpp:109-129
-                    erjs = M::kBoundable;
-                    if (erjs) bound = model.bound(S);
-                }
-                {
-                    const uint32_t hb = 2 * degree_bucket(deg) + (erjs ? 1 : 0);
-                    if (atomicAdd(&s_hist[hb], 1u) == 0x7FFFFFFFu) {  // spill before overflow
-                        atomicSub(&s_hist[hb], 0x80000000u);
-                        atomicAdd(&s_cnt[kCHist + hb], 0x80000000ull);
-                    }
-                }
-                // §8(d): 32 B offsets + 4 B path write (+ 32 B aggregates)
-                c_alg4 += (36 + ((MODE == kAdaptive || MODE == kForceErjs) && M::kAggregates ? 32 : 0)) / 4;
-                bool dead_row = false;
-                if (M::kUsesLabels && FAT) {
-                    // MetaPath row without an edge of label schema[step]: every
-                    // weight is 0 (models.hpp:99-104).  The reference burns the
-                    // 64·d trial cap, falls back to eRVS and finds no candidate;
-                    // the counters of that sequence are known in closed form
-                    // (samplers.hpp:156-177), so the walk ends here.
-                    const uint32_t want = p.mp.schema[step];
-                    dead_row = want < kMaskLabels && !(lmask & (1u << want)) &&
-                               (!erjs || (bound > 0.0 && isfinite(bound)));
-                }
-                if (dead_row) {
-                    if (erjs) {
-                        const ull c = p.cap_per_degree * (ull)deg;
-                        nret = 0;
-                        count_erjs(c > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)c);
-                        cnt_add(&s_cnt[kCFallbacks], 1);
-                    } else {
-                        lc_add(LC_ETRIALS1, 1);  // single-shot eRVS
-                    }
-                    lc_add(LC_EREADS, deg);  // the reservoir pass reads every weight, draws none
-                    c_alg4 += (uint32_t)(((8ull * deg + 31) / 32) * 8);
-                    cnt_add(&s_cnt[kCDeadEnds], 1);
-                    end_walk();
-                } else if (erjs) {
-                    if (!(bound > 0.0) || !isfinite(bound)) {  // samplers.hpp:152-154
-                        fail(kDevBadBound);
-                    } else {
-                        mnr = shortcut ? model.nonreturn_max(S) : __longlong_as_double(0x7ff0000000000000ll);
-                        const ull c = p.cap_per_degree * (ull)deg;
-                        cap = c > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)c;
-                        tn = rh = rc = 0;
-                        mb = nret = sel = 0;
-                        phase = P_TRIAL;
-                        if (cap == 0) {  // immediate cap overrun
-                            cnt_add(&s_cnt[kCFallbacks], 1);
-                            start_ervs(0);
-                        }
-                    }
-                } else {
-                    lc_add(LC_ETRIALS1, 1);  // single-shot kernels report one trial (samplers.hpp:22)
-                    start_ervs(0);
-                }
-            }
-        }
-
-        // ---- batched reservoir scans of short rows: lanes whose weights are
-        // all collected wait until kEBatch of them (or one that waited
-        // kEWait iterations) can run the scan in the same instruction stream
-        if (FAT) {
-            const unsigned ready = __ballot_sync(kFull, phase == P_EMATH);
-            if (ready) {
-                const bool go = __popc(ready) >= kEBatch ||
-                                __any_sync(kFull, phase == P_EMATH && tn >= kEWait);
-                if (phase == P_EMATH) {
-                    if (go) {
-                        const ull d0 = ev_load().didx;
-                        uint32_t bidx = 0;
-                        const ull d1 = ervs_scan_short(
-                            reinterpret_cast<const double*>(&s_rec[0][0][tid]), deg, key_of(), d0,
-                            &bidx);
-                        lc_add(LC_EREADS, deg);
-                        lc_add(LC_EDRAWS, d1 - d0);
-                        if (bidx == kInvalid) {  // all weights zero: dead end
-                            cnt_add(&s_cnt[kCDeadEnds], 1);
-                            end_walk();
-                        } else {
-                            ErvsState e = ev_load();
-                            e.didx = begin + bidx;  // its fat record starts the next step
-                            ev_store(e);
-                            phase = P_FETCH;
-                        }
-                    } else {
-                        ++tn;
-                    }
-                }
-            }
-        }
-
-        // ---- warp-cooperative eRVS for long rows (ballot hand-off)
-        unsigned coop = __ballot_sync(kFull, phase == P_COOP);
-        while (coop) {
-            const int L = __ffs(coop) - 1;
-            coop &= coop - 1;
-            Step T;
-            T.cur = __shfl_sync(kFull, cur, L);
-            T.prev = __shfl_sync(kFull, prev, L);
-            T.prev_degree = __shfl_sync(kFull, pdeg, L);
-            T.step = __shfl_sync(kFull, step, L);
-            T.degree = __shfl_sync(kFull, deg, L);
-            T.hmax = T.hsum = 0.0;
-            const uint32_t tph = __shfl_sync(kFull, phoff, L);
-            const ull tb = __shfl_sync(kFull, begin, L);
-            const ull q = p.qid_base + __shfl_sync(kFull, qi, L);
-            const WalkerKey K{p.seed_lo, p.seed_hi, (uint32_t)q, (uint32_t)(q >> 32), T.step};
-            const ull db = __shfl_sync(kFull, lane == L ? ev_load().didx : 0ull, L);
-            uint32_t nx = kInvalid, ni = 0;
-            ull dr = 0;
-            const int st = ervs_warp<M, kNoJump>(p.mp, T, K, g, tb, tph, db, &nx, &ni, &dr);
-            if (lane == L) {
-                if (st < 0) {
-                    fail(-st);
-                } else {
-                    lc_add(LC_EREADS, T.degree);
-                    lc_add(LC_EDRAWS, dr);
-                    if (nx == kInvalid) {
-                        cnt_add(&s_cnt[kCDeadEnds], 1);
-                        end_walk();
-                    } else if (FAT) {
-                        ErvsState e = ev_load();
-                        e.didx = tb + ni;
-                        ev_store(e);
-                        phase = P_FETCH;
-                    } else {
-                        // advance here (rare path); the node record comes next iteration
-                        prev = cur;
-                        pdeg = deg;
-                        phoff = hoff;
-                        plg = hash_log2_buckets(deg);
-                        cur = nx;
-                        ++step;
-                        if (p.paths) p.paths[qi * p.stride + step] = nx;
-                        if (step >= p.target)
-                            end_walk();
-                        else
-                            phase = P_NODE;
-                    }
-                }
-            }
-        }
-    }
-
-    // ---- flush counters: eRJS trials count as trials, reads and 2 draws each
-    __syncthreads();
-    if (tid < 66 && s_hist[tid]) s_cnt[kCHist + tid] += s_hist[tid];
-    const ull et = warp_sum((ull)s_lc[LC_ETRIALS][tid]), e1 = warp_sum((ull)s_lc[LC_ETRIALS1][tid]);
-    const ull er = warp_sum((ull)s_lc[LC_EREADS][tid]), ed = warp_sum((ull)s_lc[LC_EDRAWS][tid]);
-    const ull ea = warp_sum((ull)s_lc[LC_ALG4][tid]);
-    if (lane == 0) {
-        atomicAdd(&s_lct[LC_ETRIALS], et);
-        atomicAdd(&s_lct[LC_ETRIALS1], e1);
-        atomicAdd(&s_lct[LC_EREADS], er);
-        atomicAdd(&s_lct[LC_EDRAWS], ed);
-        atomicAdd(&s_lct[LC_ALG4], ea);
-    }
-    __syncthreads();
-    if (tid == 0) {
-        const ull t = s_lct[LC_ETRIALS];
-        s_cnt[kCTrials] = t + s_lct[LC_ETRIALS1];
-        s_cnt[kCWeightReads] = t + s_lct[LC_EREADS];
-        s_cnt[kCRngDraws] = 2 * t + s_lct[LC_EDRAWS];
-        s_cnt[kCAlgBytes] = 4 * s_lct[LC_ALG4];
-    }
-    __syncthreads();
-    for (int i = tid; i < kCNum; i += blockDim.x)
-        if (s_cnt[i]) atomicAdd(&p.counters[i], s_cnt[i]);
-}
 
 template <class M, int MODE, bool FAT>
 static cudaError_t launch_t(const WalkParams& p, int num_sms, cudaStream_t stream) {

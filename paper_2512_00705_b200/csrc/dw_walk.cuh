@@ -40,8 +40,10 @@ struct WalkParams {
 
 enum Mode : int { kAdaptive = 0, kForceErvs = 1, kForceErjs = 2, kErvsNoJump = 3 };
 
+#ifndef __CUDACC_RTC__
 // Launches the walk over p.nq walkers on `stream`; returns the CUDA error.
 cudaError_t launch_walk(int model_kind, bool weighted, int mode, const WalkParams& p,
                         int num_sms, cudaStream_t stream);
+#endif
 
 }  // namespace dwb

@@ -13,8 +13,10 @@
 // start, RunStats counters exactly as runtime.cpp:141-149, output independent
 // of the device count.  Errors surface as dynwalk::Error with the reference's
 // wording.  Options the GPU runtime does not implement (ForceIts, ForceAls,
-// check_bounds, bound_scale != 1, collect_cv, DslWalk models) throw
-// dynwalk::Error naming the option; the CPU run_queries still serves them.
+// check_bounds, bound_scale != 1, collect_cv) throw dynwalk::Error naming the
+// option; the CPU run_queries still serves them.  DslWalk models are compiled
+// into the walk kernel (dsl_codegen.hpp, dw_model_compile); their device
+// calibration is not supported, so pass CostModelParams explicitly.
 // Walker randomness is the Philox (seed, walker, step) stream, so paths equal
 // the reference samplers driven by that stream (tests/golden/ref_walks.json),
 // not the mt19937 stream of the CPU run_queries.
@@ -31,6 +33,7 @@
 #include <variant>
 #include <vector>
 
+#include "dsl_codegen.hpp"
 #include "dynwalk/cost_model.hpp"
 #include "dynwalk/runtime.hpp"
 #include "dynwalk_b200.h"
@@ -73,8 +76,26 @@ private:
 
 namespace detail {
 
+// A DslWalk compiled into the walk kernel (dsl_codegen.hpp + dw_model_compile),
+// cached by program source so each program compiles once per process.
+inline dw_custom_model_t compiled_dsl(const DslWalk& w) {
+    static std::mutex mu;
+    static std::map<std::string, dw_custom_model_t> cache;
+    const dsl::Program& prog = w.program();
+    const DslCode code = dsl_codegen(prog, w.analysis(), w.max_steps());
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(code.source);
+    if (it != cache.end()) return it->second;
+    dw_custom_model_t h = nullptr;
+    check(dw_model_compile(code.source.c_str(), w.max_steps(),
+                           code.label_aggregates ? DW_CUSTOM_LABEL_AGGREGATES : 0u, &h));
+    cache.emplace(code.source, h);
+    return h;
+}
+
 // AnyModel (models.hpp:200) -> dw_model_desc; the device functor is picked by
-// kind inside the library (compile-time specialised kernels).
+// kind inside the library (compile-time specialised kernels); a DslWalk is
+// compiled to its own kernel.
 struct ModelDesc {
     dw_model_desc d{};
     std::vector<std::uint16_t> schema;
@@ -98,12 +119,12 @@ inline ModelDesc to_desc(const AnyModel& model) {
             } else if constexpr (std::is_same_v<T, SecondOrderPr>) {
                 m.d.kind = DW_MODEL_PR2;
                 m.d.gamma = v.gamma;
+            } else if constexpr (std::is_same_v<T, DslWalk>) {
+                m.d.kind = DW_MODEL_CUSTOM;
+                m.d.custom = compiled_dsl(v);
             }
         },
         model);
-    if (std::holds_alternative<DslWalk>(model))
-        throw Error("model '" + model_name(model) +
-                    "' is a DSL model; the GPU runtime needs it compiled to a device functor");
     m.d.schema = m.schema.empty() ? nullptr : m.schema.data();
     m.d.schema_len = static_cast<std::uint32_t>(m.schema.size());
     return m;

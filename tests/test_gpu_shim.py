@@ -52,3 +52,30 @@ def test_shim_rejects_unsupported_options(tmp_path):
     p = subprocess.run([SHIM, "mode=force-its", f"out={tmp_path}/x"], capture_output=True,
                        text=True, timeout=120)
     assert p.returncode == 2 and "not supported" in p.stderr
+
+
+def test_shim_runs_dsl_models(ref, tmp_path):
+    """A DslWalk handed to dynwalk::gpu::run_queries is compiled into the walk
+    kernel by the shim (dsl_codegen.hpp + dw_model_compile) and equals the
+    reference DslWalk on the Philox stream."""
+    if not os.path.exists(SHIM):
+        pytest.skip("oracle/_ref/shim_check not built")
+    from tests.test_dsl import PROGRAMS
+    g = ref.RefGraph.gen("ba", 400, 6, 13).synth("uniform", 1.0, 5.0, seed=113)
+    g.synth("labels", 0, 3, seed=213)
+    q = np.arange(400, dtype=np.uint32)
+    for name in ("second_order", "label_degree"):
+        src = tmp_path / f"{name}.wf"
+        src.write_text(PROGRAMS[name])
+        out = str(tmp_path / name)
+        p = subprocess.run([SHIM, "graph=ba", "n=400", "deg=6", "gseed=13", "labels=0,3",
+                            f"dsl={src}", "L=25", "ratio=1.4", "seed=7", "mode=adaptive",
+                            f"out={out}"], capture_output=True, text=True, timeout=300)
+        assert p.returncode == 0, p.stderr
+        stats = json.loads(p.stdout.strip().splitlines()[-1])
+        paths = np.fromfile(out + ".paths", dtype=np.uint32).reshape(-1, 26)
+        ref.set_dsl_source(PROGRAMS[name])
+        r = ref.ref_run(g, ref.Model("dsl"), q, mode="adaptive", walk_length=25, seed=7,
+                        ratio=1.4, rng="philox", workers=2)
+        assert stats_core(stats) == stats_core(r.stats), name
+        assert np.array_equal(paths, r.paths), name
