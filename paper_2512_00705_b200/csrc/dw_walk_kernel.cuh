@@ -72,13 +72,6 @@ constexpr uint32_t kRing = DW_RING;  // queued trials per lane (power of two)
 constexpr uint32_t kGen = DW_GEN;    // Philox blocks per lane per iteration
 static_assert((kRing & (kRing - 1)) == 0, "kRing must be a power of two");
 constexpr uint32_t kCoopMinDegree = 64;
-#ifndef DW_SPEC
-#define DW_SPEC 0
-#endif
-#ifndef DW_SPEC_FRAC
-#define DW_SPEC_FRAC 0.5
-#endif
-constexpr double kSpecFrac = DW_SPEC_FRAC;
 #ifndef DW_EBATCH
 #define DW_EBATCH 8
 #endif
@@ -556,12 +549,6 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
             };
 #pragma unroll 1
             for (uint32_t gen = 0; gen < kGen && rc < kRing && tn < cap; ++gen) {
-#if DW_SPEC
-                // a second record is speculation (wasted when the head accepts):
-                // queue it only while the head is parked on a membership probe
-                // or its y is high enough that it is likely rejected
-                if (rc == 1 && !(mb & kParked) && s_y[rh][tid] < kSpecFrac * mnr) break;
-#endif
                 trial(philox4x32_10_rk(U4{tn, step, (uint32_t)q, (uint32_t)(q >> 32)}, p.rk));
             }
         } else if (phase == P_NODE) {
