@@ -524,11 +524,16 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                 cp16(&s_mb[1][tid], b + 4);
             }
             const ull q = p.qid_base + qi;
+            // step constants into registers once per iteration: the ring's
+            // shared-memory stores below would otherwise force a reload of
+            // the shared-memory state on every trial
+            const double bound_r = bound, mnr_r = mnr;
+            const uint32_t twlo_r = tw_lo, twcnt_r = tw_cnt, cap_r = cap;
             // one trial: free rejection, or queue its record gather in the ring
             auto trial = [&](const U4& b) {
                 const uint32_t x = (uint32_t)bounded(lo64(b), deg);  // draw 2t:   bounded(d)
-                const double y = uniform01(hi64(b)) * bound;          // draw 2t+1: uniform01()*c
-                if (!(y >= mnr && x - tw_lo >= tw_cnt)) {             // else rejected, no gather
+                const double y = uniform01(hi64(b)) * bound_r;        // draw 2t+1: uniform01()*c
+                if (!(y >= mnr_r && x - twlo_r >= twcnt_r)) {         // else rejected, no gather
                     const uint32_t k = (rh + rc) & (kRing - 1);
                     s_y[k][tid] = y;
                     s_t[k][tid] = tn;
@@ -548,7 +553,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                 ++tn;
             };
 #pragma unroll 1
-            for (uint32_t gen = 0; gen < kGen && rc < kRing && tn < cap; ++gen) {
+            for (uint32_t gen = 0; gen < kGen && rc < kRing && tn < cap_r; ++gen) {
                 trial(philox4x32_10_rk(U4{tn, step, (uint32_t)q, (uint32_t)(q >> 32)}, p.rk));
             }
         } else if (phase == P_NODE) {
