@@ -516,8 +516,11 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
         }
         if (__ballot_sync(kFull, phase != P_IDLE) == 0) break;
 
-        // ---- A: issue this iteration's gathers
-        if (phase == P_TRIAL) {
+        // ---- A: issue this iteration's gathers.  Independent blocks (not an
+        // if/else chain): a divergent warp skips the blocks none of its lanes
+        // need instead of serialising through a jump table (BRX)
+        const uint32_t ph0 = phase;
+        if (ph0 == P_TRIAL) {
             if (mb & kParked) {
                 const uint32_t* b = g.hslots + 8ull * (phoff + (mb & ~kParked));
                 cp16(&s_mb[0][tid], b);
@@ -556,22 +559,26 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
             for (uint32_t gen = 0; gen < kGen && rc < kRing && tn < cap_r; ++gen) {
                 trial(philox4x32_10_rk(U4{tn, step, (uint32_t)q, (uint32_t)(q >> 32)}, p.rk));
             }
-        } else if (phase == P_NODE) {
+        }
+        if (ph0 == P_NODE) {
             const char* nr = reinterpret_cast<const char*>(g.nodes + cur);
             cp16(&s_mb[0][tid], nr);
             cp16(&s_mb[1][tid], nr + 16);
             if (M::kLabelAgg) cp16(&s_rec[0][0][tid], g.lagg + cur);  // the ring is empty here
-        } else if (phase == P_FETCH) {
+        }
+        if (ph0 == P_FETCH) {
             const ull fe = ev_load().didx;
             const uint4* r = reinterpret_cast<const uint4*>(g.fat + fe);
             cp16(&s_rec[0][0][tid], r);
             cp16(&s_rec[0][1][tid], r + 1);
             cp16(&s_rec[0][2][tid], r + 2);
-        } else if (phase == P_VMEMB) {
+        }
+        if (ph0 == P_VMEMB) {
             const uint32_t* b = g.hslots + 8ull * (phoff + mb);
             cp16(&s_mb[0][tid], b);
             cp16(&s_mb[1][tid], b + 4);
-        } else if (phase == P_VREC) {
+        }
+        if (ph0 == P_VREC) {
             const ull e = begin + tn;
             sel = (uint32_t)(e & 1);
             cp16(&s_mb[0][tid], pair_of(g.edges, e));
@@ -581,9 +588,10 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
         cp_wait_all();
 
         // ---- C: consume; a finished step leaves its outcome in `next_ev`
+        // (blocks test the phase the lane had when this iteration started)
         enum : uint32_t { E_NONE = 0, E_FAT, E_ADV, E_NODE };
         uint32_t next_ev = E_NONE, next_slot = 0, next_u = 0;
-        if (phase == P_TRIAL) {
+        if (ph0 == P_TRIAL) {
             int acc = -1;
             const Step S = mkstep(0.0, 0.0);
             if (mb & kParked) {  // resolve the head's membership probe
@@ -669,11 +677,14 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                     start_ervs(2ull * tn);
                 }
             }
-        } else if (phase == P_NODE) {
+        }
+        if (ph0 == P_NODE) {
             next_ev = E_NODE;
-        } else if (phase == P_FETCH) {
+        }
+        if (ph0 == P_FETCH) {
             next_ev = E_FAT;
-        } else if (phase == P_VMEMB || phase == P_VREC) {
+        }
+        if (ph0 == P_VMEMB || ph0 == P_VREC) {
             uint32_t u;
             float h;
             uint16_t lab = 0;
