@@ -535,11 +535,38 @@ struct RunOut {
     ull flat_cap = 0;
 };
 
-// Walkers per batch: ~8 batches per device so H2D/D2H overlap the walks, at
-// least 256K walkers per launch, at most 4M (1.3 GB of padded paths at L=80)
+// Walkers per batch: ~4 batches per device so H2D/D2H overlap the walks (each
+// launch ends in a ~1 ms tail while its last walkers finish, so fewer is
+// better; batch_plan shortens the last ones), at least 256K walkers per
+// launch, at most 4M (1.3 GB of padded paths at L=80)
 ull batch_size(ull n) {
-    const ull want = (n + 7) / 8;
+    if (const char* env = std::getenv("DW_BATCH"))  // experiments: fixed walkers per batch
+        if (std::atoll(env) > 0) return std::min<ull>(std::max<ull>(n, 1), (ull)std::atoll(env));
+    ull div = 4;
+    if (const char* env = std::getenv("DW_BATCH_DIV")) div = std::max(1, std::atoi(env));
+    const ull want = (n + div - 1) / div;
     return std::max<ull>(1, std::min<ull>(n, std::max<ull>(1ull << 18, std::min<ull>(want, 1ull << 22))));
+}
+
+// Batch boundaries of one device's n walkers: batches of batch_size(n), the
+// last two batches' worth split geometrically (1/2, 1/4, 1/8, 1/8) so the copy
+// of the final batch, which nothing overlaps, is short.  `cap` bounds every
+// batch (the ring slot size).
+std::vector<ull> batch_plan(ull n, ull cap) {
+    std::vector<ull> at{0};
+    if (n == 0) return at;
+    const ull bs = std::min(cap, batch_size(n));
+    ull pos = 0;
+    while (n - pos > 2 * bs) at.push_back(pos += bs);
+    ull rem = n - pos;
+    if (rem > bs && !std::getenv("DW_BATCH")) {
+        for (int k = 0; k < 3 && rem >= 4 * (1ull << 16); ++k) {
+            at.push_back(pos += rem / 2);
+            rem -= rem / 2;
+        }
+    }
+    while (pos < n) at.push_back(pos = std::min(n, pos + bs));
+    return at;
 }
 
 // The batched H2D -> walk -> (compaction) -> D2H pipeline behind dw_run and
@@ -553,6 +580,7 @@ int run_engine(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries
     const ull stride = (ull)opts->walk_length + 1;
     struct Dev {
         ull lo = 0, n = 0, bs = 1, nb = 0, eb = 0, db = 0, end = 0;
+        std::vector<ull> at;  // batch starts (batch_plan), at[nb] == n
     };
     std::vector<Dev> dv(nd);
     cudaEvent_t wall0 = nullptr, wall1 = nullptr;
@@ -568,7 +596,8 @@ int run_engine(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries
         d.lo = nq * di / nd;
         d.n = nq * (di + 1) / nd - d.lo;
         d.bs = out.text ? std::min<ull>(batch_size(d.n), 1ull << 20) : batch_size(d.n);
-        d.nb = d.n ? (d.n + d.bs - 1) / d.bs : 0;
+        d.at = batch_plan(d.n, d.bs);
+        d.nb = d.at.size() - 1;
         CU(cudaSetDevice(r.device), "cudaSetDevice");
         if ((rc = prepare_model(r, model))) return rc;
         if ((rc = ensure_ring(r, d.bs, stride, out.compact, out.text != nullptr))) return rc;
@@ -582,17 +611,18 @@ int run_engine(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries
         Replica& r = g->reps[di];
         Dev& d = dv[di];
         Replica::Slot& sl = r.slots[b % kRingSlots];
-        const ull blo = b * d.bs, bn = std::min(d.bs, d.n - blo);
+        const ull blo = d.at[b], bn = d.at[b + 1] - blo;
+        cudaStream_t ws = r.stream;
         CU(cudaSetDevice(r.device), "cudaSetDevice");
         if (b >= (ull)kRingSlots) {  // the slot's previous batch must be walked and drained
             CU(cudaStreamWaitEvent(r.copy, sl.walk, 0), "event");
-            CU(cudaStreamWaitEvent(r.stream, sl.d2h, 0), "event");
+            CU(cudaStreamWaitEvent(ws, sl.d2h, 0), "event");
         }
         CU(cudaMemcpyAsync(sl.q, queries + d.lo + blo, bn * sizeof(uint32_t),
                            cudaMemcpyHostToDevice, r.copy),
            "H2D queries");
         CU(cudaEventRecord(sl.h2d, r.copy), "event");
-        CU(cudaStreamWaitEvent(r.stream, sl.h2d, 0), "event");
+        CU(cudaStreamWaitEvent(ws, sl.h2d, 0), "event");
         dwb::WalkParams p = make_params(r, model, opts);
         p.queries = sl.q;
         p.nq = bn;
@@ -600,28 +630,26 @@ int run_engine(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries
         p.paths = (out.compact || out.text || out.paths) ? sl.paths : nullptr;
         p.lengths = sl.len;
         p.next_walker = r.queues + (b % kRingSlots);
-        CU(cudaMemsetAsync(p.next_walker, 0, sizeof(ull), r.stream), "memset");
+        CU(cudaMemsetAsync(p.next_walker, 0, sizeof(ull), ws), "memset");
         if (p.paths && !out.compact && !out.text)  // compaction copies only the written ids
-            CU(cudaMemsetAsync(p.paths, 0xFF, bn * stride * sizeof(uint32_t), r.stream),
+            CU(cudaMemsetAsync(p.paths, 0xFF, bn * stride * sizeof(uint32_t), ws),
                "memset paths");
-        CU(launch_model(r, model, opts->mode, p, r.stream), "walk");
+        CU(launch_model(r, model, opts->mode, p, ws), "walk");
         ++launches;
         if (out.compact) {
             size_t tb = r.scan_bytes;
-            CU(dwb::path_offsets(sl.len, bn, sl.offs, r.d_base, r.d_scan, tb, r.stream), "scan");
-            CU(dwb::compact_paths(sl.paths, sl.len, bn, stride, sl.offs, sl.flat, r.stream),
-               "compact");
+            CU(dwb::path_offsets(sl.len, bn, sl.offs, r.d_base, r.d_scan, tb, ws), "scan");
+            CU(dwb::compact_paths(sl.paths, sl.len, bn, stride, sl.offs, sl.flat, ws), "compact");
             launches += 5;
         } else if (out.text) {  // write_paths bytes, formatted on the device
             uint32_t* bytes = sl.flat;
             size_t tb = r.scan_bytes;
-            CU(dwb::path_text_bytes(sl.paths, sl.len, bn, stride, bytes, r.stream), "text");
-            CU(dwb::path_offsets(bytes, bn, sl.offs, r.d_base, r.d_scan, tb, r.stream), "scan");
-            CU(dwb::path_text_write(sl.paths, sl.len, bn, stride, sl.offs, sl.txt, r.stream),
-               "text");
+            CU(dwb::path_text_bytes(sl.paths, sl.len, bn, stride, bytes, ws), "text");
+            CU(dwb::path_offsets(bytes, bn, sl.offs, r.d_base, r.d_scan, tb, ws), "scan");
+            CU(dwb::path_text_write(sl.paths, sl.len, bn, stride, sl.offs, sl.txt, ws), "text");
             launches += 6;
         }
-        CU(cudaEventRecord(sl.walk, r.stream), "event");
+        CU(cudaEventRecord(sl.walk, ws), "event");
         if (out.compact || out.text) {
             CU(cudaStreamWaitEvent(r.ends, sl.walk, 0), "event");
             CU(cudaMemcpyAsync(r.h_ends + (b % kRingSlots), sl.offs + bn, sizeof(ull),
@@ -649,7 +677,7 @@ int run_engine(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries
         Dev& d = dv[di];
         Replica::Slot& sl = r.slots[b % kRingSlots];
         if (!out.compact && !out.text) return DW_OK;  // the D2H was enqueued with the walk
-        const ull blo = b * d.bs, bn = std::min(d.bs, d.n - blo);
+        const ull blo = d.at[b], bn = d.at[b + 1] - blo;
         CU(cudaSetDevice(r.device), "cudaSetDevice");
         CU(cudaEventSynchronize(sl.end), "walk");
         const ull end = r.h_ends[b % kRingSlots];
@@ -673,7 +701,10 @@ int run_engine(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries
         }
         if (end > d.end) {
             if (!out.flat) return fail(DW_EINVAL, "flat is NULL");
-            CU(cudaMemcpyAsync(out.flat + gbase + d.end, sl.flat, (end - d.end) * sizeof(uint32_t),
+            // every walk full length: the padded rows are the flat layout and
+            // compact_paths skipped the copy
+            const uint32_t* src = (end - d.end == bn * stride) ? sl.paths : sl.flat;
+            CU(cudaMemcpyAsync(out.flat + gbase + d.end, src, (end - d.end) * sizeof(uint32_t),
                                cudaMemcpyDeviceToHost, r.d2h),
                "D2H paths");
         }

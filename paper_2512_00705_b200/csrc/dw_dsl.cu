@@ -108,7 +108,7 @@ cudaError_t launch_custom(const dw_custom_model_s* cm_, int mode, const WalkPara
         }
     }
     cudaKernel_t k = cm->kernels[mode];
-    constexpr int kThreadsRtc = 256;
+    constexpr int kThreadsRtc = kThreads;
     const size_t smem = sizeof(WalkSmem);
     if (!cm->attr_set[mode]) {
         e = cudaKernelSetAttributeForDevice(k, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -681,26 +681,48 @@ cudaError_t path_offsets(const uint32_t* lengths, ull n, ull* offs, ull* d_base,
     return cudaGetLastError();
 }
 
-__global__ void compact_paths_kernel(const uint32_t* __restrict__ paths,
-                                     const uint32_t* __restrict__ len, ull n, ull stride,
-                                     const ull* __restrict__ offs, uint32_t* __restrict__ flat) {
+// Padded [n][stride] rows -> flat ids at offs[i] - offs[0].  A block owns
+// kCompactRows rows and walks their padded elements with consecutive threads on
+// consecutive ids (coalesced both ways); row/column advance incrementally.
+// Every row full (no dead end, no early stop) means the padded rows already
+// are the flat layout: the kernel returns and the engine copies the padded
+// buffer (dw_capi.cu drain).
+constexpr int kCompactRows = 128;
+__global__ void __launch_bounds__(256) compact_paths_kernel(
+    const uint32_t* __restrict__ paths, const uint32_t* __restrict__ len, ull n, ull stride,
+    const ull* __restrict__ offs, uint32_t* __restrict__ flat) {
     const ull flat_base = offs[0];
-    const ull warp = (blockIdx.x * (ull)blockDim.x + threadIdx.x) >> 5;
-    const ull nwarps = ((ull)gridDim.x * blockDim.x) >> 5;
-    const uint32_t lane = threadIdx.x & 31;
-    for (ull i = warp; i < n; i += nwarps) {
-        const uint32_t l = len[i];
-        const uint32_t* src = paths + i * stride;
-        uint32_t* dst = flat + (offs[i] - flat_base);
-        for (uint32_t j = lane; j < l; j += 32) dst[j] = src[j];
+    if (offs[n] - flat_base == n * stride) return;
+    __shared__ ull s_off[kCompactRows];
+    __shared__ uint32_t s_len[kCompactRows];
+    for (ull r0 = (ull)blockIdx.x * kCompactRows; r0 < n; r0 += (ull)gridDim.x * kCompactRows) {
+        const ull rows = min((ull)kCompactRows, n - r0);
+        __syncthreads();
+        for (int t = threadIdx.x; t < (int)rows; t += blockDim.x) {
+            s_len[t] = len[r0 + t];
+            s_off[t] = offs[r0 + t] - flat_base;
+        }
+        __syncthreads();
+        const ull total = rows * stride;
+        ull i = threadIdx.x / stride, j = threadIdx.x % stride;
+        const uint32_t* src = paths + r0 * stride;
+        for (ull k = threadIdx.x; k < total; k += blockDim.x) {
+            if (j < s_len[i]) flat[s_off[i] + j] = src[k];
+            j += blockDim.x;
+            if (j >= stride) {
+                const ull q = j / stride;
+                i += q;
+                j -= q * stride;
+            }
+        }
     }
 }
 
 cudaError_t compact_paths(const uint32_t* paths, const uint32_t* lengths, ull n, ull stride,
                           const ull* offs, uint32_t* flat, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    compact_paths_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(paths, lengths, n, stride, offs,
-                                                               flat);
+    compact_paths_kernel<<<grid_for(n, kCompactRows), 256, 0, s>>>(paths, lengths, n, stride,
+                                                                  offs, flat);
     return cudaGetLastError();
 }
 

@@ -67,7 +67,10 @@ namespace dwb {
 #ifndef DW_GEN
 #define DW_GEN 4
 #endif
-constexpr int kThreads = 256;
+#ifndef DW_THREADS
+#define DW_THREADS 256
+#endif
+constexpr int kThreads = DW_THREADS;
 constexpr uint32_t kRing = DW_RING;  // queued trials per lane (power of two)
 constexpr uint32_t kGen = DW_GEN;    // Philox blocks per lane per iteration
 static_assert((kRing & (kRing - 1)) == 0, "kRing must be a power of two");
@@ -368,6 +371,9 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
         }
     };
 
+    // a block's 32-bit histogram cells cannot overflow unless the launch
+    // walks 2^32 steps in total
+    const bool hist_wide = __umul64hi(p.nq, (ull)p.target) != 0 || p.nq * (ull)p.target >= 0xFFFFFFFFull;
     M model(p.mp);
     const int lane = tid & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -376,6 +382,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
 
     uint32_t phase = P_IDLE;
     bool drained = false;  // warp-uniform
+    uint32_t nrefill = 0;  // warp-uniform
     ull qi = 0;
     // walker state
     uint32_t prev = kInvalid, pdeg = 0, step = 0, deg = 0;
@@ -479,7 +486,8 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
         // ---- refill idle lanes: one atomic per warp (runtime.cpp:209-211)
         unsigned need = __ballot_sync(kFull, phase == P_IDLE);
         if (need && !drained) {
-            if (*(volatile int*)p.error != 0) drained = true;  // abandon after an error
+            // abandon after an error (polled on every 16th refill of the warp)
+            if ((nrefill++ & 15u) == 0 && *(volatile int*)p.error != 0) drained = true;
             drained = __any_sync(kFull, drained);
             while (need && !drained) {
                 const int leader = __ffs(need) - 1;
@@ -488,10 +496,11 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                 if (lane == leader) base = atomicAdd(p.next_walker, (ull)n);
                 base = __shfl_sync(kFull, base, leader);
                 if (base + (ull)n >= p.nq) drained = true;
+                if (lane == leader && base < p.nq)  // one counter add per claim
+                    cnt_add(&s_cnt[kCQueries], min((ull)n, p.nq - base));
                 if (phase == P_IDLE) {
                     const ull i = base + (ull)__popc(need & lt_mask);
                     if (i < p.nq) {
-                        cnt_add(&s_cnt[kCQueries], 1);
                         const uint32_t start = p.queries[i];
                         if (start >= g.nv) {  // runtime.cpp:213-217
                             cnt_add(&s_cnt[kCQueryErrors], 1);
@@ -825,7 +834,9 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                 }
                 {
                     const uint32_t hb = 2 * degree_bucket(deg) + (erjs ? 1 : 0);
-                    if (atomicAdd(&s_hist[hb], 1u) == 0x7FFFFFFFu) {  // spill before overflow
+                    if (!hist_wide) {
+                        atomicAdd(&s_hist[hb], 1u);  // no result to wait for
+                    } else if (atomicAdd(&s_hist[hb], 1u) == 0x7FFFFFFFu) {  // spill before overflow
                         atomicSub(&s_hist[hb], 0x80000000u);
                         atomicAdd(&s_cnt[kCHist + hb], 0x80000000ull);
                     }
