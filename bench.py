@@ -53,6 +53,12 @@ CONFIGS = {
     4: dict(scale=25, model="pr2", gamma=0.15, weights="pareto", labels=None,
             desc="second-order PR gamma=0.15 (no restart in the reference, SURVEY 7.3), "
                  "R-MAT/Kronecker s25 ef16, Pareto alpha=1 weights"),
+    # 10 walkers per vertex (qid = r*V + v): 1.34B walkers, 435 GB of paths per
+    # pass, so the timed pass keeps lengths only (paths discarded on the device)
+    5: dict(scale=27, model="node2vec", a=0.5, b=2.0, weights="uniform", labels=None,
+            walkers_per_vertex=10, discard_paths=True,
+            desc="node2vec p=0.5 q=2, walk length 80, 10 walkers per vertex, weighted R-MAT "
+                 "s27 ef16 (2.1B edges in one GPU's HBM), paths discarded on the device"),
 }
 TOPO_SEED, WEIGHT_SEED, WALK_SEED, PROFILE_SEED, LABEL_SEED = 1, 2, 7, 5, 3
 
@@ -107,7 +113,8 @@ def workload(args) -> dict:
             else c["desc"] + f" (run at scale {args.scale})",
             "graph": f"rmat s{args.scale} ef16 (A,B,C,D)=(.57,.19,.19,.05), mirrored, {w}",
             "model": c["model"], **{k: v for k, v in model_kw(c).items() if k != "schema"},
-            "walk_length": args.walk_length, "mode": args.mode, "walkers": 2 ** args.scale,
+            "walk_length": args.walk_length, "mode": args.mode,
+            "walkers": c.get("walkers_per_vertex", 1) * 2 ** args.scale,
             "l2": "inputs larger than L2 (graph >= 2 GB vs 126 MB L2), no flush"}
 
 
@@ -257,22 +264,40 @@ def run_ours(args):
                          qid_base=rank * nv)
     lib = dw.load_library()
     q = torch.arange(lo, hi, dtype=torch.int64, device=dev).to(torch.int32)
-    paths = torch.empty((max(n, 1), L + 1), dtype=torch.int32, device=dev)
+    wpv = cfg.get("walkers_per_vertex", 1)
+    discard = cfg.get("discard_paths", False)
+    paths = None if discard else torch.empty((max(n, 1), L + 1), dtype=torch.int32, device=dev)
     lengths = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
-    mdesc, odesc = model.c(), opts.c()
+    mdesc = model.c()
+    # one launch per walker round r (qid = (rank * wpv + r) * V + v)
+    odescs = [dw.RunOptions(mode=args.mode, walk_length=L, seed=WALK_SEED, edge_cost_ratio=ratio,
+                            qid_base=(rank * wpv + r) * nv).c() for r in range(wpv)]
+    odesc = odescs[0]
+    graph_bytes = torch.cuda.mem_get_info(dev)
 
     def step():
-        rc = lib.dw_run_device(dg.h, 0, C.byref(mdesc), C.c_void_p(q.data_ptr()), n,
-                               C.byref(odesc), C.c_void_p(paths.data_ptr()),
-                               C.c_void_p(lengths.data_ptr()), C.c_void_p(stream.cuda_stream))
-        if rc:
-            raise dw.DynwalkError(rc, lib.dw_last_error().decode())
-        st = dw.RunStatsC()
-        rc = lib.dw_run_device_sync(dg.h, 0, C.byref(st))
-        if rc:
-            raise dw.DynwalkError(rc, lib.dw_last_error().decode())
-        return st
+        agg = None
+        for od in odescs:
+            rc = lib.dw_run_device(dg.h, 0, C.byref(mdesc), C.c_void_p(q.data_ptr()), n,
+                                   C.byref(od), C.c_void_p(paths.data_ptr() if paths is not None
+                                                           else None),
+                                   C.c_void_p(lengths.data_ptr()), C.c_void_p(stream.cuda_stream))
+            if rc:
+                raise dw.DynwalkError(rc, lib.dw_last_error().decode())
+            st = dw.RunStatsC()
+            rc = lib.dw_run_device_sync(dg.h, 0, C.byref(st))
+            if rc:
+                raise dw.DynwalkError(rc, lib.dw_last_error().decode())
+            if agg is None:
+                agg = st
+            else:
+                for k in ("steps", "select_erjs", "select_ervs", "trials", "weight_reads",
+                          "rng_draws", "erjs_fallbacks", "dead_ends", "algorithmic_bytes",
+                          "kernel_launches"):
+                    setattr(agg, k, getattr(agg, k) + getattr(st, k))
+                agg.kernel_ms += st.kernel_ms
+        return agg
 
     if args.profile_only:
         step()
@@ -309,7 +334,7 @@ def run_ours(args):
     # dw_run_compact returns RunResult.paths flattened (offsets + ids), so only
     # ids that exist cross PCIe
     e2e = None
-    if args.e2e_steps > 0 and n > 0:
+    if args.e2e_steps > 0 and n > 0 and wpv == 1 and not discard:
         hq = C.c_void_p()
         ho = C.c_void_p()
         hf = C.c_void_p()
@@ -350,7 +375,7 @@ def run_ours(args):
 
     # ---- CPU baseline (oracle port, host cores), rank 0 at N=1 only
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.scale <= 24:
         cpu = cpu_baseline_port(dg, args, ratio, nv)
 
     if rank != 0:
@@ -386,7 +411,8 @@ def run_ours(args):
             "steps", "select_erjs", "select_ervs", "trials", "weight_reads", "rng_draws",
             "erjs_fallbacks", "dead_ends")},
         "setup_s": {"graph_build": build_s, "calibration": calib_s},
-        "graph": info,
+        "graph": dict(info, device_free_after_build_gb=graph_bytes[0] / 1e9,
+                      device_total_gb=graph_bytes[1] / 1e9),
     }
     print(json.dumps(out), flush=True)
 

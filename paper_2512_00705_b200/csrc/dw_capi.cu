@@ -274,6 +274,7 @@ int upload_replica(Replica& r, const dw_graph_desc* d) {
     cudaFree(prop);
     cudaFree(nmax);
     cudaFree(nsum);
+    CU(dwb::finish_graph(r.g, s), "fat records");
     return DW_OK;
 }
 
@@ -991,6 +992,10 @@ extern "C" int dw_graph_load_dwg1(const char* path, const int* devices, int ndev
         CU(cudaStreamSynchronize(r.stream), "pack");
     }
     free_all();
+    for (auto& r : g->reps) {
+        CU(cudaSetDevice(r.device), "cudaSetDevice");
+        CU(dwb::finish_graph(r.g, r.stream), "fat records");
+    }
     g->nv = nv;
     g->ne = ne;
     g->has_labels = labels != 0;
@@ -1039,7 +1044,7 @@ int dw_graph_create(const dw_graph_desc* desc, const int* devices, int ndev, dw_
 int dw_graph_generate_rmat(const dw_rmat_desc* d, const int* devices, int ndev, dw_graph_t* out) {
     if (!out || !d) return fail(DW_EINVAL, "NULL argument");
     *out = nullptr;
-    if (d->scale > 30 || d->edge_factor < 2 || (2ull * (d->edge_factor / 2) << d->scale) > 0x7FFFFFFFull)
+    if (d->scale > 30 || d->edge_factor < 2 || (2ull * (d->edge_factor / 2) << d->scale) > (1ull << 34))
         return fail(DW_EINVAL, "rmat: scale %u / edge factor %u out of range", d->scale,
                     d->edge_factor);
     if (d->weights == 0 && !(d->low > 0.0 && d->low < d->high))

@@ -12,6 +12,7 @@
 #include <cub/device/device_segmented_sort.cuh>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -199,16 +200,46 @@ __global__ void fat_build_kernel(const NodeRec* __restrict__ nodes, uint32_t nv,
     }
 }
 
+// Above ~100 GB of fat records the walk slows down instead of speeding up:
+// measured on one B200, node2vec (0.5, 2), walker-steps/s fat vs slim:
+// s25 (34 GB of records) 6.04e9 vs 4.19e9, s26 (69 GB) 5.87e9 vs 4.20e9,
+// s27 (137 GB) 3.27e9 vs 4.42e9 (random gathers spread over 175 GB of HBM).
+// DW_FAT=0 disables the layout, DW_FAT=1 builds it whenever it fits.
+constexpr unsigned long long kFatMaxBytes = 96ull * 1000 * 1000 * 1000;
+
 static cudaError_t build_fat(DeviceGraphBuffers& g, cudaStream_t s) {
     g.fat = nullptr;
-    if (const char* env = getenv("DW_FAT"))
+    bool force = false;
+    if (const char* env = getenv("DW_FAT")) {
         if (env[0] == '0') return cudaSuccess;
+        force = env[0] == '1';
+    }
     if (g.ne == 0 || g.ne > kBeginMask) return cudaSuccess;
-    // the fat layout is an accelerator: skip it when it would crowd HBM
+    if (!force && g.ne * sizeof(FatRec) > kFatMaxBytes) {
+        if (getenv("DW_VERBOSE"))
+            fprintf(stderr, "dynwalk: fat records skipped (%.1f GB above the %.0f GB cap)\n",
+                    g.ne * sizeof(FatRec) / 1e9, kFatMaxBytes / 1e9);
+        return cudaSuccess;
+    }
+    // the fat layout is an accelerator: skip it when it would crowd HBM.
+    // Build temporaries freed with cudaFreeAsync stay in the stream-ordered
+    // pool until trimmed; return them first so they count as free.
+    DW_TRY(cudaStreamSynchronize(s));
+    {
+        int dev = 0;
+        cudaMemPool_t pool;
+        DW_TRY(cudaGetDevice(&dev));
+        DW_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
+        DW_TRY(cudaMemPoolTrimTo(pool, 0));
+    }
     size_t free_b = 0, total_b = 0;
     DW_TRY(cudaMemGetInfo(&free_b, &total_b));
     const ull need = g.ne * sizeof(FatRec);
-    if (need + (4ull << 30) > free_b) return cudaSuccess;
+    const bool fits = need + (4ull << 30) <= free_b;
+    if (getenv("DW_VERBOSE"))
+        fprintf(stderr, "dynwalk: fat records %s (%.1f GB needed, %.1f GB free)\n",
+                fits ? "built" : "skipped", need / 1e9, free_b / 1e9);
+    if (!fits) return cudaSuccess;
     DW_TRY(cudaMallocAsync(&g.fat, need, s));
     uint8_t* lmask = nullptr;
     if (g.labels) {
@@ -278,9 +309,10 @@ cudaError_t pack_graph(const ull* d_row, const uint32_t* d_col, const float* d_p
     DW_TRY(cudaStreamSynchronize(s));
     g.max_degree = h;
     DW_TRY(cudaFreeAsync(d_maxd, s));
-    DW_TRY(build_member_index(g, s));
-    return build_fat(g, s);
+    return build_member_index(g, s);
 }
+
+cudaError_t finish_graph(DeviceGraphBuffers& g, cudaStream_t s) { return build_fat(g, s); }
 
 __global__ void unpack_kernel(const NodeRec* __restrict__ nodes, const EdgeRec* __restrict__ edges,
                               uint32_t nv, ull ne, ull* row, uint32_t* col, float* prop,
@@ -421,7 +453,7 @@ cudaError_t build_rmat(const RmatSpec& spec, DeviceGraphBuffers& g, cudaStream_t
     const uint32_t nv = 1u << spec.scale;
     const ull ns = (ull)(spec.edge_factor / 2) * nv;
     const ull nkeys = 2 * ns;
-    if (nkeys > 0x7FFFFFFFull) return cudaErrorInvalidValue;  // cub int item counts
+    if (nkeys > (1ull << 34)) return cudaErrorInvalidValue;
     const ull ks = host_derive_seed(spec.seed, 0x726d6174ULL);
     const ull pk = host_derive_seed(spec.seed, 0x7065726dULL);
 
@@ -435,11 +467,12 @@ cudaError_t build_rmat(const RmatSpec& spec, DeviceGraphBuffers& g, cudaStream_t
 
     cub::DoubleBuffer<ull> db(keys, keys_alt);
     size_t tmp_bytes = 0;
-    DW_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, db, (int)nkeys, 0,
+    // 64-bit item count: s27 draws 2^31 directed keys
+    DW_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, db, (long long)nkeys, 0,
                                           32 + spec.scale + 1, s));
     void* tmp = nullptr;
     DW_TRY(cudaMallocAsync(&tmp, tmp_bytes, s));
-    DW_TRY(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, db, (int)nkeys, 0, 32 + spec.scale + 1,
+    DW_TRY(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, db, (long long)nkeys, 0, 32 + spec.scale + 1,
                                           s));
     DW_TRY(cudaFreeAsync(tmp, s));
     ull loops = 0;
@@ -474,7 +507,7 @@ cudaError_t build_rmat(const RmatSpec& spec, DeviceGraphBuffers& g, cudaStream_t
     DW_TRY(cudaFreeAsync(keys_alt, s));
     DW_TRY(cudaFreeAsync(d_loops, s));
     DW_TRY(cudaFreeAsync(row, s));
-    return cudaStreamSynchronize(s);
+    return finish_graph(g, s);  // after the sort buffers are gone
 }
 
 // ---- K4: calibration (cost_model.cpp:37-126) -------------------------------

@@ -24,6 +24,11 @@ cudaError_t pack_graph(const unsigned long long* d_row, const uint32_t* d_col, c
                        const double* d_nmax, const double* d_nsum, DeviceGraphBuffers& out,
                        cudaStream_t s);
 
+// Optional accelerators built once the packed graph is final and the build's
+// temporaries are freed: the fat edge records (skipped when they would crowd
+// HBM).  Every graph constructor calls it last.
+cudaError_t finish_graph(DeviceGraphBuffers& g, cudaStream_t s);
+
 // R-MAT topology + mirrored CSR + Philox weights/labels on the device.
 // Definition identical to oracle.c orc_gen_rmat / orc_synth_philox.
 struct RmatSpec {
