@@ -81,6 +81,22 @@ int main(int argc, char** argv) {
         params.edge_cost_ratio = std::stod(get("ratio", "1.2"));
         const std::vector<dw::VertexId> queries = dw::all_vertices(g);
 
+        // sweep=a1,a2,...: dynwalk::gpu::selection_ratio_sweep, one JSON row per alpha
+        if (get("sweep", "") != "") {
+            std::vector<double> alphas;
+            std::istringstream as(get("sweep", ""));
+            for (std::string t; std::getline(as, t, ',');) alphas.push_back(std::stod(t));
+            const auto rows = dw::gpu::selection_ratio_sweep(g, model, params, alphas, queries, opts);
+            std::cout << "[";
+            for (std::size_t i = 0; i < rows.size(); ++i)
+                std::cout << (i ? "," : "") << "{\"alpha\":" << rows[i].alpha
+                          << ",\"erjs_steps\":" << rows[i].erjs_steps
+                          << ",\"ervs_steps\":" << rows[i].ervs_steps
+                          << ",\"pct_erjs\":" << rows[i].pct_erjs << "}";
+            std::cout << "]" << std::endl;
+            return 0;
+        }
+
         const dw::RunResult rr = dw::gpu::run_queries(g, model, params, queries, opts);
 
         const std::string out = get("out", "shim_out");

@@ -7,6 +7,8 @@
 //     -> dynwalk::gpu::run_queries(g, model, params, queries, opts)  (same signature)
 //   dynwalk::profile_edge_cost_ratio(g, model, cfg)                cost_model.hpp:39-40
 //     -> dynwalk::gpu::profile_edge_cost_ratio(g, model, cfg)
+//   dynwalk::selection_ratio_sweep(base, model, params, alphas, q, opts)  runtime.hpp:99-103
+//     -> dynwalk::gpu::selection_ratio_sweep(...)                        (same signature)
 //
 // Semantics kept: query order, path[0] = start, length
 // <= min(L, max_steps) + 1, empty path + query_errors++ for an out-of-range
@@ -23,6 +25,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cstring>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -35,6 +38,8 @@
 
 #include "dsl_codegen.hpp"
 #include "dynwalk/cost_model.hpp"
+#include "dynwalk/graph.hpp"
+#include "dynwalk/rng.hpp"
 #include "dynwalk/runtime.hpp"
 #include "dynwalk_b200.h"
 
@@ -142,15 +147,50 @@ inline int to_mode(SamplerMode mode) {
     return -1;
 }
 
-// Cached replicas keyed by graph identity (arrays are never mutated in place:
-// set_edge_props replaces the vector, which changes the data pointer).
+// FNV-1a over a strided sample (<= ~4K positions) of every CSR array.  Graphs
+// built in a loop (selection_ratio_sweep, repeated synthesize_weights) free and
+// reallocate their vectors, and a new graph can land on the old addresses; the
+// sample tells such graphs apart at O(4K) cost per call.
+inline std::uint64_t sample_fingerprint(const Graph& g) {
+    std::uint64_t h = 1469598103934665603ull;
+    auto mix = [&h](std::uint64_t v) {
+        h ^= v;
+        h *= 1099511628211ull;
+    };
+    auto sample = [&mix](auto span) {
+        const std::size_t n = span.size();
+        const std::size_t step = std::max<std::size_t>(1, n / 4096);
+        mix(n);
+        for (std::size_t i = 0; i < n; i += step) {
+            std::uint64_t v = 0;
+            std::memcpy(&v, &span[i], sizeof(span[i]));
+            mix(v);
+        }
+        if (n) {
+            std::uint64_t v = 0;
+            std::memcpy(&v, &span[n - 1], sizeof(span[n - 1]));
+            mix(v);
+        }
+    };
+    sample(g.row_offsets());
+    sample(g.col_indices());
+    sample(g.edge_props());
+    if (g.has_labels()) sample(g.edge_labels());
+    return h;
+}
+
+// Cached replicas keyed by graph identity: addresses plus the sampled content
+// fingerprint (arrays are never mutated in place: set_edge_props replaces the
+// vector).  An edit that touches none of the sampled positions is not seen;
+// callers that rewrite graphs in place should pass a DeviceGraph explicitly.
 inline std::shared_ptr<DeviceGraph> cached(const Graph& g) {
-    using Key = std::tuple<const Graph*, const void*, const void*, const void*, std::uint64_t>;
+    using Key = std::tuple<const Graph*, const void*, const void*, const void*, std::uint64_t,
+                           std::uint64_t>;
     static std::mutex mu;
     static std::map<Key, std::shared_ptr<DeviceGraph>> cache;
     const Key k{&g, g.col_indices().data(), g.edge_props().data(),
                 g.has_labels() ? static_cast<const void*>(g.edge_labels().data()) : nullptr,
-                g.num_edges()};
+                g.num_edges(), sample_fingerprint(g)};
     std::lock_guard<std::mutex> lk(mu);
     auto it = cache.find(k);
     if (it != cache.end()) return it->second;
@@ -218,6 +258,41 @@ inline RunResult run_queries(const DeviceGraph& dg, const AnyModel& model,
 inline RunResult run_queries(const Graph& g, const AnyModel& model, const CostModelParams& params,
                              std::span<const VertexId> queries, const RunOptions& opts) {
     return run_queries(*detail::cached(g), model, params, queries, opts);
+}
+
+// Same signature as dynwalk::selection_ratio_sweep (runtime.hpp:96-103): per
+// alpha, the base graph's properties are regenerated as Pareto(alpha) with one
+// draw seed for every row (runtime.cpp:249-278), the queries walk adaptively
+// on the GPU, and the row reports the eRJS / eRVS selection split.
+inline std::vector<SweepRow> selection_ratio_sweep(const Graph& base, const AnyModel& model,
+                                                   const CostModelParams& params,
+                                                   std::span<const double> alphas,
+                                                   std::span<const VertexId> queries,
+                                                   const RunOptions& opts) {
+    RunOptions adaptive = opts;
+    adaptive.mode = SamplerMode::Adaptive;
+    WeightGenSpec spec;
+    spec.kind = WeightGenSpec::Kind::Pareto;
+    spec.seed = derive_seed(opts.seed, 0x7377656570ULL);  // shared by every row
+    std::vector<SweepRow> rows;
+    rows.reserve(alphas.size());
+    for (const double alpha : alphas) {
+        spec.alpha = alpha;
+        const Graph g = synthesize_weights(base, spec);
+        const DeviceGraph dg(g);  // one upload per row, never a stale cache entry
+        const RunStats s = run_queries(dg, model, params, queries, adaptive).stats;
+        const std::uint64_t total = s.select_erjs + s.select_ervs;
+        SweepRow row{};
+        row.alpha = alpha;
+        row.erjs_steps = s.select_erjs;
+        row.ervs_steps = s.select_ervs;
+        if (total) {
+            row.pct_erjs = 100.0 * static_cast<double>(s.select_erjs) / static_cast<double>(total);
+            row.pct_ervs = 100.0 - row.pct_erjs;
+        }
+        rows.push_back(row);
+    }
+    return rows;
 }
 
 // Same signature as dynwalk::profile_edge_cost_ratio (cost_model.hpp:39-40);

@@ -79,3 +79,32 @@ def test_shim_runs_dsl_models(ref, tmp_path):
                         ratio=1.4, rng="philox", workers=2)
         assert stats_core(stats) == stats_core(r.stats), name
         assert np.array_equal(paths, r.paths), name
+
+
+def test_shim_selection_ratio_sweep(ref):
+    """dynwalk::gpu::selection_ratio_sweep (runtime.hpp:99-103 signature):
+    per alpha, Pareto(alpha) properties drawn with the shared sweep seed
+    (runtime.cpp:263) and an adaptive walk; every row's eRJS / eRVS split
+    equals the reference samplers on the Philox stream."""
+    if not os.path.exists(SHIM):
+        pytest.skip("oracle/_ref/shim_check not built")
+    alphas = (0.5, 1.0, 2.0, 4.0)
+    p = subprocess.run([SHIM, "graph=ba", "n=300", "deg=5", "gseed=11", "L=20", "ratio=1.2",
+                        "seed=7", "model=node2vec", "sweep=" + ",".join(map(str, alphas))],
+                       capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0, p.stderr
+    rows = json.loads(p.stdout.strip().splitlines()[-1])
+    assert [r["alpha"] for r in rows] == list(alphas)
+    q = np.arange(300, dtype=np.uint32)
+    sweep_seed = ref.derive_seed(7, 0x7377656570)
+    for row, alpha in zip(rows, alphas):
+        g = ref.RefGraph.gen("ba", 300, 5, 11).synth("uniform", 1.0, 5.0, seed=111)
+        g.synth("pareto", alpha=alpha, seed=sweep_seed)
+        r = ref.ref_run(g, ref.Model("node2vec", a=2.0, b=0.5), q, mode="adaptive",
+                        walk_length=20, seed=7, ratio=1.2, rng="philox", workers=2)
+        assert row["erjs_steps"] == r.stats["select_erjs"], alpha
+        assert row["ervs_steps"] == r.stats["select_ervs"], alpha
+        total = row["erjs_steps"] + row["ervs_steps"]
+        assert total and abs(row["pct_erjs"] - 100.0 * row["erjs_steps"] / total) < 1e-3
+    # the rows differ: the shape changes the selection split
+    assert len({r["erjs_steps"] for r in rows}) > 1
