@@ -97,6 +97,19 @@ int main(int argc, char** argv) {
             return 0;
         }
 
+        // write=<file>: the one-pass GPU walk + write_paths; also writes
+        // <file>.ref from the run_queries paths through the reference's write_paths
+        if (get("write", "") != "") {
+            const std::string file = get("write", "");
+            const dw::RunStats ws =
+                dw::gpu::run_queries_write_paths(g, model, params, queries, opts, file);
+            const dw::RunResult rr2 = dw::gpu::run_queries(g, model, params, queries, opts);
+            dw::write_paths(file + ".ref", rr2.paths);
+            std::cout << "{\"steps\":" << ws.steps << ",\"steps_rq\":" << rr2.stats.steps << "}"
+                      << std::endl;
+            return 0;
+        }
+
         const dw::RunResult rr = dw::gpu::run_queries(g, model, params, queries, opts);
 
         const std::string out = get("out", "shim_out");

@@ -9,6 +9,8 @@
 //     -> dynwalk::gpu::profile_edge_cost_ratio(g, model, cfg)
 //   dynwalk::selection_ratio_sweep(base, model, params, alphas, q, opts)  runtime.hpp:99-103
 //     -> dynwalk::gpu::selection_ratio_sweep(...)                        (same signature)
+//   dynwalk::write_paths(file, dynwalk::run_queries(...).paths)         runtime.cpp:280-291
+//     -> dynwalk::gpu::run_queries_write_paths(g, model, params, q, opts, file)
 //
 // Semantics kept: query order, path[0] = start, length
 // <= min(L, max_steps) + 1, empty path + query_errors++ for an out-of-range
@@ -202,22 +204,51 @@ inline std::shared_ptr<DeviceGraph> cached(const Graph& g) {
 
 }  // namespace detail
 
-inline RunResult run_queries(const DeviceGraph& dg, const AnyModel& model,
-                             const CostModelParams& params, std::span<const VertexId> queries,
-                             const RunOptions& opts) {
+namespace detail {
+
+inline dw_run_opts to_opts(const CostModelParams& params, const RunOptions& opts) {
     if (opts.workers < 1) throw Error("worker count must be >= 1");  // runtime.cpp:194
     if (opts.check_bounds) throw Error("RunOptions.check_bounds is not supported by the GPU runtime");
     if (opts.bound_scale != 1.0)
         throw Error("RunOptions.bound_scale is not supported by the GPU runtime");
     if (opts.collect_cv) throw Error("RunOptions.collect_cv is not supported by the GPU runtime");
-    const detail::ModelDesc m = detail::to_desc(model);
     dw_run_opts o{};
-    o.mode = detail::to_mode(opts.mode);
+    o.mode = to_mode(opts.mode);
     o.walk_length = opts.walk_length;
     o.seed = opts.seed;
     o.erjs_cap_per_degree = opts.erjs_cap_per_degree;
     o.edge_cost_ratio = params.edge_cost_ratio;
     o.qid_base = 0;
+    return o;
+}
+
+inline RunStats to_stats(const dw_run_stats& st) {
+    RunStats s;
+    s.queries = st.queries;
+    s.query_errors = st.query_errors;
+    s.dead_ends = st.dead_ends;
+    s.steps = st.steps;
+    s.select_ervs = st.select_ervs;
+    s.select_erjs = st.select_erjs;
+    s.trials = st.trials;
+    s.weight_reads = st.weight_reads;
+    s.rng_draws = st.rng_draws;
+    s.erjs_fallbacks = st.erjs_fallbacks;
+    for (std::size_t b = 0; b < s.selection_by_degree.size(); ++b) {
+        s.selection_by_degree[b][0] = st.selection_by_degree[b][0];
+        s.selection_by_degree[b][1] = st.selection_by_degree[b][1];
+    }
+    s.wall_ms = st.total_ms;
+    return s;
+}
+
+}  // namespace detail
+
+inline RunResult run_queries(const DeviceGraph& dg, const AnyModel& model,
+                             const CostModelParams& params, std::span<const VertexId> queries,
+                             const RunOptions& opts) {
+    const dw_run_opts o = detail::to_opts(params, opts);
+    const detail::ModelDesc m = detail::to_desc(model);
     const std::size_t nq = queries.size();
     const std::size_t stride = static_cast<std::size_t>(opts.walk_length) + 1;
     // compact transfer: offsets + the ids that exist (dw_run_compact)
@@ -234,24 +265,33 @@ inline RunResult run_queries(const DeviceGraph& dg, const AnyModel& model,
         rr.paths[i].assign(flat.begin() + offsets[i], flat.begin() + offsets[i + 1]);
         lengths[i] = static_cast<std::uint32_t>(offsets[i + 1] - offsets[i]);
     }
-    RunStats& s = rr.stats;
-    s.queries = st.queries;
-    s.query_errors = st.query_errors;
-    s.dead_ends = st.dead_ends;
-    s.steps = st.steps;
-    s.select_ervs = st.select_ervs;
-    s.select_erjs = st.select_erjs;
-    s.trials = st.trials;
-    s.weight_reads = st.weight_reads;
-    s.rng_draws = st.rng_draws;
-    s.erjs_fallbacks = st.erjs_fallbacks;
-    for (std::size_t b = 0; b < s.selection_by_degree.size(); ++b) {
-        s.selection_by_degree[b][0] = st.selection_by_degree[b][0];
-        s.selection_by_degree[b][1] = st.selection_by_degree[b][1];
-    }
-    s.path_lengths = std::move(lengths);
-    s.wall_ms = st.total_ms;
+    rr.stats = detail::to_stats(st);
+    rr.stats.path_lengths = std::move(lengths);
     return rr;
+}
+
+// write_paths(path, run_queries(g, model, params, queries, opts).paths)
+// (runtime.cpp:280-291) in one pass: the text is formatted on the device and
+// written batch by batch while later batches walk, so host memory stays
+// bounded for any number of queries (BASELINE config 5).  The file is
+// byte-identical; the returned RunStats has no path_lengths.
+inline RunStats run_queries_write_paths(const DeviceGraph& dg, const AnyModel& model,
+                                        const CostModelParams& params,
+                                        std::span<const VertexId> queries, const RunOptions& opts,
+                                        const std::string& path) {
+    const dw_run_opts o = detail::to_opts(params, opts);
+    const detail::ModelDesc m = detail::to_desc(model);
+    dw_run_stats st{};
+    check(dw_run_write_paths(dg.handle(), &m.d, queries.data(), queries.size(), &o, path.c_str(),
+                             &st));
+    return detail::to_stats(st);
+}
+
+inline RunStats run_queries_write_paths(const Graph& g, const AnyModel& model,
+                                        const CostModelParams& params,
+                                        std::span<const VertexId> queries, const RunOptions& opts,
+                                        const std::string& path) {
+    return run_queries_write_paths(*detail::cached(g), model, params, queries, opts, path);
 }
 
 // Same signature as dynwalk::run_queries (runtime.hpp:85-86).

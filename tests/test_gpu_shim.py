@@ -108,3 +108,21 @@ def test_shim_selection_ratio_sweep(ref):
         assert total and abs(row["pct_erjs"] - 100.0 * row["erjs_steps"] / total) < 1e-3
     # the rows differ: the shape changes the selection split
     assert len({r["erjs_steps"] for r in rows}) > 1
+
+
+def test_shim_run_queries_write_paths(tmp_path):
+    """dynwalk::gpu::run_queries_write_paths writes the same bytes as the
+    reference's write_paths over gpu::run_queries paths (runtime.cpp:280-291)."""
+    if not os.path.exists(SHIM):
+        pytest.skip("oracle/_ref/shim_check not built")
+    out = str(tmp_path / "walks.txt")
+    for mk in ("node2vec", "metapath"):
+        extra = ["labels=0,3", "schema=0,1,2,3"] if mk == "metapath" else []
+        p = subprocess.run([SHIM, "graph=ba", "n=500", "deg=6", "gseed=5", "L=15", "ratio=1.2",
+                            "seed=9", f"model={mk}", f"write={out}"] + extra,
+                           capture_output=True, text=True, timeout=300)
+        assert p.returncode == 0, p.stderr
+        st = json.loads(p.stdout.strip().splitlines()[-1])
+        assert st["steps"] == st["steps_rq"] > 0
+        a, b = open(out, "rb").read(), open(out + ".ref", "rb").read()
+        assert a == b and a.count(b"\n") == 500, mk
