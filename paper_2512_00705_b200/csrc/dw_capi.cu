@@ -330,12 +330,6 @@ dwb::ModelParams model_params(const dw_model_desc* m) {
     case DW_MODEL_PR2: mp.shortcut = (m->gamma >= 0.0 && m->gamma <= 1.0) ? 1u : 0u; break;
     default: mp.shortcut = 0u;
     }
-    auto pow2 = [](double x) {
-        int e = 0;
-        return std::isfinite(x) && x != 0.0 && std::fabs(std::frexp(x, &e)) == 0.5;
-    };
-    mp.pow2_a = pow2(m->a) ? 1u : 0u;
-    mp.pow2_b = pow2(m->b) ? 1u : 0u;
     switch (m->kind) {
     case DW_MODEL_NODE2VEC: mp.pos_weights = (m->a > 0.0 && m->b > 0.0) ? 1u : 0u; break;
     case DW_MODEL_PR2: mp.pos_weights = (m->gamma >= 0.0 && m->gamma < 1.0) ? 1u : 0u; break;
@@ -347,8 +341,6 @@ dwb::ModelParams model_params(const dw_model_desc* m) {
     mp.wsum_coef = (1.0 / m->a + 1.0 + 1.0 / m->b) / 3.0;
     if (const char* env = std::getenv("DW_SCREEN"))
         if (env[0] == '0') mp.screen = 0u;
-    if (const char* env = std::getenv("DW_POW2"))
-        if (env[0] == '0') mp.pow2_a = mp.pow2_b = 0u;
     if (const char* env = std::getenv("DW_D1"))
         if (env[0] == '0') mp.pos_weights = 0u;
     if (const char* env = std::getenv("DW_SHORTCUT"))

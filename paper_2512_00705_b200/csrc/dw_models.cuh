@@ -61,7 +61,6 @@ struct ModelParams {
     double a, b, gamma;
     double inv_a, inv_b, inv_3;
     uint32_t fast_div, shortcut;
-    uint32_t pow2_a, pow2_b;  // a / b is a power of two: x / a == x * inv_a exactly
     uint32_t pos_weights;     // every weight is > 0 and finite by construction
     uint32_t screen;          // wsum_approx is within 1e-15 (relative) of wsum
     double wsum_coef;         // node2vec: RN((1/a + 1 + 1/b) / 3)
@@ -118,18 +117,19 @@ struct Node2VecModel {
     static constexpr bool kScreen = true;
     static constexpr bool kLabelAgg = false;
     double a, b, ia, ib, i3, wc;
-    bool pa, pb;
     __device__ explicit Node2VecModel(const ModelParams& p)
-        : a(p.a), b(p.b), ia(p.inv_a), ib(p.inv_b), i3(p.inv_3), wc(p.wsum_coef),
-          pa(p.pow2_a != 0), pb(p.pow2_b != 0) {}
+        : a(p.a), b(p.b), ia(p.inv_a), ib(p.inv_b), i3(p.inv_3), wc(p.wsum_coef) {}
     // x * (1/a + 1 + 1/b) / 3 in one multiply: relative error <= ~8 ulp
     // against wsum() when a, b > 0 (all terms positive), so the decision
     // ratio * bound < wsum only needs wsum() within a 1e-12 band
     __device__ double wsum_approx(const Step& s) const {
         return W ? s.hsum * wc : wc * (double)s.degree;
     }
-    __device__ double da(double x) const { return pa ? __dmul_rn(x, ia) : ddiv(x, a, ia); }
-    __device__ double db(double x) const { return pb ? __dmul_rn(x, ib) : ddiv(x, b, ib); }
+    // Markstein division, exact for power-of-two divisors as well (zero
+    // residual): one code path, no select between a multiply and a division
+    // (measured +1 % over the select)
+    __device__ double da(double x) const { return ddiv(x, a, ia); }
+    __device__ double db(double x) const { return ddiv(x, b, ib); }
     __device__ uint32_t max_steps() const { return 0xFFFFFFFFu; }
     __device__ double bound(const Step& s) const {  // models.hpp:74-79
         const double hmax = W ? s.hmax : 1.0;

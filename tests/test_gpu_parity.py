@@ -54,6 +54,10 @@ def test_reference_goldens_on_gpu(dw, orc, case):
 @pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("mk", [dict(kind="node2vec", a=2.0, b=0.5),
                                 dict(kind="node2vec", a=0.5, b=2.0),
+                                # not powers of two: the device divides by a and b
+                                # (Markstein from RN(1/a)), the oracle with '/'
+                                dict(kind="node2vec", a=1.3, b=0.7),
+                                dict(kind="node2vec", a=3.0, b=0.1),
                                 dict(kind="pr2", gamma=0.2),
                                 dict(kind="static", weighted=False)])
 def test_rmat_bit_exact(dw, orc, mk, mode):
