@@ -580,6 +580,17 @@ __global__ void probe_pass_kernel(DevGraph g, __grid_constant__ const ModelParam
     const Step& S = P.S;
     m.prepare(S);
     const uint32_t k = S.degree < 32 ? S.degree : 32;
+    // The random pass times one eRJS trial as the walk kernel runs it: the
+    // (x, y) draw, then a weight evaluation only when y is below the row's
+    // non-return maximum -- a trial above it is rejected without reading the
+    // edge (the free rejection of dw_walk_kernel.cuh).  The ratio then prices
+    // a trial, not a random read, against a sequential read (the eRJS-vs-eRVS
+    // cost balance decide_sampler encodes, cost_model.hpp:46-56).
+    double bnd = 1.0, mnr = __longlong_as_double(0x7ff0000000000000ll);
+    if (RANDOM && M::kBoundable && mp.shortcut) {
+        bnd = m.bound(S);
+        mnr = m.nonreturn_max(S);
+    }
     double acc = 0.0;
     if (lane < k) {
         for (int r = 0; r < rounds; ++r) {
@@ -588,6 +599,7 @@ __global__ void probe_pass_kernel(DevGraph g, __grid_constant__ const ModelParam
                 const U4 b = philox4x32_10(U4{lane, (uint32_t)r, w, 0x72616e64u}, (uint32_t)seed,
                                            (uint32_t)(seed >> 32));
                 e = P.begin + bounded(lo64(b), S.degree);
+                if (uniform01(hi64(b)) * bnd >= mnr) continue;  // rejected, nothing read
             } else {
                 e = P.begin + lane;
             }

@@ -387,3 +387,19 @@ def test_two_replicas_on_one_device(dw, orc, tmp_path):
     dw.run_write_paths(one, model, q[:200_000], opts, str(tmp_path / "a.txt"))
     dw.run_write_paths(two, model, q[:200_000], opts, str(tmp_path / "b.txt"))
     assert open(tmp_path / "a.txt", "rb").read() == open(tmp_path / "b.txt", "rb").read()
+
+
+def test_calibration_prices_free_rejections(dw):
+    """node2vec (0.5, 2) rejects half of its trials without reading an edge
+    (y >= the non-return maximum); the device calibration's random pass does
+    the same, so its ratio is below the one measured with the screen off."""
+    import os
+    dg = dw.DeviceGraph.rmat(16, 16, seed=5)
+    m = dw.Model(kind="node2vec", a=0.5, b=2.0)
+    with_screen = dw.profile_edge_cost_ratio(dg, m, seed=1)
+    os.environ["DW_SHORTCUT"] = "0"
+    try:
+        without = dw.profile_edge_cost_ratio(dg, m, seed=1)
+    finally:
+        del os.environ["DW_SHORTCUT"]
+    assert 0 < with_screen < without
