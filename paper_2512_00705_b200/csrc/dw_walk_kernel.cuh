@@ -90,11 +90,17 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 typedef unsigned long long ull;
 
 enum Phase : uint32_t { P_IDLE = 0, P_NODE, P_TRIAL, P_FETCH, P_VREC, P_VMEMB, P_COOP, P_EMATH };
-// per-lane counters kept in shared memory (updated per walker or per eRVS
-// neighbour): eRJS trials, single-shot eRVS trials, eRVS reads and draws,
-// algorithmic bytes / 4.  Their block totals sit in the last LC_NUM slots of
-// the shared counter array (scratch slots of Counter, dw_walk.cuh).
-enum LaneCounter : int { LC_ETRIALS = 0, LC_ETRIALS1, LC_EREADS, LC_EDRAWS, LC_ALG4, LC_NUM };
+// per-lane 64-bit counters kept in shared memory (updated per walker, per
+// eRVS neighbour or per rare event): eRJS trials, single-shot eRVS trials,
+// eRVS reads and draws, algorithmic bytes / 4, cap fallbacks, dead ends,
+// query errors, queries.  A plain shared-memory add per update: no atomics
+// and no overflow branch inside the walk loop (the 64-bit shared atomics
+// those need compile to CAS loops, ~580 cold instructions that crowded the
+// loop's instruction cache).  Summed per block at kernel end.
+enum LaneCounter : int {
+    LC_ETRIALS = 0, LC_ETRIALS1, LC_EREADS, LC_EDRAWS, LC_ALG4,
+    LC_FALLBACKS, LC_DEADENDS, LC_QERRORS, LC_QUERIES, LC_NUM
+};
 
 __device__ __forceinline__ bool valid_w(double w) { return !(w < 0.0) && isfinite(w); }
 
@@ -125,7 +131,6 @@ __device__ __forceinline__ const EdgeRec* pair_of(const EdgeRec* edges, ull e) {
     return edges + (e & ~1ull);  // 16 B aligned pair holding record e
 }
 
-__device__ __forceinline__ void cnt_add(ull* c, ull v) { atomicAdd(c, v); }
 
 // ---- K2 (warp form): one row, 32 lanes; all lanes call with equal args ----
 // Returns the chosen target and its relative edge index (for the fat record).
@@ -325,7 +330,7 @@ struct WalkSmem {
     double y[kRing][kThreads];       // y of the queued trials
     uint32_t t[kRing][kThreads];     // trial index of the queued trials
     uint4 mb[2][kThreads];           // node record / hash bucket / eRVS pair
-    uint32_t lc[LC_NUM][kThreads];   // per-lane RunStats counters (spill at 2^31)
+    ull lc[LC_NUM][kThreads];        // per-lane RunStats counters
     // walker state read once per step or per iteration, kept out of registers
     // so the loop fits the register budget of 3-4 CTAs/SM without spills
     uint32_t cur[kThreads], phoff[kThreads], plg[kThreads], hoff[kThreads], cap[kThreads],
@@ -359,17 +364,8 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
 #pragma unroll
     for (int c = 0; c < LC_NUM; ++c) s_lc[c][tid] = 0;
     __syncthreads();
-    // lane counters: LC_* accumulate per lane in shared memory and spill into
-    // the block's 64-bit totals (s_lct) before they can overflow
-    auto lc_add = [&](int c, ull v) {
-        const ull t = (ull)s_lc[c][tid] + v;
-        if (t >= 0x80000000ull) {
-            atomicAdd(&s_lct[c], t);
-            s_lc[c][tid] = 0;
-        } else {
-            s_lc[c][tid] = (uint32_t)t;
-        }
-    };
+    // lane counters: LC_* accumulate per lane in shared memory
+    auto lc_add = [&](int c, ull v) { s_lc[c][tid] += v; };
 
     // a block's 32-bit histogram cells cannot overflow unless the launch
     // walks 2^32 steps in total
@@ -497,13 +493,13 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                 base = __shfl_sync(kFull, base, leader);
                 if (base + (ull)n >= p.nq) drained = true;
                 if (lane == leader && base < p.nq)  // one counter add per claim
-                    cnt_add(&s_cnt[kCQueries], min((ull)n, p.nq - base));
+                    lc_add(LC_QUERIES, min((ull)n, p.nq - base));
                 if (phase == P_IDLE) {
                     const ull i = base + (ull)__popc(need & lt_mask);
                     if (i < p.nq) {
                         const uint32_t start = p.queries[i];
                         if (start >= g.nv) {  // runtime.cpp:213-217
-                            cnt_add(&s_cnt[kCQueryErrors], 1);
+                            lc_add(LC_QERRORS, 1);
                             if (p.lengths) p.lengths[i] = 0;
                         } else {
                             if (p.paths) p.paths[i * p.stride] = start;
@@ -682,7 +678,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                     }
                 } else if (!(mb & kParked) && rc == 0 && tn >= cap) {
                     count_erjs(tn);
-                    cnt_add(&s_cnt[kCFallbacks], 1);  // cap overrun -> reservoir, same stream
+                    lc_add(LC_FALLBACKS, 1);  // cap overrun -> reservoir, same stream
                     start_ervs(2ull * tn);
                 }
             }
@@ -741,7 +737,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                         lc_add(LC_EREADS, 1);
                         if (++tn == deg) {  // the scan is complete
                             if (ev.best == kInvalid) {  // all weights zero: dead end
-                                cnt_add(&s_cnt[kCDeadEnds], 1);
+                                lc_add(LC_DEADENDS, 1);
                                 end_walk();
                             } else if (FAT) {
                                 ErvsState e = ev;
@@ -859,13 +855,13 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                         const ull c = p.cap_per_degree * (ull)deg;
                         nret = 0;
                         count_erjs(c > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)c);
-                        cnt_add(&s_cnt[kCFallbacks], 1);
+                        lc_add(LC_FALLBACKS, 1);
                     } else {
                         lc_add(LC_ETRIALS1, 1);  // single-shot eRVS
                     }
                     lc_add(LC_EREADS, deg);  // the reservoir pass reads every weight, draws none
                     c_alg4 += (uint32_t)(((8ull * deg + 31) / 32) * 8);
-                    cnt_add(&s_cnt[kCDeadEnds], 1);
+                    lc_add(LC_DEADENDS, 1);
                     end_walk();
                 } else if (erjs) {
                     if (!(bound > 0.0) || !isfinite(bound)) {  // samplers.hpp:152-154
@@ -878,7 +874,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                         mb = nret = sel = 0;
                         phase = P_TRIAL;
                         if (cap == 0) {  // immediate cap overrun
-                            cnt_add(&s_cnt[kCFallbacks], 1);
+                            lc_add(LC_FALLBACKS, 1);
                             start_ervs(0);
                         }
                     }
@@ -907,7 +903,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                         lc_add(LC_EREADS, deg);
                         lc_add(LC_EDRAWS, d1 - d0);
                         if (bidx == kInvalid) {  // all weights zero: dead end
-                            cnt_add(&s_cnt[kCDeadEnds], 1);
+                            lc_add(LC_DEADENDS, 1);
                             end_walk();
                         } else {
                             ErvsState e = ev_load();
@@ -949,7 +945,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                     lc_add(LC_EREADS, T.degree);
                     lc_add(LC_EDRAWS, dr);
                     if (nx == kInvalid) {
-                        cnt_add(&s_cnt[kCDeadEnds], 1);
+                        lc_add(LC_DEADENDS, 1);
                         end_walk();
                     } else if (FAT) {
                         ErvsState e = ev_load();
@@ -978,15 +974,10 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
     // ---- flush counters: eRJS trials count as trials, reads and 2 draws each
     __syncthreads();
     if (tid < 66 && s_hist[tid]) s_cnt[kCHist + tid] += s_hist[tid];
-    const ull et = warp_sum((ull)s_lc[LC_ETRIALS][tid]), e1 = warp_sum((ull)s_lc[LC_ETRIALS1][tid]);
-    const ull er = warp_sum((ull)s_lc[LC_EREADS][tid]), ed = warp_sum((ull)s_lc[LC_EDRAWS][tid]);
-    const ull ea = warp_sum((ull)s_lc[LC_ALG4][tid]);
-    if (lane == 0) {
-        atomicAdd(&s_lct[LC_ETRIALS], et);
-        atomicAdd(&s_lct[LC_ETRIALS1], e1);
-        atomicAdd(&s_lct[LC_EREADS], er);
-        atomicAdd(&s_lct[LC_EDRAWS], ed);
-        atomicAdd(&s_lct[LC_ALG4], ea);
+#pragma unroll 1
+    for (int c = 0; c < LC_NUM; ++c) {
+        const ull v = warp_sum(s_lc[c][tid]);
+        if (lane == 0 && v) atomicAdd(&s_lct[c], v);
     }
     __syncthreads();
     if (tid == 0) {
@@ -995,6 +986,10 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
         s_cnt[kCWeightReads] = t + s_lct[LC_EREADS];
         s_cnt[kCRngDraws] = 2 * t + s_lct[LC_EDRAWS];
         s_cnt[kCAlgBytes] = 4 * s_lct[LC_ALG4];
+        s_cnt[kCFallbacks] += s_lct[LC_FALLBACKS];
+        s_cnt[kCDeadEnds] += s_lct[LC_DEADENDS];
+        s_cnt[kCQueryErrors] += s_lct[LC_QERRORS];
+        s_cnt[kCQueries] += s_lct[LC_QUERIES];
     }
     __syncthreads();
     for (int i = tid; i < kCNum; i += blockDim.x)
