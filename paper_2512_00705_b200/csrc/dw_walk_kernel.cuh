@@ -144,6 +144,7 @@ __device__ __forceinline__ const EdgeRec* pair_of(const EdgeRec* edges, ull e) {
 #endif
 template <class M, bool NOJUMP>
 __device__ DW_COOP_ATTR int ervs_warp(const ModelParams& mp, Step S, const WalkerKey key,
+                                      const PhiloxKeys& rk,
                                       const DevGraph& g, ull begin, uint32_t phoff, ull idx0,
                                       uint32_t* next, uint32_t* nidx, ull* draws) {
     M m(mp);
@@ -183,7 +184,7 @@ __device__ DW_COOP_ATTR int ervs_warp(const ModelParams& mp, Step S, const Walke
             double lk = -DBL_MAX;
             int has = 0;
             if (in) {
-                const double u = open01(walker_draw(key, idx0 + i));
+                const double u = open01(walker_draw(key, rk, idx0 + i));
                 if (w != 0.0) {
                     lk = log(u) / w;
                     has = 1;
@@ -215,19 +216,19 @@ __device__ DW_COOP_ATTR int ervs_warp(const ModelParams& mp, Step S, const Walke
                 const uint32_t uj = __shfl_sync(kFull, er.col, j);
                 if (wj == 0.0) continue;
                 if (best == kInvalid) {
-                    best_log_key = log(open01(walker_draw(key, idx++))) / wj;
+                    best_log_key = log(open01(walker_draw(key, rk, idx++))) / wj;
                     best = uj;
                     bi = base + j;
                     continue;
                 }
                 if (!have) {
-                    skip = log(open01(walker_draw(key, idx++))) / best_log_key;
+                    skip = log(open01(walker_draw(key, rk, idx++))) / best_log_key;
                     have = true;
                 }
                 skip -= wj;
                 if (skip <= 0.0) {
                     const double floor_u = exp(wj * best_log_key);
-                    const double u = floor_u + open01(walker_draw(key, idx++)) * (1.0 - floor_u);
+                    const double u = floor_u + open01(walker_draw(key, rk, idx++)) * (1.0 - floor_u);
                     const double lk = log(u) / wj;
                     if (lk > best_log_key) {
                         best_log_key = lk;
@@ -257,10 +258,11 @@ struct ErvsState {
 constexpr uint32_t kHave = 0x80000000u;
 
 template <bool NOJUMP>
-__device__ __forceinline__ ErvsState ervs_visit_impl(ErvsState s, const WalkerKey& key, uint32_t vi,
+__device__ __forceinline__ ErvsState ervs_visit_impl(ErvsState s, const WalkerKey& key,
+                                                     const PhiloxKeys& rk, uint32_t vi,
                                                      uint32_t u, double w) {
     if (NOJUMP) {
-        const double r = open01(walker_draw(key, s.didx + vi));
+        const double r = open01(walker_draw(key, rk, s.didx + vi));
         if (w != 0.0) {
             const double lk = log(r) / w;
             if (s.best == kInvalid || lk > s.best_key) {
@@ -273,19 +275,19 @@ __device__ __forceinline__ ErvsState ervs_visit_impl(ErvsState s, const WalkerKe
     }
     if (w == 0.0) return s;
     if (s.best == kInvalid) {
-        s.best_key = log(open01(walker_draw(key, s.didx++))) / w;
+        s.best_key = log(open01(walker_draw(key, rk, s.didx++))) / w;
         s.best = u;
         s.bidx = vi;
         return s;
     }
     if (!(s.bidx & kHave)) {
-        s.skip = log(open01(walker_draw(key, s.didx++))) / s.best_key;
+        s.skip = log(open01(walker_draw(key, rk, s.didx++))) / s.best_key;
         s.bidx |= kHave;
     }
     s.skip -= w;
     if (s.skip <= 0.0) {
         const double floor_u = exp(w * s.best_key);
-        const double uu = floor_u + open01(walker_draw(key, s.didx++)) * (1.0 - floor_u);
+        const double uu = floor_u + open01(walker_draw(key, rk, s.didx++)) * (1.0 - floor_u);
         const double lk = log(uu) / w;
         s.bidx &= ~kHave;
         if (lk > s.best_key) {
@@ -298,9 +300,10 @@ __device__ __forceinline__ ErvsState ervs_visit_impl(ErvsState s, const WalkerKe
 }
 
 template <bool NOJUMP>
-__device__ __forceinline__ ErvsState ervs_visit(ErvsState s, const WalkerKey key, uint32_t vi,
+__device__ __forceinline__ ErvsState ervs_visit(ErvsState s, const WalkerKey key,
+                                             const PhiloxKeys& rk, uint32_t vi,
                                              uint32_t u, double w) {
-    return ervs_visit_impl<NOJUMP>(s, key, vi, u, w);
+    return ervs_visit_impl<NOJUMP>(s, key, rk, vi, u, w);
 }
 
 // The whole jump scan (samplers.hpp:65-107) over d <= kEBatchMaxDeg weights in
@@ -308,10 +311,11 @@ __device__ __forceinline__ ErvsState ervs_visit(ErvsState s, const WalkerKey key
 // half j%2 of uint4 j/2 of the lane); returns the draw index after the scan
 // and the kept neighbour's index (kInvalid when every weight is zero).
 __device__ __forceinline__ ull ervs_scan_short(const double* w, uint32_t d, const WalkerKey key,
+                                            const PhiloxKeys& rk,
                                             ull didx, uint32_t* bidx) {
     ErvsState s{-DBL_MAX, 0.0, didx, kInvalid, 0};
     for (uint32_t j = 0; j < d; ++j)
-        s = ervs_visit_impl<false>(s, key, j, 0u, w[(j >> 1) * 2 * kThreads + (j & 1)]);
+        s = ervs_visit_impl<false>(s, key, rk, j, 0u, w[(j >> 1) * 2 * kThreads + (j & 1)]);
     *bidx = s.best == kInvalid ? kInvalid : (s.bidx & ~kHave);
     return s.didx;
 }
@@ -731,7 +735,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                     } else {
                         phase = P_VREC;
                         const ErvsState e0 = ev_load();
-                        const ErvsState ev = ervs_visit<kNoJump>(e0, key_of(), tn, u, w);
+                        const ErvsState ev = ervs_visit<kNoJump>(e0, key_of(), p.rk, tn, u, w);
                         ev_store(ev);
                         lc_add(LC_EDRAWS, kNoJump ? 1ull : ev.didx - e0.didx);
                         lc_add(LC_EREADS, 1);
@@ -898,8 +902,8 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                         const ull d0 = ev_load().didx;
                         uint32_t bidx = 0;
                         const ull d1 = ervs_scan_short(
-                            reinterpret_cast<const double*>(&s_rec[0][0][tid]), deg, key_of(), d0,
-                            &bidx);
+                            reinterpret_cast<const double*>(&s_rec[0][0][tid]), deg, key_of(), p.rk,
+                            d0, &bidx);
                         lc_add(LC_EREADS, deg);
                         lc_add(LC_EDRAWS, d1 - d0);
                         if (bidx == kInvalid) {  // all weights zero: dead end
@@ -937,7 +941,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
             const ull db = __shfl_sync(kFull, lane == L ? ev_load().didx : 0ull, L);
             uint32_t nx = kInvalid, ni = 0;
             ull dr = 0;
-            const int st = ervs_warp<M, kNoJump>(p.mp, T, K, g, tb, tph, db, &nx, &ni, &dr);
+            const int st = ervs_warp<M, kNoJump>(p.mp, T, K, p.rk, g, tb, tph, db, &nx, &ni, &dr);
             if (lane == L) {
                 if (st < 0) {
                     fail(-st);
