@@ -694,36 +694,111 @@ cudaError_t calibrate_ratio(const DeviceGraphBuffers& g, int kind, bool weighted
 }
 
 // ---- path compaction (dw_run_compact) ---------------------------------------
-__global__ void widen_lengths_kernel(const uint32_t* __restrict__ len, ull n,
-                                     ull* __restrict__ out) {
-    for (ull i = blockIdx.x * (ull)blockDim.x + threadIdx.x; i <= n;
-         i += (ull)gridDim.x * blockDim.x)
-        out[i] = i < n ? len[i] : 0ull;
+// Offsets as three small kernels of 128-thread blocks limited to 32 registers
+// (__launch_bounds__(128, 16)): a block of them fits beside three resident
+// walk-kernel CTAs (61,440 of 65,536 registers), so a batch's offsets and
+// compaction run on a high-priority stream while the next batch walks
+// (dw_capi.cu run engine).  Tiles of 1024 walkers: per-tile sums, a one-block
+// scan of the tile sums chained through *d_base, per-tile offsets.
+constexpr int kScanThreads = 128, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ ull block_excl_scan(ull v, ull* s_warp, ull* total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    ull x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const ull y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[w] = x;
+    __syncthreads();
+    ull wbase = 0, all = 0;
+#pragma unroll
+    for (int i = 0; i < kScanThreads / 32; ++i) {
+        if (i < w) wbase += s_warp[i];
+        all += s_warp[i];
+    }
+    __syncthreads();
+    *total = all;
+    return wbase + x - v;
 }
 
-__global__ void add_base_kernel(ull* __restrict__ offs, ull n, ull* __restrict__ d_base) {
-    const ull base = *d_base;  // read by every thread before the last block advances it
-    for (ull i = blockIdx.x * (ull)blockDim.x + threadIdx.x; i <= n;
-         i += (ull)gridDim.x * blockDim.x)
-        offs[i] += base;
+__global__ void __launch_bounds__(kScanThreads, 16)
+    tile_sums_kernel(const uint32_t* __restrict__ len, ull n, ull* __restrict__ sums) {
+    __shared__ ull s_warp[kScanThreads / 32];
+    const ull t0 = (ull)blockIdx.x * kScanTile;
+    ull v = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const ull i = t0 + (ull)k * kScanThreads + threadIdx.x;
+        if (i < n) v += len[i];
+    }
+    ull total;
+    block_excl_scan(v, s_warp, &total);
+    if (threadIdx.x == 0) sums[blockIdx.x] = total;
 }
 
-__global__ void advance_base_kernel(const ull* __restrict__ offs, ull n, ull* __restrict__ d_base) {
-    *d_base = offs[n];
+// sums[t] <- base + exclusive prefix over tiles; offs[n] and *d_base <- the end
+__global__ void __launch_bounds__(kScanThreads, 16)
+    tile_scan_kernel(ull* __restrict__ sums, ull ntiles, ull n, ull* __restrict__ offs,
+                     ull* __restrict__ d_base) {
+    __shared__ ull s_warp[kScanThreads / 32];
+    ull run = *d_base;
+    for (ull c = 0; c < ntiles; c += kScanThreads) {
+        const ull i = c + threadIdx.x;
+        const ull v = i < ntiles ? sums[i] : 0ull;
+        ull total;
+        const ull ex = block_excl_scan(v, s_warp, &total);
+        if (i < ntiles) sums[i] = run + ex;
+        run += total;
+    }
+    if (threadIdx.x == 0) {
+        offs[n] = run;
+        *d_base = run;
+    }
+}
+
+// thread t owns walkers t*8 .. t*8+7 of the tile
+__global__ void __launch_bounds__(kScanThreads, 16)
+    tile_offsets_kernel(const uint32_t* __restrict__ len, ull n, const ull* __restrict__ sums,
+                        ull* __restrict__ offs) {
+    __shared__ ull s_warp[kScanThreads / 32];
+    const ull i0 = (ull)blockIdx.x * kScanTile + (ull)threadIdx.x * kScanItems;
+    uint32_t l[kScanItems];
+    ull v = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        l[k] = i0 + k < n ? len[i0 + k] : 0u;
+        v += l[k];
+    }
+    ull total;
+    ull o = sums[blockIdx.x] + block_excl_scan(v, s_warp, &total);
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        if (i0 + k < n) offs[i0 + k] = o;
+        o += l[k];
+    }
 }
 
 cudaError_t path_offsets(const uint32_t* lengths, ull n, ull* offs, ull* d_base, void* tmp,
                          size_t& tmp_bytes, cudaStream_t s) {
+    const ull ntiles = (n + kScanTile - 1) / kScanTile;
     if (!tmp) {
-        return cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, offs, offs, (int)(n + 1), s);
+        tmp_bytes = std::max<ull>(ntiles, 1) * sizeof(ull);
+        return cudaSuccess;
     }
-    widen_lengths_kernel<<<grid_for(n + 1, 256), 256, 0, s>>>(lengths, n, offs);
+    ull* sums = static_cast<ull*>(tmp);
+    if (ntiles) {
+        tile_sums_kernel<<<(unsigned)ntiles, kScanThreads, 0, s>>>(lengths, n, sums);
+        DW_TRY(cudaGetLastError());
+    }
+    tile_scan_kernel<<<1, kScanThreads, 0, s>>>(sums, ntiles, n, offs, d_base);
     DW_TRY(cudaGetLastError());
-    DW_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, offs, offs, (int)(n + 1), s));
-    add_base_kernel<<<grid_for(n + 1, 256), 256, 0, s>>>(offs, n, d_base);
-    DW_TRY(cudaGetLastError());
-    advance_base_kernel<<<1, 1, 0, s>>>(offs, n, d_base);
-    return cudaGetLastError();
+    if (ntiles) {
+        tile_offsets_kernel<<<(unsigned)ntiles, kScanThreads, 0, s>>>(lengths, n, sums, offs);
+        DW_TRY(cudaGetLastError());
+    }
+    return cudaSuccess;
 }
 
 // Padded [n][stride] rows -> flat ids at offs[i] - offs[0].  A block owns
@@ -733,7 +808,7 @@ cudaError_t path_offsets(const uint32_t* lengths, ull n, ull* offs, ull* d_base,
 // are the flat layout: the kernel returns and the engine copies the padded
 // buffer (dw_capi.cu drain).
 constexpr int kCompactRows = 128;
-__global__ void __launch_bounds__(256) compact_paths_kernel(
+__global__ void __launch_bounds__(kScanThreads, 16) compact_paths_kernel(
     const uint32_t* __restrict__ paths, const uint32_t* __restrict__ len, ull n, ull stride,
     const ull* __restrict__ offs, uint32_t* __restrict__ flat) {
     const ull flat_base = offs[0];
@@ -766,8 +841,8 @@ __global__ void __launch_bounds__(256) compact_paths_kernel(
 cudaError_t compact_paths(const uint32_t* paths, const uint32_t* lengths, ull n, ull stride,
                           const ull* offs, uint32_t* flat, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    compact_paths_kernel<<<grid_for(n, kCompactRows), 256, 0, s>>>(paths, lengths, n, stride,
-                                                                  offs, flat);
+    compact_paths_kernel<<<grid_for(n, kCompactRows), kScanThreads, 0, s>>>(paths, lengths, n,
+                                                                           stride, offs, flat);
     return cudaGetLastError();
 }
 
