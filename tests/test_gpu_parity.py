@@ -403,3 +403,47 @@ def test_calibration_prices_free_rejections(dw):
     finally:
         del os.environ["DW_SHORTCUT"]
     assert 0 < with_screen < without
+
+
+@pytest.mark.parametrize("batch", [None, 37_000])
+def test_batched_engine_equals_one_launch(dw, batch):
+    """The run engine's batches (default plan with its geometric tail, or
+    DW_BATCH-forced small batches cycling the three ring slots many times)
+    give the same paths, lengths and counters as one device-resident launch
+    over all queries: per-batch qid bases, slot reuse and the offset chain
+    are invisible in the output."""
+    import ctypes as C
+    import os
+    import torch
+    dg = dw.DeviceGraph.rmat(12, 16, seed=31)
+    rng = np.random.default_rng(9)
+    q = rng.integers(0, 1 << 12, 620_000).astype(np.uint32)  # > 2 default batches
+    L = 12
+    model = dw.Model(a=0.5, b=2.0)
+    opts = dw.RunOptions(walk_length=L, seed=3, edge_cost_ratio=1.4)
+    dq = torch.from_numpy(q.view(np.int32)).cuda()
+    dp = torch.empty((len(q), L + 1), dtype=torch.int32, device="cuda")
+    dl = torch.empty(len(q), dtype=torch.int32, device="cuda")
+    lib = dw.load_library()
+    m, o = model.c(), opts.c()
+    torch.cuda.synchronize()
+    assert lib.dw_run_device(dg.h, 0, C.byref(m), C.c_void_p(dq.data_ptr()), len(q), C.byref(o),
+                             C.c_void_p(dp.data_ptr()), C.c_void_p(dl.data_ptr()), None) == 0
+    st = dw.RunStatsC()
+    assert lib.dw_run_device_sync(dg.h, 0, C.byref(st)) == 0
+    one_paths = dp.cpu().numpy().view(np.uint32)
+    one_len = dl.cpu().numpy().view(np.uint32)
+    if batch:
+        os.environ["DW_BATCH"] = str(batch)
+    try:
+        r = dw.run_queries(dg, model, q, opts)
+        offs, flat, st2 = dw.run_queries_compact(dg, model, q, opts)
+    finally:
+        os.environ.pop("DW_BATCH", None)
+    assert np.array_equal(r.lengths, one_len)
+    mask = np.arange(L + 1)[None, :] < one_len[:, None]
+    assert np.array_equal(r.paths[mask], one_paths[mask])
+    assert np.array_equal(np.diff(offs.astype(np.int64)), one_len.astype(np.int64))
+    assert np.array_equal(flat, one_paths[mask])
+    for k in ("steps", "trials", "rng_draws", "weight_reads", "select_erjs", "select_ervs"):
+        assert r.stats[k] == getattr(st, k) == st2[k], k
