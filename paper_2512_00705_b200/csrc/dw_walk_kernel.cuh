@@ -89,7 +89,22 @@ constexpr uint32_t kEWait = DW_EWAIT;
 constexpr unsigned kFull = 0xFFFFFFFFu;
 typedef unsigned long long ull;
 
-enum Phase : uint32_t { P_IDLE = 0, P_NODE, P_TRIAL, P_FETCH, P_VREC, P_VMEMB, P_COOP, P_EMATH };
+enum Phase : uint32_t { P_IDLE = 0, P_NODE, P_TRIAL, P_FETCH, P_VREC, P_VMEMB, P_COOP, P_EMATH, P_CJS };
+
+// Warp-cooperative eRJS for models whose bounds can be far above the typical
+// weight (second-order PageRank: thousands of trials on hub rows, SURVEY
+// Appendix A).  A lane whose step has run kCjsMin trials without acceptance
+// hands the step to the warp: 32 consecutive trials per round, judged in
+// parallel, the first accepted one (in trial order) wins -- the same trial
+// the sequential loop would accept, with the same counters.  A launch is
+// otherwise bound by its slowest walker: at s20, a quarter of the config-4
+// walkers took 74 % of the full run's time (tools/tail_probe.py).
+template <class M> struct CoopErjs { static constexpr bool value = false; };
+template <bool W> struct CoopErjs<Pr2Model<W>> { static constexpr bool value = true; };
+#ifndef DW_CJS_MIN
+#define DW_CJS_MIN 128
+#endif
+constexpr uint32_t kCjsMin = DW_CJS_MIN;
 // per-lane 64-bit counters kept in shared memory (updated per walker, per
 // eRVS neighbour or per rare event): eRJS trials, single-shot eRVS trials,
 // eRVS reads and draws, algorithmic bytes / 4, cap fallbacks, dead ends,
@@ -684,6 +699,8 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                     count_erjs(tn);
                     lc_add(LC_FALLBACKS, 1);  // cap overrun -> reservoir, same stream
                     start_ervs(2ull * tn);
+                } else if (CoopErjs<M>::value && !(mb & kParked) && rc == 0 && tn >= kCjsMin) {
+                    phase = P_CJS;  // every trial before tn judged and rejected
                 }
             }
         }
@@ -969,6 +986,121 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                             end_walk();
                         else
                             phase = P_NODE;
+                    }
+                }
+            }
+        }
+
+        // ---- warp-cooperative eRJS (CoopErjs models): 32 trials per round
+        if (CoopErjs<M>::value) {
+            unsigned cj = __ballot_sync(kFull, phase == P_CJS);
+            while (cj) {
+                const int L = __ffs(cj) - 1;
+                cj &= cj - 1;
+                const int Lt = (tid & ~31) + L;
+                Step T;
+                T.cur = __shfl_sync(kFull, cur, L);
+                T.prev = __shfl_sync(kFull, prev, L);
+                T.prev_degree = __shfl_sync(kFull, pdeg, L);
+                T.step = __shfl_sync(kFull, step, L);
+                T.degree = __shfl_sync(kFull, deg, L);
+                T.hmax = T.hsum = 0.0;
+                T.lmax = T.lsum = 0.0;
+                M mw(p.mp);
+                mw.prepare(T);
+                const ull tb = __shfl_sync(kFull, begin, L);
+                const uint32_t t0 = __shfl_sync(kFull, tn, L);
+                const uint32_t tph = sm.phoff[Lt], tcap = sm.cap[Lt];
+                const uint32_t twl = sm.twlo[Lt], twc = sm.twcnt[Lt];
+                const double tbnd = sm.bound[Lt], tmnr = sm.mnr[Lt];
+                const ull q = p.qid_base + __shfl_sync(kFull, qi, L);
+                int win = -1;
+                bool bad = false;
+                uint32_t judged = 0, rets = 0, wu = 0;
+                ull we = 0;
+                for (uint32_t base = t0; base < tcap && win < 0 && !bad; base += 32) {
+                    const uint32_t t = base + lane;
+                    bool acc = false, badw = false, isret = false;
+                    ull e = 0;
+                    uint32_t u = 0;
+                    if (t < tcap) {
+                        const U4 b = philox4x32_10_rk(U4{t, T.step, (uint32_t)q, (uint32_t)(q >> 32)}, p.rk);
+                        const uint32_t x = (uint32_t)bounded(lo64(b), T.degree);
+                        const double y = uniform01(hi64(b)) * tbnd;
+                        if (!(y >= tmnr && x - twl >= twc)) {  // else a free rejection
+                            e = tb + x;
+                            float h;
+                            uint16_t lab = 0;
+                            if (FAT) {
+                                const uint4 r0 = __ldg(reinterpret_cast<const uint4*>(g.fat + e));
+                                u = r0.x;
+                                h = __uint_as_float(r0.y);
+                                if (M::kUsesLabels) lab = (uint16_t)(r0.w >> 8);
+                            } else {
+                                const EdgeRec er = load_edge(g.edges + e);
+                                u = er.col;
+                                h = er.h;
+                                lab = edge_label<M>(g, e);
+                            }
+                            const WeightCase wc = mw.weight(T, u, h, lab);
+                            isret = kSO && u == T.prev;
+                            const double w = !wc.needs_member
+                                                 ? wc.w
+                                                 : (member(g, T.prev_degree, tph, u) ? wc.w_in : wc.w_out);
+                            if (!valid_w(w))
+                                badw = true;
+                            else
+                                acc = y < w;
+                        }
+                    }
+                    const unsigned am = __ballot_sync(kFull, acc), bm = __ballot_sync(kFull, badw);
+                    const unsigned rm = __ballot_sync(kFull, isret);
+                    if (am | bm) {  // the first decided trial in trial order ends the step
+                        const int f = __ffs(am | bm) - 1;
+                        const unsigned upto = f == 31 ? kFull : ((2u << f) - 1u);
+                        rets += __popc(rm & upto);
+                        judged = base + f + 1 - t0;
+                        if ((bm >> f) & 1) {
+                            bad = true;
+                        } else {
+                            win = f;
+                            we = __shfl_sync(kFull, e, f);
+                            wu = __shfl_sync(kFull, u, f);
+                        }
+                    } else {
+                        rets += __popc(rm);
+                        judged = min(base + 32, tcap) - t0;
+                    }
+                }
+                if (lane == L) {
+                    tn = t0 + judged;
+                    nret += rets;
+                    if (bad) {
+                        fail(kDevBadWeight);
+                    } else if (win >= 0) {
+                        count_erjs(tn);
+                        if (FAT) {
+                            ErvsState ev = ev_load();
+                            ev.didx = we;  // its fat record starts the next step
+                            ev_store(ev);
+                            phase = P_FETCH;
+                        } else {
+                            prev = cur;
+                            pdeg = deg;
+                            phoff = hoff;
+                            plg = hash_log2_buckets(deg);
+                            cur = wu;
+                            ++step;
+                            if (p.paths) p.paths[qi * p.stride + step] = wu;
+                            if (step >= p.target)
+                                end_walk();
+                            else
+                                phase = P_NODE;
+                        }
+                    } else {  // cap overrun -> reservoir, same stream
+                        count_erjs(tn);
+                        lc_add(LC_FALLBACKS, 1);
+                        start_ervs(2ull * tn);
                     }
                 }
             }

@@ -447,3 +447,23 @@ def test_batched_engine_equals_one_launch(dw, batch):
     assert np.array_equal(flat, one_paths[mask])
     for k in ("steps", "trials", "rng_draws", "weight_reads", "select_erjs", "select_ervs"):
         assert r.stats[k] == getattr(st, k) == st2[k], k
+
+
+@pytest.mark.parametrize("fat", ["1", "0"])
+@pytest.mark.parametrize("mode", ["adaptive", "force-erjs"])
+def test_pr2_pareto_cooperative_erjs(dw, orc, mode, fat):
+    """Second-order PageRank on Pareto weights: steps run thousands of trials,
+    so lanes hand their steps to the warp-cooperative eRJS (32 trials per
+    round, first acceptance in trial order).  Paths and counters stay
+    bit-exact, in the fat and the slim layout."""
+    import os
+    og = orc.Graph.rmat(11, 16, 3).synth_philox("pareto", alpha=1.0, seed=4)
+    os.environ["DW_FAT"] = fat
+    try:
+        dg = dw.DeviceGraph.rmat(11, 16, seed=3, weights="pareto", alpha=1.0, weight_seed=4)
+    finally:
+        del os.environ["DW_FAT"]
+    q = np.arange(og.nv, dtype=np.uint32)
+    r_dev, r_orc = run_both(dw, orc, og, dg, dict(kind="pr2", gamma=0.15), q, mode, 30, 1.2)
+    assert r_orc.stats["trials"] > 50 * r_orc.stats["steps"]  # heavy-tailed steps: CJS engaged
+    assert_same(r_dev, r_orc, (mode, fat))
