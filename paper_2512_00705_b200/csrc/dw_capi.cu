@@ -542,8 +542,9 @@ ull batch_size(ull n) {
 }
 
 // Batch boundaries of one device's n walkers: batches of batch_size(n), the
-// last two batches' worth split geometrically (1/2, 1/4, 1/8, 1/8) so the copy
-// of the final batch, which nothing overlaps, is short.  `cap` bounds every
+// last two batches' worth split geometrically (1/2, 1/4, 1/8, 1/8, pieces of
+// at least 1M walkers) so the copy of the final batch, which nothing
+// overlaps, is short.  `cap` bounds every
 // batch (the ring slot size).
 std::vector<ull> batch_plan(ull n, ull cap) {
     std::vector<ull> at{0};
@@ -552,8 +553,12 @@ std::vector<ull> batch_plan(ull n, ull cap) {
     ull pos = 0;
     while (n - pos > 2 * bs) at.push_back(pos += bs);
     ull rem = n - pos;
+    // pieces stay >= 1M walkers: a launch ends when its slowest walker does,
+    // and models with heavy-tailed walks (PR2: thousands of trials on hub
+    // rows) pay that at every batch boundary, while the copies the split
+    // hides are small for small batches
     if (rem > bs && !std::getenv("DW_BATCH")) {
-        for (int k = 0; k < 3 && rem >= 4 * (1ull << 16); ++k) {
+        for (int k = 0; k < 3 && rem / 2 >= (1ull << 20); ++k) {
             at.push_back(pos += rem / 2);
             rem -= rem / 2;
         }

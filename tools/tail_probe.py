@@ -18,7 +18,8 @@ def main():
     scale = int(sys.argv[1]) if len(sys.argv) > 1 else 20
     cfg = bench.CONFIGS[int(sys.argv[2]) if len(sys.argv) > 2 else 4]
     g = dw.DeviceGraph.rmat(scale, 16, seed=bench.TOPO_SEED, weights=cfg["weights"], low=1.0,
-                            high=5.0, alpha=1.0, weight_seed=bench.WEIGHT_SEED)
+                            high=5.0, alpha=1.0, weight_seed=bench.WEIGHT_SEED,
+                            labels=cfg["labels"], label_seed=bench.LABEL_SEED)
     nv = g.info()["num_vertices"]
     m = dw.Model(cfg["model"], **bench.model_kw(cfg))
     ratio = dw.profile_edge_cost_ratio(g, m, seed=bench.PROFILE_SEED)
