@@ -2,7 +2,7 @@
 R-MAT graph (the bench's generator) against the oracle's copy of it, every
 model and sampler mode, a sample of walkers at walk length 80.
 
-    python tools/parity_stress.py [scale] [walkers]
+    python tools/parity_stress.py [scale] [walkers] [mode,mode,...] [model,model,...]
 
 Prints one JSON line per (model, mode) with the walker-steps compared and
 whether paths, lengths and counters were identical.  TEST INFRASTRUCTURE:
@@ -28,6 +28,8 @@ MODES = ("adaptive", "force-erjs", "force-ervs", "ervs-nojump")
 def main():
     scale = int(sys.argv[1]) if len(sys.argv) > 1 else 18
     nw = int(sys.argv[2]) if len(sys.argv) > 2 else 20000
+    modes = sys.argv[3].split(",") if len(sys.argv) > 3 else MODES
+    kinds = sys.argv[4].split(",") if len(sys.argv) > 4 else None
     dg = dw.DeviceGraph.rmat(scale, 16, seed=1, weights="uniform", weight_seed=2, labels=(0, 3),
                              label_seed=3)
     a = dg.download()
@@ -37,7 +39,9 @@ def main():
     threads = os.cpu_count() or 4
     ok_all = True
     for mk in MODELS:
-        for mode in MODES:
+        if kinds and mk["kind"] not in kinds:
+            continue
+        for mode in modes:
             opts = dw.RunOptions(mode=mode, walk_length=80, seed=11, edge_cost_ratio=1.6)
             r = dw.run_queries(dg, dw.Model(**mk), q, opts)
             o = oracle.run(og, oracle.Model(**mk), q, mode=mode, walk_length=80, seed=11,
