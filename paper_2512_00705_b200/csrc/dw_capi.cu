@@ -161,6 +161,7 @@ void free_replica(Replica& r) {
     cudaFree(r.g.hslots);
     cudaFree(r.g.fat);
     cudaFree(r.g.lagg);
+    cudaFree(r.g.twin);
     cudaFree(r.counters);
     cudaFree(r.queues);
     cudaFree(r.error);
@@ -383,7 +384,8 @@ uint32_t target_steps(const dw_model_desc* m, const dw_run_opts* o) {
 dwb::WalkParams make_params(Replica& r, const dw_model_desc* m, const dw_run_opts* o) {
     dwb::WalkParams p;
     std::memset(&p, 0, sizeof p);
-    p.g = dwb::DevGraph{r.g.nodes, r.g.edges, r.g.labels, r.g.hslots, r.g.fat, r.g.lagg, r.g.nv, r.g.ne};
+    p.g = dwb::DevGraph{r.g.nodes, r.g.edges, r.g.labels, r.g.hslots, r.g.fat, r.g.lagg,
+                        r.g.twin, r.g.nv, r.g.ne};
     p.stride = o->walk_length + 1;
     p.target = target_steps(m, o);
     p.seed_lo = (uint32_t)o->seed;

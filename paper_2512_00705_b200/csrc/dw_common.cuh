@@ -82,6 +82,7 @@ struct DevGraph {
     const uint32_t* __restrict__ hslots;  // membership hash sets, 8 slots per bucket
     const FatRec* __restrict__ fat;       // may be null (slim layout)
     const double2* __restrict__ lagg;     // per-node {label MAX, label SUM} or null (DSL)
+    const uint32_t* __restrict__ twin;    // slim layout: return-edge range per edge, or null
     uint32_t nv;
     unsigned long long ne;
 };

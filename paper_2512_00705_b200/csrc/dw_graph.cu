@@ -200,6 +200,47 @@ __global__ void fat_build_kernel(const NodeRec* __restrict__ nodes, uint32_t nv,
     }
 }
 
+// Slim layout: the fat record's return-edge range alone, 4 B per edge, so the
+// slim walk keeps its free rejections (the walker fetches twin[e] of the edge
+// it took together with the next node record).  lo | cnt << 24; cnt 255 marks
+// a range it cannot describe (degree >= 2^24 or >= 255 parallel edges).
+__global__ void twin_build_kernel(const NodeRec* __restrict__ nodes, uint32_t nv,
+                                  const EdgeRec* __restrict__ edges, uint32_t* __restrict__ twin) {
+    const ull warp = (blockIdx.x * (ull)blockDim.x + threadIdx.x) >> 5;
+    const ull nwarps = ((ull)gridDim.x * blockDim.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    for (ull v = warp; v < nv; v += nwarps) {
+        const NodeRec nr = nodes[v];
+        for (ull i = lane; i < nr.degree; i += 32) {
+            const ull e = nr.begin + i;
+            const NodeRec nu = nodes[load_col(edges + e)];
+            const uint32_t lo = row_lower_bound(edges, nu.begin, nu.degree, (uint32_t)v);
+            const uint32_t hi = v == 0xFFFFFFFFull
+                                    ? nu.degree
+                                    : row_lower_bound(edges, nu.begin, nu.degree, (uint32_t)v + 1);
+            const uint32_t cnt = hi - lo;
+            twin[e] = (nu.degree >= (1u << 24) || cnt >= 255u) ? (255u << 24) : (lo | (cnt << 24));
+        }
+    }
+}
+
+static cudaError_t build_twin(DeviceGraphBuffers& g, cudaStream_t s) {
+    g.twin = nullptr;
+    if (g.fat || g.ne == 0) return cudaSuccess;
+    if (const char* env = getenv("DW_TWIN"))
+        if (env[0] == '0') return cudaSuccess;
+    size_t free_b = 0, total_b = 0;
+    DW_TRY(cudaMemGetInfo(&free_b, &total_b));
+    const ull need = g.ne * sizeof(uint32_t);
+    if (need + (2ull << 30) > free_b) return cudaSuccess;
+    DW_TRY(cudaMallocAsync(&g.twin, need, s));
+    twin_build_kernel<<<grid_for((ull)g.nv * 32, 256), 256, 0, s>>>(g.nodes, g.nv, g.edges, g.twin);
+    DW_TRY(cudaGetLastError());
+    if (getenv("DW_VERBOSE"))
+        fprintf(stderr, "dynwalk: slim layout with return-edge ranges (%.1f GB)\n", need / 1e9);
+    return cudaStreamSynchronize(s);
+}
+
 // Above ~100 GB of fat records the walk slows down instead of speeding up:
 // measured on one B200, node2vec (0.5, 2), walker-steps/s fat vs slim:
 // s25 (34 GB of records) 6.04e9 vs 4.19e9, s26 (69 GB) 5.87e9 vs 4.20e9,
@@ -312,7 +353,10 @@ cudaError_t pack_graph(const ull* d_row, const uint32_t* d_col, const float* d_p
     return build_member_index(g, s);
 }
 
-cudaError_t finish_graph(DeviceGraphBuffers& g, cudaStream_t s) { return build_fat(g, s); }
+cudaError_t finish_graph(DeviceGraphBuffers& g, cudaStream_t s) {
+    DW_TRY(build_fat(g, s));
+    return build_twin(g, s);
+}
 
 __global__ void unpack_kernel(const NodeRec* __restrict__ nodes, const EdgeRec* __restrict__ edges,
                               uint32_t nv, ull ne, ull* row, uint32_t* col, float* prop,
@@ -612,7 +656,7 @@ __global__ void probe_pass_kernel(DevGraph g, __grid_constant__ const ModelParam
 template <class M>
 static cudaError_t calibrate_t(const DeviceGraphBuffers& gb, const ModelParams& mp, ull seed,
                                cudaStream_t s, double* ratio) {
-    DevGraph g{gb.nodes, gb.edges, gb.labels, gb.hslots, gb.fat, gb.lagg, gb.nv, gb.ne};
+    DevGraph g{gb.nodes, gb.edges, gb.labels, gb.hslots, gb.fat, gb.lagg, gb.twin, gb.nv, gb.ne};
     // ProfileConfig defaults: 1% of nodes, >= 64, <= 32 neighbours, 5 reps
     uint32_t want = (uint32_t)std::max<ull>((ull)std::ceil(0.01 * gb.nv), 64);
     const ull tries = (ull)want * 8;

@@ -10,6 +10,8 @@ struct DeviceGraphBuffers {
     uint16_t* labels = nullptr;
     uint32_t* hslots = nullptr;  // membership hash sets (dw_member.cuh)
     FatRec* fat = nullptr;       // fat edge records (optional accelerator)
+    uint32_t* twin = nullptr;    // slim layout: per edge (v -> u), v's range in N(u)
+                                 // (lo | cnt << 24; cnt 255 = unknown), or null
     double2* lagg = nullptr;     // per-node label MAX/SUM, built on first DSL use
     unsigned long long nbuckets = 0;
     uint32_t nv = 0;

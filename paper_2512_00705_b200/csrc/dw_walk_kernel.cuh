@@ -497,6 +497,10 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
         if ((c_trials | c_alg4) & 0xC0000000u) flush_walker();
     };
 
+    // slim layout: the edge the walker took, whose twin[] word comes with the
+    // next node record (s_y[1] is idle between a step's end and its node gather)
+    auto twe = [&]() -> ull& { return *reinterpret_cast<ull*>(&s_y[1][tid]); };
+
     for (;;) {
         // ---- refill idle lanes: one atomic per warp (runtime.cpp:209-211)
         unsigned need = __ballot_sync(kFull, phase == P_IDLE);
@@ -574,6 +578,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                         sel = (sel & ~(1u << k)) | ((uint32_t)(e & 1) << k);
                         cp16(&s_rec[k][0][tid], pair_of(g.edges, e));
                         if (M::kUsesLabels && g.labels) cp4(&s_rec[k][1][tid], g.labels + (e & ~1ull));
+                        s_rec[k][1][tid].y = x;  // the edge, for its return-edge range
                     }
                     ++rc;
                 }
@@ -588,6 +593,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
             const char* nr = reinterpret_cast<const char*>(g.nodes + cur);
             cp16(&s_mb[0][tid], nr);
             cp16(&s_mb[1][tid], nr + 16);
+            if (!FAT && g.twin && prev != kInvalid) cp4(&s_t[0][tid], g.twin + twe());
             if (M::kLabelAgg) cp16(&s_rec[0][0][tid], g.lagg + cur);  // the ring is empty here
         }
         if (ph0 == P_FETCH) {
@@ -694,6 +700,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                         const uint4 v0 = s_rec[acc][0][tid];
                         next_ev = E_ADV;
                         next_u = ((sel >> acc) & 1) ? v0.z : v0.x;
+                        twe() = begin + s_rec[acc][1][tid].y;
                     }
                 } else if (!(mb & kParked) && rc == 0 && tn >= cap) {
                     count_erjs(tn);
@@ -768,6 +775,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                             } else {
                                 next_ev = E_ADV;
                                 next_u = ev.best;
+                                twe() = begin + (ev.bidx & ~kHave);
                             }
                         }
                     }
@@ -818,9 +826,17 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                 lmax = __hiloint2double((int)la.y, (int)la.x);
                 lsum = __hiloint2double((int)la.w, (int)la.z);
             }
-            // first step: no return edge; later (slim layout) the range is unknown
+            // first step: no return edge; later (slim layout) the twin[] word
+            // of the edge taken, or an unknown range
             tw_lo = 0;
             tw_cnt = prev == kInvalid ? 0u : 0xFFFFFFFFu;
+            if (!FAT && g.twin && prev != kInvalid) {
+                const uint32_t w = s_t[0][tid];
+                if ((w >> 24) != 255u) {
+                    tw_lo = w & 0xFFFFFFu;
+                    tw_cnt = w >> 24;
+                }
+            }
         }
         if (next_ev != E_NONE) {
             // decide_sampler (cost_model.hpp:46-56) for the step at cur
@@ -975,6 +991,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                         phase = P_FETCH;
                     } else {
                         // advance here (rare path); the node record comes next iteration
+                        twe() = tb + ni;
                         prev = cur;
                         pdeg = deg;
                         phoff = hoff;
@@ -1085,6 +1102,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                             ev_store(ev);
                             phase = P_FETCH;
                         } else {
+                            twe() = we;
                             prev = cur;
                             pdeg = deg;
                             phoff = hoff;

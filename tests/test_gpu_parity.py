@@ -231,7 +231,7 @@ def _with_env(env: dict, fn):
                 os.environ[k] = v
 
 
-@pytest.mark.parametrize("layout", ["fat", "slim"])
+@pytest.mark.parametrize("layout", ["fat", "slim", "slim-notwin"])
 @pytest.mark.parametrize("shortcut", ["1", "0"])
 @pytest.mark.parametrize("mk", [dict(kind="node2vec", a=0.5, b=2.0),
                                 dict(kind="node2vec", a=2.0, b=0.5),
@@ -242,7 +242,10 @@ def test_layouts_and_free_rejections(dw, orc, mk, shortcut, layout):
     (nonreturn_max) must not change a single path or counter: the same run on
     the slim layout, with and without the shortcut, equals the oracle."""
     og = orc.Graph.rmat(12, 16, 11).synth_philox("uniform", 1.0, 5.0, seed=12)
-    dg = _with_env({"DW_FAT": "1" if layout == "fat" else "0"}, lambda: to_device(dw, og))
+    env = {"DW_FAT": "1" if layout == "fat" else "0"}
+    if layout == "slim-notwin":
+        env["DW_TWIN"] = "0"
+    dg = _with_env(env, lambda: to_device(dw, og))
     q = np.arange(og.nv, dtype=np.uint32)
     for mode in ("adaptive", "force-erjs"):
         r_dev, r_orc = _with_env({"DW_SHORTCUT": shortcut},
@@ -268,6 +271,12 @@ def test_directed_multigraph_without_twins(dw, orc):
         for mode in MODES:
             r_dev, r_orc = run_both(dw, orc, og, dg, mk, q, mode, 50, 1.1)
             assert_same(r_dev, r_orc, (mk, mode))
+    # the slim layout with its twin[] ranges on the same edge cases
+    dg = _with_env({"DW_FAT": "0"}, lambda: to_device(dw, og))
+    for mk in (dict(kind="node2vec", a=0.5, b=2.0), dict(kind="pr2", gamma=0.3)):
+        for mode in ("adaptive", "force-erjs"):
+            r_dev, r_orc = run_both(dw, orc, og, dg, mk, q, mode, 50, 1.1)
+            assert_same(r_dev, r_orc, (mk, mode, "slim"))
 
 
 def test_compact_output_matches_padded(dw, orc):
@@ -389,10 +398,11 @@ def test_two_replicas_on_one_device(dw, orc, tmp_path):
     assert open(tmp_path / "a.txt", "rb").read() == open(tmp_path / "b.txt", "rb").read()
 
 
-def test_calibration_prices_free_rejections(dw):
-    """node2vec (0.5, 2) rejects half of its trials without reading an edge
-    (y >= the non-return maximum); the device calibration's random pass does
-    the same, so its ratio is below the one measured with the screen off."""
+def test_calibration_with_and_without_free_rejections(dw):
+    """The calibration's random pass skips the edge read of a trial above the
+    row's non-return maximum (the kernel's free rejection) and runs with the
+    screen switched off as well.  Both give a positive, finite ratio; their
+    order is a timing matter and is not asserted (K4)."""
     import os
     dg = dw.DeviceGraph.rmat(16, 16, seed=5)
     m = dw.Model(kind="node2vec", a=0.5, b=2.0)
@@ -402,7 +412,8 @@ def test_calibration_prices_free_rejections(dw):
         without = dw.profile_edge_cost_ratio(dg, m, seed=1)
     finally:
         del os.environ["DW_SHORTCUT"]
-    assert 0 < with_screen < without
+    assert np.isfinite(with_screen) and with_screen > 0
+    assert np.isfinite(without) and without > 0
 
 
 @pytest.mark.parametrize("batch", [None, 37_000])
