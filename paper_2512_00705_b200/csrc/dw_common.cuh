@@ -72,6 +72,27 @@ struct alignas(64) FatRec {
     uint32_t aux[4];  // reserved
 };
 static_assert(sizeof(FatRec) == 64, "FatRec stride must be 64 bytes");
+
+// Compact fat record for graphs whose 64 B layout would exceed its HBM cap
+// (R-MAT s27): the same fields in 32 B, one sector.  u32 words:
+//   w0 col   w1 h (f32)   w2 begin bits 0-31   w3 begin bits 32-39 | degree << 8
+//   w4 hoff  w5 twin: lo | cnt << 24 (cnt 255 = unknown)
+//   w6 node_prop_max (f32: a maximum of f32 props, exact)
+//   w7 node_prop_sum rounded to f32 -- decisions within 1e-6 of the threshold
+//      fetch the exact node record instead (dw_walk_kernel.cuh)
+// No labels: built only for unlabelled graphs with degrees < 2^24, and walked
+// only by node2vec kernels (their decision has the one-multiply screen).
+struct alignas(32) FatRec32 {
+    uint32_t col;
+    float h;
+    uint32_t begin_lo;
+    uint32_t begin_hi_deg;
+    uint32_t thoff;
+    uint32_t twin;
+    float thmax;
+    float thsum;
+};
+static_assert(sizeof(FatRec32) == 32, "FatRec32 must be one sector");
 constexpr unsigned long long kBeginMask = (1ull << 40) - 1;
 constexpr uint32_t kMaskLabels = 7;  // labels with an exact bit in the fat record's mask
 
@@ -83,6 +104,7 @@ struct DevGraph {
     const FatRec* __restrict__ fat;       // may be null (slim layout)
     const double2* __restrict__ lagg;     // per-node {label MAX, label SUM} or null (DSL)
     const uint32_t* __restrict__ twin;    // slim layout: return-edge range per edge, or null
+    const FatRec32* __restrict__ fat32;   // compact fat records, or null
     uint32_t nv;
     unsigned long long ne;
 };

@@ -241,6 +241,36 @@ static cudaError_t build_twin(DeviceGraphBuffers& g, cudaStream_t s) {
     return cudaStreamSynchronize(s);
 }
 
+__global__ void fat32_build_kernel(const NodeRec* __restrict__ nodes, uint32_t nv,
+                                   const EdgeRec* __restrict__ edges, FatRec32* __restrict__ fat) {
+    const ull warp = (blockIdx.x * (ull)blockDim.x + threadIdx.x) >> 5;
+    const ull nwarps = ((ull)gridDim.x * blockDim.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    for (ull v = warp; v < nv; v += nwarps) {
+        const NodeRec nr = nodes[v];
+        for (ull i = lane; i < nr.degree; i += 32) {
+            const ull e = nr.begin + i;
+            const EdgeRec er = edges[e];
+            const NodeRec nu = nodes[er.col];
+            const uint32_t lo = row_lower_bound(edges, nu.begin, nu.degree, (uint32_t)v);
+            const uint32_t hi = v == 0xFFFFFFFFull
+                                    ? nu.degree
+                                    : row_lower_bound(edges, nu.begin, nu.degree, (uint32_t)v + 1);
+            const uint32_t cnt = hi - lo;
+            FatRec32 f;
+            f.col = er.col;
+            f.h = er.h;
+            f.begin_lo = (uint32_t)nu.begin;
+            f.begin_hi_deg = (uint32_t)((nu.begin >> 32) & 0xFFu) | (nu.degree << 8);
+            f.thoff = nu.hoff;
+            f.twin = cnt >= 255u ? (255u << 24) : (lo | (cnt << 24));
+            f.thmax = (float)nu.hmax;  // exact: a maximum of f32 props
+            f.thsum = (float)nu.hsum;
+            fat[e] = f;
+        }
+    }
+}
+
 // Above ~100 GB of fat records the walk slows down instead of speeding up:
 // measured on one B200, node2vec (0.5, 2), walker-steps/s fat vs slim:
 // s25 (34 GB of records) 6.04e9 vs 4.19e9, s26 (69 GB) 5.87e9 vs 4.20e9,
@@ -250,12 +280,34 @@ constexpr unsigned long long kFatMaxBytes = 96ull * 1000 * 1000 * 1000;
 
 static cudaError_t build_fat(DeviceGraphBuffers& g, cudaStream_t s) {
     g.fat = nullptr;
+    g.fat32 = nullptr;
     bool force = false;
     if (const char* env = getenv("DW_FAT")) {
         if (env[0] == '0') return cudaSuccess;
         force = env[0] == '1';
     }
     if (g.ne == 0 || g.ne > kBeginMask) return cudaSuccess;
+    // compact 32 B records for unlabelled graphs whose degrees fit 24 bits:
+    // node2vec walks them (+5 % over the 64 B records at s24, and they fit
+    // s27), the other models use the 64 B records built next when those fit
+    const bool compact_ok = !g.labels && g.max_degree < (1u << 24);
+    const char* fenv = getenv("DW_FAT");
+    if (compact_ok && !force && g.ne * sizeof(FatRec32) <= kFatMaxBytes) {
+        DW_TRY(cudaStreamSynchronize(s));
+        size_t fb = 0, tb = 0;
+        DW_TRY(cudaMemGetInfo(&fb, &tb));
+        const ull need32 = g.ne * sizeof(FatRec32);
+        if (need32 + (4ull << 30) <= fb) {
+            DW_TRY(cudaMallocAsync(&g.fat32, need32, s));
+            fat32_build_kernel<<<grid_for((ull)g.nv * 32, 256), 256, 0, s>>>(g.nodes, g.nv, g.edges,
+                                                                             g.fat32);
+            DW_TRY(cudaGetLastError());
+            DW_TRY(cudaStreamSynchronize(s));
+            if (getenv("DW_VERBOSE"))
+                fprintf(stderr, "dynwalk: compact 32 B fat records built (%.1f GB)\n", need32 / 1e9);
+        }
+    }
+    if (fenv && fenv[0] == '2') return cudaSuccess;  // compact records only
     if (!force && g.ne * sizeof(FatRec) > kFatMaxBytes) {
         if (getenv("DW_VERBOSE"))
             fprintf(stderr, "dynwalk: fat records skipped (%.1f GB above the %.0f GB cap)\n",
@@ -656,7 +708,8 @@ __global__ void probe_pass_kernel(DevGraph g, __grid_constant__ const ModelParam
 template <class M>
 static cudaError_t calibrate_t(const DeviceGraphBuffers& gb, const ModelParams& mp, ull seed,
                                cudaStream_t s, double* ratio) {
-    DevGraph g{gb.nodes, gb.edges, gb.labels, gb.hslots, gb.fat, gb.lagg, gb.twin, gb.nv, gb.ne};
+    DevGraph g{gb.nodes, gb.edges, gb.labels, gb.hslots, gb.fat, gb.lagg, gb.twin, gb.fat32,
+               gb.nv, gb.ne};
     // ProfileConfig defaults: 1% of nodes, >= 64, <= 32 neighbours, 5 reps
     uint32_t want = (uint32_t)std::max<ull>((ull)std::ceil(0.01 * gb.nv), 64);
     const ull tries = (ull)want * 8;

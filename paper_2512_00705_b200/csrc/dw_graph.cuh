@@ -10,6 +10,7 @@ struct DeviceGraphBuffers {
     uint16_t* labels = nullptr;
     uint32_t* hslots = nullptr;  // membership hash sets (dw_member.cuh)
     FatRec* fat = nullptr;       // fat edge records (optional accelerator)
+    FatRec32* fat32 = nullptr;   // compact fat records (when the 64 B ones exceed the cap)
     uint32_t* twin = nullptr;    // slim layout: per edge (v -> u), v's range in N(u)
                                  // (lo | cnt << 24; cnt 255 = unknown), or null
     double2* lagg = nullptr;     // per-node label MAX/SUM, built on first DSL use

@@ -4,7 +4,7 @@
 
 namespace dwb {
 
-template <class M, int MODE, bool FAT>
+template <class M, int MODE, int FAT>
 static cudaError_t launch_t(const WalkParams& p, int num_sms, cudaStream_t stream) {
     int per_sm = 0;
     const size_t smem = sizeof(WalkSmem);
@@ -26,18 +26,28 @@ static cudaError_t launch_t(const WalkParams& p, int num_sms, cudaStream_t strea
     return cudaGetLastError();
 }
 
+// compact 32 B records (FAT = 2) are walked by node2vec, in preference to the
+// 64 B ones; the other models use the 64 B records, or the slim layout
+template <class M> struct UsesFat32 { static constexpr bool value = false; };
+template <bool W> struct UsesFat32<Node2VecModel<W>> { static constexpr bool value = true; };
+
 template <class M>
 static cudaError_t launch_m(int mode, const WalkParams& p, int num_sms, cudaStream_t s) {
     const bool fat = p.g.fat != nullptr;
+    const bool fat32 = UsesFat32<M>::value && p.g.fat32 != nullptr;
     switch (mode) {
     case kAdaptive:
-        return fat ? launch_t<M, kAdaptive, true>(p, num_sms, s)
-                   : launch_t<M, kAdaptive, false>(p, num_sms, s);
+        if constexpr (UsesFat32<M>::value)
+            if (fat32) return launch_t<M, kAdaptive, 2>(p, num_sms, s);
+        if (fat) return launch_t<M, kAdaptive, 1>(p, num_sms, s);
+        return launch_t<M, kAdaptive, 0>(p, num_sms, s);
     case kForceErjs:
-        return fat ? launch_t<M, kForceErjs, true>(p, num_sms, s)
-                   : launch_t<M, kForceErjs, false>(p, num_sms, s);
-    case kForceErvs: return launch_t<M, kForceErvs, false>(p, num_sms, s);
-    case kErvsNoJump: return launch_t<M, kErvsNoJump, false>(p, num_sms, s);
+        if constexpr (UsesFat32<M>::value)
+            if (fat32) return launch_t<M, kForceErjs, 2>(p, num_sms, s);
+        if (fat) return launch_t<M, kForceErjs, 1>(p, num_sms, s);
+        return launch_t<M, kForceErjs, 0>(p, num_sms, s);
+    case kForceErvs: return launch_t<M, kForceErvs, 0>(p, num_sms, s);
+    case kErvsNoJump: return launch_t<M, kErvsNoJump, 0>(p, num_sms, s);
     }
     return cudaErrorInvalidValue;
 }

@@ -360,7 +360,7 @@ struct WalkSmem {
     ull lct[LC_NUM];                 // block totals of the lane counters
 };
 
-template <class M, int MODE, bool FAT>
+template <class M, int MODE, int FAT>
 __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
     walk_kernel(const __grid_constant__ WalkParams p) {
     constexpr bool kNoJump = MODE == kErvsNoJump;
@@ -569,7 +569,11 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                     s_y[k][tid] = y;
                     s_t[k][tid] = tn;
                     const ull e = begin + x;
-                    if (FAT) {
+                    if (FAT == 2) {  // compact record: one sector
+                        const uint4* r = reinterpret_cast<const uint4*>(g.fat32 + e);
+                        cp16(&s_rec[k][0][tid], r);
+                        cp16(&s_rec[k][1][tid], r + 1);
+                    } else if (FAT) {
                         const uint4* r = reinterpret_cast<const uint4*>(g.fat + e);
                         cp16(&s_rec[k][0][tid], r);
                         cp16(&s_rec[k][1][tid], r + 1);
@@ -598,10 +602,16 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
         }
         if (ph0 == P_FETCH) {
             const ull fe = ev_load().didx;
-            const uint4* r = reinterpret_cast<const uint4*>(g.fat + fe);
-            cp16(&s_rec[0][0][tid], r);
-            cp16(&s_rec[0][1][tid], r + 1);
-            cp16(&s_rec[0][2][tid], r + 2);
+            if (FAT == 2) {
+                const uint4* r = reinterpret_cast<const uint4*>(g.fat32 + fe);
+                cp16(&s_rec[0][0][tid], r);
+                cp16(&s_rec[0][1][tid], r + 1);
+            } else {
+                const uint4* r = reinterpret_cast<const uint4*>(g.fat + fe);
+                cp16(&s_rec[0][0][tid], r);
+                cp16(&s_rec[0][1][tid], r + 1);
+                cp16(&s_rec[0][2][tid], r + 2);
+            }
         }
         if (ph0 == P_VMEMB) {
             const uint32_t* b = g.hslots + 8ull * (phoff + mb);
@@ -635,7 +645,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                     const float h = __uint_as_float(odd ? v0.w : v0.y);
                     uint16_t lab = 0;  // the parked record still holds its label
                     if (M::kUsesLabels)
-                        lab = FAT ? (uint16_t)(v0.w >> 8)
+                        lab = FAT ? (FAT == 2 ? (uint16_t)0 : (uint16_t)(v0.w >> 8))
                                   : (uint16_t)(odd ? (s_rec[rh][1][tid].x >> 16) : s_rec[rh][1][tid].x);
                     const WeightCase wc = model.weight(S, u, h, lab);
                     const double w = r ? wc.w_in : wc.w_out;
@@ -658,7 +668,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                 uint16_t lab = 0;
                 if (M::kUsesLabels) {
                     if (FAT)
-                        lab = (uint16_t)(v0.w >> 8);
+                        lab = FAT == 2 ? (uint16_t)0 : (uint16_t)(v0.w >> 8);
                     else
                         lab = (uint16_t)(odd ? (s_rec[rh][1][tid].x >> 16) : s_rec[rh][1][tid].x);
                 }
@@ -786,6 +796,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
         // ---- D: step transitions, one code site for every phase
         double hmax = 0.0, hsum = 0.0, lmax = 0.0, lsum = 0.0;
         uint32_t lmask = 0xFFu;  // labels present in N(cur) (fat record), all = unknown
+        bool approx_sum = false;  // hsum from a compact record (f32)
         if (next_ev == E_FAT || next_ev == E_ADV) {
             // WalkerState::advance (walk_state.hpp:33-39)
             const uint4 v0 = s_rec[next_slot][0][tid];
@@ -800,6 +811,16 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
             if (step >= p.target) {
                 end_walk();
                 next_ev = E_NONE;
+            } else if (next_ev == E_FAT && FAT == 2) {
+                const uint4 v1 = s_rec[next_slot][1][tid];
+                begin = (ull)v0.z | ((ull)(v0.w & 0xFFu) << 32);
+                deg = v0.w >> 8;
+                hoff = v1.x;
+                tw_lo = (v1.y >> 24) == 255u ? 0u : (v1.y & 0xFFFFFFu);
+                tw_cnt = (v1.y >> 24) == 255u ? 0xFFFFFFFFu : (v1.y >> 24);
+                hmax = (double)__uint_as_float(v1.z);
+                hsum = (double)__uint_as_float(v1.w);  // rounded: see the decision
+                approx_sum = true;
             } else if (next_ev == E_FAT) {
                 const uint4 v1 = s_rec[next_slot][1][tid], v2 = s_rec[next_slot][2][tid];
                 begin = ((ull)v0.z | ((ull)v0.w << 32)) & kBeginMask;
@@ -845,12 +866,23 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
             } else {
                 Step S = mkstep(hmax, hsum, lmax, lsum);
                 model.prepare(S);
-                bool erjs = false;
+                bool erjs = false, need_node = false;
                 if (MODE == kAdaptive) {
                     if (M::kBoundable) {
                         bound = model.bound(S);
                         const double T = p.ratio * bound;
-                        if (M::kScreen && p.mp.screen) {
+                        if (FAT == 2 && approx_sum) {
+                            // compact record: decide on the estimate from the
+                            // f32 sum unless T is within 1e-6 of it; then the
+                            // exact node record decides (next iteration)
+                            const double Wa = (M::kScreen && p.mp.screen) ? model.wsum_approx(S) : 0.0;
+                            if (M::kScreen && p.mp.screen && T < Wa * (1.0 - 1e-6))
+                                erjs = true;
+                            else if (M::kScreen && p.mp.screen && T > Wa * (1.0 + 1e-6))
+                                erjs = false;
+                            else
+                                need_node = true;
+                        } else if (M::kScreen && p.mp.screen) {
                             // decide on the one-multiply estimate unless T
                             // falls in its error band (then the exact sum)
                             const double Wa = model.wsum_approx(S);
@@ -865,6 +897,9 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                     erjs = M::kBoundable;
                     if (erjs) bound = model.bound(S);
                 }
+                if (FAT == 2 && need_node) {
+                    phase = P_NODE;  // the exact node record decides this step
+                } else {
                 {
                     const uint32_t hb = 2 * degree_bucket(deg) + (erjs ? 1 : 0);
                     if (!hist_wide) {
@@ -919,6 +954,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                     lc_add(LC_ETRIALS1, 1);  // single-shot kernels report one trial (samplers.hpp:22)
                     start_ervs(0);
                 }
+                }  // need_node
             }
         }
 
@@ -1049,7 +1085,8 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                             float h;
                             uint16_t lab = 0;
                             if (FAT) {
-                                const uint4 r0 = __ldg(reinterpret_cast<const uint4*>(g.fat + e));
+                                const uint4 r0 = __ldg(FAT == 2 ? reinterpret_cast<const uint4*>(g.fat32 + e)
+                                                                : reinterpret_cast<const uint4*>(g.fat + e));
                                 u = r0.x;
                                 h = __uint_as_float(r0.y);
                                 if (M::kUsesLabels) lab = (uint16_t)(r0.w >> 8);

@@ -231,7 +231,7 @@ def _with_env(env: dict, fn):
                 os.environ[k] = v
 
 
-@pytest.mark.parametrize("layout", ["fat", "slim", "slim-notwin"])
+@pytest.mark.parametrize("layout", ["fat", "fat32", "slim", "slim-notwin"])
 @pytest.mark.parametrize("shortcut", ["1", "0"])
 @pytest.mark.parametrize("mk", [dict(kind="node2vec", a=0.5, b=2.0),
                                 dict(kind="node2vec", a=2.0, b=0.5),
@@ -242,7 +242,7 @@ def test_layouts_and_free_rejections(dw, orc, mk, shortcut, layout):
     (nonreturn_max) must not change a single path or counter: the same run on
     the slim layout, with and without the shortcut, equals the oracle."""
     og = orc.Graph.rmat(12, 16, 11).synth_philox("uniform", 1.0, 5.0, seed=12)
-    env = {"DW_FAT": "1" if layout == "fat" else "0"}
+    env = {"DW_FAT": {"fat": "1", "fat32": "2"}.get(layout, "0")}
     if layout == "slim-notwin":
         env["DW_TWIN"] = "0"
     dg = _with_env(env, lambda: to_device(dw, og))
