@@ -396,7 +396,9 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"],
                      "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
                      "peak_source": pk["source"],
-                     "kernel": f"walk_kernel<{cfg['model']} model, adaptive, fat records>",
+                     "kernel": f"walk_kernel<{cfg['model']} model, adaptive, "
+                               + ("32 B fat records>" if cfg["model"] == "node2vec" and not cfg["labels"]
+                                  else "fat records>"),
                      "kernel_ms_per_launch": kernel_ms,
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "algorithmic_bytes_per_walker_step": alg_bytes / max(walker_steps, 1),
