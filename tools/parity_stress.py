@@ -30,7 +30,9 @@ def main():
     nw = int(sys.argv[2]) if len(sys.argv) > 2 else 20000
     modes = sys.argv[3].split(",") if len(sys.argv) > 3 else MODES
     kinds = sys.argv[4].split(",") if len(sys.argv) > 4 else None
-    dg = dw.DeviceGraph.rmat(scale, 16, seed=1, weights="uniform", weight_seed=2, labels=(0, 3),
+    # labels only when MetaPath runs (a labelled graph has no compact records)
+    labels = (0, 3) if kinds is None or "metapath" in kinds else None
+    dg = dw.DeviceGraph.rmat(scale, 16, seed=1, weights="uniform", weight_seed=2, labels=labels,
                              label_seed=3)
     a = dg.download()
     og = oracle.Graph.from_csr(a["row"], a["col"], a["prop"], a["label"])
