@@ -105,6 +105,12 @@ template <bool W> struct CoopErjs<Pr2Model<W>> { static constexpr bool value = t
 #define DW_CJS_MIN 128
 #endif
 constexpr uint32_t kCjsMin = DW_CJS_MIN;
+// relative band around the f32 row sum of a compact record inside which the
+// exact node record decides (DW_FAT32_BAND: tests widen it to force that path)
+#ifndef DW_FAT32_BAND
+#define DW_FAT32_BAND 1e-6
+#endif
+constexpr double kFat32Band = DW_FAT32_BAND;
 // per-lane 64-bit counters kept in shared memory (updated per walker, per
 // eRVS neighbour or per rare event): eRJS trials, single-shot eRVS trials,
 // eRVS reads and draws, algorithmic bytes / 4, cap fallbacks, dead ends,
@@ -876,9 +882,9 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                             // f32 sum unless T is within 1e-6 of it; then the
                             // exact node record decides (next iteration)
                             const double Wa = (M::kScreen && p.mp.screen) ? model.wsum_approx(S) : 0.0;
-                            if (M::kScreen && p.mp.screen && T < Wa * (1.0 - 1e-6))
+                            if (M::kScreen && p.mp.screen && T < Wa * (1.0 - kFat32Band))
                                 erjs = true;
-                            else if (M::kScreen && p.mp.screen && T > Wa * (1.0 + 1e-6))
+                            else if (M::kScreen && p.mp.screen && T > Wa * (1.0 + kFat32Band))
                                 erjs = false;
                             else
                                 need_node = true;
