@@ -9,10 +9,19 @@ MetaPath s22; 4: PR2 on Pareto-weighted s25); the default is the headline, 2.
 One step = one full walk batch: every vertex of the R-MAT s24 ef16 graph
 (uniform [1,5) weights) starts one node2vec walker (a=p=0.5, b=q=2, 80
 steps, adaptive eRJS/eRVS with the device-calibrated cost ratio).  One
-process per GPU, graph replicated, no collective in the hot loop.  Scaling is weak: every rank walks
-one walker per vertex (global walker id = rank * V + v, so every rank draws
-distinct Philox streams) and `value` is the walker-steps of all ranks over the
-slowest rank's time.  Inputs are resident in HBM when
+process per GPU, graph replicated, no collective in the hot loop.
+
+--gpus N: N ranks, one per GPU.  Launched without torchrun, bench.py re-executes
+itself under torch.distributed.run (fails if fewer than N GPUs are visible).
+Scaling is strong by default (BASELINE configs[1]: "walkers sharded across
+2/4/8"): the V global walker ids are hash-partitioned over the ranks
+(paper_2512_00705_b200.shard_of; hash beats range partitioning)
+and each walker keeps its global id as RNG key, so the union of the shards is
+exactly the 1-GPU run.  --weak: every rank walks one walker per vertex with
+global ids rank * V + v.  `value` is the walker-steps of all ranks over the
+slowest rank's time.  --gather: after timing, NCCL-gathers every rank's path
+shard to rank 0 (the optional end-of-run gather) and reports
+its time.  Inputs are resident in HBM when
 the timed region starts; the graph (2.7 GB) is far larger than L2 (126 MB),
 so no L2 flush is needed between steps.
 
@@ -81,6 +90,17 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true",
                     help="build + 1 warm walk + 1 walk, for ncu (no JSON line)")
+    ap.add_argument("--weak", action="store_true",
+                    help="weak scaling: every rank walks one walker per vertex")
+    ap.add_argument("--gather", action="store_true",
+                    help="gather the path shards to rank 0 after timing (NCCL)")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend (gloo: tests, several ranks on one GPU)")
+    ap.add_argument("--device", type=int, default=-1,
+                    help="CUDA device of every rank (tests); default LOCAL_RANK")
+    ap.add_argument("--dump", default="",
+                    help="directory: each rank saves its shard's global ids, lengths and "
+                         "paths of the last timed step (tests)")
     a = ap.parse_args()
     a.cfg = dict(CONFIGS[a.config])
     if a.scale:
@@ -152,6 +172,39 @@ def reduce_sum(x: int, dist, device) -> int:
     t = torch.tensor([x], dtype=torch.int64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return int(t.item())
+
+
+def self_launch(args) -> None:
+    """`bench.py --gpus N` outside torchrun: re-execute under torch.distributed.run
+    with N ranks (one per GPU), or fail loudly if N GPUs are not visible."""
+    import socket
+    if args.device < 0:
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(json.dumps({"error": f"--gpus {args.gpus} but only {have} CUDA device(s) "
+                                       "visible"}), flush=True)
+            sys.exit(2)
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "WARN")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd, env=env))
+
+
+def shard_ids(torch, lo: int, hi: int, world: int, rank: int, dev):
+    """Global walker ids in [lo, hi) that rank `rank` walks: the device twin of
+    paper_2512_00705_b200.shard_of (Fibonacci hashing; int64 products wrap
+    like the uint64 ones, and the mask makes the shift logical)."""
+    q = torch.arange(lo, hi, dtype=torch.int64, device=dev)
+    if world == 1:
+        return q
+    h = ((q * (0x9E3779B97F4A7C15 - (1 << 64))) >> 32) & 0xFFFFFFFF
+    return q[(h % world) == rank]
 
 
 # ---------------------------------------------------------------- clocks
@@ -231,16 +284,20 @@ def ncu_traffic(scale: int):
 def run_ours(args):
     import torch
     world, rank, local = dist_env()
-    dist = dist_init(world, local, "nccl")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} in a world of {world} rank(s)")
+    devno = args.device if args.device >= 0 else local
+    torch.cuda.set_device(devno)
+    dev = torch.device("cuda", devno)
+    dist = dist_init(world, devno, args.backend)
+    cdev = dev if args.backend == "nccl" else torch.device("cpu")  # collective tensors
     import paper_2512_00705_b200 as dw
 
     t0 = time.perf_counter()
     cfg = args.cfg
     dg = dw.DeviceGraph.rmat(args.scale, 16, seed=TOPO_SEED, weights=cfg["weights"], low=1.0,
                              high=5.0, alpha=1.0, weight_seed=WEIGHT_SEED, labels=cfg["labels"],
-                             label_seed=LABEL_SEED, devices=[local])
+                             label_seed=LABEL_SEED, devices=[devno])
     info = dg.info()
     build_s = time.perf_counter() - t0
     model = dw.Model(cfg["model"], **model_kw(cfg))
@@ -250,36 +307,42 @@ def run_ours(args):
     if ratio <= 0:
         ratio = dw.profile_edge_cost_ratio(dg, model, seed=PROFILE_SEED) if rank == 0 else 0.0
         if dist is not None:
-            t = torch.tensor([ratio], dtype=torch.float64, device=dev)
+            t = torch.tensor([ratio], dtype=torch.float64, device=cdev)
             dist.broadcast(t, 0)
             ratio = float(t.item())
     calib_s = time.perf_counter() - t0
 
     nv = info["num_vertices"]
-    # weak scaling: one walker per vertex on every rank, distinct global ids
-    lo, hi = 0, nv
-    n = nv
     L = args.walk_length
-    opts = dw.RunOptions(mode=args.mode, walk_length=L, seed=WALK_SEED, edge_cost_ratio=ratio,
-                         qid_base=rank * nv)
-    lib = dw.load_library()
-    q = torch.arange(lo, hi, dtype=torch.int64, device=dev).to(torch.int32)
     wpv = cfg.get("walkers_per_vertex", 1)
     discard = cfg.get("discard_paths", False)
+    strong = world > 1 and not args.weak
+    # one launch per walker round r: global ids r * V + v (weak: (rank * wpv + r) * V + v)
+    rounds = []
+    for r in range(wpv):
+        if strong:
+            qid = shard_ids(torch, r * nv, (r + 1) * nv, world, rank, dev)
+            queries = (qid - r * nv).to(torch.int32)
+            rounds.append((queries, qid, 0))
+        else:
+            queries = torch.arange(0, nv, dtype=torch.int64, device=dev).to(torch.int32)
+            rounds.append((queries, None, (rank * wpv + r) * nv if world > 1 else r * nv))
+    n = max(len(q) for q, _, _ in rounds)
+    lib = dw.load_library()
     paths = None if discard else torch.empty((max(n, 1), L + 1), dtype=torch.int32, device=dev)
     lengths = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
     mdesc = model.c()
-    # one launch per walker round r (qid = (rank * wpv + r) * V + v)
     odescs = [dw.RunOptions(mode=args.mode, walk_length=L, seed=WALK_SEED, edge_cost_ratio=ratio,
-                            qid_base=(rank * wpv + r) * nv).c() for r in range(wpv)]
-    odesc = odescs[0]
+                            qid_base=base,
+                            qids=None if qid is None else qid.data_ptr()).c()
+              for _, qid, base in rounds]
     graph_bytes = torch.cuda.mem_get_info(dev)
 
     def step():
         agg = None
-        for od in odescs:
-            rc = lib.dw_run_device(dg.h, 0, C.byref(mdesc), C.c_void_p(q.data_ptr()), n,
+        for (q, _, _), od in zip(rounds, odescs):
+            rc = lib.dw_run_device(dg.h, 0, C.byref(mdesc), C.c_void_p(q.data_ptr()), len(q),
                                    C.byref(od), C.c_void_p(paths.data_ptr() if paths is not None
                                                            else None),
                                    C.c_void_p(lengths.data_ptr()), C.c_void_p(stream.cuda_stream))
@@ -312,7 +375,7 @@ def run_ours(args):
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     kms, stats = [], None
-    with ClockSampler(local) as clk:
+    with ClockSampler(devno) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
             st = step()
@@ -323,33 +386,55 @@ def run_ours(args):
     if dist is not None:
         dist.barrier()
     elapsed_ms = ev0.elapsed_time(ev1)
-    elapsed_ms = reduce_max(elapsed_ms, dist, dev)
+    elapsed_ms = reduce_max(elapsed_ms, dist, cdev)
     walker_steps_rank = int(stats.steps - stats.dead_ends)
-    walker_steps = reduce_sum(walker_steps_rank, dist, dev)  # per step, all ranks
+    walker_steps = reduce_sum(walker_steps_rank, dist, cdev)  # per step, all ranks
     value = walker_steps * args.steps / (elapsed_ms / 1e3)
-    kernel_ms = reduce_max(float(np.mean(kms)), dist, dev)
-    alg_bytes = reduce_sum(int(stats.algorithmic_bytes), dist, dev)
+    kernel_ms = reduce_max(float(np.mean(kms)), dist, cdev)
+    alg_bytes = reduce_sum(int(stats.algorithmic_bytes), dist, cdev)
+    walkers_total = reduce_sum(sum(len(q) for q, _, _ in rounds), dist, cdev)
+    walkers_min = -reduce_max(-float(n), dist, cdev)
+    walkers_max = reduce_max(float(n), dist, cdev)
+
+    if args.dump and paths is not None and wpv == 1:
+        q0, qid0, base0 = rounds[0]
+        ids = (qid0 if qid0 is not None else
+               torch.arange(base0, base0 + len(q0), dtype=torch.int64, device=dev))
+        os.makedirs(args.dump, exist_ok=True)
+        np.savez(os.path.join(args.dump, f"rank{rank}.npz"), qids=ids.cpu().numpy(),
+                 lengths=lengths[:len(q0)].cpu().numpy(), paths=paths[:len(q0)].cpu().numpy(),
+                 steps=walker_steps_rank)
+
+    # ---- optional end-of-run gather of the path shards to rank 0
+    gather = None
+    if args.gather and dist is not None and paths is not None and wpv == 1:
+        gather = gather_shards(torch, dist, cdev, rounds[0], lengths, paths, rank, world, nv)
 
     # ---- e2e through the C ABI with pinned host buffers (H2D + D2H timed):
     # dw_run_compact returns RunResult.paths flattened (offsets + ids), so only
     # ids that exist cross PCIe
     e2e = None
     if args.e2e_steps > 0 and n > 0 and wpv == 1 and not discard:
+        q0, qid0, base0 = rounds[0]
+        nq = len(q0)
         hq = C.c_void_p()
         ho = C.c_void_p()
         hf = C.c_void_p()
-        cap = n * (L + 1)
-        for buf, nbytes in ((hq, n * 4), (ho, (n + 1) * 8), (hf, cap * 4)):
+        cap = nq * (L + 1)
+        for buf, nbytes in ((hq, nq * 4), (ho, (nq + 1) * 8), (hf, cap * 4)):
             rc = lib.dw_host_alloc(nbytes, C.byref(buf))
             if rc:
                 raise dw.DynwalkError(rc, lib.dw_last_error().decode())
-        qa = np.ctypeslib.as_array(C.cast(hq, dw.u32p), (n,))
-        qa[:] = np.arange(lo, hi, dtype=np.uint32)
-        oa = np.ctypeslib.as_array(C.cast(ho, dw.u64p), (n + 1,))
+        qa = np.ctypeslib.as_array(C.cast(hq, dw.u32p), (nq,))
+        qa[:] = q0.cpu().numpy().astype(np.uint32)
+        oa = np.ctypeslib.as_array(C.cast(ho, dw.u64p), (nq + 1,))
+        hqid = None if qid0 is None else np.ascontiguousarray(qid0.cpu().numpy().astype(np.uint64))
+        odesc = dw.RunOptions(mode=args.mode, walk_length=L, seed=WALK_SEED,
+                              edge_cost_ratio=ratio, qid_base=base0, qids=hqid).c()
         st = dw.RunStatsC()
 
         def e2e_step():
-            rc = lib.dw_run_compact(dg.h, C.byref(mdesc), C.cast(hq, dw.u32p), n,
+            rc = lib.dw_run_compact(dg.h, C.byref(mdesc), C.cast(hq, dw.u32p), nq,
                                     C.byref(odesc), C.cast(ho, dw.u64p), C.cast(hf, dw.u32p),
                                     cap, C.byref(st))
             if rc:
@@ -363,11 +448,12 @@ def run_ours(args):
             t0 = time.perf_counter()
             e2e_step()
             ts.append(time.perf_counter() - t0)
-        t_e2e = reduce_max(float(np.mean(ts)), dist, dev)
-        ids = int(oa[n])
+        t_e2e = reduce_max(float(np.mean(ts)), dist, cdev)
+        ids = int(oa[nq])
         e2e = {"value": walker_steps / t_e2e, "unit": UNIT,
-               "h2d_bytes_per_step": reduce_sum(n * 4, dist, dev),
-               "d2h_bytes_per_step": reduce_sum((n + 1) * 8 + ids * 4, dist, dev),
+               "h2d_bytes_per_step": reduce_sum(nq * (4 + (8 if hqid is not None else 0)), dist,
+                                                cdev),
+               "d2h_bytes_per_step": reduce_sum((nq + 1) * 8 + ids * 4, dist, cdev),
                "ms_per_step": t_e2e * 1e3,
                "api": "dw_run_compact (C ABI): pinned host queries in, offsets + path ids out"}
         for buf in (hq, ho, hf):
@@ -383,14 +469,20 @@ def run_ours(args):
     pk = peaks()
     achieved = alg_bytes / (kernel_ms / 1e3) / 1e9
     traffic = ncu_traffic(args.scale)
+    if strong:
+        par = (f"walker-parallel x{world}: the {walkers_total} global walker ids hash-"
+               "partitioned over the ranks (Fibonacci hashing), graph replicated, no collective "
+               "in the walk")
+    else:
+        par = (f"walker-parallel x{world} (one walker per vertex per GPU, graph replicated)"
+               if world > 1 else "1 GPU, graph resident")
     out = {
         "metric": metric(args), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
-        "higher_is_better": True, "scaling": "weak",
+        "higher_is_better": True, "scaling": "strong" if (strong or world == 1) else "weak",
         "vs_baseline": None, "dtype": "f64 (bit-exact reference arithmetic), u32 ids",
         "data": "synthetic R-MAT (deterministic Philox generator, on-device)",
-        "config": dict(workload(args), parallelism=f"walker-parallel x{world} (one walker per "
-                                                   "vertex per GPU, graph replicated)",
+        "config": dict(workload(args), parallelism=par,
                        edge_cost_ratio=ratio, edge_cost_ratio_source=(
                            "override" if args.ratio > 0 else "device-calibrated (K4)")),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"],
@@ -409,6 +501,7 @@ def run_ours(args):
         "clocks": clk.summary(),
         "gpu_launches": int(stats.kernel_launches) * args.steps,
         "walker_steps_per_step": walker_steps,
+        "walkers_per_step": walkers_total,
         "stats": {k: int(getattr(stats, k)) for k in (
             "steps", "select_erjs", "select_ervs", "trials", "weight_reads", "rng_draws",
             "erjs_fallbacks", "dead_ends")},
@@ -416,7 +509,62 @@ def run_ours(args):
         "graph": dict(info, device_free_after_build_gb=graph_bytes[0] / 1e9,
                       device_total_gb=graph_bytes[1] / 1e9),
     }
+    if world > 1:
+        out["shards"] = {"min_walkers": int(walkers_min), "max_walkers": int(walkers_max)}
+    if gather is not None:
+        out["gather"] = gather
     print(json.dumps(out), flush=True)
+
+
+def gather_shards(torch, dist, cdev, round0, lengths, paths, rank, world, nv,
+                  keep=False) -> dict:
+    """End-of-run gather of every rank's path shard (global ids, lengths, padded
+    paths) to rank 0, which scatters them back into query order.  Shards have
+    different sizes, so they are padded to the largest.  keep: rank 0 returns
+    the gathered lengths and paths in query order (tests)."""
+    def sync():
+        if q0.device.type == "cuda":
+            torch.cuda.synchronize()
+    q0, qid0, base0 = round0
+    n = len(q0)
+    ids = (qid0 if qid0 is not None else
+           torch.arange(base0, base0 + n, dtype=torch.int64, device=q0.device))
+    sizes = [torch.zeros(1, dtype=torch.int64, device=cdev) for _ in range(world)]
+    dist.all_gather(sizes, torch.tensor([n], dtype=torch.int64, device=cdev))
+    m = int(max(int(x.item()) for x in sizes))
+    stride = paths.shape[1]
+    sync()
+    t0 = time.perf_counter()
+    pack = torch.full((m, stride + 3), -1, dtype=torch.int32, device=q0.device)
+    pack[:n, 0] = (ids & 0xFFFFFFFF).to(torch.int32)
+    pack[:n, 1] = (ids >> 32).to(torch.int32)
+    pack[:n, 2] = lengths[:n]
+    pack[:n, 3:] = paths[:n]
+    pack = pack.to(cdev)
+    bufs = [torch.empty_like(pack) for _ in range(world)] if rank == 0 else None
+    dist.gather(pack, bufs, dst=0)
+    out = {}
+    if rank == 0:
+        total = sum(int(x.item()) for x in sizes)
+        full_len = torch.empty(total, dtype=torch.int32, device=q0.device)
+        full_paths = torch.empty((total, stride), dtype=torch.int32, device=q0.device)
+        for k, b in enumerate(bufs):
+            nk = int(sizes[k].item())
+            b = b[:nk].to(q0.device)
+            gid = (b[:, 0].to(torch.int64) & 0xFFFFFFFF) | (b[:, 1].to(torch.int64) << 32)
+            at = gid - base0 if qid0 is None else gid
+            full_len[at] = b[:, 2]
+            full_paths[at] = b[:, 3:]
+        sync()
+        out = {"ms": (time.perf_counter() - t0) * 1e3, "walkers": total,
+               "bytes": total * (stride + 3) * 4,
+               "backend": f"{dist.get_backend()} gather (padded shards), scattered into query "
+                          "order on rank 0",
+               "walk_steps_check": int((full_len.to(torch.int64) - 1).clamp(min=0).sum().item())}
+        if keep:
+            out["lengths"], out["paths"] = full_len, full_paths
+    dist.barrier()
+    return out
 
 
 def cpu_baseline_port(dg, args, ratio, nv) -> dict:
@@ -528,6 +676,10 @@ def run_reference(args):
 
 def main():
     args = parse()
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        self_launch(args)
     if args.impl == "reference":
         run_reference(args)
     else:

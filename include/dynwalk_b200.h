@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define DW_ABI_VERSION 1
+#define DW_ABI_VERSION 2
 #define DW_INVALID_VERTEX 0xFFFFFFFFu /* kInvalidVertex, types.hpp:13 */
 
 enum {
@@ -110,6 +110,12 @@ typedef struct dw_run_opts {
     uint64_t erjs_cap_per_degree;  /* default 64 */
     double edge_cost_ratio;        /* decide_sampler threshold, > 0 */
     uint64_t qid_base;             /* global id of queries[0] (RNG key; sharding) */
+    /* [nq] global walker ids (RNG keys) of the queries, or NULL: qid_base + i.
+     * Lets one shard of a partitioned run walk any subset of the global ids
+     * (hash-partitioned walkers) with the streams, and so the
+     * paths, of the unpartitioned run.  Host memory for dw_run /
+     * dw_run_compact / dw_run_write_paths, device memory for dw_run_device. */
+    const uint64_t* qids;
 } dw_run_opts;
 
 /* RunStats (runtime.hpp:53-73) minus host-only fields. */
@@ -148,8 +154,23 @@ int dw_graph_download(dw_graph_t g, uint64_t* row_offsets, uint32_t* col_indices
                       float* edge_props, uint16_t* edge_labels, double* node_prop_max,
                       double* node_prop_sum);
 
+/* ProfileConfig (cost_model.hpp:9-15). */
+typedef struct dw_profile_config {
+    double node_fraction;         /* share of nodes probed per round, (0, 1]; default 0.01 */
+    uint32_t min_nodes;           /* probe at least this many (graph permitting); default 64 */
+    uint32_t neighbors_per_node;  /* >= 1; default 32 */
+    uint32_t repetitions;         /* >= 1; default 5 (the median is returned) */
+    uint64_t seed;
+} dw_profile_config;
+
 /* Replaces profile_edge_cost_ratio (cost_model.hpp:39-40, cost_model.cpp:37-126):
- * random-neighbour vs sequential weight evaluation timed on device 0. */
+ * random-neighbour vs sequential weight evaluation timed on device 0, the
+ * median per-edge time ratio over cfg->repetitions.  Errors follow the
+ * reference (node_fraction outside (0, 1], zero neighbours or repetitions,
+ * no node with out-edges). */
+int dw_calibrate_ex(dw_graph_t g, const dw_model_desc* model, const dw_profile_config* cfg,
+                    double* ratio);
+/* dw_calibrate_ex with the ProfileConfig defaults and `seed`. */
 int dw_calibrate(dw_graph_t g, const dw_model_desc* model, uint64_t seed, double* ratio);
 
 /* Compiles a DslWalk weight function into the walk kernel.
@@ -169,7 +190,10 @@ int dw_model_free(dw_custom_model_t model);
 /* Replaces run_queries (runtime.hpp:85-86, runtime.cpp:192-247).
  * queries: host [nq].  paths: host [nq][walk_length+1], DW_INVALID_VERTEX
  * padded, or NULL (discard).  lengths: host [nq] (0 = query error) or NULL.
- * Walkers are split in contiguous blocks over the handle's devices. */
+ * Walkers are cut into batches that go round-robin over the handle's devices;
+ * every device walks while the host drains finished batches in query order,
+ * and the output does not depend on the device count (the RNG is keyed by the
+ * global walker id). */
 int dw_run(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries, uint64_t nq,
            const dw_run_opts* opts, uint32_t* paths, uint32_t* lengths, dw_run_stats* stats);
 

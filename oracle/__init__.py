@@ -44,7 +44,7 @@ class OrcModel(C.Structure):
 class OrcOpts(C.Structure):
     _fields_ = [("mode", C.c_int), ("walk_length", C.c_uint32), ("seed", C.c_uint64),
                 ("cap_per_degree", C.c_uint64), ("edge_cost_ratio", C.c_double),
-                ("rng", C.c_int), ("qid_base", C.c_uint64)]
+                ("rng", C.c_int), ("qid_base", C.c_uint64), ("qids", C.c_void_p)]
 
 
 class OrcStats(C.Structure):
@@ -290,14 +290,19 @@ class RunResult:
 
 def run(g: Graph, model: Model, queries, mode="adaptive", walk_length=80, seed=0,
         cap_per_degree=64, ratio=1.0, rng="philox", threads=1, keep_paths=True,
-        qid_base=0) -> RunResult:
-    """Oracle run_queries (runtime.cpp:192-247)."""
+        qid_base=0, qids=None) -> RunResult:
+    """Oracle run_queries (runtime.cpp:192-247).  qids: [nq] global walker
+    ids (stream keys) of the queries, default qid_base + i."""
     q = np.ascontiguousarray(queries, np.uint32)
+    qa = None if qids is None else np.ascontiguousarray(qids, np.uint64)
+    if qa is not None and len(qa) != len(q):
+        raise ValueError("qids must hold one id per query")
     paths = np.empty((len(q), walk_length + 1), np.uint32) if keep_paths else None
     lengths = np.empty(len(q), np.uint32)
     st = OrcStats()
     m = model.c()
-    o = OrcOpts(MODES[mode], walk_length, seed, cap_per_degree, ratio, RNG[rng], qid_base)
+    o = OrcOpts(MODES[mode], walk_length, seed, cap_per_degree, ratio, RNG[rng], qid_base,
+                None if qa is None else qa.ctypes.data)
     import time
     t0 = time.perf_counter()
     rc = lib().orc_run(g.ptr, C.byref(m), C.byref(o), _ptr(q, u32p), len(q),

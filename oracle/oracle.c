@@ -1197,7 +1197,7 @@ static void* run_worker(void* arg) {
             if (sh->lengths) sh->lengths[i] = 0;
             continue;
         }
-        const int64_t len = walk_query(&c, sh->o, start, sh->o->qid_base + i, path, &ls, r);
+        const int64_t len = walk_query(&c, sh->o, start, sh->o->qids ? sh->o->qids[i] : sh->o->qid_base + i, path, &ls, r);
         if (len < 0) {
             pthread_mutex_lock(&g_err_mu);
             if (!sh->failed) {

@@ -58,6 +58,7 @@ typedef struct orc_opts {
     double edge_cost_ratio;
     int rng; /* ORC_RNG_* */
     uint64_t qid_base; /* global id of queries[0] (walker-stream key) */
+    const uint64_t* qids; /* [nq] global walker ids, or NULL: qid_base + i */
 } orc_opts;
 
 /* Mirrors RunStats (include/dynwalk/runtime.hpp:53-73), GPU-relevant fields. */

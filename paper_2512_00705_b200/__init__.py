@@ -23,8 +23,8 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-__all__ = ["DeviceGraph", "Model", "RunOptions", "RunResult", "DynwalkError", "run_queries",
-           "profile_edge_cost_ratio", "library_path", "load_library", "EXPORTED_SYMBOLS",
+__all__ = ["DeviceGraph", "Model", "RunOptions", "ProfileConfig", "RunResult", "DynwalkError", "run_queries",
+           "profile_edge_cost_ratio", "shard_of", "library_path", "load_library", "EXPORTED_SYMBOLS",
            "INVALID_VERTEX"]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -35,7 +35,7 @@ INVALID_VERTEX = 0xFFFFFFFF
 EXPORTED_SYMBOLS = (
     "dw_abi_version", "dw_last_error", "dw_device_count", "dw_graph_create", "dw_graph_load_dwg1",
     "dw_graph_generate_rmat", "dw_graph_destroy", "dw_graph_info", "dw_graph_download",
-    "dw_calibrate", "dw_model_compile", "dw_model_free", "dw_run", "dw_run_compact",
+    "dw_calibrate", "dw_calibrate_ex", "dw_model_compile", "dw_model_free", "dw_run", "dw_run_compact",
     "dw_run_write_paths", "dw_run_device",
     "dw_run_device_sync",
     "dw_host_alloc",
@@ -85,7 +85,13 @@ class ModelDesc(C.Structure):
 class RunOptsC(C.Structure):
     _fields_ = [("mode", C.c_int), ("walk_length", C.c_uint32), ("seed", C.c_uint64),
                 ("erjs_cap_per_degree", C.c_uint64), ("edge_cost_ratio", C.c_double),
-                ("qid_base", C.c_uint64)]
+                ("qid_base", C.c_uint64), ("qids", C.c_void_p)]
+
+
+class ProfileConfigC(C.Structure):
+    _fields_ = [("node_fraction", C.c_double), ("min_nodes", C.c_uint32),
+                ("neighbors_per_node", C.c_uint32), ("repetitions", C.c_uint32),
+                ("seed", C.c_uint64)]
 
 
 class RunStatsC(C.Structure):
@@ -132,6 +138,7 @@ def load_library() -> C.CDLL:
     L.dw_graph_info.argtypes = [vp, u32p, u64p, C.POINTER(C.c_int), u32p]
     L.dw_graph_download.argtypes = [vp, u64p, u32p, f32p, u16p, f64p, f64p]
     L.dw_calibrate.argtypes = [vp, C.POINTER(ModelDesc), C.c_uint64, f64p]
+    L.dw_calibrate_ex.argtypes = [vp, C.POINTER(ModelDesc), C.POINTER(ProfileConfigC), f64p]
     L.dw_model_compile.argtypes = [C.c_char_p, C.c_uint32, C.c_uint32, C.POINTER(vp)]
     L.dw_model_free.argtypes = [vp]
     L.dw_run.argtypes = [vp, C.POINTER(ModelDesc), u32p, C.c_uint64, C.POINTER(RunOptsC), u32p,
@@ -207,12 +214,20 @@ class RunOptions:
     erjs_cap_per_degree: int = 64
     edge_cost_ratio: float = 1.0
     qid_base: int = 0
+    # global walker ids (RNG keys) of the queries: a host uint64 array for
+    # run_queries*, or an int device address for dw_run_device; None = qid_base + i
+    qids: object = None
 
     def c(self) -> RunOptsC:
         if self.mode not in MODES:
             raise DynwalkError(-1, f"unknown sampler mode '{self.mode}'")
+        q = self.qids
+        if isinstance(q, np.ndarray):
+            if q.dtype != np.uint64 or not q.flags.c_contiguous:
+                raise DynwalkError(-1, "qids must be a contiguous uint64 array")
+            q = q.ctypes.data
         return RunOptsC(MODES[self.mode], self.walk_length, self.seed & (2**64 - 1),
-                        self.erjs_cap_per_degree, self.edge_cost_ratio, self.qid_base)
+                        self.erjs_cap_per_degree, self.edge_cost_ratio, self.qid_base, q)
 
 
 @dataclass
@@ -303,12 +318,46 @@ class DeviceGraph:
         return out
 
 
-def profile_edge_cost_ratio(g: DeviceGraph, model: Model, seed: int = 0) -> float:
-    """profile_edge_cost_ratio (cost_model.cpp:37-126), timed on the device."""
+@dataclass
+class ProfileConfig:
+    """ProfileConfig (cost_model.hpp:9-15)."""
+    node_fraction: float = 0.01
+    min_nodes: int = 64
+    neighbors_per_node: int = 32
+    repetitions: int = 5
+    seed: int = 0
+
+    def c(self) -> ProfileConfigC:
+        return ProfileConfigC(self.node_fraction, self.min_nodes, self.neighbors_per_node,
+                              self.repetitions, self.seed)
+
+
+def profile_edge_cost_ratio(g: DeviceGraph, model: Model, seed: int = 0,
+                            cfg: ProfileConfig | None = None) -> float:
+    """profile_edge_cost_ratio (cost_model.cpp:37-126), timed on the device.
+    `cfg` overrides the ProfileConfig defaults (its seed wins over `seed`)."""
     r = C.c_double()
     m = model.c()
-    _check(load_library().dw_calibrate(g.h, C.byref(m), seed, C.byref(r)))
+    c = (cfg if cfg is not None else ProfileConfig(seed=seed)).c()
+    _check(load_library().dw_calibrate_ex(g.h, C.byref(m), C.byref(c), C.byref(r)))
     return r.value
+
+
+def _check_qids(opts: RunOptions, nq: int) -> None:
+    if isinstance(opts.qids, np.ndarray) and len(opts.qids) != nq:
+        raise DynwalkError(-1, f"qids holds {len(opts.qids)} walker ids for {nq} queries")
+
+
+def shard_of(qids, world: int) -> np.ndarray:
+    """Rank that walks each global walker id in a `world`-way partitioned run:
+    Fibonacci hashing (high 32 bits of q * 0x9E3779B97F4A7C15 mod 2^64, mod
+    world).  Consecutive ids spread over all ranks, so a hub-heavy stretch of
+    the query list does not land on one GPU (range partitioning scales worse,
+    PAPER.md:1086).  bench.py computes the same function on the device."""
+    q = np.asarray(qids, np.uint64)
+    with np.errstate(over="ignore"):
+        h = (q * np.uint64(0x9E3779B97F4A7C15)) >> np.uint64(32)
+    return (h % np.uint64(world)).astype(np.int64)
 
 
 def run_queries(g: DeviceGraph, model: Model, queries, opts: RunOptions,
@@ -316,6 +365,7 @@ def run_queries(g: DeviceGraph, model: Model, queries, opts: RunOptions,
     """run_queries (runtime.cpp:192-247) on the device replicas of `g`."""
     L = load_library()
     q = np.ascontiguousarray(queries, np.uint32)
+    _check_qids(opts, len(q))
     stride = opts.walk_length + 1
     paths = out_paths
     if paths is None and keep_paths:
@@ -335,6 +385,7 @@ def run_queries_compact(g: DeviceGraph, model: Model, queries, opts: RunOptions)
     flat[offsets[i]:offsets[i+1]]."""
     L = load_library()
     q = np.ascontiguousarray(queries, np.uint32)
+    _check_qids(opts, len(q))
     offsets = np.empty(len(q) + 1, np.uint64)
     cap = len(q) * (opts.walk_length + 1)
     flat = np.empty(max(cap, 1), np.uint32)
@@ -351,6 +402,7 @@ def run_write_paths(g: DeviceGraph, model: Model, queries, opts: RunOptions, pat
     text formatted on the device; returns the RunStats counters."""
     L = load_library()
     q = np.ascontiguousarray(queries, np.uint32)
+    _check_qids(opts, len(q))
     st = RunStatsC()
     m = model.c()
     o = opts.c()

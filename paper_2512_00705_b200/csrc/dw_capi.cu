@@ -78,6 +78,7 @@ struct Replica {
     // bounded whatever nq is (BASELINE config 5 streams 435 GB of paths)
     struct Slot {
         uint32_t* q = nullptr;      // [cap] queries
+        ull* qids = nullptr;        // [cap] global walker ids (runs with dw_run_opts.qids)
         uint32_t* len = nullptr;    // [cap] path lengths
         uint32_t* paths = nullptr;  // [cap][stride] padded paths
         uint32_t* flat = nullptr;   // [cap * stride] compacted paths (compact runs)
@@ -87,7 +88,7 @@ struct Replica {
     };
     Slot slots[kRingSlots];
     ull slot_cap = 0, slot_stride = 0;
-    bool slot_flat = false, slot_txt = false;
+    bool slot_flat = false, slot_txt = false, slot_qids = false;
     ull* d_base = nullptr;      // running offset of the batches already compacted
     void* d_scan = nullptr;
     size_t scan_bytes = 0;
@@ -169,6 +170,7 @@ void free_replica(Replica& r) {
     cudaFree(r.error_info);
     for (auto& sl : r.slots) {
         cudaFree(sl.q);
+        cudaFree(sl.qids);
         cudaFree(sl.len);
         cudaFree(sl.paths);
         cudaFree(sl.flat);
@@ -341,6 +343,14 @@ dwb::ModelParams model_params(const dw_model_desc* m) {
     // one-multiply weight-sum screen (dw_models.cuh wsum_approx)
     mp.screen = (m->kind == DW_MODEL_NODE2VEC && m->a > 0.0 && m->b > 0.0) ? 1u : 0u;
     mp.wsum_coef = (1.0 / m->a + 1.0 + 1.0 / m->b) / 3.0;
+    // decisions within this relative distance of a compact record's f32 row
+    // sum refetch the exact node record (dw_walk_kernel.cuh); the f32 sum is
+    // within 2^-24 of the double one, so any band >= 1e-6 is exact
+    mp.fat32_band = 1e-6;
+    if (const char* env = std::getenv("DW_FAT32_BAND")) {
+        const double b = std::atof(env);
+        if (b >= 1e-6) mp.fat32_band = b;
+    }
     if (const char* env = std::getenv("DW_SCREEN"))
         if (env[0] == '0') mp.screen = 0u;
     if (const char* env = std::getenv("DW_D1"))
@@ -472,17 +482,20 @@ int collect(Replica& r, dw_run_stats* st, ull qbase) {
 
 constexpr ull kTextBytesPerId = 11;  // up to 10 digits + separator
 
-int ensure_ring(Replica& r, ull cap, ull stride, bool flat, bool txt) {
+int ensure_ring(Replica& r, ull cap, ull stride, bool flat, bool txt, bool qids) {
     if (cap <= r.slot_cap && stride <= r.slot_stride && (!flat || r.slot_flat) &&
-        (!txt || r.slot_txt))
+        (!txt || r.slot_txt) && (!qids || r.slot_qids))
         return DW_OK;
     CU(cudaDeviceSynchronize(), "ring");
     cap = std::max(cap, r.slot_cap);
     stride = std::max(stride, r.slot_stride);
     flat = flat || txt || r.slot_flat;
     txt = txt || r.slot_txt;
+    qids = qids || r.slot_qids;
     for (auto& sl : r.slots) {
         cudaFree(sl.q);
+        cudaFree(sl.qids);
+        sl.qids = nullptr;
         cudaFree(sl.len);
         cudaFree(sl.paths);
         cudaFree(sl.flat);
@@ -493,6 +506,7 @@ int ensure_ring(Replica& r, ull cap, ull stride, bool flat, bool txt) {
         sl.txt = nullptr;
         CU(cudaMalloc(&sl.q, cap * sizeof(uint32_t)), "cudaMalloc queries");
         CU(cudaMalloc(&sl.len, cap * sizeof(uint32_t)), "cudaMalloc lengths");
+        if (qids) CU(cudaMalloc(&sl.qids, cap * sizeof(ull)), "cudaMalloc walker ids");
         CU(cudaMalloc(&sl.paths, cap * stride * sizeof(uint32_t)), "cudaMalloc paths");
         if (flat) {
             CU(cudaMalloc(&sl.flat, cap * stride * sizeof(uint32_t)), "cudaMalloc flat paths");
@@ -514,6 +528,7 @@ int ensure_ring(Replica& r, ull cap, ull stride, bool flat, bool txt) {
     r.slot_stride = stride;
     r.slot_flat = flat;
     r.slot_txt = txt;
+    r.slot_qids = qids;
     return DW_OK;
 }
 
@@ -570,20 +585,40 @@ std::vector<ull> batch_plan(ull n, ull cap) {
     return at;
 }
 
-// The batched H2D -> walk -> (compaction) -> D2H pipeline behind dw_run and
-// dw_run_compact.  Each device walks a contiguous block of the queries in
-// batches that cycle through kRingSlots buffer slots; stream events order slot
-// reuse, so the host only blocks to learn a compact batch's size.
+// The batched H2D -> walk -> (compaction) -> D2H pipeline behind dw_run,
+// dw_run_compact and dw_run_write_paths.  The queries are cut into batches
+// (batch_plan) that go round-robin over the devices, so every device walks
+// at once and a hub-heavy stretch of the query list is spread over all of
+// them.  On each device, batches cycle through kRingSlots buffer slots and
+// stream events order slot reuse.  The host drains finished batches in query
+// order: it blocks only to learn a compact / text batch's size, and never on a
+// device other than the batch's own, so a device refills its ring while
+// another one is being drained.  Output is independent of the device count:
+// the RNG is keyed by the global walker id, and a batch's compact offsets are
+// shifted to their global position on the host after the last copy.
 int run_engine(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries, ull nq,
                const dw_run_opts* opts, const RunOut& out, dw_run_stats* st) {
     if (st) std::memset(st, 0, sizeof *st);
     const int nd = (int)g->reps.size();
     const ull stride = (ull)opts->walk_length + 1;
+    const bool ordered = out.compact || out.text;
+    const ull per_dev = std::max<ull>(1, (nq + nd - 1) / nd);
+    const ull bs = out.text ? std::min<ull>(batch_size(per_dev), 1ull << 20) : batch_size(per_dev);
+    const std::vector<ull> at = batch_plan(nq, bs);
+    const ull nb = at.size() - 1;
     struct Dev {
-        ull lo = 0, n = 0, bs = 1, nb = 0, eb = 0, db = 0, end = 0;
-        std::vector<ull> at;  // batch starts (batch_plan), at[nb] == n
+        ull end = 0;       // device-local running end offset (ids or text bytes)
+        ull inflight = 0;  // batches enqueued and not yet drained
     };
     std::vector<Dev> dv(nd);
+    struct Fixup {
+        ull lo, n, delta;
+    };
+    std::vector<Fixup> fixups;  // compact offsets that need the other devices' ids added
+    // DW_ENGINE_TRACE=<file>: the host schedule ("E|D batch device" per
+    // enqueue / drain), for tests of the device interleaving
+    std::unique_ptr<FILE, int (*)(FILE*)> trace(nullptr, &std::fclose);
+    if (const char* tp = std::getenv("DW_ENGINE_TRACE")) trace.reset(std::fopen(tp, "a"));
     cudaEvent_t wall0 = nullptr, wall1 = nullptr;
     CU(cudaSetDevice(g->reps[0].device), "cudaSetDevice");
     CU(cudaEventCreate(&wall0), "event");
@@ -593,46 +628,48 @@ int run_engine(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries
     int rc;
     for (int di = 0; di < nd; ++di) {
         Replica& r = g->reps[di];
-        Dev& d = dv[di];
-        d.lo = nq * di / nd;
-        d.n = nq * (di + 1) / nd - d.lo;
-        d.bs = out.text ? std::min<ull>(batch_size(d.n), 1ull << 20) : batch_size(d.n);
-        d.at = batch_plan(d.n, d.bs);
-        d.nb = d.at.size() - 1;
         CU(cudaSetDevice(r.device), "cudaSetDevice");
         if ((rc = prepare_model(r, model))) return rc;
-        if ((rc = ensure_ring(r, d.bs, stride, out.compact, out.text != nullptr))) return rc;
+        if ((rc = ensure_ring(r, bs, stride, out.compact, out.text != nullptr,
+                              opts->qids != nullptr)))
+            return rc;
         if ((rc = reset_run_state(r))) return rc;
         CU(cudaMemsetAsync(r.d_base, 0, sizeof(ull), r.stream), "memset");
         CU(cudaEventRecord(r.ev_reset, r.stream), "event");
         CU(cudaStreamWaitEvent(r.copy, r.ev_reset, 0), "event");
         CU(cudaEventRecord(r.ev_start, r.stream), "event");
     }
-    auto enqueue = [&](int di, ull b) -> int {
+    auto enqueue = [&](ull b) -> int {
+        const int di = (int)(b % nd);
+        const ull li = b / nd;  // the device's own batch index
         Replica& r = g->reps[di];
-        Dev& d = dv[di];
-        Replica::Slot& sl = r.slots[b % kRingSlots];
-        const ull blo = d.at[b], bn = d.at[b + 1] - blo;
+        Replica::Slot& sl = r.slots[li % kRingSlots];
+        const ull blo = at[b], bn = at[b + 1] - blo;
         cudaStream_t ws = r.stream;
         CU(cudaSetDevice(r.device), "cudaSetDevice");
-        if (b >= (ull)kRingSlots) {  // the slot's previous batch must be walked and drained
+        if (li >= (ull)kRingSlots) {  // the slot's previous batch must be walked and drained
             CU(cudaStreamWaitEvent(r.copy, sl.walk, 0), "event");
             CU(cudaStreamWaitEvent(ws, sl.d2h, 0), "event");
         }
-        CU(cudaMemcpyAsync(sl.q, queries + d.lo + blo, bn * sizeof(uint32_t),
-                           cudaMemcpyHostToDevice, r.copy),
+        CU(cudaMemcpyAsync(sl.q, queries + blo, bn * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                           r.copy),
            "H2D queries");
+        if (opts->qids)
+            CU(cudaMemcpyAsync(sl.qids, opts->qids + blo, bn * sizeof(ull), cudaMemcpyHostToDevice,
+                               r.copy),
+               "H2D walker ids");
         CU(cudaEventRecord(sl.h2d, r.copy), "event");
         CU(cudaStreamWaitEvent(ws, sl.h2d, 0), "event");
         dwb::WalkParams p = make_params(r, model, opts);
         p.queries = sl.q;
         p.nq = bn;
-        p.qid_base = opts->qid_base + d.lo + blo;
+        p.qid_base = opts->qid_base + blo;
+        p.qids = opts->qids ? sl.qids : nullptr;
         p.paths = (out.compact || out.text || out.paths) ? sl.paths : nullptr;
         p.lengths = sl.len;
-        p.next_walker = r.queues + (b % kRingSlots);
+        p.next_walker = r.queues + (li % kRingSlots);
         CU(cudaMemsetAsync(p.next_walker, 0, sizeof(ull), ws), "memset");
-        if (p.paths && !out.compact && !out.text)  // compaction copies only the written ids
+        if (p.paths && !ordered)  // compaction copies only the written ids
             CU(cudaMemsetAsync(p.paths, 0xFF, bn * stride * sizeof(uint32_t), ws),
                "memset paths");
         CU(launch_model(r, model, opts->mode, p, ws), "walk");
@@ -651,110 +688,92 @@ int run_engine(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries
             launches += 6;
         }
         CU(cudaEventRecord(sl.walk, ws), "event");
-        if (out.compact || out.text) {
+        if (ordered) {
             CU(cudaStreamWaitEvent(r.ends, sl.walk, 0), "event");
-            CU(cudaMemcpyAsync(r.h_ends + (b % kRingSlots), sl.offs + bn, sizeof(ull),
+            CU(cudaMemcpyAsync(r.h_ends + (li % kRingSlots), sl.offs + bn, sizeof(ull),
                                cudaMemcpyDeviceToHost, r.ends),
                "D2H end");
             CU(cudaEventRecord(sl.end, r.ends), "event");
         } else {
             CU(cudaStreamWaitEvent(r.d2h, sl.walk, 0), "event");
             if (out.paths)
-                CU(cudaMemcpyAsync(out.paths + (d.lo + blo) * stride, sl.paths,
+                CU(cudaMemcpyAsync(out.paths + blo * stride, sl.paths,
                                    bn * stride * sizeof(uint32_t), cudaMemcpyDeviceToHost, r.d2h),
                    "D2H paths");
             if (out.lengths)
-                CU(cudaMemcpyAsync(out.lengths + d.lo + blo, sl.len, bn * sizeof(uint32_t),
+                CU(cudaMemcpyAsync(out.lengths + blo, sl.len, bn * sizeof(uint32_t),
                                    cudaMemcpyDeviceToHost, r.d2h),
                    "D2H lengths");
             CU(cudaEventRecord(sl.d2h, r.d2h), "event");
         }
         return DW_OK;
     };
-    ull gbase = 0;     // compact: host offset of the device being drained
-    int drain_dev = 0;  // compact: devices drain in order (their host offsets chain)
-    auto drain = [&](int di, ull b) -> int {
+    ull gbase = 0;  // ordered runs: ids (or text bytes) of the batches drained so far
+    auto drain = [&](ull b) -> int {
+        if (!ordered) return DW_OK;  // the D2H was enqueued with the walk
+        const int di = (int)(b % nd);
+        const ull li = b / nd;
         Replica& r = g->reps[di];
         Dev& d = dv[di];
-        Replica::Slot& sl = r.slots[b % kRingSlots];
-        if (!out.compact && !out.text) return DW_OK;  // the D2H was enqueued with the walk
-        const ull blo = d.at[b], bn = d.at[b + 1] - blo;
+        Replica::Slot& sl = r.slots[li % kRingSlots];
+        const ull blo = at[b], bn = at[b + 1] - blo;
         CU(cudaSetDevice(r.device), "cudaSetDevice");
         CU(cudaEventSynchronize(sl.end), "walk");
-        const ull end = r.h_ends[b % kRingSlots];
+        const ull end = r.h_ends[li % kRingSlots];
+        const ull cnt = end - d.end;
         if (out.text) {  // the batch's text follows the previous batches in the file
-            const ull nb_bytes = end - d.end;
-            if (nb_bytes) {
-                CU(cudaMemcpyAsync(out.h_txt, sl.txt, nb_bytes, cudaMemcpyDeviceToHost, r.d2h),
+            if (cnt) {
+                CU(cudaMemcpyAsync(out.h_txt, sl.txt, cnt, cudaMemcpyDeviceToHost, r.d2h),
                    "D2H text");
                 CU(cudaStreamSynchronize(r.d2h), "D2H text");
-                if (std::fwrite(out.h_txt, 1, nb_bytes, out.text) != nb_bytes)
+                if (std::fwrite(out.h_txt, 1, cnt, out.text) != cnt)
                     return fail(DW_EINVAL, "write failed: %s", out.text_path);
             }
             CU(cudaEventRecord(sl.d2h, r.d2h), "event");
             d.end = end;
+            gbase += cnt;
             return DW_OK;
         }
-        if (gbase + end > out.flat_cap) {
-            cudaDeviceSynchronize();
+        if (gbase + cnt > out.flat_cap) {
+            for (auto& rr : g->reps) {
+                cudaSetDevice(rr.device);
+                cudaDeviceSynchronize();
+            }
             return fail(DW_EINVAL, "flat path buffer too small: need more than %llu ids",
-                        (unsigned long long)(gbase + end));
+                        (unsigned long long)(gbase + cnt));
         }
-        if (end > d.end) {
+        if (cnt) {
             if (!out.flat) return fail(DW_EINVAL, "flat is NULL");
             // every walk full length: the padded rows are the flat layout and
             // compact_paths skipped the copy
-            const uint32_t* src = (end - d.end == bn * stride) ? sl.paths : sl.flat;
-            CU(cudaMemcpyAsync(out.flat + gbase + d.end, src, (end - d.end) * sizeof(uint32_t),
+            const uint32_t* src = (cnt == bn * stride) ? sl.paths : sl.flat;
+            CU(cudaMemcpyAsync(out.flat + gbase, src, cnt * sizeof(uint32_t),
                                cudaMemcpyDeviceToHost, r.d2h),
                "D2H paths");
         }
-        CU(cudaMemcpyAsync(out.offsets + d.lo + blo, sl.offs, bn * sizeof(ull),
-                           cudaMemcpyDeviceToHost, r.d2h),
+        CU(cudaMemcpyAsync(out.offsets + blo, sl.offs, bn * sizeof(ull), cudaMemcpyDeviceToHost,
+                           r.d2h),
            "D2H offsets");
         CU(cudaEventRecord(sl.d2h, r.d2h), "event");
+        // the device's offsets count its own batches only
+        if (gbase != d.end && bn) fixups.push_back({blo, bn, gbase - d.end});
         d.end = end;
+        gbase += cnt;
         return DW_OK;
     };
-    for (;;) {
-        bool busy = false;
-        for (int di = 0; di < nd; ++di) {
-            Dev& d = dv[di];
-            while (d.eb < d.nb && d.eb - d.db < (ull)kRingSlots) {
-                if ((rc = enqueue(di, d.eb))) return rc;
-                ++d.eb;
-                busy = true;
-            }
-            const bool ordered = out.compact || out.text;
-            const bool may_drain = !ordered || di == drain_dev;
-            if (d.db < d.eb && may_drain) {
-                if ((rc = drain(di, d.db))) return rc;
-                ++d.db;
-                busy = true;
-            }
-            if (ordered && di == drain_dev && d.db == d.nb) {
-                // device finished: its offsets become global, the next device drains
-                Replica& r = g->reps[di];
-                CU(cudaSetDevice(r.device), "cudaSetDevice");
-                if (gbase && out.compact) {
-                    CU(cudaStreamSynchronize(r.d2h), "copy");
-                    for (ull i = d.lo; i < d.lo + d.n; ++i) out.offsets[i] += gbase;
-                }
-                gbase += d.end;
-                ++drain_dev;
-                busy = true;
-            }
-            if (!ordered && d.db < d.eb) {
-                d.db = d.eb;  // padded runs need no host step per batch
-                busy = true;
-            }
+    for (ull eb = 0, db = 0; db < nb;) {
+        if (eb < nb && dv[eb % nd].inflight < (ull)kRingSlots) {
+            if (trace) std::fprintf(trace.get(), "E %llu %d\n", eb, (int)(eb % nd));
+            if ((rc = enqueue(eb))) return rc;
+            ++dv[eb % nd].inflight;
+            ++eb;
+        } else {
+            if (trace) std::fprintf(trace.get(), "D %llu %d\n", db, (int)(db % nd));
+            if ((rc = drain(db))) return rc;
+            --dv[db % nd].inflight;
+            ++db;
         }
-        bool done = true;
-        for (const Dev& d : dv) done = done && d.db == d.nb;
-        if (done && (!(out.compact || out.text) || drain_dev == nd)) break;
-        if (!busy) return fail(DW_ECUDA, "run pipeline stalled");
     }
-    if (out.compact) out.offsets[nq] = gbase;
     double kmax = 0.0;
     for (int di = 0; di < nd; ++di) {
         Replica& r = g->reps[di];
@@ -768,6 +787,11 @@ int run_engine(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries
         float ms = 0.f;
         cudaEventElapsedTime(&ms, r.ev_start, r.ev_stop);
         kmax = std::max(kmax, (double)ms);
+    }
+    if (out.compact) {
+        for (const Fixup& f : fixups)
+            for (ull i = f.lo; i < f.lo + f.n; ++i) out.offsets[i] += f.delta;
+        out.offsets[nq] = gbase;
     }
     CU(cudaSetDevice(g->reps[0].device), "cudaSetDevice");
     CU(cudaEventRecord(wall1, g->reps[0].d2h), "event");
@@ -1130,8 +1154,14 @@ int dw_graph_download(dw_graph_t g, uint64_t* row, uint32_t* col, float* prop, u
     return DW_OK;
 }
 
-int dw_calibrate(dw_graph_t g, const dw_model_desc* model, uint64_t seed, double* ratio) {
-    if (!g || !ratio) return fail(DW_EINVAL, "NULL argument");
+int dw_calibrate_ex(dw_graph_t g, const dw_model_desc* model, const dw_profile_config* cfg,
+                    double* ratio) {
+    if (!g || !ratio || !cfg) return fail(DW_EINVAL, "NULL argument");
+    // cost_model.cpp:39-42
+    if (!(cfg->node_fraction > 0.0) || cfg->node_fraction > 1.0)
+        return fail(DW_EINVAL, "profile node_fraction must be in (0, 1]");
+    if (cfg->neighbors_per_node == 0 || cfg->repetitions == 0)
+        return fail(DW_EINVAL, "profile neighbors_per_node and repetitions must be >= 1");
     int rc = check_model(model);
     if (rc) return rc;
     if (model->kind == DW_MODEL_CUSTOM)
@@ -1140,13 +1170,20 @@ int dw_calibrate(dw_graph_t g, const dw_model_desc* model, uint64_t seed, double
     Replica& r = g->reps[0];
     CU(cudaSetDevice(r.device), "cudaSetDevice");
     const dwb::ModelParams mp = model_params(model);
-    cudaError_t e = dwb::calibrate_ratio(r.g, model->kind, model->weighted != 0, mp, seed,
-                                         r.num_sms, r.stream, ratio);
+    const dwb::ProfileSpec spec{cfg->node_fraction, cfg->min_nodes, cfg->neighbors_per_node,
+                                cfg->repetitions, cfg->seed};
+    cudaError_t e = dwb::calibrate_ratio(r.g, model->kind, model->weighted != 0, mp, spec,
+                                         r.stream, ratio);
     if (e == cudaErrorInvalidValue) return fail(DW_EINVAL, "profiling found no node with out-edges");
     if (e != cudaSuccess) return cuda_fail(e, "calibrate");
     if (!(*ratio > 0.0) || !std::isfinite(*ratio))
         return fail(DW_EINVAL, "profiled edge cost ratio is not positive and finite");
     return DW_OK;
+}
+
+int dw_calibrate(dw_graph_t g, const dw_model_desc* model, uint64_t seed, double* ratio) {
+    const dw_profile_config cfg{0.01, 64, 32, 5, seed};
+    return dw_calibrate_ex(g, model, &cfg, ratio);
 }
 
 int dw_run_device(dw_graph_t g, int replica, const dw_model_desc* model, const uint32_t* d_queries,
@@ -1170,6 +1207,7 @@ int dw_run_device(dw_graph_t g, int replica, const dw_model_desc* model, const u
     p.queries = d_queries;
     p.nq = nq;
     p.qid_base = opts->qid_base;
+    p.qids = reinterpret_cast<const ull*>(opts->qids);
     p.paths = d_paths;
     p.lengths = d_lengths;
     p.next_walker = r.queues;

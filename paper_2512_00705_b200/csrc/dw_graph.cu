@@ -265,7 +265,10 @@ __global__ void fat32_build_kernel(const NodeRec* __restrict__ nodes, uint32_t n
             f.thoff = nu.hoff;
             f.twin = cnt >= 255u ? (255u << 24) : (lo | (cnt << 24));
             f.thmax = (float)nu.hmax;  // exact: a maximum of f32 props
-            f.thsum = (float)nu.hsum;
+            // a row sum above FLT_MAX has no f32 neighbour: NaN fails both of
+            // the decision's band tests, so the exact node record decides
+            const float fs = (float)nu.hsum;
+            f.thsum = isfinite(fs) ? fs : __int_as_float(0x7fc00000);
             fat[e] = f;
         }
     }
@@ -287,15 +290,28 @@ static cudaError_t build_fat(DeviceGraphBuffers& g, cudaStream_t s) {
         force = env[0] == '1';
     }
     if (g.ne == 0 || g.ne > kBeginMask) return cudaSuccess;
+    // Build temporaries freed with cudaFreeAsync stay in the stream-ordered
+    // pool until trimmed; return them first so they count as free.
+    auto free_now = [&](size_t* free_b) -> cudaError_t {
+        DW_TRY(cudaStreamSynchronize(s));
+        int dev = 0;
+        cudaMemPool_t pool;
+        DW_TRY(cudaGetDevice(&dev));
+        DW_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
+        DW_TRY(cudaMemPoolTrimTo(pool, 0));
+        size_t total_b = 0;
+        return cudaMemGetInfo(free_b, &total_b);
+    };
     // compact 32 B records for unlabelled graphs whose degrees fit 24 bits:
     // node2vec walks them (+5 % over the 64 B records at s24, and they fit
-    // s27), the other models use the 64 B records built next when those fit
+    // s27), the other models use the 64 B records built next when those fit.
+    // Both layouts together stay under kFatMaxBytes and leave 4 GB free.
     const bool compact_ok = !g.labels && g.max_degree < (1u << 24);
     const char* fenv = getenv("DW_FAT");
+    ull used = 0;
     if (compact_ok && !force && g.ne * sizeof(FatRec32) <= kFatMaxBytes) {
-        DW_TRY(cudaStreamSynchronize(s));
-        size_t fb = 0, tb = 0;
-        DW_TRY(cudaMemGetInfo(&fb, &tb));
+        size_t fb = 0;
+        DW_TRY(free_now(&fb));
         const ull need32 = g.ne * sizeof(FatRec32);
         if (need32 + (4ull << 30) <= fb) {
             DW_TRY(cudaMallocAsync(&g.fat32, need32, s));
@@ -303,30 +319,21 @@ static cudaError_t build_fat(DeviceGraphBuffers& g, cudaStream_t s) {
                                                                              g.fat32);
             DW_TRY(cudaGetLastError());
             DW_TRY(cudaStreamSynchronize(s));
+            used = need32;
             if (getenv("DW_VERBOSE"))
                 fprintf(stderr, "dynwalk: compact 32 B fat records built (%.1f GB)\n", need32 / 1e9);
         }
     }
     if (fenv && fenv[0] == '2') return cudaSuccess;  // compact records only
-    if (!force && g.ne * sizeof(FatRec) > kFatMaxBytes) {
+    if (!force && used + g.ne * sizeof(FatRec) > kFatMaxBytes) {
         if (getenv("DW_VERBOSE"))
-            fprintf(stderr, "dynwalk: fat records skipped (%.1f GB above the %.0f GB cap)\n",
-                    g.ne * sizeof(FatRec) / 1e9, kFatMaxBytes / 1e9);
+            fprintf(stderr, "dynwalk: fat records skipped (%.1f GB + %.1f GB above the %.0f GB cap)\n",
+                    g.ne * sizeof(FatRec) / 1e9, used / 1e9, kFatMaxBytes / 1e9);
         return cudaSuccess;
     }
-    // the fat layout is an accelerator: skip it when it would crowd HBM.
-    // Build temporaries freed with cudaFreeAsync stay in the stream-ordered
-    // pool until trimmed; return them first so they count as free.
-    DW_TRY(cudaStreamSynchronize(s));
-    {
-        int dev = 0;
-        cudaMemPool_t pool;
-        DW_TRY(cudaGetDevice(&dev));
-        DW_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
-        DW_TRY(cudaMemPoolTrimTo(pool, 0));
-    }
-    size_t free_b = 0, total_b = 0;
-    DW_TRY(cudaMemGetInfo(&free_b, &total_b));
+    // the fat layout is an accelerator: skip it when it would crowd HBM
+    size_t free_b = 0;
+    DW_TRY(free_now(&free_b));
     const ull need = g.ne * sizeof(FatRec);
     const bool fits = need + (4ull << 30) <= free_b;
     if (getenv("DW_VERBOSE"))
@@ -607,47 +614,55 @@ cudaError_t build_rmat(const RmatSpec& spec, DeviceGraphBuffers& g, cudaStream_t
 }
 
 // ---- K4: calibration (cost_model.cpp:37-126) -------------------------------
+// Probe state of one sampled node (probe_state, cost_model.cpp:20-33: step 1
+// with the first neighbour as prev), built once per calibration so the timed
+// passes read it with one coalesced load per warp.
 struct ProbeState {
-    Step S;
-    ull begin;      // row of cur
-    uint32_t phoff; // hash set of prev
+    ull begin;       // row of cur
+    uint32_t cur, degree;
+    uint32_t prev, prev_degree;
+    uint32_t phoff;  // hash set of prev
+    uint32_t step;
+    double hmax, hsum;
 };
 
 template <class M>
-__device__ __forceinline__ double eval_weight(const M& m, const ProbeState& P, const DevGraph& g,
-                                              ull e) {
+__device__ __forceinline__ double eval_weight(const M& m, const Step& S, uint32_t phoff,
+                                              const DevGraph& g, ull e) {
     const EdgeRec er = load_edge(g.edges + e);
     const uint16_t lab = (M::kUsesLabels && g.labels) ? g.labels[e] : (uint16_t)0;
-    const WeightCase wc = m.weight(P.S, er.col, er.h, lab);
+    const WeightCase wc = m.weight(S, er.col, er.h, lab);
     if (!M::kSecondOrder || !wc.needs_member) return wc.w;
-    return member(g, P.S.prev_degree, P.phoff, er.col) ? wc.w_in : wc.w_out;
+    return member(g, S.prev_degree, phoff, er.col) ? wc.w_in : wc.w_out;
 }
 
-// probe_state (cost_model.cpp:20-33): step 1 with the first neighbour as prev
-__device__ __forceinline__ ProbeState probe_state(const DevGraph& g, uint32_t v) {
-    ProbeState P;
-    Step& S = P.S;
+__global__ void probe_states_kernel(DevGraph g, const uint32_t* __restrict__ nodes, uint32_t n,
+                                    ProbeState* __restrict__ out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t v = nodes[i];
     const NodeRec nr = load_node(g.nodes + v);
-    S.cur = v;
-    S.degree = nr.degree;
-    S.hmax = nr.hmax;
-    S.hsum = nr.hsum;
-    S.prev = kInvalid;
-    S.prev_degree = 0;
-    S.step = 0;
+    ProbeState P;
     P.begin = nr.begin;
+    P.cur = v;
+    P.degree = nr.degree;
+    P.hmax = nr.hmax;
+    P.hsum = nr.hsum;
+    P.prev = kInvalid;
+    P.prev_degree = 0;
     P.phoff = 0;
+    P.step = 0;
     if (nr.degree) {
         const uint32_t pv = load_col(g.edges + nr.begin);
         const NodeRec pr = load_node(g.nodes + pv);
         if (pr.degree) {
-            S.prev = pv;
-            S.prev_degree = pr.degree;
+            P.prev = pv;
+            P.prev_degree = pr.degree;
             P.phoff = pr.hoff;
-            S.step = 1;
+            P.step = 1;
         }
     }
-    return P;
+    out[i] = P;
 }
 
 __global__ void sample_nodes_kernel(DevGraph g, ull seed, ull tries, uint32_t want,
@@ -663,85 +678,112 @@ __global__ void sample_nodes_kernel(DevGraph g, ull seed, ull tries, uint32_t wa
     }
 }
 
-// one warp per probed node, lane k < min(d, 32) evaluates one weight per round
+// One warp per probed node and round; lane k < min(d, npn) evaluates one
+// weight.  Round r probes the pool's nodes [r*n, (r+1)*n) (mod the pool), so
+// consecutive rounds touch different rows of the whole graph, not the same
+// cached neighbours: the pool is many times the L2, like the rows a walk
+// visits.  Both passes read the same states and evaluate the same number of
+// weights; they differ only in the access pattern (cost_model.cpp:67-98).
 template <class M, bool RANDOM>
 __global__ void probe_pass_kernel(DevGraph g, __grid_constant__ const ModelParams mp,
-                                  const uint32_t* __restrict__ nodes, uint32_t n, int rounds,
-                                  ull seed, double* sink) {
+                                  const ProbeState* __restrict__ pool, uint32_t pool_n, uint32_t n,
+                                  uint32_t npn, int rounds, ull seed, double* sink) {
     M m(mp);
     const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t lane = threadIdx.x & 31;
     if (w >= n) return;
-    const ProbeState P = probe_state(g, nodes[w]);
-    const Step& S = P.S;
-    m.prepare(S);
-    const uint32_t k = S.degree < 32 ? S.degree : 32;
-    // The random pass times one eRJS trial as the walk kernel runs it: the
-    // (x, y) draw, then a weight evaluation only when y is below the row's
-    // non-return maximum -- a trial above it is rejected without reading the
-    // edge (the free rejection of dw_walk_kernel.cuh).  The ratio then prices
-    // a trial, not a random read, against a sequential read (the eRJS-vs-eRVS
-    // cost balance decide_sampler encodes, cost_model.hpp:46-56).
-    double bnd = 1.0, mnr = __longlong_as_double(0x7ff0000000000000ll);
-    if (RANDOM && M::kBoundable && mp.shortcut) {
-        bnd = m.bound(S);
-        mnr = m.nonreturn_max(S);
-    }
     double acc = 0.0;
-    if (lane < k) {
-        for (int r = 0; r < rounds; ++r) {
+    for (int r = 0; r < rounds; ++r) {
+        const ProbeState P = pool[((ull)r * n + w) % pool_n];
+        Step S;
+        S.cur = P.cur;
+        S.prev = P.prev;
+        S.prev_degree = P.prev_degree;
+        S.step = P.step;
+        S.degree = P.degree;
+        S.hmax = P.hmax;
+        S.hsum = P.hsum;
+        S.lmax = S.lsum = 0.0;
+        m.prepare(S);
+        const uint32_t k = min(S.degree, npn);
+        // The random pass times one eRJS trial as the walk kernel runs it: the
+        // (x, y) draw, then a weight evaluation only when y is below the row's
+        // non-return maximum -- a trial above it is rejected without reading
+        // the edge (the free rejection of dw_walk_kernel.cuh).  The ratio then
+        // prices a trial, not a random read, against a sequential read (the
+        // eRJS-vs-eRVS cost balance decide_sampler encodes, cost_model.hpp:46-56).
+        double bnd = 1.0, mnr = __longlong_as_double(0x7ff0000000000000ll);
+        if (RANDOM && M::kBoundable && mp.shortcut) {
+            bnd = m.bound(S);
+            mnr = m.nonreturn_max(S);
+        }
+        for (uint32_t i = lane; i < k; i += 32) {
             ull e;
             if (RANDOM) {
-                const U4 b = philox4x32_10(U4{lane, (uint32_t)r, w, 0x72616e64u}, (uint32_t)seed,
+                const U4 b = philox4x32_10(U4{i, (uint32_t)r, w, 0x72616e64u}, (uint32_t)seed,
                                            (uint32_t)(seed >> 32));
                 e = P.begin + bounded(lo64(b), S.degree);
                 if (uniform01(hi64(b)) * bnd >= mnr) continue;  // rejected, nothing read
             } else {
-                e = P.begin + lane;
+                e = P.begin + i;
             }
-            acc += eval_weight(m, P, g, e);
+            acc += eval_weight(m, S, P.phoff, g, e);
         }
     }
     if (acc == -1.0) *sink = acc;  // keeps the loads alive
 }
 
 template <class M>
-static cudaError_t calibrate_t(const DeviceGraphBuffers& gb, const ModelParams& mp, ull seed,
-                               cudaStream_t s, double* ratio) {
+static cudaError_t calibrate_t(const DeviceGraphBuffers& gb, const ModelParams& mp,
+                               const ProfileSpec& cfg, cudaStream_t s, double* ratio) {
     DevGraph g{gb.nodes, gb.edges, gb.labels, gb.hslots, gb.fat, gb.lagg, gb.twin, gb.fat32,
                gb.nv, gb.ne};
-    // ProfileConfig defaults: 1% of nodes, >= 64, <= 32 neighbours, 5 reps
-    uint32_t want = (uint32_t)std::max<ull>((ull)std::ceil(0.01 * gb.nv), 64);
-    const ull tries = (ull)want * 8;
+    // the probe set of one round (cost_model.cpp:45-54): ceil(fraction * nv),
+    // at least min_nodes; the pool holds kPoolRounds such sets (capped at the
+    // graph's nodes with out-edges, and at 2^24 states)
+    constexpr ull kPoolRounds = 64;
+    const uint32_t want = (uint32_t)std::max<ull>(
+        (ull)std::ceil(cfg.node_fraction * gb.nv), (ull)cfg.min_nodes);
+    const ull pool_want = std::min<ull>(std::max<ull>((ull)want * kPoolRounds, want), 1ull << 24);
+    const ull tries = pool_want * 8;
     uint32_t* nodes = nullptr;
+    ProbeState* pool = nullptr;
     unsigned* count = nullptr;
     double* sink = nullptr;
-    DW_TRY(cudaMallocAsync(&nodes, want * sizeof(uint32_t), s));
+    DW_TRY(cudaMallocAsync(&nodes, pool_want * sizeof(uint32_t), s));
     DW_TRY(cudaMallocAsync(&count, sizeof(unsigned), s));
     DW_TRY(cudaMallocAsync(&sink, sizeof(double), s));
     DW_TRY(cudaMemsetAsync(count, 0, sizeof(unsigned), s));
-    const ull kseed = host_derive_seed(seed, 0x70726f66ULL);
-    sample_nodes_kernel<<<grid_for(tries, 256), 256, 0, s>>>(g, kseed, tries, want, nodes, count);
+    const ull kseed = host_derive_seed(cfg.seed, 0x70726f66ULL);
+    sample_nodes_kernel<<<grid_for(tries, 256), 256, 0, s>>>(g, kseed, tries, (uint32_t)pool_want,
+                                                            nodes, count);
     unsigned got = 0;
     DW_TRY(cudaMemcpyAsync(&got, count, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
     DW_TRY(cudaStreamSynchronize(s));
-    const uint32_t n = std::min<uint32_t>(got, want);
-    if (n == 0) {
+    const uint32_t pool_n = (uint32_t)std::min<ull>(got, pool_want);
+    if (pool_n == 0) {
         cudaFreeAsync(nodes, s);
         cudaFreeAsync(count, s);
         cudaFreeAsync(sink, s);
         return cudaErrorInvalidValue;  // "profiling found no node with out-edges"
     }
+    const uint32_t n = std::min<uint32_t>(want, pool_n);
+    DW_TRY(cudaMallocAsync(&pool, (ull)pool_n * sizeof(ProbeState), s));
+    probe_states_kernel<<<(pool_n + 255) / 256, 256, 0, s>>>(g, nodes, pool_n, pool);
+    DW_TRY(cudaGetLastError());
     cudaEvent_t e0, e1, e2;
     DW_TRY(cudaEventCreate(&e0));
     DW_TRY(cudaEventCreate(&e1));
     DW_TRY(cudaEventCreate(&e2));
-    const unsigned blocks = (n * 32 + 255) / 256;
+    const unsigned blocks = (unsigned)(((ull)n * 32 + 255) / 256);
+    const uint32_t npn = cfg.neighbors_per_node;
     auto pass = [&](int rounds, float& t_rand, float& t_seq) -> cudaError_t {
         cudaEventRecord(e0, s);
-        probe_pass_kernel<M, true><<<blocks, 256, 0, s>>>(g, mp, nodes, n, rounds, kseed, sink);
+        probe_pass_kernel<M, true>
+            <<<blocks, 256, 0, s>>>(g, mp, pool, pool_n, n, npn, rounds, kseed, sink);
         cudaEventRecord(e1, s);
-        probe_pass_kernel<M, false><<<blocks, 256, 0, s>>>(g, mp, nodes, n, rounds, kseed, sink);
+        probe_pass_kernel<M, false>
+            <<<blocks, 256, 0, s>>>(g, mp, pool, pool_n, n, npn, rounds, kseed, sink);
         cudaEventRecord(e2, s);
         DW_TRY(cudaEventSynchronize(e2));
         cudaEventElapsedTime(&t_rand, e0, e1);
@@ -760,7 +802,7 @@ static cudaError_t calibrate_t(const DeviceGraphBuffers& gb, const ModelParams& 
         rounds *= 2;
     }
     std::vector<double> ratios;
-    for (int rep = 0; rep < 5; ++rep) {  // ProfileConfig::repetitions
+    for (uint32_t rep = 0; rep < cfg.repetitions; ++rep) {
         DW_TRY(pass(rounds, tr, ts));
         ratios.push_back((double)tr / (double)ts);
     }
@@ -770,22 +812,24 @@ static cudaError_t calibrate_t(const DeviceGraphBuffers& gb, const ModelParams& 
     cudaEventDestroy(e1);
     cudaEventDestroy(e2);
     cudaFreeAsync(nodes, s);
+    cudaFreeAsync(pool, s);
     cudaFreeAsync(count, s);
     cudaFreeAsync(sink, s);
     return cudaStreamSynchronize(s);
 }
 
 cudaError_t calibrate_ratio(const DeviceGraphBuffers& g, int kind, bool weighted,
-                            const ModelParams& mp, ull seed, int, cudaStream_t s, double* ratio) {
+                            const ModelParams& mp, const ProfileSpec& cfg, cudaStream_t s,
+                            double* ratio) {
     switch (kind) {
-    case 0: return weighted ? calibrate_t<StaticModel<true>>(g, mp, seed, s, ratio)
-                            : calibrate_t<StaticModel<false>>(g, mp, seed, s, ratio);
-    case 1: return weighted ? calibrate_t<Node2VecModel<true>>(g, mp, seed, s, ratio)
-                            : calibrate_t<Node2VecModel<false>>(g, mp, seed, s, ratio);
-    case 2: return weighted ? calibrate_t<MetaPathModel<true>>(g, mp, seed, s, ratio)
-                            : calibrate_t<MetaPathModel<false>>(g, mp, seed, s, ratio);
-    case 3: return weighted ? calibrate_t<Pr2Model<true>>(g, mp, seed, s, ratio)
-                            : calibrate_t<Pr2Model<false>>(g, mp, seed, s, ratio);
+    case 0: return weighted ? calibrate_t<StaticModel<true>>(g, mp, cfg, s, ratio)
+                            : calibrate_t<StaticModel<false>>(g, mp, cfg, s, ratio);
+    case 1: return weighted ? calibrate_t<Node2VecModel<true>>(g, mp, cfg, s, ratio)
+                            : calibrate_t<Node2VecModel<false>>(g, mp, cfg, s, ratio);
+    case 2: return weighted ? calibrate_t<MetaPathModel<true>>(g, mp, cfg, s, ratio)
+                            : calibrate_t<MetaPathModel<false>>(g, mp, cfg, s, ratio);
+    case 3: return weighted ? calibrate_t<Pr2Model<true>>(g, mp, cfg, s, ratio)
+                            : calibrate_t<Pr2Model<false>>(g, mp, cfg, s, ratio);
     }
     return cudaErrorInvalidValue;
 }

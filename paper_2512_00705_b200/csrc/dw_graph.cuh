@@ -50,11 +50,20 @@ cudaError_t build_rmat(const RmatSpec& spec, DeviceGraphBuffers& out, cudaStream
 cudaError_t unpack_graph(const DeviceGraphBuffers& g, unsigned long long* d_row, uint32_t* d_col,
                          float* d_prop, double* d_nmax, double* d_nsum, cudaStream_t s);
 
+// ProfileConfig (cost_model.hpp:9-15), validated by the caller.
+struct ProfileSpec {
+    double node_fraction;         // share of nodes probed per round
+    uint32_t min_nodes;           // probe at least this many (graph permitting)
+    uint32_t neighbors_per_node;  // weights evaluated per probed node
+    uint32_t repetitions;         // median over this many timed repetitions
+    unsigned long long seed;
+};
+
 // K4: the two profiling micro-passes of profile_edge_cost_ratio
 // (cost_model.cpp:37-126) on the device; returns the median ratio.
 cudaError_t calibrate_ratio(const DeviceGraphBuffers& g, int model_kind, bool weighted,
-                            const ModelParams& mp, unsigned long long seed, int num_sms,
-                            cudaStream_t s, double* ratio);
+                            const ModelParams& mp, const ProfileSpec& cfg, cudaStream_t s,
+                            double* ratio);
 
 unsigned long long host_derive_seed(unsigned long long seed, unsigned long long stream);
 

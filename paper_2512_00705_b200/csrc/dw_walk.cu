@@ -34,7 +34,11 @@ template <bool W> struct UsesFat32<Node2VecModel<W>> { static constexpr bool val
 template <class M>
 static cudaError_t launch_m(int mode, const WalkParams& p, int num_sms, cudaStream_t s) {
     const bool fat = p.g.fat != nullptr;
-    const bool fat32 = UsesFat32<M>::value && p.g.fat32 != nullptr;
+    // the compact record's f32 row sum is decided through the one-multiply
+    // screen (adaptive; mp.screen) or not at all (force-erjs); without the
+    // screen every decision would fall back to the node record
+    const bool fat32 = UsesFat32<M>::value && p.g.fat32 != nullptr &&
+                       (p.mp.screen || mode == kForceErjs || !fat);
     switch (mode) {
     case kAdaptive:
         if constexpr (UsesFat32<M>::value)

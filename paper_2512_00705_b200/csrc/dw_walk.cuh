@@ -23,6 +23,7 @@ struct WalkParams {
     const uint32_t* queries;
     unsigned long long nq;
     unsigned long long qid_base;
+    const unsigned long long* qids;  // [nq] global walker ids (RNG keys), or null: qid_base + i
     uint32_t* paths;        // [nq][stride] or null
     uint32_t* lengths;      // [nq] or null
     uint32_t stride;        // walk_length + 1

@@ -106,11 +106,8 @@ template <bool W> struct CoopErjs<Pr2Model<W>> { static constexpr bool value = t
 #endif
 constexpr uint32_t kCjsMin = DW_CJS_MIN;
 // relative band around the f32 row sum of a compact record inside which the
-// exact node record decides (DW_FAT32_BAND: tests widen it to force that path)
-#ifndef DW_FAT32_BAND
-#define DW_FAT32_BAND 1e-6
-#endif
-constexpr double kFat32Band = DW_FAT32_BAND;
+// exact node record decides: ModelParams::fat32_band (1e-6; DW_FAT32_BAND in
+// the environment widens it, which tests use to force that path)
 // per-lane 64-bit counters kept in shared memory (updated per walker, per
 // eRVS neighbour or per rare event): eRJS trials, single-shot eRVS trials,
 // eRVS reads and draws, algorithmic bytes / 4, cap fallbacks, dead ends,
@@ -361,6 +358,7 @@ struct WalkSmem {
     uint32_t cur[kThreads], phoff[kThreads], plg[kThreads], hoff[kThreads], cap[kThreads],
         twlo[kThreads], twcnt[kThreads], nret[kThreads];
     double bound[kThreads], mnr[kThreads];
+    ull qg[kThreads];                // global walker id (RNG key) of the lane's walker
     ull cnt[kCNum];
     uint32_t hist[66];
     ull lct[LC_NUM];                 // block totals of the lane counters
@@ -458,11 +456,11 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
         return S;
     };
     auto key_of = [&]() {
-        const ull q = p.qid_base + qi;
+        const ull q = sm.qg[tid];
         return WalkerKey{p.seed_lo, p.seed_hi, (uint32_t)q, (uint32_t)(q >> 32), step};
     };
     auto fail = [&](int code) {
-        raise_error(p, code, p.qid_base + qi);
+        raise_error(p, code, sm.qg[tid]);
         phase = P_IDLE;
     };
     auto flush_walker = [&]() {
@@ -537,6 +535,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                             } else {
                                 phase = P_NODE;
                                 qi = i;
+                                sm.qg[tid] = p.qids ? p.qids[i] : p.qid_base + i;
                                 cur = start;
                                 prev = kInvalid;
                                 pdeg = phoff = plg = 0;
@@ -560,7 +559,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                 cp16(&s_mb[0][tid], b);
                 cp16(&s_mb[1][tid], b + 4);
             }
-            const ull q = p.qid_base + qi;
+            const ull q = sm.qg[tid];
             // step constants into registers once per iteration: the ring's
             // shared-memory stores below would otherwise force a reload of
             // the shared-memory state on every trial
@@ -854,9 +853,12 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                 lsum = __hiloint2double((int)la.w, (int)la.z);
             }
             // first step: no return edge; later (slim layout) the twin[] word
-            // of the edge taken, or an unknown range
-            tw_lo = 0;
-            tw_cnt = prev == kInvalid ? 0u : 0xFFFFFFFFu;
+            // of the edge taken, or an unknown range.  A compact record whose
+            // decision fell back here (need_node) keeps the range it carried.
+            if (FAT != 2 || prev == kInvalid) {
+                tw_lo = 0;
+                tw_cnt = prev == kInvalid ? 0u : 0xFFFFFFFFu;
+            }
             if (!FAT && g.twin && prev != kInvalid) {
                 const uint32_t w = s_t[0][tid];
                 if ((w >> 24) != 255u) {
@@ -882,9 +884,9 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                             // f32 sum unless T is within 1e-6 of it; then the
                             // exact node record decides (next iteration)
                             const double Wa = (M::kScreen && p.mp.screen) ? model.wsum_approx(S) : 0.0;
-                            if (M::kScreen && p.mp.screen && T < Wa * (1.0 - kFat32Band))
+                            if (M::kScreen && p.mp.screen && T < Wa * (1.0 - p.mp.fat32_band))
                                 erjs = true;
-                            else if (M::kScreen && p.mp.screen && T > Wa * (1.0 + kFat32Band))
+                            else if (M::kScreen && p.mp.screen && T > Wa * (1.0 + p.mp.fat32_band))
                                 erjs = false;
                             else
                                 need_node = true;
@@ -1011,7 +1013,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
             T.hmax = T.hsum = 0.0;
             const uint32_t tph = __shfl_sync(kFull, phoff, L);
             const ull tb = __shfl_sync(kFull, begin, L);
-            const ull q = p.qid_base + __shfl_sync(kFull, qi, L);
+            const ull q = sm.qg[(tid & ~31) + L];
             const WalkerKey K{p.seed_lo, p.seed_hi, (uint32_t)q, (uint32_t)(q >> 32), T.step};
             const ull db = __shfl_sync(kFull, lane == L ? ev_load().didx : 0ull, L);
             uint32_t nx = kInvalid, ni = 0;
@@ -1072,7 +1074,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                 const uint32_t tph = sm.phoff[Lt], tcap = sm.cap[Lt];
                 const uint32_t twl = sm.twlo[Lt], twc = sm.twcnt[Lt];
                 const double tbnd = sm.bound[Lt], tmnr = sm.mnr[Lt];
-                const ull q = p.qid_base + __shfl_sync(kFull, qi, L);
+                const ull q = sm.qg[Lt];
                 int win = -1;
                 bool bad = false;
                 uint32_t judged = 0, rets = 0, wu = 0;

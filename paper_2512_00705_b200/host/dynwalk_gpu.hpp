@@ -54,6 +54,7 @@ inline void check(int rc) {
 // Device replicas of one immutable Graph (graph.hpp:47).
 class DeviceGraph {
 public:
+    // one replica per device in `devices` (dw_graph_create)
     explicit DeviceGraph(const Graph& g, std::vector<int> devices = {0}) {
         const std::uint32_t nv = g.num_vertices();
         std::vector<double> nmax(nv), nsum(nv);
@@ -185,22 +186,58 @@ inline std::uint64_t sample_fingerprint(const Graph& g) {
 // fingerprint (arrays are never mutated in place: set_edge_props replaces the
 // vector).  An edit that touches none of the sampled positions is not seen;
 // callers that rewrite graphs in place should pass a DeviceGraph explicitly.
+using CacheKey = std::tuple<const Graph*, const void*, const void*, const void*, std::uint64_t,
+                            std::uint64_t>;
+struct ReplicaCache {
+    std::mutex mu;
+    std::map<CacheKey, std::shared_ptr<DeviceGraph>> map;
+    std::vector<int> devices;  // empty: every visible device
+};
+inline ReplicaCache& replica_cache() {
+    static ReplicaCache c;
+    return c;
+}
+
+// The devices a Graph is replicated on when the reference signatures are
+// called with a `const Graph&`: every visible GPU (walkers are split over
+// them; output does not depend on the count), or the list set_devices() gave.
+inline std::vector<int> default_devices() {
+    ReplicaCache& c = replica_cache();
+    if (!c.devices.empty()) return c.devices;
+    int n = 0;
+    dw_device_count(&n);
+    std::vector<int> all;
+    for (int d = 0; d < n; ++d) all.push_back(d);
+    if (all.empty()) all.push_back(0);  // dw_graph_create reports the missing device
+    return all;
+}
+
 inline std::shared_ptr<DeviceGraph> cached(const Graph& g) {
-    using Key = std::tuple<const Graph*, const void*, const void*, const void*, std::uint64_t,
-                           std::uint64_t>;
-    static std::mutex mu;
-    static std::map<Key, std::shared_ptr<DeviceGraph>> cache;
-    const Key k{&g, g.col_indices().data(), g.edge_props().data(),
-                g.has_labels() ? static_cast<const void*>(g.edge_labels().data()) : nullptr,
-                g.num_edges(), sample_fingerprint(g)};
-    std::lock_guard<std::mutex> lk(mu);
-    auto it = cache.find(k);
-    if (it != cache.end()) return it->second;
-    if (cache.size() >= 4) cache.clear();
-    auto dg = std::make_shared<DeviceGraph>(g);
-    cache.emplace(k, dg);
+    ReplicaCache& c = replica_cache();
+    const CacheKey k{&g, g.col_indices().data(), g.edge_props().data(),
+                     g.has_labels() ? static_cast<const void*>(g.edge_labels().data()) : nullptr,
+                     g.num_edges(), sample_fingerprint(g)};
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto it = c.map.find(k);
+    if (it != c.map.end()) return it->second;
+    if (c.map.size() >= 4) c.map.clear();
+    auto dg = std::make_shared<DeviceGraph>(g, default_devices());
+    c.map.emplace(k, dg);
     return dg;
 }
+
+}  // namespace detail
+
+// Restricts the replicas behind the `const Graph&` overloads to `devices`
+// (empty: every visible GPU); drops replicas cached for another list.
+inline void set_devices(std::vector<int> devices) {
+    detail::ReplicaCache& c = detail::replica_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.devices = std::move(devices);
+    c.map.clear();
+}
+
+namespace detail {
 
 }  // namespace detail
 
@@ -336,7 +373,8 @@ inline std::vector<SweepRow> selection_ratio_sweep(const Graph& base, const AnyM
 }
 
 // Same signature as dynwalk::profile_edge_cost_ratio (cost_model.hpp:39-40);
-// the random / sequential micro-passes run on device 0.
+// the random / sequential micro-passes run on device 0 with every
+// ProfileConfig field forwarded.
 inline CostModelParams profile_edge_cost_ratio(const Graph& g, const AnyModel& model,
                                                const ProfileConfig& cfg) {
     if (!(cfg.node_fraction > 0.0) || cfg.node_fraction > 1.0)
@@ -344,8 +382,10 @@ inline CostModelParams profile_edge_cost_ratio(const Graph& g, const AnyModel& m
     if (cfg.neighbors_per_node == 0 || cfg.repetitions == 0)
         throw Error("profile neighbors_per_node and repetitions must be >= 1");
     const detail::ModelDesc m = detail::to_desc(model);
+    const dw_profile_config pc{cfg.node_fraction, cfg.min_nodes, cfg.neighbors_per_node,
+                               cfg.repetitions, cfg.seed};
     CostModelParams p;
-    check(dw_calibrate(detail::cached(g)->handle(), &m.d, cfg.seed, &p.edge_cost_ratio));
+    check(dw_calibrate_ex(detail::cached(g)->handle(), &m.d, &pc, &p.edge_cost_ratio));
     p.profiled = true;
     return p;
 }

@@ -42,7 +42,7 @@ def test_library_is_sm100a(dw):
 
 
 def test_abi_version(dw):
-    assert dw.load_library().dw_abi_version() == 1
+    assert dw.load_library().dw_abi_version() == 2
 
 
 def test_no_cpu_fallback_without_gpu(dw):

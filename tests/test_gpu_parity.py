@@ -208,6 +208,44 @@ def test_calibration(dw, orc):
         assert np.isfinite(r) and r > 0
 
 
+def test_calibration_positive_and_stable(dw, orc):
+    """test_runtime.cpp:87-105 restated: the reference's bench fixture (BA
+    n=3000 deg=6 mirrored, uniform weights), node2vec (2, 0.5), ProfileConfig
+    with 5 repetitions and seed 1: a positive, finite ratio, the same within
+    4x on a second call, and node_fraction = 0 rejected."""
+    og = orc.Graph.ba(3000, 6, 77).synth("uniform", seed=78)
+    a = og.arrays()
+    dg = dw.DeviceGraph.from_csr(a["row"], a["col"], a["prop"])
+    model = dw.Model(kind="node2vec", a=2.0, b=0.5)
+    cfg = dw.ProfileConfig(repetitions=5, seed=1)
+    p1 = dw.profile_edge_cost_ratio(dg, model, cfg=cfg)
+    assert p1 > 0 and np.isfinite(p1)
+    p2 = dw.profile_edge_cost_ratio(dg, model, cfg=cfg)
+    assert abs(np.log(p1 / p2)) < np.log(4.0)
+    with pytest.raises(dw.DynwalkError, match="node_fraction must be in"):
+        dw.profile_edge_cost_ratio(dg, model, cfg=dw.ProfileConfig(node_fraction=0.0))
+    with pytest.raises(dw.DynwalkError, match="repetitions must be >= 1"):
+        dw.profile_edge_cost_ratio(dg, model, cfg=dw.ProfileConfig(repetitions=0))
+    with pytest.raises(dw.DynwalkError, match="repetitions must be >= 1"):
+        dw.profile_edge_cost_ratio(dg, model, cfg=dw.ProfileConfig(neighbors_per_node=0))
+    # every ProfileConfig field reaches the device passes
+    for c in (dw.ProfileConfig(node_fraction=1.0, seed=3), dw.ProfileConfig(min_nodes=1000),
+              dw.ProfileConfig(neighbors_per_node=1), dw.ProfileConfig(repetitions=1)):
+        r = dw.profile_edge_cost_ratio(dg, model, cfg=c)
+        assert r > 0 and np.isfinite(r)
+
+
+def test_calibration_degree_one_ring(dw):
+    """test_runtime.cpp:107-118 restated: a directed 64-node ring (every
+    degree 1), StaticWalk weighted, seed 2: positive and finite."""
+    n = 64
+    row = np.arange(n + 1, dtype=np.uint64)
+    col = ((np.arange(n) + 1) % n).astype(np.uint32)
+    dg = dw.DeviceGraph.from_csr(row, col, np.ones(n, np.float32))
+    r = dw.profile_edge_cost_ratio(dg, dw.Model(kind="static"), cfg=dw.ProfileConfig(seed=2))
+    assert r > 0 and np.isfinite(r)
+
+
 def test_errors(dw):
     with pytest.raises(dw.DynwalkError, match="not supported"):
         dg = dw.DeviceGraph.rmat(8, 16, seed=1)
@@ -229,6 +267,44 @@ def _with_env(env: dict, fn):
                 os.environ.pop(k, None)
             else:
                 os.environ[k] = v
+
+
+@pytest.mark.parametrize("env", [{"DW_FAT": "2", "DW_FAT32_BAND": "10"},
+                                 {"DW_FAT": "2", "DW_SCREEN": "0"}],
+                         ids=["band-wide", "no-screen"])
+def test_compact_records_exact_fallback(dw, orc, env):
+    """The compact records' f32 row sum decides only outside a relative band;
+    inside it (here: every decision, band 10) or without the one-multiply
+    screen, the exact node record decides, and the return-edge range the
+    record carried survives that refetch.  Paths and counters stay equal to
+    the oracle (this path was only checked by a manual rebuild)."""
+    og = orc.Graph.rmat(12, 16, 11).synth_philox("uniform", 1.0, 5.0, seed=12)
+    dg = _with_env({"DW_FAT": env["DW_FAT"]}, lambda: to_device(dw, og))
+    q = np.arange(og.nv, dtype=np.uint32)
+    for mk in (dict(kind="node2vec", a=0.5, b=2.0), dict(kind="node2vec", a=2.0, b=0.5)):
+        for mode in ("adaptive", "force-erjs"):
+            r_dev, r_orc = _with_env(env, lambda: run_both(dw, orc, og, dg, mk, q, mode, 60, 1.6))
+            assert_same(r_dev, r_orc, (env, mk, mode))
+
+
+@pytest.mark.parametrize("scale", [3.0e38, 1.0e-38])
+@pytest.mark.parametrize("layout", ["fat", "fat32", "slim"])
+def test_extreme_prop_magnitudes(dw, orc, scale, layout):
+    """Edge properties near FLT_MAX (row sums overflow f32: the compact
+    record stores NaN and the exact node record decides) and near FLT_MIN
+    (subnormal-range sums, exact in f32) walk bit-exactly on every layout."""
+    base = orc.Graph.rmat(11, 16, 21).synth_philox("uniform", 1.0, 5.0, seed=22)
+    a = base.arrays()
+    prop = (a["prop"].astype(np.float64) / 5.0 * scale).astype(np.float32)
+    assert np.all(prop > 0) and np.all(np.isfinite(prop))
+    og = orc.Graph.from_csr(a["row"], a["col"], prop)
+    env = {"DW_FAT": {"fat": "1", "fat32": "2"}.get(layout, "0")}
+    dg = _with_env(env, lambda: dw.DeviceGraph.from_csr(a["row"], a["col"], prop))
+    q = np.arange(og.nv, dtype=np.uint32)
+    for mk in (dict(kind="node2vec", a=0.5, b=2.0), dict(kind="node2vec", a=2.0, b=0.5)):
+        for mode in ("adaptive", "force-erjs", "force-ervs"):
+            r_dev, r_orc = run_both(dw, orc, og, dg, mk, q, mode, 40, 1.6)
+            assert_same(r_dev, r_orc, (scale, layout, mk, mode))
 
 
 @pytest.mark.parametrize("layout", ["fat", "fat32", "slim", "slim-notwin"])
@@ -372,11 +448,12 @@ def test_write_paths_text_sink(dw, orc, tmp_path):
         dw.run_write_paths(dg, model, q[:10], opts, str(tmp_path / "no" / "such" / "dir.txt"))
 
 
-def test_two_replicas_on_one_device(dw, orc, tmp_path):
-    """The multi-device engine (contiguous walker blocks per replica, ordered
-    compact/text drains, offset fix-up) exercised with two replicas of the
-    graph on device 0: padded, compact and text outputs equal the
-    single-replica run."""
+def test_two_replicas_on_one_device(dw, orc, tmp_path, monkeypatch):
+    """The multi-device engine (batches round-robin over the replicas, drains
+    in query order, offset fix-up) exercised with two replicas of the graph on
+    device 0: padded, compact and text outputs equal the single-replica run,
+    and replica 1 starts walking before replica 0 is drained (no cross-device
+    drain chain)."""
     og = orc.Graph.rmat(12, 16, 51).synth_philox("uniform", 1.0, 5.0, seed=52)
     a = og.arrays()
     one = dw.DeviceGraph.from_csr(a["row"], a["col"], a["prop"], devices=[0])
@@ -391,8 +468,17 @@ def test_two_replicas_on_one_device(dw, orc, tmp_path):
     for k in ("steps", "trials", "rng_draws", "query_errors"):
         assert r1.stats[k] == r2.stats[k], k
     o1, f1, _ = dw.run_queries_compact(one, model, q, opts)
+    trace = tmp_path / "engine.trace"
+    monkeypatch.setenv("DW_ENGINE_TRACE", str(trace))
     o2, f2, _ = dw.run_queries_compact(two, model, q, opts)
+    monkeypatch.delenv("DW_ENGINE_TRACE")
     assert np.array_equal(o1, o2) and np.array_equal(f1, f2)
+    ev = [ln.split() for ln in open(trace).read().splitlines()]
+    first_drain0 = next(i for i, e in enumerate(ev) if e[0] == "D" and e[2] == "0")
+    first_enq1 = next(i for i, e in enumerate(ev) if e[0] == "E" and e[2] == "1")
+    assert first_enq1 < first_drain0
+    drains = [e[2] for e in ev if e[0] == "D"]
+    assert len(drains) >= 4 and drains[:4] == ["0", "1", "0", "1"]
     dw.run_write_paths(one, model, q[:200_000], opts, str(tmp_path / "a.txt"))
     dw.run_write_paths(two, model, q[:200_000], opts, str(tmp_path / "b.txt"))
     assert open(tmp_path / "a.txt", "rb").read() == open(tmp_path / "b.txt", "rb").read()
