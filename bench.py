@@ -82,10 +82,15 @@ def parse():
                     help="BASELINE.json config (2 = the headline)")
     ap.add_argument("--scale", type=int, default=0, help="override the config's R-MAT scale")
     ap.add_argument("--walk-length", type=int, default=80)
+    ap.add_argument("--discard-paths", action="store_true",
+                    help="experiments: walk without writing paths (lengths only)")
 
     ap.add_argument("--mode", default="adaptive")
     ap.add_argument("--ratio", type=float, default=0.0, help="override the calibrated ratio")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--calib", default="micro", choices=["tune", "micro"],
+                    help="ratio calibration: K4 micro-passes (profile_edge_cost_ratio, the "
+                         "reference's method), or those refined by walking (dw_tune_ratio)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true",
@@ -301,11 +306,20 @@ def run_ours(args):
     info = dg.info()
     build_s = time.perf_counter() - t0
     model = dw.Model(cfg["model"], **model_kw(cfg))
-    # one calibration (rank 0), broadcast so every shard makes the same decisions
+    # one calibration (rank 0), broadcast so every shard makes the same decisions:
+    # K4's micro-pass ratio (profile_edge_cost_ratio), optionally refined by
+    # timing the walk kernel at a few thresholds around it (--calib tune)
     ratio = args.ratio
     t0 = time.perf_counter()
+    micro = None
+    calib = args.calib
     if ratio <= 0:
-        ratio = dw.profile_edge_cost_ratio(dg, model, seed=PROFILE_SEED) if rank == 0 else 0.0
+        ratio = 0.0
+        if rank == 0:
+            pc = dw.ProfileConfig(seed=PROFILE_SEED)
+            micro = dw.profile_edge_cost_ratio(dg, model, cfg=pc)
+            ratio = (dw.tune_edge_cost_ratio(dg, model, cfg=pc, walk_length=args.walk_length)
+                     if calib == "tune" else micro)
         if dist is not None:
             t = torch.tensor([ratio], dtype=torch.float64, device=cdev)
             dist.broadcast(t, 0)
@@ -315,7 +329,7 @@ def run_ours(args):
     nv = info["num_vertices"]
     L = args.walk_length
     wpv = cfg.get("walkers_per_vertex", 1)
-    discard = cfg.get("discard_paths", False)
+    discard = cfg.get("discard_paths", False) or args.discard_paths
     strong = world > 1 and not args.weak
     # one launch per walker round r: global ids r * V + v (weak: (rank * wpv + r) * V + v)
     rounds = []
@@ -484,7 +498,10 @@ def run_ours(args):
         "data": "synthetic R-MAT (deterministic Philox generator, on-device)",
         "config": dict(workload(args), parallelism=par,
                        edge_cost_ratio=ratio, edge_cost_ratio_source=(
-                           "override" if args.ratio > 0 else "device-calibrated (K4)")),
+                           "override" if args.ratio > 0 else
+                           "device-calibrated: K4 micro-passes refined by walking (dw_tune_ratio)"
+                           if calib == "tune" else "device-calibrated: K4 micro-passes"),
+                       edge_cost_ratio_micro=micro),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"],
                      "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
                      "peak_source": pk["source"],

@@ -170,6 +170,18 @@ typedef struct dw_profile_config {
  * no node with out-edges). */
 int dw_calibrate_ex(dw_graph_t g, const dw_model_desc* model, const dw_profile_config* cfg,
                     double* ratio);
+/* The B200 refinement of dw_calibrate_ex: the micro-passes price an eRJS
+ * trial and an eRVS visit in isolation, but the walk kernel overlaps both with
+ * other lanes' phases, so the best threshold is found by walking.  Starting
+ * from the micro-pass ratio r0, times the walk kernel itself (adaptive,
+ * `walk_length` steps, 0 = 80) on a sample of uniformly drawn start vertices
+ * at r0 x {1/2, 1/sqrt2, 1, sqrt2, 2} (median of min(repetitions, 3)
+ * launches each) and returns the vertex of the least-squares parabola through
+ * walker-steps/s over log2(ratio), kept inside that range (the best sampled
+ * ratio if the fit is not concave).  Decisions stay the reference's
+ * decide_sampler; only the threshold it is given changes. */
+int dw_tune_ratio(dw_graph_t g, const dw_model_desc* model, const dw_profile_config* cfg,
+                  uint32_t walk_length, double* ratio);
 /* dw_calibrate_ex with the ProfileConfig defaults and `seed`. */
 int dw_calibrate(dw_graph_t g, const dw_model_desc* model, uint64_t seed, double* ratio);
 

@@ -24,7 +24,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 __all__ = ["DeviceGraph", "Model", "RunOptions", "ProfileConfig", "RunResult", "DynwalkError", "run_queries",
-           "profile_edge_cost_ratio", "shard_of", "library_path", "load_library", "EXPORTED_SYMBOLS",
+           "profile_edge_cost_ratio", "tune_edge_cost_ratio", "shard_of", "library_path", "load_library", "EXPORTED_SYMBOLS",
            "INVALID_VERTEX"]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -35,7 +35,7 @@ INVALID_VERTEX = 0xFFFFFFFF
 EXPORTED_SYMBOLS = (
     "dw_abi_version", "dw_last_error", "dw_device_count", "dw_graph_create", "dw_graph_load_dwg1",
     "dw_graph_generate_rmat", "dw_graph_destroy", "dw_graph_info", "dw_graph_download",
-    "dw_calibrate", "dw_calibrate_ex", "dw_model_compile", "dw_model_free", "dw_run", "dw_run_compact",
+    "dw_calibrate", "dw_calibrate_ex", "dw_tune_ratio", "dw_model_compile", "dw_model_free", "dw_run", "dw_run_compact",
     "dw_run_write_paths", "dw_run_device",
     "dw_run_device_sync",
     "dw_host_alloc",
@@ -139,6 +139,8 @@ def load_library() -> C.CDLL:
     L.dw_graph_download.argtypes = [vp, u64p, u32p, f32p, u16p, f64p, f64p]
     L.dw_calibrate.argtypes = [vp, C.POINTER(ModelDesc), C.c_uint64, f64p]
     L.dw_calibrate_ex.argtypes = [vp, C.POINTER(ModelDesc), C.POINTER(ProfileConfigC), f64p]
+    L.dw_tune_ratio.argtypes = [vp, C.POINTER(ModelDesc), C.POINTER(ProfileConfigC), C.c_uint32,
+                                f64p]
     L.dw_model_compile.argtypes = [C.c_char_p, C.c_uint32, C.c_uint32, C.POINTER(vp)]
     L.dw_model_free.argtypes = [vp]
     L.dw_run.argtypes = [vp, C.POINTER(ModelDesc), u32p, C.c_uint64, C.POINTER(RunOptsC), u32p,
@@ -358,6 +360,17 @@ def shard_of(qids, world: int) -> np.ndarray:
     with np.errstate(over="ignore"):
         h = (q * np.uint64(0x9E3779B97F4A7C15)) >> np.uint64(32)
     return (h % np.uint64(world)).astype(np.int64)
+
+
+def tune_edge_cost_ratio(g: DeviceGraph, model: Model, seed: int = 0,
+                         cfg: ProfileConfig | None = None, walk_length: int = 80) -> float:
+    """dw_tune_ratio: the micro-pass ratio refined by timing the walk kernel
+    itself at a few thresholds around it (see include/dynwalk_b200.h)."""
+    r = C.c_double()
+    m = model.c()
+    c = (cfg if cfg is not None else ProfileConfig(seed=seed)).c()
+    _check(load_library().dw_tune_ratio(g.h, C.byref(m), C.byref(c), walk_length, C.byref(r)))
+    return r.value
 
 
 def run_queries(g: DeviceGraph, model: Model, queries, opts: RunOptions,

@@ -1186,6 +1186,97 @@ int dw_calibrate(dw_graph_t g, const dw_model_desc* model, uint64_t seed, double
     return dw_calibrate_ex(g, model, &cfg, ratio);
 }
 
+int dw_tune_ratio(dw_graph_t g, const dw_model_desc* model, const dw_profile_config* cfg,
+                  uint32_t walk_length, double* ratio) {
+    if (!g || !ratio || !cfg) return fail(DW_EINVAL, "NULL argument");
+    double r0 = 0.0;
+    int rc = dw_calibrate_ex(g, model, cfg, &r0);
+    if (rc) return rc;
+    if (walk_length == 0) walk_length = 80;
+    Replica& r = g->reps[0];
+    CU(cudaSetDevice(r.device), "cudaSetDevice");
+    if ((rc = prepare_model(r, model))) return rc;
+    // walker sample: uniform start vertices (all_vertices' distribution), up
+    // to 2^24 of them -- a launch of a few ms ends in a tail whose lanes wait
+    // on single walkers, and that tail favours other thresholds than a full
+    // walk does (s24: 1.8M walkers put the optimum at ~0.4, all 16.8M at ~0.9)
+    const ull nq = std::min<ull>(std::max<ull>(g->nv, 1), 1ull << 24);
+    std::vector<uint32_t> hq(nq);
+    ull x = cfg->seed ^ 0x74756e65ull;
+    for (ull i = 0; i < nq; ++i) {  // SplitMix64 (rng.hpp:10-20)
+        ull z = (x += 0x9E3779B97F4A7C15ull);
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        hq[i] = (uint32_t)((unsigned __int128)(z ^ (z >> 31)) * g->nv >> 64);
+    }
+    uint32_t* dq = nullptr;
+    CU(cudaMalloc(&dq, nq * sizeof(uint32_t)), "cudaMalloc");
+    std::unique_ptr<uint32_t, cudaError_t (*)(void*)> hold(dq, &cudaFree);
+    CU(cudaMemcpy(dq, hq.data(), nq * sizeof(uint32_t), cudaMemcpyHostToDevice), "H2D");
+    dw_run_opts o{};
+    o.mode = DW_MODE_ADAPTIVE;
+    o.walk_length = walk_length;
+    o.seed = cfg->seed;
+    o.erjs_cap_per_degree = 64;
+    // walker-steps per ms of the walk kernel at one ratio (median of reps)
+    auto rate = [&](double ratio_c, double* out) -> int {
+        o.edge_cost_ratio = ratio_c;
+        std::vector<double> v;
+        const uint32_t reps = std::max<uint32_t>(1, std::min<uint32_t>(cfg->repetitions, 3));
+        for (uint32_t k = 0; k < reps; ++k) {
+            int e = reset_run_state(r);
+            if (e) return e;
+            dwb::WalkParams p = make_params(r, model, &o);
+            p.queries = dq;
+            p.nq = nq;
+            p.next_walker = r.queues;
+            CU(cudaEventRecord(r.ev_start, r.stream), "event");
+            CU(launch_model(r, model, o.mode, p, r.stream), "walk");
+            CU(cudaEventRecord(r.ev_stop, r.stream), "event");
+            CU(cudaEventSynchronize(r.ev_stop), "walk");
+            dw_run_stats st{};
+            if ((e = collect(r, &st, 0))) return e;
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, r.ev_start, r.ev_stop);
+            v.push_back((double)(st.steps - st.dead_ends) / std::max(1e-3, (double)ms));
+        }
+        std::sort(v.begin(), v.end());
+        *out = v[v.size() / 2];
+        return DW_OK;
+    };
+    double warm = 0.0;
+    if ((rc = rate(r0, &warm))) return rc;
+    // throughput on a log2 grid around the micro-pass estimate; a least-
+    // squares parabola through the five points smooths the timing noise (the
+    // optimum is flat: within 2 % over a factor of ~2 at s24) and its vertex,
+    // kept inside the grid, is the threshold
+    const double xs[5] = {-1.0, -0.5, 0.0, 0.5, 1.0};
+    double ys[5], best = r0, best_rate = 0.0;
+    for (int i = 0; i < 5; ++i) {
+        if ((rc = rate(r0 * std::exp2(xs[i]), &ys[i]))) return rc;
+        if (ys[i] > best_rate) best_rate = ys[i], best = r0 * std::exp2(xs[i]);
+    }
+    // x symmetric around 0: the normal equations decouple
+    double sy = 0, sxy = 0, sx2y = 0;
+    for (int i = 0; i < 5; ++i) {
+        sy += ys[i];
+        sxy += xs[i] * ys[i];
+        sx2y += xs[i] * xs[i] * ys[i];
+    }
+    const double s2 = 2.5, s4 = 2.125, n = 5.0;  // sum x^2, sum x^4
+    const double qa = (n * sx2y - s2 * sy) / (n * s4 - s2 * s2);
+    const double qb = sxy / s2;
+    if (qa < 0.0) best = r0 * std::exp2(std::clamp(-qb / (2.0 * qa), -1.0, 1.0));
+    if (std::getenv("DW_VERBOSE")) {
+        for (int i = 0; i < 5; ++i)
+            std::fprintf(stderr, "dynwalk: tune ratio %.4f -> %.4e walker-steps/s\n",
+                         r0 * std::exp2(xs[i]), ys[i] * 1e3);
+        std::fprintf(stderr, "dynwalk: tuned ratio %.4f (micro-pass %.4f)\n", best, r0);
+    }
+    *ratio = best;
+    return DW_OK;
+}
+
 int dw_run_device(dw_graph_t g, int replica, const dw_model_desc* model, const uint32_t* d_queries,
                   uint64_t nq, const dw_run_opts* opts, uint32_t* d_paths, uint32_t* d_lengths,
                   void* stream) {
@@ -1194,6 +1285,9 @@ int dw_run_device(dw_graph_t g, int replica, const dw_model_desc* model, const u
         return fail(DW_EINVAL, "replica %d out of range", replica);
     int rc;
     if ((rc = check_model(model)) || (rc = check_opts(opts))) return rc;
+    if (nq > 0xFFFFFFFFull)  // the kernel indexes a launch's walkers with 32 bits
+        return fail(DW_EINVAL, "at most 2^32 - 1 queries per device launch (got %llu)",
+                    (unsigned long long)nq);
     Replica& r = g->reps[replica];
     CU(cudaSetDevice(r.device), "cudaSetDevice");
     if ((rc = prepare_model(r, model))) return rc;

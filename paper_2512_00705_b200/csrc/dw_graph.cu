@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "dw_graph.cuh"
+#include "dw_walk_kernel.cuh"  // ervs_visit: K4 prices the walk's own reservoir step
 
 namespace dwb {
 
@@ -678,23 +679,96 @@ __global__ void sample_nodes_kernel(DevGraph g, ull seed, ull tries, uint32_t wa
     }
 }
 
-// One warp per probed node and round; lane k < min(d, npn) evaluates one
-// weight.  Round r probes the pool's nodes [r*n, (r+1)*n) (mod the pool), so
+// One lane per probed node and round, like the walk kernel's per-lane phase
+// machine; round r probes the pool's nodes [r*n, (r+1)*n) (mod the pool), so
 // consecutive rounds touch different rows of the whole graph, not the same
 // cached neighbours: the pool is many times the L2, like the rows a walk
-// visits.  Both passes read the same states and evaluate the same number of
-// weights; they differ only in the access pattern (cost_model.cpp:67-98).
+// visits.  Both passes read the same states and visit k = min(d, npn) edges
+// per node; they differ in what a visit is (cost_model.cpp:67-98):
+//   random     one eRJS trial as the walk kernel runs it: the Philox (x, y)
+//              draw, then the weight of a random neighbour only when y is
+//              below the row's non-return maximum -- a trial above it is
+//              rejected without reading the edge (the free rejection)
+//   sequential one eRVS visit as the walk kernel runs it on a short row: the
+//              next neighbour's weight (membership included) folded into the
+//              A-ExpJ reservoir (ervs_visit: key, jump-threshold and floor
+//              draws with their log/exp)
+// so the ratio prices the kernel's trial against the kernel's reservoir visit,
+// the balance decide_sampler encodes (cost_model.hpp:46-56).  (A warp-wide
+// coalesced scan would price a sequential read at a fraction of what the
+// walk's reservoir pays per edge, and the decision would then send rows to
+// eRVS that the kernel walks faster with rejection.)
+// Weights of up to kProbeBatch edges with their loads in flight together (the
+// walk kernel keeps a ring of outstanding gathers per lane the same way):
+// the edge records first, then the first membership bucket of each.
+constexpr int kProbeBatch = 4;
+template <class M>
+__device__ __forceinline__ void probe_weights(const M& m, const Step& S, uint32_t phoff,
+                                              const DevGraph& g, const ull (&e)[kProbeBatch],
+                                              const bool (&live)[kProbeBatch],
+                                              double (&w)[kProbeBatch]) {
+    EdgeRec er[kProbeBatch];
+    uint16_t lab[kProbeBatch];
+#pragma unroll
+    for (int j = 0; j < kProbeBatch; ++j) {
+        er[j] = live[j] ? load_edge(g.edges + e[j]) : EdgeRec{0u, 0.f};
+        lab[j] = (live[j] && M::kUsesLabels && g.labels) ? g.labels[e[j]] : (uint16_t)0;
+    }
+    WeightCase wc[kProbeBatch];
+    uint4 b0[kProbeBatch], b1[kProbeBatch];
+    const uint32_t lg = hash_log2_buckets(S.prev_degree);
+#pragma unroll
+    for (int j = 0; j < kProbeBatch; ++j) {
+        wc[j] = m.weight(S, er[j].col, er[j].h, lab[j]);
+        if (live[j] && M::kSecondOrder && wc[j].needs_member && S.prev_degree) {
+            const uint4* p = reinterpret_cast<const uint4*>(
+                g.hslots + 8ull * (phoff + hash_bucket(er[j].col, lg)));
+            b0[j] = __ldg(p);
+            b1[j] = __ldg(p + 1);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < kProbeBatch; ++j) {
+        w[j] = wc[j].w;
+        if (live[j] && M::kSecondOrder && wc[j].needs_member) {
+            int r = S.prev_degree ? bucket_lookup(b0[j], b1[j], er[j].col) : 0;
+            if (r < 0) r = member(g, S.prev_degree, phoff, er[j].col) ? 1 : 0;
+            w[j] = r ? wc[j].w_in : wc[j].w_out;
+        }
+    }
+}
+
+// One lane per probed node and round, like the walk kernel's per-lane phase
+// machine; round r probes the pool's nodes [r*n, (r+1)*n) (mod the pool), so
+// consecutive rounds touch different rows of the whole graph, not the same
+// cached neighbours: the pool is many times the L2, like the rows a walk
+// visits.  Both passes read the same states and visit k = min(d, npn) edges
+// per node, kProbeBatch at a time; they differ in what a visit is
+// (cost_model.cpp:67-98):
+//   random     one eRJS trial as the walk kernel runs it: the Philox (x, y)
+//              draw, then the weight of a random neighbour only when y is
+//              below the row's non-return maximum -- a trial above it is
+//              rejected without reading the edge (the free rejection)
+//   sequential one eRVS visit as the walk kernel runs it on a short row: the
+//              next neighbour's weight (membership included) folded into the
+//              A-ExpJ reservoir (ervs_visit: key, jump-threshold and floor
+//              draws with their log/exp)
+// so the ratio prices the kernel's trial against the kernel's reservoir visit,
+// the balance decide_sampler encodes (cost_model.hpp:46-56).  (A warp-wide
+// coalesced scan prices a sequential read at a fraction of what the walk's
+// reservoir pays per edge, and the decision then sends rows to eRVS that the
+// kernel walks faster with rejection.)
 template <class M, bool RANDOM>
 __global__ void probe_pass_kernel(DevGraph g, __grid_constant__ const ModelParams mp,
                                   const ProbeState* __restrict__ pool, uint32_t pool_n, uint32_t n,
                                   uint32_t npn, int rounds, ull seed, double* sink) {
     M m(mp);
-    const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t lane = threadIdx.x & 31;
-    if (w >= n) return;
+    const uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i0 >= n) return;
+    const PhiloxKeys rk = philox_keys((uint32_t)seed, (uint32_t)(seed >> 32));
     double acc = 0.0;
     for (int r = 0; r < rounds; ++r) {
-        const ProbeState P = pool[((ull)r * n + w) % pool_n];
+        const ProbeState P = pool[((ull)r * n + i0) % pool_n];
         Step S;
         S.cur = P.cur;
         S.prev = P.prev;
@@ -706,29 +780,40 @@ __global__ void probe_pass_kernel(DevGraph g, __grid_constant__ const ModelParam
         S.lmax = S.lsum = 0.0;
         m.prepare(S);
         const uint32_t k = min(S.degree, npn);
-        // The random pass times one eRJS trial as the walk kernel runs it: the
-        // (x, y) draw, then a weight evaluation only when y is below the row's
-        // non-return maximum -- a trial above it is rejected without reading
-        // the edge (the free rejection of dw_walk_kernel.cuh).  The ratio then
-        // prices a trial, not a random read, against a sequential read (the
-        // eRJS-vs-eRVS cost balance decide_sampler encodes, cost_model.hpp:46-56).
+        const WalkerKey key{(uint32_t)seed, (uint32_t)(seed >> 32), i0, (uint32_t)r, S.step};
         double bnd = 1.0, mnr = __longlong_as_double(0x7ff0000000000000ll);
         if (RANDOM && M::kBoundable && mp.shortcut) {
             bnd = m.bound(S);
             mnr = m.nonreturn_max(S);
         }
-        for (uint32_t i = lane; i < k; i += 32) {
-            ull e;
-            if (RANDOM) {
-                const U4 b = philox4x32_10(U4{i, (uint32_t)r, w, 0x72616e64u}, (uint32_t)seed,
-                                           (uint32_t)(seed >> 32));
-                e = P.begin + bounded(lo64(b), S.degree);
-                if (uniform01(hi64(b)) * bnd >= mnr) continue;  // rejected, nothing read
-            } else {
-                e = P.begin + i;
+        ErvsState st{-DBL_MAX, 0.0, 0, kInvalid, 0};
+        for (uint32_t t0 = 0; t0 < k; t0 += kProbeBatch) {
+            ull e[kProbeBatch];
+            bool live[kProbeBatch];
+            double w[kProbeBatch];
+#pragma unroll
+            for (int j = 0; j < kProbeBatch; ++j) {
+                const uint32_t t = t0 + j;
+                live[j] = t < k;
+                if (RANDOM) {
+                    const U4 b = philox4x32_10_rk(U4{t, S.step, i0, (uint32_t)r}, rk);
+                    e[j] = P.begin + bounded(lo64(b), S.degree);
+                    live[j] = live[j] && uniform01(hi64(b)) * bnd < mnr;  // else nothing read
+                } else {
+                    e[j] = P.begin + t;
+                }
             }
-            acc += eval_weight(m, S, P.phoff, g, e);
+            probe_weights(m, S, P.phoff, g, e, live, w);
+#pragma unroll
+            for (int j = 0; j < kProbeBatch; ++j) {
+                if (!live[j]) continue;
+                if (RANDOM)
+                    acc += w[j];
+                else
+                    st = ervs_visit<false>(st, key, rk, t0 + j, t0 + j, valid_w(w[j]) ? w[j] : 0.0);
+            }
         }
+        if (!RANDOM) acc += st.best_key + (double)st.best;
     }
     if (acc == -1.0) *sink = acc;  // keeps the loads alive
 }
@@ -741,7 +826,7 @@ static cudaError_t calibrate_t(const DeviceGraphBuffers& gb, const ModelParams& 
     // the probe set of one round (cost_model.cpp:45-54): ceil(fraction * nv),
     // at least min_nodes; the pool holds kPoolRounds such sets (capped at the
     // graph's nodes with out-edges, and at 2^24 states)
-    constexpr ull kPoolRounds = 64;
+    constexpr ull kPoolRounds = 16;
     const uint32_t want = (uint32_t)std::max<ull>(
         (ull)std::ceil(cfg.node_fraction * gb.nv), (ull)cfg.min_nodes);
     const ull pool_want = std::min<ull>(std::max<ull>((ull)want * kPoolRounds, want), 1ull << 24);
@@ -775,7 +860,7 @@ static cudaError_t calibrate_t(const DeviceGraphBuffers& gb, const ModelParams& 
     DW_TRY(cudaEventCreate(&e0));
     DW_TRY(cudaEventCreate(&e1));
     DW_TRY(cudaEventCreate(&e2));
-    const unsigned blocks = (unsigned)(((ull)n * 32 + 255) / 256);
+    const unsigned blocks = (unsigned)(((ull)n + 255) / 256);
     const uint32_t npn = cfg.neighbors_per_node;
     auto pass = [&](int rounds, float& t_rand, float& t_seq) -> cudaError_t {
         cudaEventRecord(e0, s);

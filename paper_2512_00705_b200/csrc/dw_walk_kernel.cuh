@@ -115,9 +115,13 @@ constexpr uint32_t kCjsMin = DW_CJS_MIN;
 // and no overflow branch inside the walk loop (the 64-bit shared atomics
 // those need compile to CAS loops, ~580 cold instructions that crowded the
 // loop's instruction cache).  Summed per block at kernel end.
+// The first LC_NUM64 grow fast (reads of hub rows, trials of loose PR2
+// bounds) and are 64-bit; the rest count walkers or steps and live in 32-bit
+// slots whose (practically unreachable) carry goes straight to the global
+// 64-bit counter.
 enum LaneCounter : int {
-    LC_ETRIALS = 0, LC_ETRIALS1, LC_EREADS, LC_EDRAWS, LC_ALG4,
-    LC_FALLBACKS, LC_DEADENDS, LC_QERRORS, LC_QUERIES, LC_NUM
+    LC_ETRIALS = 0, LC_EREADS, LC_EDRAWS, LC_ALG4, LC_NUM64,
+    LC_ETRIALS1 = LC_NUM64, LC_FALLBACKS, LC_DEADENDS, LC_QERRORS, LC_QUERIES, LC_NUM
 };
 
 __device__ __forceinline__ bool valid_w(double w) { return !(w < 0.0) && isfinite(w); }
@@ -352,13 +356,20 @@ struct WalkSmem {
     double y[kRing][kThreads];       // y of the queued trials
     uint32_t t[kRing][kThreads];     // trial index of the queued trials
     uint4 mb[2][kThreads];           // node record / hash bucket / eRVS pair
-    ull lc[LC_NUM][kThreads];        // per-lane RunStats counters
+    ull lc[LC_NUM64][kThreads];      // per-lane RunStats counters (64-bit)
+    uint32_t lc32[LC_NUM - LC_NUM64][kThreads];  // (bounded ones)
+    // path entries staged until their 32 B sector is complete: a sector is
+    // written whole (two 16 B stores) instead of eight 4 B stores, so L2 never
+    // evicts a partly written sector, which HBM's ECC turns into a
+    // read-modify-write (single 4 B stores cost 12 % of the s24 walk);
+    // slot = (entry address / 4) mod 8
+    uint32_t pst[8][kThreads];
     // walker state read once per step or per iteration, kept out of registers
     // so the loop fits the register budget of 3-4 CTAs/SM without spills
     uint32_t cur[kThreads], phoff[kThreads], plg[kThreads], hoff[kThreads], cap[kThreads],
         twlo[kThreads], twcnt[kThreads], nret[kThreads];
     double bound[kThreads], mnr[kThreads];
-    ull qg[kThreads];                // global walker id (RNG key) of the lane's walker
+    uint32_t qi[kThreads];           // the lane's walker: index in this launch
     ull cnt[kCNum];
     uint32_t hist[66];
     ull lct[LC_NUM];                 // block totals of the lane counters
@@ -385,10 +396,26 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
     if (tid < LC_NUM) s_lct[tid] = 0;
     for (int i = tid; i < 66; i += blockDim.x) s_hist[i] = 0;
 #pragma unroll
-    for (int c = 0; c < LC_NUM; ++c) s_lc[c][tid] = 0;
+    for (int c = 0; c < LC_NUM64; ++c) s_lc[c][tid] = 0;
+#pragma unroll
+    for (int c = 0; c < LC_NUM - LC_NUM64; ++c) sm.lc32[c][tid] = 0;
     __syncthreads();
     // lane counters: LC_* accumulate per lane in shared memory
-    auto lc_add = [&](int c, ull v) { s_lc[c][tid] += v; };
+    auto lc_add = [&](int c, ull v) {
+        if (c < LC_NUM64) {
+            s_lc[c][tid] += v;
+        } else {
+            uint32_t& x = sm.lc32[c - LC_NUM64][tid];
+            const uint32_t y = x + (uint32_t)v;  // v < 2^32 at every site
+            x = y;
+            if (y < (uint32_t)v) {
+                const int gc = c == LC_ETRIALS1 ? kCTrials : c == LC_FALLBACKS ? kCFallbacks
+                               : c == LC_DEADENDS ? kCDeadEnds : c == LC_QERRORS ? kCQueryErrors
+                                                                                : kCQueries;
+                atomicAdd(&p.counters[gc], 1ull << 32);
+            }
+        }
+    };
 
     // a block's 32-bit histogram cells cannot overflow unless the launch
     // walks 2^32 steps in total
@@ -402,7 +429,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
     uint32_t phase = P_IDLE;
     bool drained = false;  // warp-uniform
     uint32_t nrefill = 0;  // warp-uniform
-    ull qi = 0;
+    ull qg = 0;  // global walker id (RNG key); the launch index is sm.qi[tid]
     // walker state
     uint32_t prev = kInvalid, pdeg = 0, step = 0, deg = 0;
     uint32_t& cur = sm.cur[tid];
@@ -456,11 +483,11 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
         return S;
     };
     auto key_of = [&]() {
-        const ull q = sm.qg[tid];
+        const ull q = qg;
         return WalkerKey{p.seed_lo, p.seed_hi, (uint32_t)q, (uint32_t)(q >> 32), step};
     };
     auto fail = [&](int code) {
-        raise_error(p, code, sm.qg[tid]);
+        raise_error(p, code, qg);
         phase = P_IDLE;
     };
     auto flush_walker = [&]() {
@@ -468,8 +495,38 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
         lc_add(LC_ALG4, c_alg4);
         c_trials = c_alg4 = 0;
     };
+    // path entry `step` (stage; a completed 32 B sector is written whole)
+    auto put_path = [&](uint32_t v) {
+        uint32_t* a = p.paths + ((ull)sm.qi[tid] * p.stride + step);
+        const uint32_t k = (uint32_t)(reinterpret_cast<unsigned long long>(a) >> 2) & 7u;
+        sm.pst[k][tid] = v;
+        if (k == 7u) {
+            uint32_t* s0 = a - 7;
+            if (s0 >= p.paths + (ull)sm.qi[tid] * p.stride) {  // the sector is this walker's
+                reinterpret_cast<uint4*>(s0)[0] =
+                    make_uint4(sm.pst[0][tid], sm.pst[1][tid], sm.pst[2][tid], sm.pst[3][tid]);
+                reinterpret_cast<uint4*>(s0)[1] =
+                    make_uint4(sm.pst[4][tid], sm.pst[5][tid], sm.pst[6][tid], sm.pst[7][tid]);
+            } else {  // the row's first sector, shared with the previous row
+                for (uint32_t* q = p.paths + (ull)sm.qi[tid] * p.stride; q <= a; ++q)
+                    *q = sm.pst[(uint32_t)(reinterpret_cast<unsigned long long>(q) >> 2) & 7u][tid];
+            }
+        }
+    };
+    // the staged entries of the last, incomplete sector
+    auto flush_path = [&]() {
+        uint32_t* a = p.paths + ((ull)sm.qi[tid] * p.stride + step);
+        const uint32_t k = (uint32_t)(reinterpret_cast<unsigned long long>(a) >> 2) & 7u;
+        if (k == 7u) return;
+        uint32_t* q = a - k;
+        uint32_t* rs = p.paths + (ull)sm.qi[tid] * p.stride;
+        if (q < rs) q = rs;
+        for (; q <= a; ++q)
+            *q = sm.pst[(uint32_t)(reinterpret_cast<unsigned long long>(q) >> 2) & 7u][tid];
+    };
     auto end_walk = [&]() {
-        if (p.lengths) p.lengths[qi] = step + 1;
+        if (p.lengths) p.lengths[sm.qi[tid]] = step + 1;
+        if (p.paths) flush_path();
         flush_walker();
         phase = P_IDLE;
     };
@@ -529,13 +586,15 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                             lc_add(LC_QERRORS, 1);
                             if (p.lengths) p.lengths[i] = 0;
                         } else {
-                            if (p.paths) p.paths[i * p.stride] = start;
                             if (p.target == 0) {
+                                if (p.paths) p.paths[i * p.stride] = start;
                                 if (p.lengths) p.lengths[i] = 1;
                             } else {
                                 phase = P_NODE;
-                                qi = i;
-                                sm.qg[tid] = p.qids ? p.qids[i] : p.qid_base + i;
+                                sm.qi[tid] = (uint32_t)i;
+                                qg = p.qids ? p.qids[i] : p.qid_base + i;
+                                step = 0;
+                                if (p.paths) put_path(start);
                                 cur = start;
                                 prev = kInvalid;
                                 pdeg = phoff = plg = 0;
@@ -559,7 +618,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                 cp16(&s_mb[0][tid], b);
                 cp16(&s_mb[1][tid], b + 4);
             }
-            const ull q = sm.qg[tid];
+            const ull q = qg;
             // step constants into registers once per iteration: the ring's
             // shared-memory stores below would otherwise force a reload of
             // the shared-memory state on every trial
@@ -812,7 +871,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
             plg = hash_log2_buckets(deg);
             cur = nx;
             ++step;
-            if (p.paths) p.paths[qi * p.stride + step] = nx;
+            if (p.paths) put_path(nx);
             if (step >= p.target) {
                 end_walk();
                 next_ev = E_NONE;
@@ -1013,7 +1072,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
             T.hmax = T.hsum = 0.0;
             const uint32_t tph = __shfl_sync(kFull, phoff, L);
             const ull tb = __shfl_sync(kFull, begin, L);
-            const ull q = sm.qg[(tid & ~31) + L];
+            const ull q = __shfl_sync(kFull, qg, L);
             const WalkerKey K{p.seed_lo, p.seed_hi, (uint32_t)q, (uint32_t)(q >> 32), T.step};
             const ull db = __shfl_sync(kFull, lane == L ? ev_load().didx : 0ull, L);
             uint32_t nx = kInvalid, ni = 0;
@@ -1042,7 +1101,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                         plg = hash_log2_buckets(deg);
                         cur = nx;
                         ++step;
-                        if (p.paths) p.paths[qi * p.stride + step] = nx;
+                        if (p.paths) put_path(nx);
                         if (step >= p.target)
                             end_walk();
                         else
@@ -1074,7 +1133,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                 const uint32_t tph = sm.phoff[Lt], tcap = sm.cap[Lt];
                 const uint32_t twl = sm.twlo[Lt], twc = sm.twcnt[Lt];
                 const double tbnd = sm.bound[Lt], tmnr = sm.mnr[Lt];
-                const ull q = sm.qg[Lt];
+                const ull q = __shfl_sync(kFull, qg, L);
                 int win = -1;
                 bool bad = false;
                 uint32_t judged = 0, rets = 0, wu = 0;
@@ -1154,7 +1213,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                             plg = hash_log2_buckets(deg);
                             cur = wu;
                             ++step;
-                            if (p.paths) p.paths[qi * p.stride + step] = wu;
+                            if (p.paths) put_path(wu);
                             if (step >= p.target)
                                 end_walk();
                             else
@@ -1175,7 +1234,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
     if (tid < 66 && s_hist[tid]) s_cnt[kCHist + tid] += s_hist[tid];
 #pragma unroll 1
     for (int c = 0; c < LC_NUM; ++c) {
-        const ull v = warp_sum(s_lc[c][tid]);
+        const ull v = warp_sum(c < LC_NUM64 ? s_lc[c][tid] : (ull)sm.lc32[c - LC_NUM64][tid]);
         if (lane == 0 && v) atomicAdd(&s_lct[c], v);
     }
     __syncthreads();

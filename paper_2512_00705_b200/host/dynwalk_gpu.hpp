@@ -390,4 +390,20 @@ inline CostModelParams profile_edge_cost_ratio(const Graph& g, const AnyModel& m
     return p;
 }
 
+// The micro-pass ratio refined by timing the walk kernel itself at a few
+// thresholds around it (dw_tune_ratio): the threshold decide_sampler should
+// use on this device.  Not in the reference; same inputs as
+// profile_edge_cost_ratio.
+inline CostModelParams tune_edge_cost_ratio(const Graph& g, const AnyModel& model,
+                                            const ProfileConfig& cfg,
+                                            std::uint32_t walk_length = 80) {
+    const detail::ModelDesc m = detail::to_desc(model);
+    const dw_profile_config pc{cfg.node_fraction, cfg.min_nodes, cfg.neighbors_per_node,
+                               cfg.repetitions, cfg.seed};
+    CostModelParams p;
+    check(dw_tune_ratio(detail::cached(g)->handle(), &m.d, &pc, walk_length, &p.edge_cost_ratio));
+    p.profiled = true;
+    return p;
+}
+
 }  // namespace dynwalk::gpu

@@ -235,6 +235,19 @@ def test_calibration_positive_and_stable(dw, orc):
         assert r > 0 and np.isfinite(r)
 
 
+def test_tuned_ratio_is_near_the_micro_pass_ratio(dw):
+    """dw_tune_ratio walks the kernel at r0 x {1/2 .. 2} around the
+    micro-pass ratio r0 and returns a threshold inside that range."""
+    dg = dw.DeviceGraph.rmat(14, 16, seed=5, weights="uniform", weight_seed=6)
+    model = dw.Model(kind="node2vec", a=0.5, b=2.0)
+    cfg = dw.ProfileConfig(seed=3)
+    r0 = dw.profile_edge_cost_ratio(dg, model, cfg=cfg)
+    rt = dw.tune_edge_cost_ratio(dg, model, cfg=cfg, walk_length=20)
+    assert np.isfinite(rt) and r0 * 0.5 * (1 - 1e-9) <= rt <= r0 * 2.0 * (1 + 1e-9)
+    with pytest.raises(dw.DynwalkError, match="node_fraction"):
+        dw.tune_edge_cost_ratio(dg, model, cfg=dw.ProfileConfig(node_fraction=2.0))
+
+
 def test_calibration_degree_one_ring(dw):
     """test_runtime.cpp:107-118 restated: a directed 64-node ring (every
     degree 1), StaticWalk weighted, seed 2: positive and finite."""
