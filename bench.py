@@ -274,13 +274,31 @@ def peaks() -> dict:
     return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
-def ncu_traffic(scale: int):
-    """Per-launch DRAM bytes of the walk kernel from the committed ncu --set full capture."""
+def lib_sha16() -> str:
+    """Build identity of the product library: sha256 over its sources, Makefile and
+    public header (deterministic, unlike the linked .so)."""
+    import glob
+    import hashlib
+    h = hashlib.sha256()
+    pkg = os.path.join(ROOT, "paper_2512_00705_b200")
+    files = sorted(glob.glob(os.path.join(pkg, "csrc", "*"))) + [
+        os.path.join(pkg, "Makefile"), os.path.join(ROOT, "include", "dynwalk_b200.h")]
+    for fn in files:
+        h.update(os.path.relpath(fn, ROOT).encode())
+        with open(fn, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()[:16]
+
+
+def ncu_traffic(scale: int, sha: str):
+    """Per-launch DRAM bytes of the walk kernel from the committed ncu --set full capture
+    (tools/ncu_profile_json.py), only when that capture was taken of this very library
+    build (same lib_sha16) on this scale; otherwise null."""
     p = os.path.join(ROOT, "profiles", "ncu_walk_kernel.json")
     if not os.path.exists(p):
         return None
     d = json.load(open(p))
-    if d.get("scale") != scale:
+    if d.get("scale") != scale or d.get("lib_sha16") != sha:
         return None
     return d.get("dram_bytes_per_launch")
 
@@ -482,7 +500,8 @@ def run_ours(args):
         return
     pk = peaks()
     achieved = alg_bytes / (kernel_ms / 1e3) / 1e9
-    traffic = ncu_traffic(args.scale)
+    sha = lib_sha16()
+    traffic = ncu_traffic(args.scale, sha)
     if strong:
         par = (f"walker-parallel x{world}: the {walkers_total} global walker ids hash-"
                "partitioned over the ranks (Fibonacci hashing), graph replicated, no collective "
@@ -515,6 +534,9 @@ def run_ours(args):
                                     "on the device"},
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "build": {"lib_sha16": sha, "traffic_source": (
+            "profiles/ncu_walk_kernel.json (ncu --set full of this build)" if traffic is not None
+            else "null: no committed capture of this library build")},
         "clocks": clk.summary(),
         "gpu_launches": int(stats.kernel_launches) * args.steps,
         "walker_steps_per_step": walker_steps,
