@@ -56,18 +56,24 @@ CONFIGS = {
             desc="node2vec p=0.5 q=2, walk length 80, one walker per vertex, weighted R-MAT "
                  "scale-24 ef16 (BASELINE configs[1])"),
     3: dict(scale=22, model="metapath", schema=(0, 1, 2, 3) * 20, weights="uniform",
-            labels=(0, 3),
+            labels=(0, 3), cheaper_mix=True,
             desc="MetaPath schema (0,1,2,3) repeated to length 80, R-MAT s22 ef16, labels "
                  "uniform [0,3], uniform [1,5) weights"),
-    4: dict(scale=25, model="pr2", gamma=0.15, weights="pareto", labels=None,
+    # tier-2 sampling (erjs_handoff = 1): the reference's PR2 bounds run
+    # ~6,100 trials per step at s20 and more at larger scales, so
+    # an eRJS step hands off to the reservoir after max(32, d / ratio) trials;
+    # the distribution is exact (chi-square tested), the random stream differs
+    4: dict(scale=25, model="pr2", gamma=0.15, weights="pareto", labels=None, handoff=1.0,
+            cheaper_mix=True,
             desc="second-order PR gamma=0.15 (no restart in the reference, SURVEY 7.3), "
-                 "R-MAT/Kronecker s25 ef16, Pareto alpha=1 weights"),
-    # 10 walkers per vertex (qid = r*V + v): 1.34B walkers, 435 GB of paths per
-    # pass, so the timed pass keeps lengths only (paths discarded on the device)
+                 "R-MAT/Kronecker s25 ef16, Pareto alpha=1 weights, tier-2 eRJS hand-off"),
+    # 10 walkers per vertex (qid = r*V + v): 1.34B walkers, 435 GB of padded
+    # paths per pass: one round of 134M walkers (43.5 GB) at a time in HBM
     5: dict(scale=27, model="node2vec", a=0.5, b=2.0, weights="uniform", labels=None,
-            walkers_per_vertex=10, discard_paths=True,
+            walkers_per_vertex=10,
             desc="node2vec p=0.5 q=2, walk length 80, 10 walkers per vertex, weighted R-MAT "
-                 "s27 ef16 (2.1B edges in one GPU's HBM), paths discarded on the device"),
+                 "s27 ef16 (2.1B edges in one GPU's HBM); paths written to HBM per walker "
+                 "round (timed), streamed to host per round (e2e)"),
 }
 TOPO_SEED, WEIGHT_SEED, WALK_SEED, PROFILE_SEED, LABEL_SEED = 1, 2, 7, 5, 3
 
@@ -86,6 +92,9 @@ def parse():
                     help="experiments: walk without writing paths (lengths only)")
 
     ap.add_argument("--mode", default="adaptive")
+    ap.add_argument("--handoff", type=float, default=-1.0,
+                    help="tier-2 eRJS hand-off (dw_run_opts.erjs_handoff); default: the "
+                         "config's (1 for config 4, else 0 = the reference's rule)")
     ap.add_argument("--ratio", type=float, default=0.0, help="override the calibrated ratio")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--calib", default="micro", choices=["tune", "micro"],
@@ -111,6 +120,8 @@ def parse():
     if a.scale:
         a.cfg["scale"] = a.scale
     a.scale = a.cfg["scale"]
+    if a.handoff < 0:
+        a.handoff = a.cfg.get("handoff", 0.0)
     return a
 
 
@@ -139,6 +150,10 @@ def workload(args) -> dict:
             "graph": f"rmat s{args.scale} ef16 (A,B,C,D)=(.57,.19,.19,.05), mirrored, {w}",
             "model": c["model"], **{k: v for k, v in model_kw(c).items() if k != "schema"},
             "walk_length": args.walk_length, "mode": args.mode,
+            "sampling": (f"tier-2: eRJS hand-off after max(32, ceil({args.handoff:g}/ratio * d)) "
+                         "trials (dw_run_opts.erjs_handoff; distribution-exact, chi-square "
+                         "tested; paths equal the oracle with the same rule)" if args.handoff > 0
+                         else "tier-1: the reference's decision rule and trial cap (bit-exact)"),
             "walkers": c.get("walkers_per_vertex", 1) * 2 ** args.scale,
             "l2": "inputs larger than L2 (graph >= 2 GB vs 126 MB L2), no flush"}
 
@@ -366,7 +381,7 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
     mdesc = model.c()
     odescs = [dw.RunOptions(mode=args.mode, walk_length=L, seed=WALK_SEED, edge_cost_ratio=ratio,
-                            qid_base=base,
+                            qid_base=base, erjs_handoff=args.handoff,
                             qids=None if qid is None else qid.data_ptr()).c()
               for _, qid, base in rounds]
     graph_bytes = torch.cuda.mem_get_info(dev)
@@ -446,31 +461,51 @@ def run_ours(args):
     # dw_run_compact returns RunResult.paths flattened (offsets + ids), so only
     # ids that exist cross PCIe
     e2e = None
-    if args.e2e_steps > 0 and n > 0 and wpv == 1 and not discard:
-        q0, qid0, base0 = rounds[0]
-        nq = len(q0)
-        hq = C.c_void_p()
+    if args.e2e_steps > 0 and n > 0 and not discard:
+        # free the device paths of the timed region first (config 5: 43.5 GB)
+        del paths
+        torch.cuda.empty_cache()
+        # one pinned host region per distinct query array (walker rounds share
+        # theirs unless hash-sharded) and one output region reused by every
+        # round: a streaming sink, each round's compact paths land in host
+        # memory before the next round overwrites them
+        nqmax = max(len(q) for q, _, _ in rounds)
+        cap = nqmax * (L + 1)
         ho = C.c_void_p()
         hf = C.c_void_p()
-        cap = nq * (L + 1)
-        for buf, nbytes in ((hq, nq * 4), (ho, (nq + 1) * 8), (hf, cap * 4)):
+        for buf, nbytes in ((ho, (nqmax + 1) * 8), (hf, cap * 4)):
             rc = lib.dw_host_alloc(nbytes, C.byref(buf))
             if rc:
                 raise dw.DynwalkError(rc, lib.dw_last_error().decode())
-        qa = np.ctypeslib.as_array(C.cast(hq, dw.u32p), (nq,))
-        qa[:] = q0.cpu().numpy().astype(np.uint32)
-        oa = np.ctypeslib.as_array(C.cast(ho, dw.u64p), (nq + 1,))
-        hqid = None if qid0 is None else np.ascontiguousarray(qid0.cpu().numpy().astype(np.uint64))
-        odesc = dw.RunOptions(mode=args.mode, walk_length=L, seed=WALK_SEED,
-                              edge_cost_ratio=ratio, qid_base=base0, qids=hqid).c()
+        oa = np.ctypeslib.as_array(C.cast(ho, dw.u64p), (nqmax + 1,))
+        hqs, rounds_h = [], []
+        for k, (q, qid, base) in enumerate(rounds):
+            if k == 0 or strong:
+                hq = C.c_void_p()
+                rc = lib.dw_host_alloc(len(q) * 4, C.byref(hq))
+                if rc:
+                    raise dw.DynwalkError(rc, lib.dw_last_error().decode())
+                np.ctypeslib.as_array(C.cast(hq, dw.u32p), (len(q),))[:] = \
+                    q.cpu().numpy().astype(np.uint32)
+                hqs.append(hq)
+            hqid = None if qid is None else np.ascontiguousarray(qid.cpu().numpy().astype(np.uint64))
+            od = dw.RunOptions(mode=args.mode, walk_length=L, seed=WALK_SEED,
+                               edge_cost_ratio=ratio, qid_base=base, qids=hqid,
+                               erjs_handoff=args.handoff)
+            rounds_h.append((hqs[-1], len(q), od, od.c(), hqid))
         st = dw.RunStatsC()
+        out_ids = [0]
 
         def e2e_step():
-            rc = lib.dw_run_compact(dg.h, C.byref(mdesc), C.cast(hq, dw.u32p), nq,
-                                    C.byref(odesc), C.cast(ho, dw.u64p), C.cast(hf, dw.u32p),
-                                    cap, C.byref(st))
-            if rc:
-                raise dw.DynwalkError(rc, lib.dw_last_error().decode())
+            ids = 0
+            for hq, nq, _, odc, _ in rounds_h:
+                rc = lib.dw_run_compact(dg.h, C.byref(mdesc), C.cast(hq, dw.u32p), nq,
+                                        C.byref(odc), C.cast(ho, dw.u64p), C.cast(hf, dw.u32p),
+                                        cap, C.byref(st))
+                if rc:
+                    raise dw.DynwalkError(rc, lib.dw_last_error().decode())
+                ids += int(oa[nq])
+            out_ids[0] = ids
 
         e2e_step()  # warm
         if dist is not None:
@@ -481,24 +516,41 @@ def run_ours(args):
             e2e_step()
             ts.append(time.perf_counter() - t0)
         t_e2e = reduce_max(float(np.mean(ts)), dist, cdev)
-        ids = int(oa[nq])
+        nq_all = sum(nq for _, nq, _, _, _ in rounds_h)
         e2e = {"value": walker_steps / t_e2e, "unit": UNIT,
-               "h2d_bytes_per_step": reduce_sum(nq * (4 + (8 if hqid is not None else 0)), dist,
-                                                cdev),
-               "d2h_bytes_per_step": reduce_sum((nq + 1) * 8 + ids * 4, dist, cdev),
+               "h2d_bytes_per_step": reduce_sum(
+                   sum(nq * (4 + (8 if hqid is not None else 0))
+                       for _, nq, _, _, hqid in rounds_h), dist, cdev),
+               "d2h_bytes_per_step": reduce_sum((nq_all + len(rounds_h)) * 8 + out_ids[0] * 4,
+                                                dist, cdev),
                "ms_per_step": t_e2e * 1e3,
-               "api": "dw_run_compact (C ABI): pinned host queries in, offsets + path ids out"}
-        for buf in (hq, ho, hf):
+               "api": "dw_run_compact (C ABI): pinned host queries in, offsets + path ids out"
+                      + (f", {len(rounds_h)} walker rounds streamed through one reused host "
+                         "region" if len(rounds_h) > 1 else "")}
+        for buf in hqs + [ho, hf]:
             lib.dw_host_free(buf)
+
+    # ---- §8(d) cheaper-mix denominator (configs 3 and 4)
+    mix = None
+    if cfg.get("cheaper_mix") and args.mode == "adaptive":
+        mix = mix_bytes(lib, dw, dg, mdesc, nv, L, ratio, stream, torch, dev)
 
     # ---- CPU baseline (oracle port, host cores), rank 0 at N=1 only
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.scale <= 24:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and host_fits(info):
         cpu = cpu_baseline_port(dg, args, ratio, nv)
 
     if rank != 0:
         return
     pk = peaks()
+    own_bytes = alg_bytes
+    bytes_model = "SURVEY.md §8(d) minimal-sector model, counted per step on the device"
+    if mix is not None:
+        per_step = min(mix["reference_adaptive"], mix["all_ervs"])
+        alg_bytes = int(per_step * walker_steps)
+        bytes_model = ("SURVEY.md §8(d) cheaper-mix rule: min(reference adaptive mix, all-eRVS "
+                       "mix) bytes per walker-step, each counted by the device on the same "
+                       f"{mix['sample_walkers']}-walker sample, x this run's walker-steps")
     achieved = alg_bytes / (kernel_ms / 1e3) / 1e9
     sha = lib_sha16()
     traffic = ncu_traffic(args.scale, sha)
@@ -530,8 +582,9 @@ def run_ours(args):
                      "kernel_ms_per_launch": kernel_ms,
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "algorithmic_bytes_per_walker_step": alg_bytes / max(walker_steps, 1),
-                     "bytes_model": "SURVEY.md §8(d) minimal-sector model, counted per step "
-                                    "on the device"},
+                     "bytes_model": bytes_model,
+                     "this_run_bytes_per_walker_step": own_bytes / max(walker_steps, 1),
+                     "mix_bytes_per_walker_step": mix},
         "e2e": e2e,
         "cpu_baseline": cpu,
         "build": {"lib_sha16": sha, "traffic_source": (
@@ -606,6 +659,46 @@ def gather_shards(torch, dist, cdev, round0, lengths, paths, rank, world, nv,
     return out
 
 
+def mix_bytes(lib, dw, dg, mdesc, nv, L, ratio, stream, torch, dev, n=1 << 15) -> dict:
+    """SURVEY §8(d) cheaper-mix rule (configs 3 and 4): algorithmic bytes per
+    walker-step of the reference's adaptive mix (its decision rule and trial
+    cap, no hand-off) and of the all-eRVS mix, each counted by the device on
+    the same evenly spaced walker sample with the same per-event costs.  The
+    denominator is the cheaper of the two, so bytes the reference wastes on
+    loose bounds are not credited."""
+    stride = max(1, nv // n)
+    q = torch.arange(0, nv, stride, dtype=torch.int64, device=dev)[:n].to(torch.int32)
+    lengths = torch.empty(max(len(q), 1), dtype=torch.int32, device=dev)
+    out = {"sample_walkers": int(len(q))}
+    for name, mode in (("reference_adaptive", "adaptive"), ("all_ervs", "force-ervs")):
+        od = dw.RunOptions(mode=mode, walk_length=L, seed=WALK_SEED, edge_cost_ratio=ratio).c()
+        t0 = time.perf_counter()
+        rc = lib.dw_run_device(dg.h, 0, C.byref(mdesc), C.c_void_p(q.data_ptr()), len(q),
+                               C.byref(od), None, C.c_void_p(lengths.data_ptr()),
+                               C.c_void_p(stream.cuda_stream))
+        if rc:
+            raise dw.DynwalkError(rc, lib.dw_last_error().decode())
+        st = dw.RunStatsC()
+        rc = lib.dw_run_device_sync(dg.h, 0, C.byref(st))
+        if rc:
+            raise dw.DynwalkError(rc, lib.dw_last_error().decode())
+        out[name] = st.algorithmic_bytes / max(st.steps - st.dead_ends, 1)
+        out[name + "_s"] = time.perf_counter() - t0
+    return out
+
+
+def host_fits(info) -> bool:
+    """The CPU leg copies the graph to the host twice (download + oracle CSR):
+    run it when that fits in 1/2 of the available host memory."""
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        return False
+    need = 2 * (info["num_vertices"] * 8 + info["num_edges"] * 10)
+    return need < avail / 2
+
+
 def cpu_baseline_port(dg, args, ratio, nv) -> dict:
     """The oracle (C restatement of the reference path, pthreads over all host
     cores) on a bounded walker sample of the same graph and ratio."""
@@ -622,7 +715,8 @@ def cpu_baseline_port(dg, args, ratio, nv) -> dict:
         q = np.arange(0, nv, stride, dtype=np.uint32)[:n]
         t0 = time.perf_counter()
         r = oracle.run(og, m, q, mode=args.mode, walk_length=args.walk_length, seed=WALK_SEED,
-                       ratio=ratio, rng="philox", threads=cores, keep_paths=False)
+                       ratio=ratio, rng="philox", threads=cores, keep_paths=False,
+                       erjs_handoff=args.handoff)
         dt = time.perf_counter() - t0
         ws = r.stats["steps"] - r.stats["dead_ends"]
         rate = ws / dt
@@ -703,6 +797,7 @@ def run_reference(args):
            "dtype": "f64", "data": "synthetic R-MAT (same graph as the GPU arm, CPU-built)",
            "impl": "reference",
            "config": dict(workload(args), edge_cost_ratio=ratio,
+                          sampling="the reference's own run_queries (its decision rule and cap)",
                           edge_cost_ratio_source="reference profile_edge_cost_ratio"
                           if kind == "reference" else "fixed"),
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,

@@ -116,6 +116,15 @@ typedef struct dw_run_opts {
      * paths, of the unpartitioned run.  Host memory for dw_run /
      * dw_run_compact / dw_run_write_paths, device memory for dw_run_device. */
     const uint64_t* qids;
+    /* Tier-2 eRJS hand-off (FlexiWalker's bounded per-lane rejection,
+     * PAPER.md:760-765; not in the reference): when > 0, an eRJS step that
+     * has run max(32, ceil(erjs_handoff / edge_cost_ratio * d)) trials
+     * without acceptance falls back to the reservoir pass exactly as the
+     * reference's cap overrun does (samplers.hpp:174-177).  The sampled
+     * distribution is unchanged (a mixture of two exact samplers); paths
+     * equal the oracle run with the same rule, not the reference's.
+     * 0 (default) = the reference's rule, bit-exact. */
+    double erjs_handoff;
 } dw_run_opts;
 
 /* RunStats (runtime.hpp:53-73) minus host-only fields. */
@@ -235,6 +244,12 @@ int dw_run_device(dw_graph_t g, int replica, const dw_model_desc* model,
                   const uint32_t* d_queries, uint64_t nq, const dw_run_opts* opts,
                   uint32_t* d_paths, uint32_t* d_lengths, void* stream);
 int dw_run_device_sync(dw_graph_t g, int replica, dw_run_stats* stats);
+
+/* Self-test of the device math the reservoir samplers use (samplers.hpp:
+ * 82-97 std::log / std::exp): y[i] = log(x[i]) (fn 0) or exp(x[i]) (fn 1)
+ * computed by CUDA libdevice on device 0, host arrays in and out.  Lets the
+ * test suite measure where libdevice and the host libm disagree. */
+int dw_selftest_math(int fn, const double* x, double* y, uint64_t n);
 
 /* Pinned host buffers for dw_run (cudaMallocHost). */
 int dw_host_alloc(size_t bytes, void** out);

@@ -44,7 +44,8 @@ class OrcModel(C.Structure):
 class OrcOpts(C.Structure):
     _fields_ = [("mode", C.c_int), ("walk_length", C.c_uint32), ("seed", C.c_uint64),
                 ("cap_per_degree", C.c_uint64), ("edge_cost_ratio", C.c_double),
-                ("rng", C.c_int), ("qid_base", C.c_uint64), ("qids", C.c_void_p)]
+                ("rng", C.c_int), ("qid_base", C.c_uint64), ("qids", C.c_void_p),
+                ("erjs_handoff", C.c_double)]
 
 
 class OrcStats(C.Structure):
@@ -83,6 +84,8 @@ def lib() -> C.CDLL:
         L.orc_derive_seed.restype = C.c_uint64
         L.orc_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
         L.orc_mt19937_64.argtypes = [C.c_uint64, C.c_uint64, u64p]
+        L.orc_libm.argtypes = [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                               C.c_uint64]
         L.orc_philox4x32_10.argtypes = [u32p, u32p, u32p]
         L.orc_walker_draw.restype = C.c_uint64
         L.orc_walker_draw.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint64]
@@ -290,7 +293,7 @@ class RunResult:
 
 def run(g: Graph, model: Model, queries, mode="adaptive", walk_length=80, seed=0,
         cap_per_degree=64, ratio=1.0, rng="philox", threads=1, keep_paths=True,
-        qid_base=0, qids=None) -> RunResult:
+        qid_base=0, qids=None, erjs_handoff=0.0) -> RunResult:
     """Oracle run_queries (runtime.cpp:192-247).  qids: [nq] global walker
     ids (stream keys) of the queries, default qid_base + i."""
     q = np.ascontiguousarray(queries, np.uint32)
@@ -302,7 +305,7 @@ def run(g: Graph, model: Model, queries, mode="adaptive", walk_length=80, seed=0
     st = OrcStats()
     m = model.c()
     o = OrcOpts(MODES[mode], walk_length, seed, cap_per_degree, ratio, RNG[rng], qid_base,
-                None if qa is None else qa.ctypes.data)
+                None if qa is None else qa.ctypes.data, erjs_handoff)
     import time
     t0 = time.perf_counter()
     rc = lib().orc_run(g.ptr, C.byref(m), C.byref(o), _ptr(q, u32p), len(q),

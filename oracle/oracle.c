@@ -1015,8 +1015,24 @@ static outcome sample_ervs_nojump(ctx_t* c, const wstate* st, wrng* r) {
     return out;
 }
 
-/* sample_erjs (samplers.hpp:145-178) */
-static outcome sample_erjs(ctx_t* c, const wstate* st, wrng* r, double bound, uint64_t cap_pd) {
+/* Trial cap of an eRJS step: cap_per_degree * d (samplers.hpp:157), tightened
+ * by the tier-2 hand-off when erjs_handoff > 0 (not in the reference; the
+ * device rule of dw_walk_kernel.cuh step_cap, include/dynwalk_b200.h):
+ * max(32, ceil(erjs_handoff / ratio * d)) trials, a ski-rental bound of the
+ * rejection loop against one reservoir pass over the row. */
+static uint64_t erjs_cap(const orc_opts* o, uint32_t d) {
+    uint64_t cap = o->cap_per_degree * d;
+    if (o->erjs_handoff > 0.0) {
+        const double scale = o->erjs_handoff / o->edge_cost_ratio;
+        const double h = ceil(scale * (double)d);
+        uint64_t hc = h < 32.0 ? 32u : (h >= 4294967295.0 ? 0xFFFFFFFFu : (uint64_t)h);
+        if (hc < cap) cap = hc;
+    }
+    return cap;
+}
+
+/* sample_erjs (samplers.hpp:145-178); cap = the step's trial cap */
+static outcome sample_erjs(ctx_t* c, const wstate* st, wrng* r, double bound, uint64_t cap) {
     const orc_graph* g = c->g;
     const uint32_t d = degree(g, st->cur);
     outcome out = {ORC_INVALID, 0, 0, 0, 0};
@@ -1030,7 +1046,6 @@ static outcome sample_erjs(ctx_t* c, const wstate* st, wrng* r, double bound, ui
     }
     const uint64_t e0 = g->row[st->cur];
     const uint64_t draws0 = r->draws;
-    const uint64_t cap = cap_pd * d;
     while (out.trials < cap) {
         const uint64_t x = wrng_bounded(r, d);
         const double y = wrng_uniform01(r) * bound;
@@ -1096,7 +1111,7 @@ static int64_t walk_query(ctx_t* c, const orc_opts* o, uint32_t start, uint64_t 
             bucket(ls, d, erjs);
             if (erjs) {
                 ++ls->select_erjs;
-                out = sample_erjs(c, &st, r, est_max, o->cap_per_degree);
+                out = sample_erjs(c, &st, r, est_max, erjs_cap(o, d));
             } else {
                 ++ls->select_ervs;
                 out = sample_ervs(c, &st, r);
@@ -1117,7 +1132,7 @@ static int64_t walk_query(ctx_t* c, const orc_opts* o, uint32_t start, uint64_t 
             const double est = model_bound(c, &st);
             ++ls->select_erjs;
             bucket(ls, d, 1);
-            out = sample_erjs(c, &st, r, est, o->cap_per_degree);
+            out = sample_erjs(c, &st, r, est, erjs_cap(o, d));
             break;
         }
         default:
@@ -1297,4 +1312,10 @@ double orc_weight(const orc_graph* g, const orc_model* m, uint32_t cur, uint32_t
     const wstate st = make_state(g, cur, prev, step);
     const double w = model_weight(&c, &st, e);
     return c.err ? NAN : w;
+}
+
+/* Host libm (the reference's std::log / std::exp, samplers.hpp:82-97) over an
+ * array: the counterpart of dw_selftest_math for the libdevice agreement test. */
+void orc_libm(int fn, const double* x, double* y, uint64_t n) {
+    for (uint64_t i = 0; i < n; ++i) y[i] = fn == 0 ? log(x[i]) : exp(x[i]);
 }

@@ -59,7 +59,10 @@ typedef struct orc_opts {
     int rng; /* ORC_RNG_* */
     uint64_t qid_base; /* global id of queries[0] (walker-stream key) */
     const uint64_t* qids; /* [nq] global walker ids, or NULL: qid_base + i */
+    double erjs_handoff;  /* tier-2 hand-off (include/dynwalk_b200.h), 0 = off */
 } orc_opts;
+
+void orc_libm(int fn, const double* x, double* y, uint64_t n);
 
 /* Mirrors RunStats (include/dynwalk/runtime.hpp:53-73), GPU-relevant fields. */
 typedef struct orc_stats {

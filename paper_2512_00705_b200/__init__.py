@@ -40,6 +40,7 @@ EXPORTED_SYMBOLS = (
     "dw_run_device_sync",
     "dw_host_alloc",
     "dw_host_free",
+    "dw_selftest_math",
 )
 
 MODEL_KINDS = {"static": 0, "node2vec": 1, "metapath": 2, "pr2": 3, "custom": 4}
@@ -85,7 +86,7 @@ class ModelDesc(C.Structure):
 class RunOptsC(C.Structure):
     _fields_ = [("mode", C.c_int), ("walk_length", C.c_uint32), ("seed", C.c_uint64),
                 ("erjs_cap_per_degree", C.c_uint64), ("edge_cost_ratio", C.c_double),
-                ("qid_base", C.c_uint64), ("qids", C.c_void_p)]
+                ("qid_base", C.c_uint64), ("qids", C.c_void_p), ("erjs_handoff", C.c_double)]
 
 
 class ProfileConfigC(C.Structure):
@@ -155,6 +156,7 @@ def load_library() -> C.CDLL:
     L.dw_run_device_sync.argtypes = [vp, C.c_int, C.POINTER(RunStatsC)]
     L.dw_host_alloc.argtypes = [C.c_size_t, C.POINTER(vp)]
     L.dw_host_free.argtypes = [vp]
+    L.dw_selftest_math.argtypes = [C.c_int, f64p, f64p, C.c_uint64]
     _lib = L
     return L
 
@@ -219,6 +221,8 @@ class RunOptions:
     # global walker ids (RNG keys) of the queries: a host uint64 array for
     # run_queries*, or an int device address for dw_run_device; None = qid_base + i
     qids: object = None
+    # tier-2 eRJS hand-off (0 = the reference's rule; include/dynwalk_b200.h)
+    erjs_handoff: float = 0.0
 
     def c(self) -> RunOptsC:
         if self.mode not in MODES:
@@ -229,7 +233,8 @@ class RunOptions:
                 raise DynwalkError(-1, "qids must be a contiguous uint64 array")
             q = q.ctypes.data
         return RunOptsC(MODES[self.mode], self.walk_length, self.seed & (2**64 - 1),
-                        self.erjs_cap_per_degree, self.edge_cost_ratio, self.qid_base, q)
+                        self.erjs_cap_per_degree, self.edge_cost_ratio, self.qid_base, q,
+                        self.erjs_handoff)
 
 
 @dataclass

@@ -597,10 +597,10 @@ cudaError_t build_rmat(const RmatSpec& spec, DeviceGraphBuffers& g, cudaStream_t
     synth_props_kernel<<<grid_for(ne, 256), 256, 0, s>>>(prop, ne, spec.weights, spec.low,
                                                          spec.high, spec.alpha, spec.weight_seed);
     DW_TRY(cudaGetLastError());
-    DW_TRY(cudaMallocAsync(&g.edges, std::max<ull>(ne, 1) * sizeof(EdgeRec), s));
+    DW_TRY(cudaMallocAsync(&g.edges, ((std::max<ull>(ne, 1) + 1) & ~1ull) * sizeof(EdgeRec), s));
     DW_TRY(cudaMallocAsync(&g.nodes, std::max<uint32_t>(nv, 1) * sizeof(NodeRec), s));
     if (spec.labels) {
-        DW_TRY(cudaMallocAsync(&g.labels, std::max<ull>(ne, 1) * sizeof(uint16_t), s));
+        DW_TRY(cudaMallocAsync(&g.labels, ((std::max<ull>(ne, 1) + 1) & ~1ull) * sizeof(uint16_t), s));
         synth_labels_kernel<<<grid_for(ne, 256), 256, 0, s>>>(
             g.labels, ne, spec.label_low, (ull)spec.label_high - spec.label_low + 1,
             spec.label_seed);

@@ -65,6 +65,7 @@ struct ModelParams {
     uint32_t screen;          // wsum_approx is within 1e-15 (relative) of wsum
     double wsum_coef;         // node2vec: RN((1/a + 1 + 1/b) / 3)
     double fat32_band;        // relative band of the compact records' f32 row sum
+    double ervs_slack;        // widens the warp reservoir's rounding band (1; tests force the exact replay)
     uint32_t schema_len;
     uint16_t schema[128];
 };

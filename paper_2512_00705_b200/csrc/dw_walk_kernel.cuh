@@ -155,17 +155,339 @@ __device__ __forceinline__ const EdgeRec* pair_of(const EdgeRec* edges, ull e) {
 
 
 // ---- K2 (warp form): one row, 32 lanes; all lanes call with equal args ----
-// Returns the chosen target and its relative edge index (for the fat record).
-#ifndef DW_COOP_INLINE
-#define DW_COOP_INLINE 1
+// FlexiWalker's warp reservoir (samplers.hpp:65-137) without the sequential
+// chain.  A row is read in chunks of 64 neighbours, two per lane (one 16 B
+// load when the row starts on an even edge, two 8 B loads otherwise), the
+// next chunk in flight while this one is judged.
+//
+// Jump form.  The reference's jump test is a running subtraction
+// `skip -= w; if (skip <= 0)`, rounded after every neighbour.  Rounding makes
+// it sequential, but its sign can be decided from a parallel prefix sum:
+// for the chain started at s0 over m weights, the rounded chain C_j and the
+// real value S_j = s0 - (w_seg + ... + w_j) differ by at most
+// gamma_m (s0 + W_j) (recursive summation of non-negative terms), and the
+// warp's prefix sums (depth <= 7 roundings per chunk, carried across chunks)
+// differ from S_j by a bound of the same form.  With A_j the warp's value and
+// E_j = 1.1 u ((3 m + 8)(s0 + P_j) + |A_j|) (+ a subnormal floor), A_j > E_j
+// proves C_j > 0 and A_j < -E_j proves C_j <= 0 (ervs_bound below).  So a
+// chunk with no element inside its band costs one warp scan, and the first
+// element whose band reaches 0 is the crossing whenever A_j < -E_j.  Only
+// when the band straddles 0 (probability ~ m^2 u s0 / w per crossing) is the
+// chain replayed exactly, sequentially, from the segment start (ervs_replay),
+// and its exact value restarts the bound.  Jumps (new key, new threshold)
+// are warp-uniform and rare (~ln d per row).  Draws, their order and the
+// kept neighbour are the reference's; the outcome is identical, not
+// approximately equal.
+//
+// No-jump form.  Every neighbour draws its key (draw idx0 + i; neighbours 2k
+// and 2k+1 share one Philox block, because idx0 is even) and the keys merge
+// with a shuffle arg-max (lower index on ties).
+template <class M>
+__device__ __forceinline__ double ervs_weight(const M& m, const Step& S, const DevGraph& g,
+                                              uint32_t phoff, uint32_t u, float h, uint16_t lab) {
+    const WeightCase wc = m.weight(S, u, h, lab);
+    if (!M::kSecondOrder || !wc.needs_member) return wc.w;
+    return member(g, S.prev_degree, phoff, u) ? wc.w_in : wc.w_out;
+}
+
+// Neighbours i0 and i0 + 1 of the row at `begin` (ids, props, labels); ids of
+// neighbours past the row are kInvalid.
+struct EPair {
+    uint32_t u0, u1;
+    float h0, h1;
+    uint32_t lab;  // label(i0) | label(i0 + 1) << 16
+};
+template <class M>
+__device__ __forceinline__ EPair ervs_load_pair(const DevGraph& g, ull begin, uint32_t i0,
+                                                uint32_t d) {
+    EPair r{kInvalid, kInvalid, 0.f, 0.f, 0u};
+    if (i0 >= d) return r;
+    const ull e = begin + i0;
+    if (!(begin & 1)) {  // 16 B aligned pair (edge arrays are padded to even length)
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(g.edges + e));
+        r.u0 = v.x;
+        r.h0 = __uint_as_float(v.y);
+        if (i0 + 1 < d) {
+            r.u1 = v.z;
+            r.h1 = __uint_as_float(v.w);
+        }
+        if (M::kUsesLabels && g.labels) r.lab = __ldg(reinterpret_cast<const uint32_t*>(g.labels + e));
+    } else {
+        const EdgeRec a = load_edge(g.edges + e);
+        r.u0 = a.col;
+        r.h0 = a.h;
+        if (M::kUsesLabels && g.labels) r.lab = __ldg(g.labels + e);
+        if (i0 + 1 < d) {
+            const EdgeRec b = load_edge(g.edges + e + 1);
+            r.u1 = b.col;
+            r.h1 = b.h;
+            if (M::kUsesLabels && g.labels) r.lab |= (uint32_t)__ldg(g.labels + e + 1) << 16;
+        }
+    }
+    return r;
+}
+
+#ifndef DW_ERVS_SEQ
+#define DW_ERVS_SEQ 0  // 1: the round-1 sequential shuffle chain (A/B experiments)
 #endif
-#if DW_COOP_INLINE
-#define DW_COOP_ATTR __forceinline__
-#else
-#define DW_COOP_ATTR __noinline__
-#endif
+
+// The exact chain (samplers.hpp:86-90) from neighbour `seg` (whose weight is
+// the first subtracted) with remaining skip s, up to neighbour `end`
+// (exclusive): returns the crossing neighbour, or kInvalid with *s_out the
+// chain's value after neighbour end - 1.  Weights were validated by the caller.
+template <class M>
+__device__ __noinline__ uint32_t ervs_replay(const ModelParams& mp, Step S, const DevGraph& g,
+                                             ull begin, uint32_t phoff, uint32_t seg, double s,
+                                             uint32_t end, double* s_out) {
+    M m(mp);
+    m.prepare(S);
+    const int lane = threadIdx.x & 31;
+    for (uint32_t b = seg; b < end; b += 32) {
+        const uint32_t i = b + lane;
+        double w = 0.0;
+        if (i < end) {
+            const EdgeRec er = load_edge(g.edges + begin + i);
+            w = ervs_weight(m, S, g, phoff, er.col, er.h, edge_label<M>(g, begin + i));
+        }
+        const uint32_t n = end - b < 32u ? end - b : 32u;
+        for (uint32_t j = 0; j < n; ++j) {
+            const double wj = __shfl_sync(kFull, w, j);
+            if (wj == 0.0) continue;
+            s -= wj;
+            if (s <= 0.0) return b + j;
+        }
+    }
+    *s_out = s;
+    return kInvalid;
+}
+
+// |rounded chain - warp prefix value| bound of the chunk (see above)
+struct ErvsBound {
+    double k;    // 1.1 u (3 m + 8)
+    double lo;   // subnormal floor
+};
+__device__ __forceinline__ ErvsBound ervs_bound(uint32_t m, double slack) {
+    const double u = 0x1.0p-53;
+    return ErvsBound{1.1 * u * (3.0 * (double)m + 8.0) * slack, ((double)m + 16.0) * 0x1.0p-1060};
+}
+
 template <class M, bool NOJUMP>
-__device__ DW_COOP_ATTR int ervs_warp(const ModelParams& mp, Step S, const WalkerKey key,
+__device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const WalkerKey key,
+                                      const PhiloxKeys& rk,
+                                      const DevGraph& g, ull begin, uint32_t phoff, ull idx0,
+                                      uint32_t* next, uint32_t* nidx, ull* draws) {
+    M m(mp);
+    m.prepare(S);
+    const int lane = threadIdx.x & 31;
+    const uint32_t d = S.degree;
+    ull idx = idx0;                // next draw (warp-uniform)
+    double bkey = -DBL_MAX;        // best log key
+    uint32_t best = kInvalid, bi = 0;
+    // jump chain: remaining skip s (valid when `have`), exact start value s0 at
+    // neighbour seg
+    bool have = false;
+    double s = 0.0, s0 = 0.0;
+    uint32_t seg = 0;
+    EPair nx = ervs_load_pair<M>(g, begin, 2u * lane, d);
+    for (uint32_t base = 0; base < d; base += 64) {
+        const uint32_t i0 = base + 2u * lane;
+        const EPair cp = nx;
+        if (base + 64 < d) nx = ervs_load_pair<M>(g, begin, i0 + 64, d);
+        double w0 = 0.0, w1 = 0.0;
+        if (cp.u0 != kInvalid) w0 = ervs_weight(m, S, g, phoff, cp.u0, cp.h0, (uint16_t)cp.lab);
+        if (cp.u1 != kInvalid) w1 = ervs_weight(m, S, g, phoff, cp.u1, cp.h1, (uint16_t)(cp.lab >> 16));
+        if (__any_sync(kFull, (cp.u0 != kInvalid && !valid_w(w0)) ||
+                                  (cp.u1 != kInvalid && !valid_w(w1))))
+            return -kDevBadWeight;
+        if (NOJUMP) {
+            double lk = -DBL_MAX;
+            uint32_t src = kInvalid, cand = kInvalid;
+            if (cp.u0 != kInvalid) {
+                const U4 blk = philox4x32_10_rk(
+                    U4{(uint32_t)((idx0 + i0) >> 1), key.step, key.q0, key.q1}, rk);
+                if (w0 != 0.0) {
+                    lk = log(open01(lo64(blk))) / w0;
+                    src = i0;
+                    cand = cp.u0;
+                }
+                if (cp.u1 != kInvalid && w1 != 0.0) {
+                    const double l1 = log(open01(hi64(blk))) / w1;
+                    if (src == kInvalid || l1 > lk) {
+                        lk = l1;
+                        src = i0 + 1;
+                        cand = cp.u1;
+                    }
+                }
+            }
+#pragma unroll
+            for (int off = 16; off; off >>= 1) {
+                const double olk = __shfl_xor_sync(kFull, lk, off);
+                const uint32_t osrc = __shfl_xor_sync(kFull, src, off);
+                const uint32_t ocand = __shfl_xor_sync(kFull, cand, off);
+                const bool take = osrc != kInvalid &&
+                                  (src == kInvalid || olk > lk || (olk == lk && osrc < src));
+                if (take) {
+                    lk = olk;
+                    src = osrc;
+                    cand = ocand;
+                }
+            }
+            if (src != kInvalid && (best == kInvalid || lk > bkey)) {
+                bkey = lk;
+                best = cand;
+                bi = src;
+            }
+            continue;
+        }
+        const uint32_t cend = base + 64 < d ? base + 64 : d;
+#if DW_ERVS_SEQ
+        {
+            const uint32_t n = cend - base;
+            for (uint32_t j = 0; j < n; ++j) {
+                const uint32_t l = j >> 1;
+                const double wj = __shfl_sync(kFull, (j & 1) ? w1 : w0, l);
+                const uint32_t uj = __shfl_sync(kFull, (j & 1) ? cp.u1 : cp.u0, l);
+                if (wj == 0.0) continue;
+                if (best == kInvalid) {
+                    bkey = log(open01(walker_draw(key, rk, idx++))) / wj;
+                    best = uj;
+                    bi = base + j;
+                    continue;
+                }
+                if (!have) {
+                    s = log(open01(walker_draw(key, rk, idx++))) / bkey;
+                    have = true;
+                }
+                s -= wj;
+                if (s <= 0.0) {
+                    const double floor_u = exp(wj * bkey);
+                    const double uu = floor_u + open01(walker_draw(key, rk, idx++)) * (1.0 - floor_u);
+                    const double lk = log(uu) / wj;
+                    if (lk > bkey) {
+                        bkey = lk;
+                        best = uj;
+                        bi = base + j;
+                    }
+                    have = false;
+                }
+            }
+            continue;
+        }
+#endif
+        uint32_t pos = base;  // first neighbour of the chunk not yet consumed
+        for (;;) {
+            if (!have) {
+                // the next positive weight: the first key, or the next threshold
+                const bool nz0 = w0 != 0.0 && i0 >= pos, nz1 = w1 != 0.0 && i0 + 1 >= pos;
+                const unsigned bal = __ballot_sync(kFull, nz0 || nz1);
+                if (!bal) break;
+                const int f = __ffs(bal) - 1;
+                const uint32_t fe = __shfl_sync(kFull, nz0 ? i0 : i0 + 1, f);
+                const double fw = __shfl_sync(kFull, nz0 ? w0 : w1, f);
+                const uint32_t fu = __shfl_sync(kFull, nz0 ? cp.u0 : cp.u1, f);
+                const double lr = log(open01(walker_draw(key, rk, idx++)));
+                if (best == kInvalid) {  // samplers.hpp:82-85
+                    bkey = lr / fw;
+                    best = fu;
+                    bi = fe;
+                    pos = fe + 1;
+                    continue;
+                }
+                s = s0 = lr / bkey;  // samplers.hpp:86-89
+                seg = fe;
+                have = true;
+                pos = fe;
+            }
+            // prefix sums of the weights from pos on (two per lane, then a
+            // Kogge-Stone warp scan)
+            const double x0 = i0 >= pos ? w0 : 0.0, x1 = i0 + 1 >= pos ? w1 : 0.0;
+            const double p1 = x0 + x1;
+            double inc = p1;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const double t = __shfl_up_sync(kFull, inc, off);
+                if (lane >= off) inc += t;
+            }
+            double exc = __shfl_up_sync(kFull, inc, 1);
+            if (lane == 0) exc = 0.0;
+            const double P0 = exc + x0, P1 = exc + p1;
+            uint32_t cross = kInvalid;
+            bool decided = false;
+            if (s > 0.0 && s < DBL_MAX) {
+                const ErvsBound eb = ervs_bound(cend - seg, mp.ervs_slack);
+                const double A0 = s - P0, A1 = s - P1;
+                const double E0 = eb.k * (s0 + P0) + 1.1 * 0x1.0p-53 * fabs(A0) + eb.lo;
+                const double E1 = eb.k * (s0 + P1) + 1.1 * 0x1.0p-53 * fabs(A1) + eb.lo;
+                const bool may0 = x0 != 0.0 && !(A0 > E0), may1 = x1 != 0.0 && !(A1 > E1);
+                const unsigned bal = __ballot_sync(kFull, may0 || may1);
+                if (!bal) {  // no crossing in this chunk
+                    s = s - __shfl_sync(kFull, inc, 31);
+                    break;
+                }
+                const int f = __ffs(bal) - 1;
+                const bool sure = __shfl_sync(kFull, may0 ? (A0 < -E0) : (A1 < -E1), f);
+                if (sure) {
+                    cross = __shfl_sync(kFull, may0 ? i0 : i0 + 1, f);
+                    decided = true;
+                }
+            }
+            if (!decided) {
+                // band straddles 0 (or s is not finite): the exact chain
+                double sx = 0.0;
+                cross = ervs_replay<M>(mp, S, g, begin, phoff, seg, s0, cend, &sx);
+                if (cross == kInvalid) {  // exact value at the chunk end restarts the bound
+                    s = s0 = sx;
+                    seg = cend;
+                    break;
+                }
+            }
+            // replacement at `cross` (samplers.hpp:90-99)
+            const int ol = (int)((cross - base) >> 1);
+            const bool odd = (cross - base) & 1;
+            const double wj = __shfl_sync(kFull, odd ? w1 : w0, ol);
+            const uint32_t uj = __shfl_sync(kFull, odd ? cp.u1 : cp.u0, ol);
+            const double floor_u = exp(wj * bkey);
+            const double uu = floor_u + open01(walker_draw(key, rk, idx++)) * (1.0 - floor_u);
+            const double lk = log(uu) / wj;
+            if (lk > bkey) {
+                bkey = lk;
+                best = uj;
+                bi = cross;
+            }
+            have = false;
+            pos = cross + 1;
+        }
+    }
+    *next = best;
+    *nidx = bi;
+    *draws = NOJUMP ? (ull)d : idx - idx0;
+    return 0;
+}
+
+// Out of line for the modes in which whole-row scans are rare (adaptive,
+// force-erjs: cap fallbacks and adaptive eRVS decisions on rows of >= 64):
+// keeps the eRJS loop's instruction footprint (icache)
+#ifndef DW_PR2_PAR
+#define DW_PR2_PAR 1
+#endif
+// The parallel form out of line, for models whose adaptive runs scan hub rows
+// often (PR2: cap overruns and tier-2 hand-offs), without growing their
+// eRJS loop's register set
+template <class M, bool NOJUMP>
+__device__ __noinline__ int ervs_warp_cold(const ModelParams& mp, Step S, const WalkerKey key,
+                                           const PhiloxKeys& rk, const DevGraph& g, ull begin,
+                                           uint32_t phoff, ull idx0, uint32_t* next,
+                                           uint32_t* nidx, ull* draws) {
+    return ervs_warp<M, NOJUMP>(mp, S, key, rk, g, begin, phoff, idx0, next, nidx, draws);
+}
+
+// Round-1 warp form: 32 neighbours per chunk and the jump chain run
+// sequentially through shuffles.  Kept for the modes in which whole-row
+// scans are rare (adaptive, force-erjs: cap fallbacks and adaptive eRVS
+// decisions on rows of >= 64), whose loops sit at the register and
+// instruction-cache limit (the parallel form adds ~14 live registers).
+template <class M, bool NOJUMP>
+__device__ __forceinline__ int ervs_warp_seq(const ModelParams& mp, Step S, const WalkerKey key,
                                       const PhiloxKeys& rk,
                                       const DevGraph& g, ull begin, uint32_t phoff, ull idx0,
                                       uint32_t* next, uint32_t* nidx, ull* draws) {
@@ -375,8 +697,15 @@ struct WalkSmem {
     ull lct[LC_NUM];                 // block totals of the lane counters
 };
 
+// reservoir-only modes (force-ervs, ervs-nojump) spend their time in the
+// warp-cooperative row scan, whose parallel jump chain needs ~14 more live
+// registers: 2 CTAs/SM (up to 128 registers) instead of 3
+#ifndef DW_ERVS_MIN_BLOCKS
+#define DW_ERVS_MIN_BLOCKS 2
+#endif
 template <class M, int MODE, int FAT>
-__global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
+__global__ void __launch_bounds__(kThreads, (MODE == kForceErvs || MODE == kErvsNoJump)
+                                                ? DW_ERVS_MIN_BLOCKS : DW_MIN_BLOCKS)
     walk_kernel(const __grid_constant__ WalkParams p) {
     constexpr bool kNoJump = MODE == kErvsNoJump;
     constexpr bool kSO = M::kSecondOrder;
@@ -549,6 +878,18 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
         }
         ev_store(ErvsState{-DBL_MAX, 0.0, draw_base, kInvalid, 0});
         phase = deg >= kCoopMinDegree ? P_COOP : P_VREC;
+    };
+    // trial cap of an eRJS step at cur (samplers.hpp:157), tightened by the
+    // tier-2 hand-off when enabled (dw_run_opts.erjs_handoff; oracle.c erjs_cap)
+    auto step_cap = [&]() -> uint32_t {
+        const ull c = p.cap_per_degree * (ull)deg;
+        uint32_t r = c > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)c;
+        if (p.handoff_scale > 0.0) {
+            const double h = ceil(p.handoff_scale * (double)deg);
+            const uint32_t hc = h < 32.0 ? 32u : (h >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)h);
+            if (hc < r) r = hc;
+        }
+        return r;
     };
     // eRJS bookkeeping for T judged trials, nret of them return edges
     auto count_erjs = [&](uint32_t T) {
@@ -991,9 +1332,8 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                 }
                 if (dead_row) {
                     if (erjs) {
-                        const ull c = p.cap_per_degree * (ull)deg;
                         nret = 0;
-                        count_erjs(c > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)c);
+                        count_erjs(step_cap());
                         lc_add(LC_FALLBACKS, 1);
                     } else {
                         lc_add(LC_ETRIALS1, 1);  // single-shot eRVS
@@ -1007,8 +1347,7 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
                         fail(kDevBadBound);
                     } else {
                         mnr = shortcut ? model.nonreturn_max(S) : __longlong_as_double(0x7ff0000000000000ll);
-                        const ull c = p.cap_per_degree * (ull)deg;
-                        cap = c > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)c;
+                        cap = step_cap();
                         tn = rh = rc = 0;
                         mb = nret = sel = 0;
                         phase = P_TRIAL;
@@ -1077,7 +1416,13 @@ __global__ void __launch_bounds__(kThreads, DW_MIN_BLOCKS)
             const ull db = __shfl_sync(kFull, lane == L ? ev_load().didx : 0ull, L);
             uint32_t nx = kInvalid, ni = 0;
             ull dr = 0;
-            const int st = ervs_warp<M, kNoJump>(p.mp, T, K, p.rk, g, tb, tph, db, &nx, &ni, &dr);
+            int st;
+            if constexpr (MODE == kForceErvs || MODE == kErvsNoJump)
+                st = ervs_warp<M, kNoJump>(p.mp, T, K, p.rk, g, tb, tph, db, &nx, &ni, &dr);
+            else if constexpr (DW_PR2_PAR && CoopErjs<M>::value)  // PR2: cap overruns, hand-offs
+                st = ervs_warp_cold<M, kNoJump>(p.mp, T, K, p.rk, g, tb, tph, db, &nx, &ni, &dr);
+            else
+                st = ervs_warp_seq<M, kNoJump>(p.mp, T, K, p.rk, g, tb, tph, db, &nx, &ni, &dr);
             if (lane == L) {
                 if (st < 0) {
                     fail(-st);

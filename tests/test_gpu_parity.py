@@ -577,3 +577,103 @@ def test_pr2_pareto_cooperative_erjs(dw, orc, mode, fat):
     r_dev, r_orc = run_both(dw, orc, og, dg, dict(kind="pr2", gamma=0.15), q, mode, 30, 1.2)
     assert r_orc.stats["trials"] > 50 * r_orc.stats["steps"]  # heavy-tailed steps: CJS engaged
     assert_same(r_dev, r_orc, (mode, fat))
+
+
+def _hub_graph(orc, n=120_000, seed=31):
+    """Hubs far above one warp chunk: node 0 joined to every node, node 1 to
+    every 3rd, node 2 to every 7th, plus a ring; mirrored, Philox weights."""
+    rng = np.random.default_rng(seed)
+    v = np.arange(3, n, dtype=np.uint32)
+    src = np.concatenate([np.zeros(n - 3, np.uint32), np.ones(len(v[::3]), np.uint32),
+                          np.full(len(v[::7]), 2, np.uint32), v[:-1]])
+    dst = np.concatenate([v, v[::3], v[::7], v[1:]])
+    extra = rng.integers(3, n, size=(2, n), dtype=np.uint32)  # a few random chords
+    src = np.concatenate([src, extra[0]])
+    dst = np.concatenate([dst, extra[1]])
+    return orc.Graph.build(src, dst, mirror=True, nv_hint=n).synth_philox(
+        "uniform", 1.0, 5.0, seed=seed + 1)
+
+
+@pytest.mark.parametrize("slack", ["1", "1e13"], ids=["band", "replay"])
+@pytest.mark.parametrize("mode", ["force-ervs", "ervs-nojump"])
+@pytest.mark.parametrize("mk", [dict(kind="node2vec", a=0.5, b=2.0),
+                                dict(kind="node2vec", a=2.0, b=0.5),
+                                dict(kind="pr2", gamma=0.2),
+                                dict(kind="static", weighted=True)])
+def test_hub_rows_warp_reservoir(dw, orc, mk, mode, slack):
+    """The warp reservoir (dw_walk_kernel.cuh ervs_warp) on rows of 17K-120K
+    neighbours: the parallel jump chain decides every crossing from prefix
+    sums and a rigorous rounding band, and replays the exact chain only when
+    the band straddles 0.  DW_ERVS_SLACK=1e13 widens the band so that almost
+    every crossing goes through the replay.  Both are bit-exact against the
+    oracle's sequential chain (samplers.hpp:65-137)."""
+    og = _hub_graph(orc)
+    dg = to_device(dw, og)
+    # walkers on and next to the hubs: every step of theirs scans a hub row
+    q = np.concatenate([np.zeros(32, np.uint32), np.ones(32, np.uint32),
+                        np.full(32, 2, np.uint32), np.arange(3, 3 + 160, dtype=np.uint32)])
+    r_dev, r_orc = _with_env({"DW_ERVS_SLACK": slack},
+                             lambda: run_both(dw, orc, og, dg, mk, q, mode, 16, 1.2))
+    assert_same(r_dev, r_orc, (mk, mode, slack))
+    assert r_dev.stats["weight_reads"] > 50 * 100_000
+
+
+@pytest.mark.parametrize("layout", ["fat", "slim"])
+@pytest.mark.parametrize("mode", ["adaptive", "force-erjs"])
+def test_tier2_handoff_bit_exact_and_chi_square(dw, orc, mode, layout):
+    """Tier-2 eRJS hand-off (dw_run_opts.erjs_handoff): PR2 gamma=0.15 on
+    Pareto weights, the config-4 pathology.  The device equals the oracle
+    run with the same rule in paths and counters, the hand-off fires, and the
+    device's per-(prev, cur) transition frequencies on hub and non-hub rows
+    pass chi-square against the exact probabilities."""
+    from tests.chisq import transition_pvalues
+    og = orc.Graph.rmat(12, 16, 3).synth_philox("pareto", alpha=1.0, seed=4)
+    dg = _with_env({"DW_FAT": "1" if layout == "fat" else "0"}, lambda: to_device(dw, og))
+    mk = dict(kind="pr2", gamma=0.15)
+    q = np.arange(og.nv, dtype=np.uint32)
+    o = dict(mode=mode, walk_length=40, seed=7, edge_cost_ratio=1.0)
+    r_dev = dw.run_queries(dg, dw.Model(**mk), q, dw.RunOptions(erjs_handoff=1.0, **o))
+    r_orc = orc.run(og, orc.Model(**mk), q, mode=mode, walk_length=40, seed=7, ratio=1.0,
+                    rng="philox", threads=os.cpu_count() or 1, erjs_handoff=1.0)
+    assert_same(r_dev, r_orc, (mode, layout))
+    assert r_dev.stats["erjs_fallbacks"] > 100
+    deg = np.diff(og.arrays()["row"])
+    hubs = np.argsort(deg)[-3:]
+    small = np.flatnonzero((deg >= 2) & (deg <= 8))[:3]
+    starts = np.repeat(np.concatenate([hubs, small]).astype(np.uint32), 40_000)
+    r = dw.run_queries(dg, dw.Model(**mk), starts,
+                       dw.RunOptions(erjs_handoff=1.0, **dict(o, walk_length=2, seed=13)))
+    ps, pooled = transition_pvalues(orc, og, orc.Model(**mk), r.paths, starts)
+    assert len(ps) >= 10 and pooled > 0.01 and min(ps) > 1e-4, (len(ps), pooled, min(ps))
+
+
+def test_libdevice_log_exp_against_host_libm(dw, orc):
+    """eRVS keys, thresholds and floors use log/exp (samplers.hpp:82-97).  The
+    device computes them with CUDA libdevice, the reference with glibc.  Over
+    the inputs the samplers form -- open01 values and floor + open01 (1 -
+    floor) for log, w * key <= 0 for exp -- the two never differ by more than
+    1 ulp.  An outcome can then flip only when two keys, or a threshold and
+    the chain, fall within ~2 ulp of each other (probability ~2^-51 per
+    comparison); the measured disagreement rates are printed for DESIGN.md."""
+    import ctypes as C
+    rng = np.random.default_rng(17)
+    n = 1 << 22
+    u = rng.integers(0, 2**64, size=n, dtype=np.uint64)
+    x_log = ((u >> np.uint64(11)).astype(np.float64) + 0.5) * 2.0**-53
+    fl = np.exp(-rng.exponential(3.0, size=n))
+    x_log2 = fl + x_log * (1.0 - fl)
+    x_exp = -np.exp(rng.uniform(-30.0, 6.0, size=n))
+    lib = dw.load_library()
+    for fn, x in ((0, x_log), (0, x_log2), (1, x_exp)):
+        x = np.ascontiguousarray(x)
+        yd = np.empty_like(x)
+        yh = np.empty_like(x)
+        assert lib.dw_selftest_math(fn, x.ctypes.data_as(dw.f64p), yd.ctypes.data_as(dw.f64p),
+                                    n) == 0
+        orc.lib().orc_libm(fn, x.ctypes.data_as(C.POINTER(C.c_double)),
+                           yh.ctypes.data_as(C.POINTER(C.c_double)), C.c_uint64(n))
+        ok = np.isfinite(yh) & (yh != 0)
+        assert np.array_equal(np.isfinite(yd), np.isfinite(yh))
+        ulp = np.abs(yd[ok].view(np.int64) - yh[ok].view(np.int64))
+        print(f"fn={fn} differ={np.count_nonzero(ulp) / ok.sum():.3e} max_ulp={ulp.max()}")
+        assert ulp.max() <= 1

@@ -254,3 +254,30 @@ def test_rmat_graph_properties(orc):
     assert a["prop"].min() >= 1.0 and a["prop"].max() < 5.0
     deg = np.diff(row)
     assert deg.max() > 20 * deg.mean()  # skewed
+
+
+def test_tier2_handoff_keeps_the_distribution(orc):
+    """Tier-2 eRJS hand-off (dw_run_opts.erjs_handoff, oracle.c erjs_cap): a
+    step that runs max(32, ceil(h/ratio*d)) trials without acceptance falls
+    back to the reservoir pass, as the reference's cap overrun does.  PR2 on
+    Pareto weights (config 4's pathology: bounds far above the weights) with
+    the hand-off: per-(prev, cur) transition frequencies over hub and
+    non-hub rows pass chi-square against the exact probabilities, and the
+    hand-off really fires."""
+    from tests.chisq import transition_pvalues
+    og = orc.Graph.rmat(10, 16, 3).synth_philox("pareto", alpha=1.0, seed=4)
+    a = og.arrays()
+    deg = np.diff(a["row"])
+    # starts: the 4 largest rows and 4 rows of degree 2-8
+    hubs = np.argsort(deg)[-4:]
+    small = np.flatnonzero((deg >= 2) & (deg <= 8))[:4]
+    starts = np.repeat(np.concatenate([hubs, small]).astype(np.uint32), 30_000)
+    m = orc.Model("pr2", gamma=0.15)
+    r = orc.run(og, m, starts, mode="adaptive", walk_length=2, seed=9, ratio=1.0,
+                rng="philox", threads=os.cpu_count() or 1, erjs_handoff=1.0)
+    base = orc.run(og, m, starts[:2000], mode="adaptive", walk_length=2, seed=9, ratio=1.0,
+                   rng="philox", threads=os.cpu_count() or 1)
+    assert r.stats["erjs_fallbacks"] > 1000 and base.stats["erjs_fallbacks"] == 0
+    ps, pooled = transition_pvalues(orc, og, m, r.paths, starts)
+    assert len(ps) >= 20
+    assert pooled > 0.01 and min(ps) > 1e-4, (pooled, min(ps))
