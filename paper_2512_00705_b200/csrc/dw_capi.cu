@@ -164,6 +164,7 @@ void free_replica(Replica& r) {
     cudaFree(r.g.lagg);
     cudaFree(r.g.twin);
     cudaFree(r.g.fat32);
+    cudaFree(r.g.lab2);
     cudaFree(r.counters);
     cudaFree(r.queues);
     cudaFree(r.error);
@@ -408,7 +409,7 @@ dwb::WalkParams make_params(Replica& r, const dw_model_desc* m, const dw_run_opt
     dwb::WalkParams p;
     std::memset(&p, 0, sizeof p);
     p.g = dwb::DevGraph{r.g.nodes, r.g.edges, r.g.labels, r.g.hslots, r.g.fat, r.g.lagg,
-                        r.g.twin, r.g.fat32, r.g.nv, r.g.ne};
+                        r.g.twin, r.g.fat32, r.g.lab2, r.g.nv, r.g.ne};
     p.stride = o->walk_length + 1;
     p.target = target_steps(m, o);
     p.seed_lo = (uint32_t)o->seed;

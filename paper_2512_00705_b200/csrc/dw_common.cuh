@@ -105,6 +105,10 @@ struct DevGraph {
     const double2* __restrict__ lagg;     // per-node {label MAX, label SUM} or null (DSL)
     const uint32_t* __restrict__ twin;    // slim layout: return-edge range per edge, or null
     const FatRec32* __restrict__ fat32;   // compact fat records, or null
+    // labels packed 2 bits each (16 per word) when every label is < 4, or
+    // null: L2-resident at config-3 sizes (E/4 bytes), they let a MetaPath
+    // trial be judged on its label before its record is gathered
+    const uint32_t* __restrict__ lab2;
     uint32_t nv;
     unsigned long long ne;
 };

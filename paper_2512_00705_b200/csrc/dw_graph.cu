@@ -413,8 +413,55 @@ cudaError_t pack_graph(const ull* d_row, const uint32_t* d_col, const float* d_p
     return build_member_index(g, s);
 }
 
+__global__ void label_max_kernel(const uint16_t* __restrict__ label, ull ne,
+                                 unsigned* __restrict__ mx) {
+    unsigned m = 0;
+    for (ull i = blockIdx.x * (ull)blockDim.x + threadIdx.x; i < ne; i += (ull)gridDim.x * blockDim.x)
+        m = max(m, (unsigned)label[i]);
+    m = __reduce_max_sync(0xFFFFFFFFu, m);
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(mx, m);
+}
+
+__global__ void label_pack_kernel(const uint16_t* __restrict__ label, ull ne,
+                                  uint32_t* __restrict__ out, ull nw) {
+    for (ull w = blockIdx.x * (ull)blockDim.x + threadIdx.x; w < nw; w += (ull)gridDim.x * blockDim.x) {
+        uint32_t v = 0;
+        for (uint32_t k = 0; k < 16; ++k) {
+            const ull e = w * 16 + k;
+            if (e < ne) v |= ((uint32_t)label[e] & 3u) << (2 * k);
+        }
+        out[w] = v;
+    }
+}
+
+// Labels packed 2 bits per edge when every label is < 4 (DevGraph::lab2).
+// DW_LAB2=0 disables it.
+static cudaError_t build_lab2(DeviceGraphBuffers& g, cudaStream_t s) {
+    g.lab2 = nullptr;
+    if (!g.labels || g.ne == 0) return cudaSuccess;
+    if (const char* env = getenv("DW_LAB2"))
+        if (env[0] == '0') return cudaSuccess;
+    unsigned* d_mx = nullptr;
+    DW_TRY(cudaMallocAsync(&d_mx, sizeof(unsigned), s));
+    DW_TRY(cudaMemsetAsync(d_mx, 0, sizeof(unsigned), s));
+    label_max_kernel<<<grid_for(g.ne, 256) < 4096 ? grid_for(g.ne, 256) : 4096, 256, 0, s>>>(
+        g.labels, g.ne, d_mx);
+    unsigned mx = 0;
+    DW_TRY(cudaMemcpyAsync(&mx, d_mx, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    DW_TRY(cudaStreamSynchronize(s));
+    DW_TRY(cudaFreeAsync(d_mx, s));
+    if (mx >= 4) return cudaSuccess;
+    const ull nw = (g.ne + 15) / 16;
+    DW_TRY(cudaMallocAsync(&g.lab2, nw * sizeof(uint32_t), s));
+    label_pack_kernel<<<grid_for(nw, 256) < 8192 ? grid_for(nw, 256) : 8192, 256, 0, s>>>(
+        g.labels, g.ne, g.lab2, nw);
+    DW_TRY(cudaGetLastError());
+    return cudaStreamSynchronize(s);
+}
+
 cudaError_t finish_graph(DeviceGraphBuffers& g, cudaStream_t s) {
     DW_TRY(build_fat(g, s));
+    DW_TRY(build_lab2(g, s));
     return build_twin(g, s);
 }
 
@@ -821,7 +868,7 @@ __global__ void probe_pass_kernel(DevGraph g, __grid_constant__ const ModelParam
 template <class M>
 static cudaError_t calibrate_t(const DeviceGraphBuffers& gb, const ModelParams& mp,
                                const ProfileSpec& cfg, cudaStream_t s, double* ratio) {
-    DevGraph g{gb.nodes, gb.edges, gb.labels, gb.hslots, gb.fat, gb.lagg, gb.twin, gb.fat32,
+    DevGraph g{gb.nodes, gb.edges, gb.labels, gb.hslots, gb.fat, gb.lagg, gb.twin, gb.fat32, gb.lab2,
                gb.nv, gb.ne};
     // the probe set of one round (cost_model.cpp:45-54): ceil(fraction * nv),
     // at least min_nodes; the pool holds kPoolRounds such sets (capped at the

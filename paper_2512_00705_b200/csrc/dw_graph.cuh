@@ -14,6 +14,7 @@ struct DeviceGraphBuffers {
     uint32_t* twin = nullptr;    // slim layout: per edge (v -> u), v's range in N(u)
                                  // (lo | cnt << 24; cnt 255 = unknown), or null
     double2* lagg = nullptr;     // per-node label MAX/SUM, built on first DSL use
+    uint32_t* lab2 = nullptr;    // labels packed 2 bits each when all are < 4, or null
     unsigned long long nbuckets = 0;
     uint32_t nv = 0;
     unsigned long long ne = 0;

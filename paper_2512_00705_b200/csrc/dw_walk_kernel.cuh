@@ -190,43 +190,154 @@ __device__ __forceinline__ double ervs_weight(const M& m, const Step& S, const D
     return member(g, S.prev_degree, phoff, u) ? wc.w_in : wc.w_out;
 }
 
-// Neighbours i0 and i0 + 1 of the row at `begin` (ids, props, labels); ids of
-// neighbours past the row are kInvalid.
-struct EPair {
-    uint32_t u0, u1;
-    float h0, h1;
-    uint32_t lab;  // label(i0) | label(i0 + 1) << 16
+// Membership from prev's side (graph.cpp:114-118 has_edge, answered for a
+// whole row at once).  When prev has at most kCorrMaxPrev distinct
+// neighbours, each lane takes up to kCorrPerLane of them from prev's hash
+// set (its slots hold exactly the slice's distinct targets, dw_member.cuh)
+// and binary-searches each in cur's sorted row for the range of positions
+// with that target.  A chunk's "in N(prev)" bits are then the union of the
+// ranges that overlap it (two redux.sync ORs) instead of one hash probe per
+// neighbour; the answers are identical.
+constexpr uint32_t kCorrPerLane = 2;
+constexpr uint32_t kCorrMaxPrev = 16 * kCorrPerLane;  // hash set of <= 32 * kCorrPerLane slots
+#ifndef DW_CORR_MIN_DEG
+#define DW_CORR_MIN_DEG 512
+#endif
+struct CorrRanges {
+    uint32_t lo[kCorrPerLane], hi[kCorrPerLane];  // neighbour index ranges in cur's row
 };
-template <class M>
-__device__ __forceinline__ EPair ervs_load_pair(const DevGraph& g, ull begin, uint32_t i0,
-                                                uint32_t d) {
-    EPair r{kInvalid, kInvalid, 0.f, 0.f, 0u};
-    if (i0 >= d) return r;
-    const ull e = begin + i0;
-    if (!(begin & 1)) {  // 16 B aligned pair (edge arrays are padded to even length)
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(g.edges + e));
-        r.u0 = v.x;
-        r.h0 = __uint_as_float(v.y);
-        if (i0 + 1 < d) {
-            r.u1 = v.z;
-            r.h1 = __uint_as_float(v.w);
-        }
-        if (M::kUsesLabels && g.labels) r.lab = __ldg(reinterpret_cast<const uint32_t*>(g.labels + e));
-    } else {
-        const EdgeRec a = load_edge(g.edges + e);
-        r.u0 = a.col;
-        r.h0 = a.h;
-        if (M::kUsesLabels && g.labels) r.lab = __ldg(g.labels + e);
-        if (i0 + 1 < d) {
-            const EdgeRec b = load_edge(g.edges + e + 1);
-            r.u1 = b.col;
-            r.h1 = b.h;
-            if (M::kUsesLabels && g.labels) r.lab |= (uint32_t)__ldg(g.labels + e + 1) << 16;
-        }
+__device__ __forceinline__ CorrRanges corr_ranges(const DevGraph& g, ull begin, uint32_t d,
+                                                  uint32_t pdeg, uint32_t phoff) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t nslots = hash_buckets(pdeg) * 8u;
+    const uint32_t* hs = g.hslots + 8ull * phoff;
+    uint32_t v[kCorrPerLane];
+#pragma unroll
+    for (uint32_t k = 0; k < kCorrPerLane; ++k) {
+        const uint32_t sl = lane + 32u * k;
+        v[k] = sl < nslots ? __ldg(hs + sl) : kHashEmpty;
+    }
+    // branchless lower_bound of every v[k] in the row, all searches in step
+    uint32_t at[kCorrPerLane];
+#pragma unroll
+    for (uint32_t k = 0; k < kCorrPerLane; ++k) at[k] = 0;
+    for (uint32_t len = d; len > 1;) {
+        const uint32_t half = len >> 1;
+#pragma unroll
+        for (uint32_t k = 0; k < kCorrPerLane; ++k)
+            if (load_col(g.edges + begin + at[k] + half) < v[k]) at[k] += half;
+        len -= half;
+    }
+    CorrRanges r;
+#pragma unroll
+    for (uint32_t k = 0; k < kCorrPerLane; ++k) {
+        uint32_t lo = at[k];
+        if (lo < d && load_col(g.edges + begin + lo) < v[k]) ++lo;
+        uint32_t hi = lo;
+        if (v[k] != kHashEmpty)
+            while (hi < d && load_col(g.edges + begin + hi) == v[k]) ++hi;
+        r.lo[k] = lo;
+        r.hi[k] = hi;  // empty when v is not in the row (or the slot is empty)
     }
     return r;
 }
+// bits p of the chunk at aligned position `base` (neighbour base + p - off)
+// whose neighbour's target is in N(prev)
+__device__ __forceinline__ ull corr_chunk_mask(const CorrRanges& r, uint32_t base, uint32_t off,
+                                               uint32_t cbeg, uint32_t cend) {
+    ull m = 0;
+#pragma unroll
+    for (uint32_t k = 0; k < kCorrPerLane; ++k) {
+        const uint32_t lo = r.lo[k] > cbeg ? r.lo[k] : cbeg;
+        const uint32_t hi = r.hi[k] < cend ? r.hi[k] : cend;
+        if (lo < hi) {
+            const uint32_t a = lo + off - base, n = hi - lo;  // a + n <= 64
+            m |= (n >= 64 ? ~0ull : ((1ull << n) - 1ull)) << a;
+        }
+    }
+    const uint32_t mlo = __reduce_or_sync(kFull, (uint32_t)m);
+    const uint32_t mhi = __reduce_or_sync(kFull, (uint32_t)(m >> 32));
+    return (ull)mlo | ((ull)mhi << 32);
+}
 
+// The row is read as 16 B aligned pairs: aligned position q holds neighbour
+// q - off with off = begin & 1 (edge arrays are padded to even length, so the
+// last pair is in bounds).  Ids of positions outside the row are kInvalid.
+struct EPair {
+    uint32_t u0, u1;
+    float h0, h1;
+    uint32_t lab;  // label(q) | label(q + 1) << 16
+};
+__device__ __forceinline__ EPair ervs_pair(uint4 v, uint32_t lab, uint32_t i0, uint32_t d) {
+    EPair r{kInvalid, kInvalid, __uint_as_float(v.y), __uint_as_float(v.w), lab};
+    if (i0 < d) r.u0 = v.x;        // i0 = q - off wraps to 2^32 - 1 before the row
+    if (i0 + 1 < d) r.u1 = v.z;
+    return r;
+}
+template <class M>
+__device__ __forceinline__ EPair ervs_load_pair(const DevGraph& g, ull abase, uint32_t q,
+                                                uint32_t npos, uint32_t off, uint32_t d) {
+    const uint32_t i0 = q - off;
+    if (q >= npos) return EPair{kInvalid, kInvalid, 0.f, 0.f, 0u};
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(g.edges + abase + q));
+    uint32_t lab = 0;
+    if (M::kUsesLabels && g.labels) lab = __ldg(reinterpret_cast<const uint32_t*>(g.labels + abase + q));
+    return ervs_pair(v, lab, i0, d);
+}
+
+// ---- TMA (cp.async.bulk) staging of a row's chunks ------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(ull* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(ull* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+                 "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(ull* bar, uint32_t parity) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    } while (!done);
+}
+// bytes from global to this CTA's shared memory, completion counted on bar
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, ull* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+// order this thread's earlier generic shared-memory accesses before later
+// async-proxy (bulk copy) writes to the same bytes
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+// A warp's bulk-copy ring: kTmaStages chunks of 64 neighbours (512 B) in
+// flight, each landing in its own shared-memory stage and counted on its own
+// mbarrier; parity bits persist across calls (the ring is reused by every
+// long row the warp scans).
+constexpr uint32_t kTmaStages = 3;
+struct TmaRing {
+    uint4* stage[kTmaStages];  // 32 x 16 B each
+    ull* bar;                  // [kTmaStages]
+    uint32_t* parity;          // bit s: parity of stage s's next completion
+};
+
+#ifndef DW_LAB_SCREEN
+#define DW_LAB_SCREEN 1
+#endif
+// models whose weight is h when the edge label equals schema[step] and 0
+// otherwise (MetaPath, models.hpp:95-118): their trials can be screened on
+// the packed labels
+template <class M> struct LabelScreen { static constexpr bool value = false; };
+template <bool W> struct LabelScreen<MetaPathModel<W>> { static constexpr bool value = true; };
+#ifndef DW_ERVS_TMA
+#define DW_ERVS_TMA 1  // reservoir-only modes stage long rows through a bulk-copy ring
+#endif
 #ifndef DW_ERVS_SEQ
 #define DW_ERVS_SEQ 0  // 1: the round-1 sequential shuffle chain (A/B experiments)
 #endif
@@ -271,15 +382,20 @@ __device__ __forceinline__ ErvsBound ervs_bound(uint32_t m, double slack) {
     return ErvsBound{1.1 * u * (3.0 * (double)m + 8.0) * slack, ((double)m + 16.0) * 0x1.0p-1060};
 }
 
-template <class M, bool NOJUMP>
+template <class M, bool NOJUMP, bool TMA>
 __device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const WalkerKey key,
-                                      const PhiloxKeys& rk,
-                                      const DevGraph& g, ull begin, uint32_t phoff, ull idx0,
-                                      uint32_t* next, uint32_t* nidx, ull* draws) {
+                                         const PhiloxKeys& rk,
+                                         const DevGraph& g, ull begin, uint32_t phoff, ull idx0,
+                                         uint32_t* next, uint32_t* nidx, ull* draws,
+                                         const TmaRing& ring) {
     M m(mp);
     m.prepare(S);
     const int lane = threadIdx.x & 31;
     const uint32_t d = S.degree;
+    const uint32_t off = (uint32_t)(begin & 1);
+    const ull abase = begin - off;               // 16 B aligned start of the row
+    const uint32_t npos = (d + off + 1) & ~1u;   // aligned positions covering the row
+    const uint32_t nch = (npos + 63) / 64;
     ull idx = idx0;                // next draw (warp-uniform)
     double bkey = -DBL_MAX;        // best log key
     uint32_t best = kInvalid, bi = 0;
@@ -288,30 +404,98 @@ __device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const Wa
     bool have = false;
     double s = 0.0, s0 = 0.0;
     uint32_t seg = 0;
-    EPair nx = ervs_load_pair<M>(g, begin, 2u * lane, d);
-    for (uint32_t base = 0; base < d; base += 64) {
-        const uint32_t i0 = base + 2u * lane;
-        const EPair cp = nx;
-        if (base + 64 < d) nx = ervs_load_pair<M>(g, begin, i0 + 64, d);
+    int status = 0;
+    // chunk c = aligned positions [64c, 64c + 64): bytes of its bulk copy
+    auto chunk_bytes = [&](uint32_t c) { return min(64u, npos - 64u * c) * 8u; };
+    // membership from prev's side for long rows and a small prev
+    const bool corr = M::kSecondOrder && !M::kUsesLabels && S.prev != kInvalid &&
+                      d >= DW_CORR_MIN_DEG && S.prev_degree <= kCorrMaxPrev;
+    CorrRanges cr{};
+    if (M::kSecondOrder && corr) cr = corr_ranges(g, begin, d, S.prev_degree, phoff);
+    uint32_t par = 0;
+    EPair nx{};
+    if (TMA) {
+        par = *ring.parity;
+        if (lane == 0) {
+            fence_proxy_async();
+            for (uint32_t c = 0; c < kTmaStages && c < nch; ++c) {
+                mbar_expect_tx(&ring.bar[c], chunk_bytes(c));
+                bulk_g2s(ring.stage[c], g.edges + abase + 64ull * c, chunk_bytes(c), &ring.bar[c]);
+            }
+        }
+    } else {
+        nx = ervs_load_pair<M>(g, abase, 2u * lane, npos, off, d);
+    }
+    uint32_t c = 0;
+    for (; c < nch; ++c) {
+        const uint32_t base = 64u * c;           // aligned position of the chunk
+        const uint32_t q = base + 2u * lane;
+        const uint32_t i0 = q - off;             // this lane's first neighbour
+        EPair cp;
+        if (TMA) {
+            const uint32_t st = c % kTmaStages;
+            mbar_wait(&ring.bar[st], (par >> st) & 1u);
+            par ^= 1u << st;
+            const uint4 v = ring.stage[st][lane];
+            cp = q < npos ? ervs_pair(v, 0u, i0, d) : EPair{kInvalid, kInvalid, 0.f, 0.f, 0u};
+            __syncwarp();
+            if (lane == 0 && c + kTmaStages < nch) {  // refill the stage just read
+                fence_proxy_async();
+                mbar_expect_tx(&ring.bar[st], chunk_bytes(c + kTmaStages));
+                bulk_g2s(ring.stage[st], g.edges + abase + 64ull * (c + kTmaStages),
+                         chunk_bytes(c + kTmaStages), &ring.bar[st]);
+            }
+        } else {
+            cp = nx;
+            if (base + 64 < npos) nx = ervs_load_pair<M>(g, abase, q + 64, npos, off, d);
+        }
         double w0 = 0.0, w1 = 0.0;
-        if (cp.u0 != kInvalid) w0 = ervs_weight(m, S, g, phoff, cp.u0, cp.h0, (uint16_t)cp.lab);
-        if (cp.u1 != kInvalid) w1 = ervs_weight(m, S, g, phoff, cp.u1, cp.h1, (uint16_t)(cp.lab >> 16));
-        if (__any_sync(kFull, (cp.u0 != kInvalid && !valid_w(w0)) ||
-                                  (cp.u1 != kInvalid && !valid_w(w1))))
-            return -kDevBadWeight;
+        if (M::kSecondOrder && corr) {
+            const uint32_t cb = base > off ? base - off : 0u;
+            const uint32_t ce = base + 64 - off < d ? base + 64 - off : d;
+            const ull inm = corr_chunk_mask(cr, base, off, cb, ce) >> (2u * lane);
+            if (cp.u0 != kInvalid) {
+                const WeightCase wc = m.weight(S, cp.u0, cp.h0, 0);
+                w0 = !wc.needs_member ? wc.w : ((inm & 1u) ? wc.w_in : wc.w_out);
+            }
+            if (cp.u1 != kInvalid) {
+                const WeightCase wc = m.weight(S, cp.u1, cp.h1, 0);
+                w1 = !wc.needs_member ? wc.w : ((inm & 2u) ? wc.w_in : wc.w_out);
+            }
+        } else {
+            if (cp.u0 != kInvalid) w0 = ervs_weight(m, S, g, phoff, cp.u0, cp.h0, (uint16_t)cp.lab);
+            if (cp.u1 != kInvalid) w1 = ervs_weight(m, S, g, phoff, cp.u1, cp.h1, (uint16_t)(cp.lab >> 16));
+        }
+        // weights valid by construction (mp.pos_weights) need no vote
+        if (!mp.pos_weights &&
+            __any_sync(kFull, (cp.u0 != kInvalid && !valid_w(w0)) ||
+                                  (cp.u1 != kInvalid && !valid_w(w1)))) {
+            status = -kDevBadWeight;
+            break;
+        }
         if (NOJUMP) {
             double lk = -DBL_MAX;
             uint32_t src = kInvalid, cand = kInvalid;
-            if (cp.u0 != kInvalid) {
-                const U4 blk = philox4x32_10_rk(
-                    U4{(uint32_t)((idx0 + i0) >> 1), key.step, key.q0, key.q1}, rk);
-                if (w0 != 0.0) {
-                    lk = log(open01(lo64(blk))) / w0;
+            if (cp.u0 != kInvalid || cp.u1 != kInvalid) {
+                // draws idx0 + i0 and idx0 + i0 + 1: one Philox block when
+                // idx0 + i0 is even (idx0 is even: rows starting on an even edge)
+                const ull da = idx0 + i0;
+                const U4 blk = philox4x32_10_rk(U4{(uint32_t)(da >> 1), key.step, key.q0, key.q1}, rk);
+                ull r0, r1;
+                if (!(da & 1)) {
+                    r0 = lo64(blk);
+                    r1 = hi64(blk);
+                } else {
+                    r0 = hi64(blk);
+                    r1 = lo64(philox4x32_10_rk(U4{(uint32_t)((da + 1) >> 1), key.step, key.q0, key.q1}, rk));
+                }
+                if (cp.u0 != kInvalid && w0 != 0.0) {
+                    lk = log(open01(r0)) / w0;
                     src = i0;
                     cand = cp.u0;
                 }
                 if (cp.u1 != kInvalid && w1 != 0.0) {
-                    const double l1 = log(open01(hi64(blk))) / w1;
+                    const double l1 = log(open01(r1)) / w1;
                     if (src == kInvalid || l1 > lk) {
                         lk = l1;
                         src = i0 + 1;
@@ -320,10 +504,10 @@ __device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const Wa
                 }
             }
 #pragma unroll
-            for (int off = 16; off; off >>= 1) {
-                const double olk = __shfl_xor_sync(kFull, lk, off);
-                const uint32_t osrc = __shfl_xor_sync(kFull, src, off);
-                const uint32_t ocand = __shfl_xor_sync(kFull, cand, off);
+            for (int o = 16; o; o >>= 1) {
+                const double olk = __shfl_xor_sync(kFull, lk, o);
+                const uint32_t osrc = __shfl_xor_sync(kFull, src, o);
+                const uint32_t ocand = __shfl_xor_sync(kFull, cand, o);
                 const bool take = osrc != kInvalid &&
                                   (src == kInvalid || olk > lk || (olk == lk && osrc < src));
                 if (take) {
@@ -339,19 +523,22 @@ __device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const Wa
             }
             continue;
         }
-        const uint32_t cend = base + 64 < d ? base + 64 : d;
+        // neighbours [cbeg, cend) are this chunk's
+        const uint32_t cbeg = base > off ? base - off : 0u;
+        const uint32_t cend = base + 64 - off < d ? base + 64 - off : d;
+        // the lane that holds neighbour i, and which half
+        auto owner = [&](uint32_t i) { return (int)((i + off - base) >> 1); };
+        auto odd = [&](uint32_t i) { return ((i + off - base) & 1u) != 0; };
 #if DW_ERVS_SEQ
         {
-            const uint32_t n = cend - base;
-            for (uint32_t j = 0; j < n; ++j) {
-                const uint32_t l = j >> 1;
-                const double wj = __shfl_sync(kFull, (j & 1) ? w1 : w0, l);
-                const uint32_t uj = __shfl_sync(kFull, (j & 1) ? cp.u1 : cp.u0, l);
+            for (uint32_t j = cbeg; j < cend; ++j) {
+                const double wj = __shfl_sync(kFull, odd(j) ? w1 : w0, owner(j));
+                const uint32_t uj = __shfl_sync(kFull, odd(j) ? cp.u1 : cp.u0, owner(j));
                 if (wj == 0.0) continue;
                 if (best == kInvalid) {
                     bkey = log(open01(walker_draw(key, rk, idx++))) / wj;
                     best = uj;
-                    bi = base + j;
+                    bi = j;
                     continue;
                 }
                 if (!have) {
@@ -366,7 +553,7 @@ __device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const Wa
                     if (lk > bkey) {
                         bkey = lk;
                         best = uj;
-                        bi = base + j;
+                        bi = j;
                     }
                     have = false;
                 }
@@ -374,7 +561,7 @@ __device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const Wa
             continue;
         }
 #endif
-        uint32_t pos = base;  // first neighbour of the chunk not yet consumed
+        uint32_t pos = cbeg;  // first neighbour of the chunk not yet consumed
         for (;;) {
             if (!have) {
                 // the next positive weight: the first key, or the next threshold
@@ -404,9 +591,9 @@ __device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const Wa
             const double p1 = x0 + x1;
             double inc = p1;
 #pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const double t = __shfl_up_sync(kFull, inc, off);
-                if (lane >= off) inc += t;
+            for (int o = 1; o < 32; o <<= 1) {
+                const double t = __shfl_up_sync(kFull, inc, o);
+                if (lane >= o) inc += t;
             }
             double exc = __shfl_up_sync(kFull, inc, 1);
             if (lane == 0) exc = 0.0;
@@ -442,10 +629,8 @@ __device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const Wa
                 }
             }
             // replacement at `cross` (samplers.hpp:90-99)
-            const int ol = (int)((cross - base) >> 1);
-            const bool odd = (cross - base) & 1;
-            const double wj = __shfl_sync(kFull, odd ? w1 : w0, ol);
-            const uint32_t uj = __shfl_sync(kFull, odd ? cp.u1 : cp.u0, ol);
+            const double wj = __shfl_sync(kFull, odd(cross) ? w1 : w0, owner(cross));
+            const uint32_t uj = __shfl_sync(kFull, odd(cross) ? cp.u1 : cp.u0, owner(cross));
             const double floor_u = exp(wj * bkey);
             const double uu = floor_u + open01(walker_draw(key, rk, idx++)) * (1.0 - floor_u);
             const double lk = log(uu) / wj;
@@ -458,15 +643,25 @@ __device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const Wa
             pos = cross + 1;
         }
     }
+    if (TMA) {
+        // drain the copies still in flight (an early exit leaves up to
+        // kTmaStages - 1 of them), so the stages and parities stay consistent
+        for (uint32_t k = c + 1; k < nch && k <= c + kTmaStages; ++k) {
+            const uint32_t st = k % kTmaStages;
+            mbar_wait(&ring.bar[st], (par >> st) & 1u);
+            par ^= 1u << st;
+        }
+        __syncwarp();
+        if (lane == 0) *ring.parity = par;
+        __syncwarp();
+    }
+    if (status) return status;
     *next = best;
     *nidx = bi;
     *draws = NOJUMP ? (ull)d : idx - idx0;
     return 0;
 }
 
-// Out of line for the modes in which whole-row scans are rare (adaptive,
-// force-erjs: cap fallbacks and adaptive eRVS decisions on rows of >= 64):
-// keeps the eRJS loop's instruction footprint (icache)
 #ifndef DW_PR2_PAR
 #define DW_PR2_PAR 1
 #endif
@@ -478,7 +673,8 @@ __device__ __noinline__ int ervs_warp_cold(const ModelParams& mp, Step S, const 
                                            const PhiloxKeys& rk, const DevGraph& g, ull begin,
                                            uint32_t phoff, ull idx0, uint32_t* next,
                                            uint32_t* nidx, ull* draws) {
-    return ervs_warp<M, NOJUMP>(mp, S, key, rk, g, begin, phoff, idx0, next, nidx, draws);
+    return ervs_warp<M, NOJUMP, false>(mp, S, key, rk, g, begin, phoff, idx0, next, nidx, draws,
+                                       TmaRing{});
 }
 
 // Round-1 warp form: 32 neighbours per chunk and the jump chain run
@@ -695,6 +891,10 @@ struct WalkSmem {
     ull cnt[kCNum];
     uint32_t hist[66];
     ull lct[LC_NUM];                 // block totals of the lane counters
+    // reservoir-only modes: each warp's bulk-copy ring (ervs_warp, TmaRing);
+    // its stages are the warp's part of ring slot 0, idle in those modes
+    ull mbar[kThreads / 32][kTmaStages];
+    uint32_t tmaph[kThreads / 32];
 };
 
 // reservoir-only modes (force-ervs, ervs-nojump) spend their time in the
@@ -708,6 +908,11 @@ __global__ void __launch_bounds__(kThreads, (MODE == kForceErvs || MODE == kErvs
                                                 ? DW_ERVS_MIN_BLOCKS : DW_MIN_BLOCKS)
     walk_kernel(const __grid_constant__ WalkParams p) {
     constexpr bool kNoJump = MODE == kErvsNoJump;
+    // MetaPath trials judged on a packed label first (DevGraph::lab2); the
+    // label batch lives in mb (count | consumed << 4), its positions in sel
+    constexpr bool kLabScreen = DW_LAB_SCREEN && LabelScreen<M>::value && FAT == 1 &&
+                                (MODE == kAdaptive || MODE == kForceErjs);
+    constexpr uint32_t kLabBatch = 4;
     constexpr bool kSO = M::kSecondOrder;
     // dynamic shared memory (WalkSmem): may exceed the 48 KB static limit
     extern __shared__ __align__(16) unsigned char dsm[];
@@ -728,6 +933,13 @@ __global__ void __launch_bounds__(kThreads, (MODE == kForceErvs || MODE == kErvs
     for (int c = 0; c < LC_NUM64; ++c) s_lc[c][tid] = 0;
 #pragma unroll
     for (int c = 0; c < LC_NUM - LC_NUM64; ++c) sm.lc32[c][tid] = 0;
+    constexpr bool kTma = DW_ERVS_TMA && (MODE == kForceErvs || MODE == kErvsNoJump) &&
+                          !M::kUsesLabels && !M::kLabelAgg;
+    if (kTma && (tid & 31) == 0) {
+        for (uint32_t k = 0; k < kTmaStages; ++k) mbar_init(&sm.mbar[tid >> 5][k]);
+        sm.tmaph[tid >> 5] = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
     __syncthreads();
     // lane counters: LC_* accumulate per lane in shared memory
     auto lc_add = [&](int c, ull v) {
@@ -993,9 +1205,49 @@ __global__ void __launch_bounds__(kThreads, (MODE == kForceErvs || MODE == kErvs
                 }
                 ++tn;
             };
+            if (kLabScreen && g.lab2) {
+                // label screen (MetaPath): the previous iteration fetched the
+                // packed label words of a batch of trials; a trial whose edge
+                // label is not schema[step] has weight 0 (models.hpp:105-110)
+                // and is rejected without gathering its record, the others
+                // are regenerated and queued in trial order
+                const uint32_t want = p.mp.schema[step];
+                uint32_t lbn = mb & 7u, lbk = (mb >> 4) & 7u;
+                const uint32_t* lw = reinterpret_cast<const uint32_t*>(&s_mb[0][tid]);
+                while (lbk < lbn && rc < kRing) {
+                    const uint32_t t = tn - lbn + lbk;
+                    const uint32_t lab = (lw[lbk] >> (2u * ((sel >> (4u * lbk)) & 15u))) & 3u;
+                    if (lab == want) {
+                        const U4 b = philox4x32_10_rk(U4{t, step, (uint32_t)q, (uint32_t)(q >> 32)}, p.rk);
+                        const uint32_t x = (uint32_t)bounded(lo64(b), deg);
+                        const uint32_t k = (rh + rc) & (kRing - 1);
+                        s_y[k][tid] = uniform01(hi64(b)) * bound_r;
+                        s_t[k][tid] = t;
+                        const uint4* r = reinterpret_cast<const uint4*>(g.fat + begin + x);
+                        cp16(&s_rec[k][0][tid], r);
+                        cp16(&s_rec[k][1][tid], r + 1);
+                        cp16(&s_rec[k][2][tid], r + 2);
+                        ++rc;
+                    }
+                    ++lbk;
+                }
+                if (lbk == lbn) {  // the next batch of label probes
+                    lbn = lbk = 0;
+                    sel = 0;
+#pragma unroll 1
+                    for (; lbn < kLabBatch && tn < cap_r; ++lbn, ++tn) {
+                        const U4 b = philox4x32_10_rk(U4{tn, step, (uint32_t)q, (uint32_t)(q >> 32)}, p.rk);
+                        const ull e = begin + (uint32_t)bounded(lo64(b), deg);
+                        cp4(reinterpret_cast<uint32_t*>(&s_mb[0][tid]) + lbn, g.lab2 + (e >> 4));
+                        sel |= (uint32_t)(e & 15u) << (4u * lbn);
+                    }
+                }
+                mb = lbn | (lbk << 4);
+            } else {
 #pragma unroll 1
             for (uint32_t gen = 0; gen < kGen && rc < kRing && tn < cap_r; ++gen) {
                 trial(philox4x32_10_rk(U4{tn, step, (uint32_t)q, (uint32_t)(q >> 32)}, p.rk));
+            }
             }
         }
         if (ph0 == P_NODE) {
@@ -1117,7 +1369,8 @@ __global__ void __launch_bounds__(kThreads, (MODE == kForceErvs || MODE == kErvs
                         next_u = ((sel >> acc) & 1) ? v0.z : v0.x;
                         twe() = begin + s_rec[acc][1][tid].y;
                     }
-                } else if (!(mb & kParked) && rc == 0 && tn >= cap) {
+                } else if (!(mb & kParked) && rc == 0 && tn >= cap &&
+                           (!kLabScreen || (mb & 7u) == ((mb >> 4) & 7u))) {
                     count_erjs(tn);
                     lc_add(LC_FALLBACKS, 1);  // cap overrun -> reservoir, same stream
                     start_ervs(2ull * tn);
@@ -1417,8 +1670,13 @@ __global__ void __launch_bounds__(kThreads, (MODE == kForceErvs || MODE == kErvs
             uint32_t nx = kInvalid, ni = 0;
             ull dr = 0;
             int st;
-            if constexpr (MODE == kForceErvs || MODE == kErvsNoJump)
-                st = ervs_warp<M, kNoJump>(p.mp, T, K, p.rk, g, tb, tph, db, &nx, &ni, &dr);
+            if constexpr (MODE == kForceErvs || MODE == kErvsNoJump) {
+                const int w = tid >> 5;
+                const TmaRing ring{{&sm.rec[0][0][w * 32], &sm.rec[0][1][w * 32], &sm.rec[0][2][w * 32]},
+                                   sm.mbar[w], &sm.tmaph[w]};
+                st = ervs_warp<M, kNoJump, kTma>(p.mp, T, K, p.rk, g, tb, tph, db, &nx, &ni, &dr,
+                                                 ring);
+            }
             else if constexpr (DW_PR2_PAR && CoopErjs<M>::value)  // PR2: cap overruns, hand-offs
                 st = ervs_warp_cold<M, kNoJump>(p.mp, T, K, p.rk, g, tb, tph, db, &nx, &ni, &dr);
             else

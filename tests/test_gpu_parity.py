@@ -581,15 +581,20 @@ def test_pr2_pareto_cooperative_erjs(dw, orc, mode, fat):
 
 def _hub_graph(orc, n=120_000, seed=31):
     """Hubs far above one warp chunk: node 0 joined to every node, node 1 to
-    every 3rd, node 2 to every 7th, plus a ring; mirrored, Philox weights."""
+    every 3rd, node 2 to every 7th, the hubs joined to each other, plus a ring
+    and random chords; mirrored, Philox weights.  A hub scan's prev is a small
+    node (membership from prev's side, corr_ranges) or another hub (hash
+    probes)."""
     rng = np.random.default_rng(seed)
     v = np.arange(3, n, dtype=np.uint32)
     src = np.concatenate([np.zeros(n - 3, np.uint32), np.ones(len(v[::3]), np.uint32),
                           np.full(len(v[::7]), 2, np.uint32), v[:-1]])
     dst = np.concatenate([v, v[::3], v[::7], v[1:]])
     extra = rng.integers(3, n, size=(2, n), dtype=np.uint32)  # a few random chords
-    src = np.concatenate([src, extra[0]])
-    dst = np.concatenate([dst, extra[1]])
+    # hub-hub edges (a hub's scan with a hub as prev: hash probes) and a
+    # multi-edge (one target repeated in a hub row)
+    src = np.concatenate([src, extra[0], np.array([0, 0, 1, 0, 0], np.uint32)])
+    dst = np.concatenate([dst, extra[1], np.array([1, 2, 2, 5, 5], np.uint32)])
     return orc.Graph.build(src, dst, mirror=True, nv_hint=n).synth_philox(
         "uniform", 1.0, 5.0, seed=seed + 1)
 
@@ -677,3 +682,25 @@ def test_libdevice_log_exp_against_host_libm(dw, orc):
         ulp = np.abs(yd[ok].view(np.int64) - yh[ok].view(np.int64))
         print(f"fn={fn} differ={np.count_nonzero(ulp) / ok.sum():.3e} max_ulp={ulp.max()}")
         assert ulp.max() <= 1
+
+
+@pytest.mark.parametrize("lab2", ["1", "0"], ids=["packed-labels", "no-screen"])
+@pytest.mark.parametrize("labels,schema", [((0, 3), (0, 1, 2, 3) * 20),
+                                           ((0, 3), (2, 0, 7, 1) * 10),
+                                           ((0, 5), (0, 4, 5, 1) * 20)],
+                         ids=["4-labels", "absent-label", "6-labels"])
+def test_metapath_label_screen(dw, orc, labels, schema, lab2):
+    """MetaPath trials are judged on a 2-bit packed label (DevGraph::lab2,
+    built when every label is < 4) before their record is gathered; a label
+    miss is a rejection with no gather.  Paths and counters equal the oracle
+    with the screen (packed labels), without it (DW_LAB2=0) and when labels
+    do not fit 2 bits (no packing), including a schema label that no edge
+    carries (dead rows)."""
+    og = orc.Graph.rmat(12, 16, 8).synth_philox("uniform", 1.0, 5.0, seed=9)
+    og.synth_philox("labels", labels[0], labels[1], seed=10)
+    dg = _with_env({"DW_LAB2": lab2, "DW_FAT": "1"}, lambda: to_device(dw, og))
+    q = np.arange(og.nv, dtype=np.uint32)
+    mk = dict(kind="metapath", schema=schema)
+    for mode in ("adaptive", "force-erjs"):
+        r_dev, r_orc = run_both(dw, orc, og, dg, mk, q, mode, len(schema), 1.2)
+        assert_same(r_dev, r_orc, (labels, schema, lab2, mode))
