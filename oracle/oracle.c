@@ -1018,14 +1018,13 @@ static outcome sample_ervs_nojump(ctx_t* c, const wstate* st, wrng* r) {
 /* Trial cap of an eRJS step: cap_per_degree * d (samplers.hpp:157), tightened
  * by the tier-2 hand-off when erjs_handoff > 0 (not in the reference; the
  * device rule of dw_walk_kernel.cuh step_cap, include/dynwalk_b200.h):
- * max(32, ceil(erjs_handoff / ratio * d)) trials, a ski-rental bound of the
- * rejection loop against one reservoir pass over the row. */
-static uint64_t erjs_cap(const orc_opts* o, uint32_t d) {
+ * max(32, ceil(erjs_handoff * d * bound / wsum)) trials, erjs_handoff times
+ * the trials the cost model expected from the model's estimators. */
+static uint64_t erjs_cap(const orc_opts* o, uint32_t d, double bound, double wsum) {
     uint64_t cap = o->cap_per_degree * d;
     if (o->erjs_handoff > 0.0) {
-        const double scale = o->erjs_handoff / o->edge_cost_ratio;
-        const double h = ceil(scale * (double)d);
-        uint64_t hc = h < 32.0 ? 32u : (h >= 4294967295.0 ? 0xFFFFFFFFu : (uint64_t)h);
+        const double h = ceil(o->erjs_handoff * ((double)d * bound / wsum));
+        const uint64_t hc = !(h >= 32.0) ? 32u : (h >= 4294967295.0 ? 0xFFFFFFFFu : (uint64_t)h);
         if (hc < cap) cap = hc;
     }
     return cap;
@@ -1111,7 +1110,7 @@ static int64_t walk_query(ctx_t* c, const orc_opts* o, uint32_t start, uint64_t 
             bucket(ls, d, erjs);
             if (erjs) {
                 ++ls->select_erjs;
-                out = sample_erjs(c, &st, r, est_max, erjs_cap(o, d));
+                out = sample_erjs(c, &st, r, est_max, erjs_cap(o, d, est_max, est_sum));
             } else {
                 ++ls->select_ervs;
                 out = sample_ervs(c, &st, r);
@@ -1132,7 +1131,8 @@ static int64_t walk_query(ctx_t* c, const orc_opts* o, uint32_t start, uint64_t 
             const double est = model_bound(c, &st);
             ++ls->select_erjs;
             bucket(ls, d, 1);
-            out = sample_erjs(c, &st, r, est, erjs_cap(o, d));
+            out = sample_erjs(c, &st, r, est,
+                              erjs_cap(o, d, est, o->erjs_handoff > 0.0 ? model_sum(c, &st) : 1.0));
             break;
         }
         default:

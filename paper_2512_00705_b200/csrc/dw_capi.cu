@@ -393,8 +393,6 @@ int check_opts(const dw_run_opts* o) {
     if (o->walk_length == 0xFFFFFFFFu) return fail(DW_EINVAL, "walk_length too large");
     if (!(o->erjs_handoff >= 0.0) || !std::isfinite(o->erjs_handoff))
         return fail(DW_EINVAL, "erjs_handoff must be >= 0 and finite");
-    if (o->erjs_handoff > 0.0 && (!(o->edge_cost_ratio > 0.0) || !std::isfinite(o->edge_cost_ratio)))
-        return fail(DW_EINVAL, "erjs_handoff needs a positive finite edge_cost_ratio");
     return DW_OK;
 }
 
@@ -417,7 +415,7 @@ dwb::WalkParams make_params(Replica& r, const dw_model_desc* m, const dw_run_opt
     p.rk = dwb::philox_keys(p.seed_lo, p.seed_hi);
     p.cap_per_degree = o->erjs_cap_per_degree;
     p.ratio = o->edge_cost_ratio;
-    p.handoff_scale = o->erjs_handoff > 0.0 ? o->erjs_handoff / o->edge_cost_ratio : 0.0;
+    p.handoff = o->erjs_handoff;
     p.counters = r.counters;
     p.error = r.error;
     p.error_info = r.error_info;

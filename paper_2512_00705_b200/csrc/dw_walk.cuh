@@ -32,7 +32,7 @@ struct WalkParams {
     PhiloxKeys rk;          // round keys of seed (dw_common.cuh philox_keys)
     unsigned long long cap_per_degree;
     double ratio;
-    double handoff_scale;   // tier-2 eRJS hand-off: erjs_handoff / ratio, or 0 (off)
+    double handoff;         // tier-2 eRJS hand-off (dw_run_opts.erjs_handoff), 0 = off
     unsigned long long* counters;     // [kCNum]
     unsigned long long* next_walker;  // queue head
     int* error;                       // first DevError

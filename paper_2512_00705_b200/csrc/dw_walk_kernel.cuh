@@ -190,74 +190,49 @@ __device__ __forceinline__ double ervs_weight(const M& m, const Step& S, const D
     return member(g, S.prev_degree, phoff, u) ? wc.w_in : wc.w_out;
 }
 
-// Membership from prev's side (graph.cpp:114-118 has_edge, answered for a
-// whole row at once).  When prev has at most kCorrMaxPrev distinct
-// neighbours, each lane takes up to kCorrPerLane of them from prev's hash
-// set (its slots hold exactly the slice's distinct targets, dw_member.cuh)
-// and binary-searches each in cur's sorted row for the range of positions
-// with that target.  A chunk's "in N(prev)" bits are then the union of the
-// ranges that overlap it (two redux.sync ORs) instead of one hash probe per
-// neighbour; the answers are identical.
-constexpr uint32_t kCorrPerLane = 2;
-constexpr uint32_t kCorrMaxPrev = 16 * kCorrPerLane;  // hash set of <= 32 * kCorrPerLane slots
-#ifndef DW_CORR_MIN_DEG
-#define DW_CORR_MIN_DEG 512
-#endif
-struct CorrRanges {
-    uint32_t lo[kCorrPerLane], hi[kCorrPerLane];  // neighbour index ranges in cur's row
+// Membership by merging cur's sorted row with prev's sorted row
+// (graph.cpp:114-118 has_edge, answered a chunk at a time).  The warp holds a
+// window of 32 of prev's neighbours (one coalesced 256 B load) and slides it
+// forward with the chunks: a chunk whose targets all lie below the window's
+// first id needs no test; otherwise each lane binary-searches its two targets
+// in the window with shuffles, and the window advances until it covers the
+// chunk's last target.  Over a row scan the window reads prev's row at most
+// once (plus one binary search to place it), instead of one hash-bucket
+// probe per neighbour; the answers are the same.  Used when prev's row begin
+// is known (the reservoir-only modes keep it per lane).
+constexpr ull kNoRow = ~0ull;
+struct PrevWindow {
+    ull pbegin;                 // prev's row
+    uint32_t pdeg;
+    uint32_t pp;                // window = prev's neighbours [pp, pp + 32)
+    uint32_t v;                 // this lane's entry (kInvalid past the row)
+    uint32_t vfirst, vlast;     // the window's first and last entries
 };
-__device__ __forceinline__ CorrRanges corr_ranges(const DevGraph& g, ull begin, uint32_t d,
-                                                  uint32_t pdeg, uint32_t phoff) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t nslots = hash_buckets(pdeg) * 8u;
-    const uint32_t* hs = g.hslots + 8ull * phoff;
-    uint32_t v[kCorrPerLane];
-#pragma unroll
-    for (uint32_t k = 0; k < kCorrPerLane; ++k) {
-        const uint32_t sl = lane + 32u * k;
-        v[k] = sl < nslots ? __ldg(hs + sl) : kHashEmpty;
-    }
-    // branchless lower_bound of every v[k] in the row, all searches in step
-    uint32_t at[kCorrPerLane];
-#pragma unroll
-    for (uint32_t k = 0; k < kCorrPerLane; ++k) at[k] = 0;
-    for (uint32_t len = d; len > 1;) {
+__device__ __forceinline__ void win_load(PrevWindow& w, const DevGraph& g) {
+    const uint32_t lane = threadIdx.x & 31;
+    w.v = w.pp + lane < w.pdeg ? load_col(g.edges + w.pbegin + w.pp + lane) : kInvalid;
+    w.vfirst = __shfl_sync(kFull, w.v, 0);
+    w.vlast = __shfl_sync(kFull, w.v, 31);
+}
+// place the window at the first of prev's neighbours >= u
+__device__ __forceinline__ void win_seek(PrevWindow& w, const DevGraph& g, uint32_t u) {
+    uint32_t at = 0;
+    for (uint32_t len = w.pdeg; len > 1;) {  // branchless lower_bound
         const uint32_t half = len >> 1;
-#pragma unroll
-        for (uint32_t k = 0; k < kCorrPerLane; ++k)
-            if (load_col(g.edges + begin + at[k] + half) < v[k]) at[k] += half;
+        if (load_col(g.edges + w.pbegin + at + half) < u) at += half;
         len -= half;
     }
-    CorrRanges r;
-#pragma unroll
-    for (uint32_t k = 0; k < kCorrPerLane; ++k) {
-        uint32_t lo = at[k];
-        if (lo < d && load_col(g.edges + begin + lo) < v[k]) ++lo;
-        uint32_t hi = lo;
-        if (v[k] != kHashEmpty)
-            while (hi < d && load_col(g.edges + begin + hi) == v[k]) ++hi;
-        r.lo[k] = lo;
-        r.hi[k] = hi;  // empty when v is not in the row (or the slot is empty)
-    }
-    return r;
+    if (w.pdeg && load_col(g.edges + w.pbegin + at) < u) ++at;
+    w.pp = at;
+    win_load(w, g);
 }
-// bits p of the chunk at aligned position `base` (neighbour base + p - off)
-// whose neighbour's target is in N(prev)
-__device__ __forceinline__ ull corr_chunk_mask(const CorrRanges& r, uint32_t base, uint32_t off,
-                                               uint32_t cbeg, uint32_t cend) {
-    ull m = 0;
+// is u one of the window's entries (sorted ascending)?
+__device__ __forceinline__ bool win_has(const PrevWindow& w, uint32_t u) {
+    uint32_t lo = 0;
 #pragma unroll
-    for (uint32_t k = 0; k < kCorrPerLane; ++k) {
-        const uint32_t lo = r.lo[k] > cbeg ? r.lo[k] : cbeg;
-        const uint32_t hi = r.hi[k] < cend ? r.hi[k] : cend;
-        if (lo < hi) {
-            const uint32_t a = lo + off - base, n = hi - lo;  // a + n <= 64
-            m |= (n >= 64 ? ~0ull : ((1ull << n) - 1ull)) << a;
-        }
-    }
-    const uint32_t mlo = __reduce_or_sync(kFull, (uint32_t)m);
-    const uint32_t mhi = __reduce_or_sync(kFull, (uint32_t)(m >> 32));
-    return (ull)mlo | ((ull)mhi << 32);
+    for (uint32_t step = 16; step; step >>= 1)
+        if (__shfl_sync(kFull, w.v, lo + step - 1) < u) lo += step;
+    return __shfl_sync(kFull, w.v, lo) == u;
 }
 
 // The row is read as 16 B aligned pairs: aligned position q holds neighbour
@@ -322,7 +297,9 @@ __device__ __forceinline__ void fence_proxy_async() {
 // long row the warp scans).
 constexpr uint32_t kTmaStages = 3;
 struct TmaRing {
-    uint4* stage[kTmaStages];  // 32 x 16 B each
+    uint4* stage0;             // stage s = stage0 + s * stride (32 x 16 B each)
+    uint32_t stride;           // in uint4 (no array: a dynamically indexed
+                               // pointer array would live in local memory)
     ull* bar;                  // [kTmaStages]
     uint32_t* parity;          // bit s: parity of stage s's next completion
 };
@@ -387,7 +364,7 @@ __device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const Wa
                                          const PhiloxKeys& rk,
                                          const DevGraph& g, ull begin, uint32_t phoff, ull idx0,
                                          uint32_t* next, uint32_t* nidx, ull* draws,
-                                         const TmaRing& ring) {
+                                         const TmaRing& ring, ull pbegin = kNoRow) {
     M m(mp);
     m.prepare(S);
     const int lane = threadIdx.x & 31;
@@ -407,11 +384,10 @@ __device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const Wa
     int status = 0;
     // chunk c = aligned positions [64c, 64c + 64): bytes of its bulk copy
     auto chunk_bytes = [&](uint32_t c) { return min(64u, npos - 64u * c) * 8u; };
-    // membership from prev's side for long rows and a small prev
-    const bool corr = M::kSecondOrder && !M::kUsesLabels && S.prev != kInvalid &&
-                      d >= DW_CORR_MIN_DEG && S.prev_degree <= kCorrMaxPrev;
-    CorrRanges cr{};
-    if (M::kSecondOrder && corr) cr = corr_ranges(g, begin, d, S.prev_degree, phoff);
+    // membership by merging with prev's sorted row when its begin is known
+    const bool merge = M::kSecondOrder && !M::kUsesLabels && S.prev != kInvalid &&
+                       pbegin != kNoRow && S.prev_degree > 0;
+    PrevWindow pw{pbegin, S.prev_degree, 0u, kInvalid, kInvalid, kInvalid};
     uint32_t par = 0;
     EPair nx{};
     if (TMA) {
@@ -420,7 +396,8 @@ __device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const Wa
             fence_proxy_async();
             for (uint32_t c = 0; c < kTmaStages && c < nch; ++c) {
                 mbar_expect_tx(&ring.bar[c], chunk_bytes(c));
-                bulk_g2s(ring.stage[c], g.edges + abase + 64ull * c, chunk_bytes(c), &ring.bar[c]);
+                bulk_g2s(ring.stage0 + c * ring.stride, g.edges + abase + 64ull * c, chunk_bytes(c),
+                         &ring.bar[c]);
             }
         }
     } else {
@@ -436,13 +413,13 @@ __device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const Wa
             const uint32_t st = c % kTmaStages;
             mbar_wait(&ring.bar[st], (par >> st) & 1u);
             par ^= 1u << st;
-            const uint4 v = ring.stage[st][lane];
+            const uint4 v = ring.stage0[st * ring.stride + lane];
             cp = q < npos ? ervs_pair(v, 0u, i0, d) : EPair{kInvalid, kInvalid, 0.f, 0.f, 0u};
             __syncwarp();
             if (lane == 0 && c + kTmaStages < nch) {  // refill the stage just read
                 fence_proxy_async();
                 mbar_expect_tx(&ring.bar[st], chunk_bytes(c + kTmaStages));
-                bulk_g2s(ring.stage[st], g.edges + abase + 64ull * (c + kTmaStages),
+                bulk_g2s(ring.stage0 + st * ring.stride, g.edges + abase + 64ull * (c + kTmaStages),
                          chunk_bytes(c + kTmaStages), &ring.bar[st]);
             }
         } else {
@@ -450,17 +427,35 @@ __device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const Wa
             if (base + 64 < npos) nx = ervs_load_pair<M>(g, abase, q + 64, npos, off, d);
         }
         double w0 = 0.0, w1 = 0.0;
-        if (M::kSecondOrder && corr) {
+        if (M::kSecondOrder && merge) {
+            // the chunk's targets span [ulo, uhi] (the row is sorted)
             const uint32_t cb = base > off ? base - off : 0u;
             const uint32_t ce = base + 64 - off < d ? base + 64 - off : d;
-            const ull inm = corr_chunk_mask(cr, base, off, cb, ce) >> (2u * lane);
+            const uint32_t lf = (cb + off - base) >> 1, ll = (ce - 1 + off - base) >> 1;
+            const uint32_t ulo = __shfl_sync(kFull, ((cb + off - base) & 1) ? cp.u1 : cp.u0, lf);
+            const uint32_t uhi = __shfl_sync(kFull, ((ce - 1 + off - base) & 1) ? cp.u1 : cp.u0, ll);
+            if (c == 0) win_seek(pw, g, ulo);
+            while (pw.vlast < ulo && pw.pp + 32 < pw.pdeg) {
+                pw.pp += 32;
+                win_load(pw, g);
+            }
+            bool in0 = false, in1 = false;
+            if (pw.vfirst <= uhi) {
+                for (;;) {
+                    in0 |= win_has(pw, cp.u0);
+                    in1 |= win_has(pw, cp.u1);
+                    if (pw.vlast >= uhi || pw.pp + 32 >= pw.pdeg) break;
+                    pw.pp += 32;
+                    win_load(pw, g);
+                }
+            }
             if (cp.u0 != kInvalid) {
                 const WeightCase wc = m.weight(S, cp.u0, cp.h0, 0);
-                w0 = !wc.needs_member ? wc.w : ((inm & 1u) ? wc.w_in : wc.w_out);
+                w0 = !wc.needs_member ? wc.w : (in0 ? wc.w_in : wc.w_out);
             }
             if (cp.u1 != kInvalid) {
                 const WeightCase wc = m.weight(S, cp.u1, cp.h1, 0);
-                w1 = !wc.needs_member ? wc.w : ((inm & 2u) ? wc.w_in : wc.w_out);
+                w1 = !wc.needs_member ? wc.w : (in1 ? wc.w_in : wc.w_out);
             }
         } else {
             if (cp.u0 != kInvalid) w0 = ervs_weight(m, S, g, phoff, cp.u0, cp.h0, (uint16_t)cp.lab);
@@ -478,16 +473,18 @@ __device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const Wa
             uint32_t src = kInvalid, cand = kInvalid;
             if (cp.u0 != kInvalid || cp.u1 != kInvalid) {
                 // draws idx0 + i0 and idx0 + i0 + 1: one Philox block when
-                // idx0 + i0 is even (idx0 is even: rows starting on an even edge)
-                const ull da = idx0 + i0;
-                const U4 blk = philox4x32_10_rk(U4{(uint32_t)(da >> 1), key.step, key.q0, key.q1}, rk);
-                ull r0, r1;
-                if (!(da & 1)) {
+                // i0 is valid and idx0 + i0 is even (idx0 is even: rows
+                // starting on an even edge); i0 wraps to 2^32 - 1 before
+                // the row, so each draw index is formed from its own element
+                const ull d0 = idx0 + (ull)i0, d1 = idx0 + (ull)(uint32_t)(i0 + 1u);
+                ull r0 = 0, r1;
+                if (cp.u0 != kInvalid && !(d0 & 1)) {
+                    const U4 blk = philox4x32_10_rk(U4{(uint32_t)(d0 >> 1), key.step, key.q0, key.q1}, rk);
                     r0 = lo64(blk);
                     r1 = hi64(blk);
                 } else {
-                    r0 = hi64(blk);
-                    r1 = lo64(philox4x32_10_rk(U4{(uint32_t)((da + 1) >> 1), key.step, key.q0, key.q1}, rk));
+                    if (cp.u0 != kInvalid) r0 = walker_draw(key, rk, d0);
+                    r1 = walker_draw(key, rk, d1);
                 }
                 if (cp.u0 != kInvalid && w0 != 0.0) {
                     lk = log(open01(r0)) / w0;
@@ -585,10 +582,25 @@ __device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const Wa
                 have = true;
                 pos = fe;
             }
-            // prefix sums of the weights from pos on (two per lane, then a
-            // Kogge-Stone warp scan)
             const double x0 = i0 >= pos ? w0 : 0.0, x1 = i0 + 1 >= pos ? w1 : 0.0;
             const double p1 = x0 + x1;
+            // The chain never increases (w >= 0), so a chunk whose last value
+            // is provably positive has no crossing: test that first with a
+            // butterfly sum (every term through <= 6 roundings), and run the
+            // per-neighbour scan only for the chunk that may cross.
+            if (s > 0.0 && s < DBL_MAX) {
+                double tot = p1;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(kFull, tot, o);
+                const ErvsBound eb = ervs_bound(cend - seg, mp.ervs_slack);
+                const double A = s - tot;
+                if (A > eb.k * (s0 + tot) + 1.1 * 0x1.0p-53 * fabs(A) + eb.lo) {
+                    s = A;
+                    break;
+                }
+            }
+            // prefix sums of the weights from pos on (two per lane, then a
+            // Kogge-Stone warp scan)
             double inc = p1;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -1092,13 +1104,15 @@ __global__ void __launch_bounds__(kThreads, (MODE == kForceErvs || MODE == kErvs
         phase = deg >= kCoopMinDegree ? P_COOP : P_VREC;
     };
     // trial cap of an eRJS step at cur (samplers.hpp:157), tightened by the
-    // tier-2 hand-off when enabled (dw_run_opts.erjs_handoff; oracle.c erjs_cap)
-    auto step_cap = [&]() -> uint32_t {
+    // tier-2 hand-off when enabled (dw_run_opts.erjs_handoff; oracle.c erjs_cap);
+    // needs the exact row sum (compact records refetch the node record)
+    auto step_cap = [&](const Step& S) -> uint32_t {
         const ull c = p.cap_per_degree * (ull)deg;
         uint32_t r = c > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)c;
-        if (p.handoff_scale > 0.0) {
-            const double h = ceil(p.handoff_scale * (double)deg);
-            const uint32_t hc = h < 32.0 ? 32u : (h >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)h);
+        if (p.handoff > 0.0) {
+            // handoff x the trials the cost model expected: d * bound / wsum
+            const double h = ceil(p.handoff * ((double)deg * bound / model.wsum(S)));
+            const uint32_t hc = !(h >= 32.0) ? 32u : (h >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)h);
             if (hc < r) r = hc;
         }
         return r;
@@ -1114,6 +1128,10 @@ __global__ void __launch_bounds__(kThreads, (MODE == kForceErvs || MODE == kErvs
     // slim layout: the edge the walker took, whose twin[] word comes with the
     // next node record (s_y[1] is idle between a step's end and its node gather)
     auto twe = [&]() -> ull& { return *reinterpret_cast<ull*>(&s_y[1][tid]); };
+    // reservoir-only modes: prev's row begin (the warp reservoir merges cur's
+    // row with prev's), in ring slot 0's y, idle in those modes
+    constexpr bool kPrevRow = (MODE == kForceErvs || MODE == kErvsNoJump) && M::kSecondOrder;
+    auto pbeg = [&]() -> ull& { return *reinterpret_cast<ull*>(&s_y[0][tid]); };
 
     for (;;) {
         // ---- refill idle lanes: one atomic per warp (runtime.cpp:209-211)
@@ -1459,6 +1477,7 @@ __global__ void __launch_bounds__(kThreads, (MODE == kForceErvs || MODE == kErvs
             // WalkerState::advance (walk_state.hpp:33-39)
             const uint4 v0 = s_rec[next_slot][0][tid];
             const uint32_t nx = next_ev == E_FAT ? v0.x : next_u;
+            if (kPrevRow) pbeg() = begin;
             prev = cur;
             pdeg = deg;
             phoff = hoff;
@@ -1558,6 +1577,8 @@ __global__ void __launch_bounds__(kThreads, (MODE == kForceErvs || MODE == kErvs
                     erjs = M::kBoundable;
                     if (erjs) bound = model.bound(S);
                 }
+                // tier-2 hand-off caps need the exact wsum (not the f32 row sum)
+                if (FAT == 2 && approx_sum && erjs && p.handoff > 0.0) need_node = true;
                 if (FAT == 2 && need_node) {
                     phase = P_NODE;  // the exact node record decides this step
                 } else {
@@ -1586,7 +1607,7 @@ __global__ void __launch_bounds__(kThreads, (MODE == kForceErvs || MODE == kErvs
                 if (dead_row) {
                     if (erjs) {
                         nret = 0;
-                        count_erjs(step_cap());
+                        count_erjs(step_cap(S));
                         lc_add(LC_FALLBACKS, 1);
                     } else {
                         lc_add(LC_ETRIALS1, 1);  // single-shot eRVS
@@ -1600,7 +1621,7 @@ __global__ void __launch_bounds__(kThreads, (MODE == kForceErvs || MODE == kErvs
                         fail(kDevBadBound);
                     } else {
                         mnr = shortcut ? model.nonreturn_max(S) : __longlong_as_double(0x7ff0000000000000ll);
-                        cap = step_cap();
+                        cap = step_cap(S);
                         tn = rh = rc = 0;
                         mb = nret = sel = 0;
                         phase = P_TRIAL;
@@ -1672,10 +1693,10 @@ __global__ void __launch_bounds__(kThreads, (MODE == kForceErvs || MODE == kErvs
             int st;
             if constexpr (MODE == kForceErvs || MODE == kErvsNoJump) {
                 const int w = tid >> 5;
-                const TmaRing ring{{&sm.rec[0][0][w * 32], &sm.rec[0][1][w * 32], &sm.rec[0][2][w * 32]},
-                                   sm.mbar[w], &sm.tmaph[w]};
+                const TmaRing ring{&sm.rec[0][0][w * 32], (uint32_t)kThreads, sm.mbar[w], &sm.tmaph[w]};
+                const ull tpb = kPrevRow ? __shfl_sync(kFull, pbeg(), L) : kNoRow;
                 st = ervs_warp<M, kNoJump, kTma>(p.mp, T, K, p.rk, g, tb, tph, db, &nx, &ni, &dr,
-                                                 ring);
+                                                 ring, T.prev != kInvalid ? tpb : kNoRow);
             }
             else if constexpr (DW_PR2_PAR && CoopErjs<M>::value)  // PR2: cap overruns, hand-offs
                 st = ervs_warp_cold<M, kNoJump>(p.mp, T, K, p.rk, g, tb, tph, db, &nx, &ni, &dr);
@@ -1698,6 +1719,7 @@ __global__ void __launch_bounds__(kThreads, (MODE == kForceErvs || MODE == kErvs
                     } else {
                         // advance here (rare path); the node record comes next iteration
                         twe() = tb + ni;
+                        if (kPrevRow) pbeg() = begin;
                         prev = cur;
                         pdeg = deg;
                         phoff = hoff;
@@ -1810,6 +1832,7 @@ __global__ void __launch_bounds__(kThreads, (MODE == kForceErvs || MODE == kErvs
                             phase = P_FETCH;
                         } else {
                             twe() = we;
+                            if (kPrevRow) pbeg() = begin;
                             prev = cur;
                             pdeg = deg;
                             phoff = hoff;
