@@ -59,12 +59,12 @@ CONFIGS = {
             labels=(0, 3), cheaper_mix=True,
             desc="MetaPath schema (0,1,2,3) repeated to length 80, R-MAT s22 ef16, labels "
                  "uniform [0,3], uniform [1,5) weights"),
-    # tier-2 sampling (erjs_handoff = 4): the reference's PR2 bounds run
+    # tier-2 sampling (erjs_handoff = 0.25): the reference's PR2 bounds run
     # ~6,100 trials per step at s20 and more at larger scales, so
-    # an eRJS step hands off to the reservoir after 4x the trials the cost
-    # model expected; the distribution is exact (chi-square tested), the
+    # an eRJS step hands off to the reservoir after trials worth a quarter of
+    # a pass over the row; the distribution is exact (chi-square tested), the
     # random stream differs from the reference's
-    4: dict(scale=25, model="pr2", gamma=0.15, weights="pareto", labels=None, handoff=4.0,
+    4: dict(scale=25, model="pr2", gamma=0.15, weights="pareto", labels=None, handoff=0.25,
             cheaper_mix=True,
             desc="second-order PR gamma=0.15 (no restart in the reference, SURVEY 7.3), "
                  "R-MAT/Kronecker s25 ef16, Pareto alpha=1 weights, tier-2 eRJS hand-off"),
@@ -151,7 +151,7 @@ def workload(args) -> dict:
             "graph": f"rmat s{args.scale} ef16 (A,B,C,D)=(.57,.19,.19,.05), mirrored, {w}",
             "model": c["model"], **{k: v for k, v in model_kw(c).items() if k != "schema"},
             "walk_length": args.walk_length, "mode": args.mode,
-            "sampling": (f"tier-2: eRJS hand-off after max(32, ceil({args.handoff:g} d bound/wsum)) "
+            "sampling": (f"tier-2: eRJS hand-off after max(32, ceil({args.handoff:g} d / ratio)) "
                          "trials (dw_run_opts.erjs_handoff; distribution-exact, chi-square "
                          "tested; paths equal the oracle with the same rule)" if args.handoff > 0
                          else "tier-1: the reference's decision rule and trial cap (bit-exact)"),

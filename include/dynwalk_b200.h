@@ -118,9 +118,9 @@ typedef struct dw_run_opts {
     const uint64_t* qids;
     /* Tier-2 eRJS hand-off (FlexiWalker's bounded per-lane rejection,
      * PAPER.md:760-765; not in the reference): when > 0, an eRJS step that
-     * has run max(32, ceil(erjs_handoff * d * bound / wsum)) trials without
-     * acceptance -- erjs_handoff times the trials the cost model expected
-     * from the model's own estimators (cost_model.hpp:46-56) -- falls back to
+     * has run max(32, ceil(erjs_handoff * d / edge_cost_ratio)) trials
+     * without acceptance -- trials worth erjs_handoff reservoir passes over
+     * the row under the cost model (cost_model.hpp:46-56) -- falls back to
      * the reservoir pass exactly as the reference's cap overrun does
      * (samplers.hpp:174-177).  The sampled distribution is unchanged (a
      * mixture of two exact samplers); paths equal the oracle run with the

@@ -1018,12 +1018,13 @@ static outcome sample_ervs_nojump(ctx_t* c, const wstate* st, wrng* r) {
 /* Trial cap of an eRJS step: cap_per_degree * d (samplers.hpp:157), tightened
  * by the tier-2 hand-off when erjs_handoff > 0 (not in the reference; the
  * device rule of dw_walk_kernel.cuh step_cap, include/dynwalk_b200.h):
- * max(32, ceil(erjs_handoff * d * bound / wsum)) trials, erjs_handoff times
- * the trials the cost model expected from the model's estimators. */
-static uint64_t erjs_cap(const orc_opts* o, uint32_t d, double bound, double wsum) {
+ * max(32, ceil(erjs_handoff * d / ratio)) trials, i.e. trials worth
+ * erjs_handoff reservoir passes over the row under the cost model
+ * (cost_model.hpp:46-56): a ski-rental bound of the rejection loop. */
+static uint64_t erjs_cap(const orc_opts* o, uint32_t d) {
     uint64_t cap = o->cap_per_degree * d;
     if (o->erjs_handoff > 0.0) {
-        const double h = ceil(o->erjs_handoff * ((double)d * bound / wsum));
+        const double h = ceil(o->erjs_handoff * (double)d / o->edge_cost_ratio);
         const uint64_t hc = !(h >= 32.0) ? 32u : (h >= 4294967295.0 ? 0xFFFFFFFFu : (uint64_t)h);
         if (hc < cap) cap = hc;
     }
@@ -1110,7 +1111,7 @@ static int64_t walk_query(ctx_t* c, const orc_opts* o, uint32_t start, uint64_t 
             bucket(ls, d, erjs);
             if (erjs) {
                 ++ls->select_erjs;
-                out = sample_erjs(c, &st, r, est_max, erjs_cap(o, d, est_max, est_sum));
+                out = sample_erjs(c, &st, r, est_max, erjs_cap(o, d));
             } else {
                 ++ls->select_ervs;
                 out = sample_ervs(c, &st, r);
@@ -1131,8 +1132,7 @@ static int64_t walk_query(ctx_t* c, const orc_opts* o, uint32_t start, uint64_t 
             const double est = model_bound(c, &st);
             ++ls->select_erjs;
             bucket(ls, d, 1);
-            out = sample_erjs(c, &st, r, est,
-                              erjs_cap(o, d, est, o->erjs_handoff > 0.0 ? model_sum(c, &st) : 1.0));
+            out = sample_erjs(c, &st, r, est, erjs_cap(o, d));
             break;
         }
         default:

@@ -393,6 +393,8 @@ int check_opts(const dw_run_opts* o) {
     if (o->walk_length == 0xFFFFFFFFu) return fail(DW_EINVAL, "walk_length too large");
     if (!(o->erjs_handoff >= 0.0) || !std::isfinite(o->erjs_handoff))
         return fail(DW_EINVAL, "erjs_handoff must be >= 0 and finite");
+    if (o->erjs_handoff > 0.0 && (!(o->edge_cost_ratio > 0.0) || !std::isfinite(o->edge_cost_ratio)))
+        return fail(DW_EINVAL, "erjs_handoff needs a positive finite edge_cost_ratio");
     return DW_OK;
 }
 

@@ -226,6 +226,40 @@ __device__ __forceinline__ void win_seek(PrevWindow& w, const DevGraph& g, uint3
     w.pp = at;
     win_load(w, g);
 }
+// Chunk positions whose target is one of the window's entries, as a 64-bit
+// mask (bit 2l + h = lane l's half h), warp-uniform.  k0/k1 are the chunk's
+// sorted keys (targets; 0 before the row, kInvalid past it).  Each lane
+// looks its window entry up among the 32 pairs (5 shuffle steps over the
+// pairs' upper keys, then the pair and the next lane's lower key) and the
+// lanes' bits are OR-reduced (redux.sync).  A run of one target over more
+// than three positions (a multigraph) is reported as ~0ull: the caller then
+// tests its own targets instead (win_has).
+constexpr ull kWinRun = ~0ull;
+__device__ __forceinline__ ull win_mark(const PrevWindow& w, uint32_t k0, uint32_t k1) {
+    const uint32_t v = w.v;
+    uint32_t L = 0;
+#pragma unroll
+    for (uint32_t step = 16; step; step >>= 1)
+        if (__shfl_sync(kFull, k1, L + step - 1) < v) L += step;
+    const uint32_t Ln = L < 31 ? L + 1 : 31;
+    const uint32_t a0 = __shfl_sync(kFull, k0, L), a1 = __shfl_sync(kFull, k1, L);
+    const uint32_t b0 = __shfl_sync(kFull, k0, Ln), b1 = __shfl_sync(kFull, k1, Ln);
+    ull bits = 0;
+    bool run = false;
+    if (v != kInvalid) {
+        if (a0 == v) bits |= 1ull << (2 * L);
+        if (a1 == v) bits |= 1ull << (2 * L + 1);
+        if (L < 31 && b0 == v) {
+            bits |= 1ull << (2 * Ln);
+            run = a1 == v && b1 == v;  // v continues past lane L + 1's first half
+        }
+    }
+    if (__any_sync(kFull, run)) return kWinRun;
+    const uint32_t lo = __reduce_or_sync(kFull, (uint32_t)bits);
+    const uint32_t hi = __reduce_or_sync(kFull, (uint32_t)(bits >> 32));
+    return (ull)lo | ((ull)hi << 32);
+}
+
 // is u one of the window's entries (sorted ascending)?
 __device__ __forceinline__ bool win_has(const PrevWindow& w, uint32_t u) {
     uint32_t lo = 0;
@@ -441,9 +475,17 @@ __device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const Wa
             }
             bool in0 = false, in1 = false;
             if (pw.vfirst <= uhi) {
+                const uint32_t k0 = cp.u0 != kInvalid ? cp.u0 : (q == 0 ? 0u : kInvalid);
+                const uint32_t k1 = cp.u1;
                 for (;;) {
-                    in0 |= win_has(pw, cp.u0);
-                    in1 |= win_has(pw, cp.u1);
+                    const ull mk = win_mark(pw, k0, k1);
+                    if (mk == kWinRun) {
+                        in0 |= win_has(pw, cp.u0);
+                        in1 |= win_has(pw, cp.u1);
+                    } else {
+                        in0 |= (mk >> (2 * lane)) & 1u;
+                        in1 |= (mk >> (2 * lane + 1)) & 1u;
+                    }
                     if (pw.vlast >= uhi || pw.pp + 32 >= pw.pdeg) break;
                     pw.pp += 32;
                     win_load(pw, g);
@@ -1104,14 +1146,14 @@ __global__ void __launch_bounds__(kThreads, (MODE == kForceErvs || MODE == kErvs
         phase = deg >= kCoopMinDegree ? P_COOP : P_VREC;
     };
     // trial cap of an eRJS step at cur (samplers.hpp:157), tightened by the
-    // tier-2 hand-off when enabled (dw_run_opts.erjs_handoff; oracle.c erjs_cap);
-    // needs the exact row sum (compact records refetch the node record)
-    auto step_cap = [&](const Step& S) -> uint32_t {
+    // tier-2 hand-off when enabled (dw_run_opts.erjs_handoff; oracle.c erjs_cap)
+    auto step_cap = [&](const Step&) -> uint32_t {
         const ull c = p.cap_per_degree * (ull)deg;
         uint32_t r = c > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)c;
         if (p.handoff > 0.0) {
-            // handoff x the trials the cost model expected: d * bound / wsum
-            const double h = ceil(p.handoff * ((double)deg * bound / model.wsum(S)));
+            // trials worth `handoff` reservoir passes over the row (d / ratio
+            // trials cost one pass under the cost model, cost_model.hpp:46-56)
+            const double h = ceil(p.handoff * (double)deg / p.ratio);
             const uint32_t hc = !(h >= 32.0) ? 32u : (h >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)h);
             if (hc < r) r = hc;
         }
@@ -1577,8 +1619,6 @@ __global__ void __launch_bounds__(kThreads, (MODE == kForceErvs || MODE == kErvs
                     erjs = M::kBoundable;
                     if (erjs) bound = model.bound(S);
                 }
-                // tier-2 hand-off caps need the exact wsum (not the f32 row sum)
-                if (FAT == 2 && approx_sum && erjs && p.handoff > 0.0) need_node = true;
                 if (FAT == 2 && need_node) {
                     phase = P_NODE;  // the exact node record decides this step
                 } else {
