@@ -528,13 +528,28 @@ __device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const Wa
                     if (cp.u0 != kInvalid) r0 = walker_draw(key, rk, d0);
                     r1 = walker_draw(key, rk, d1);
                 }
-                if (cp.u0 != kInvalid && w0 != 0.0) {
-                    lk = log(open01(r0)) / w0;
+                // A key can only matter if it beats the best key of the
+                // earlier chunks (ties keep the earlier neighbour).  Screen
+                // with a single-precision log first: log(u) <= La + dl with
+                // La = ln2 * __log2f((float)u) (the float conversion and
+                // MUFU.LG2 err by < 2e-5 + 1e-6 |La| in the log), so a key
+                // with La + dl <= bkey * w loses for certain and skips the
+                // double log and division; the keys that remain are exact.
+                const double ua = open01(r0), ub = open01(r1);
+                auto may_win = [&](double u, double w) {
+                    if (best == kInvalid) return true;
+                    const float la = 0.69314718f * __log2f((float)u);
+                    const double dl = 2e-5 + 1e-6 * fabs((double)la);
+                    const double bw = bkey * w;
+                    return (double)la + dl > bw - 1e-12 * fabs(bw);
+                };
+                if (cp.u0 != kInvalid && w0 != 0.0 && may_win(ua, w0)) {
+                    lk = log(ua) / w0;
                     src = i0;
                     cand = cp.u0;
                 }
-                if (cp.u1 != kInvalid && w1 != 0.0) {
-                    const double l1 = log(open01(r1)) / w1;
+                if (cp.u1 != kInvalid && w1 != 0.0 && may_win(ub, w1)) {
+                    const double l1 = log(ub) / w1;
                     if (src == kInvalid || l1 > lk) {
                         lk = l1;
                         src = i0 + 1;
@@ -542,6 +557,7 @@ __device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const Wa
                     }
                 }
             }
+            if (!__any_sync(kFull, src != kInvalid)) continue;  // nothing can beat bkey
 #pragma unroll
             for (int o = 16; o; o >>= 1) {
                 const double olk = __shfl_xor_sync(kFull, lk, o);
