@@ -226,40 +226,6 @@ __device__ __forceinline__ void win_seek(PrevWindow& w, const DevGraph& g, uint3
     w.pp = at;
     win_load(w, g);
 }
-// Chunk positions whose target is one of the window's entries, as a 64-bit
-// mask (bit 2l + h = lane l's half h), warp-uniform.  k0/k1 are the chunk's
-// sorted keys (targets; 0 before the row, kInvalid past it).  Each lane
-// looks its window entry up among the 32 pairs (5 shuffle steps over the
-// pairs' upper keys, then the pair and the next lane's lower key) and the
-// lanes' bits are OR-reduced (redux.sync).  A run of one target over more
-// than three positions (a multigraph) is reported as ~0ull: the caller then
-// tests its own targets instead (win_has).
-constexpr ull kWinRun = ~0ull;
-__device__ __forceinline__ ull win_mark(const PrevWindow& w, uint32_t k0, uint32_t k1) {
-    const uint32_t v = w.v;
-    uint32_t L = 0;
-#pragma unroll
-    for (uint32_t step = 16; step; step >>= 1)
-        if (__shfl_sync(kFull, k1, L + step - 1) < v) L += step;
-    const uint32_t Ln = L < 31 ? L + 1 : 31;
-    const uint32_t a0 = __shfl_sync(kFull, k0, L), a1 = __shfl_sync(kFull, k1, L);
-    const uint32_t b0 = __shfl_sync(kFull, k0, Ln), b1 = __shfl_sync(kFull, k1, Ln);
-    ull bits = 0;
-    bool run = false;
-    if (v != kInvalid) {
-        if (a0 == v) bits |= 1ull << (2 * L);
-        if (a1 == v) bits |= 1ull << (2 * L + 1);
-        if (L < 31 && b0 == v) {
-            bits |= 1ull << (2 * Ln);
-            run = a1 == v && b1 == v;  // v continues past lane L + 1's first half
-        }
-    }
-    if (__any_sync(kFull, run)) return kWinRun;
-    const uint32_t lo = __reduce_or_sync(kFull, (uint32_t)bits);
-    const uint32_t hi = __reduce_or_sync(kFull, (uint32_t)(bits >> 32));
-    return (ull)lo | ((ull)hi << 32);
-}
-
 // is u one of the window's entries (sorted ascending)?
 __device__ __forceinline__ bool win_has(const PrevWindow& w, uint32_t u) {
     uint32_t lo = 0;
@@ -415,12 +381,15 @@ __device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const Wa
     bool have = false;
     double s = 0.0, s0 = 0.0;
     uint32_t seg = 0;
+    ErvsBound eb{0.0, 0.0};  // the segment's rounding band (m = neighbours left in the row)
     int status = 0;
     // chunk c = aligned positions [64c, 64c + 64): bytes of its bulk copy
     auto chunk_bytes = [&](uint32_t c) { return min(64u, npos - 64u * c) * 8u; };
     // membership by merging with prev's sorted row when its begin is known
+    // and prev is at most half as long as cur (about one window pass per
+    // chunk at most; denser windows cost more shuffles than hash probes)
     const bool merge = M::kSecondOrder && !M::kUsesLabels && S.prev != kInvalid &&
-                       pbegin != kNoRow && S.prev_degree > 0;
+                       pbegin != kNoRow && S.prev_degree > 0 && 2u * S.prev_degree <= d;
     PrevWindow pw{pbegin, S.prev_degree, 0u, kInvalid, kInvalid, kInvalid};
     uint32_t par = 0;
     EPair nx{};
@@ -475,17 +444,9 @@ __device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const Wa
             }
             bool in0 = false, in1 = false;
             if (pw.vfirst <= uhi) {
-                const uint32_t k0 = cp.u0 != kInvalid ? cp.u0 : (q == 0 ? 0u : kInvalid);
-                const uint32_t k1 = cp.u1;
                 for (;;) {
-                    const ull mk = win_mark(pw, k0, k1);
-                    if (mk == kWinRun) {
-                        in0 |= win_has(pw, cp.u0);
-                        in1 |= win_has(pw, cp.u1);
-                    } else {
-                        in0 |= (mk >> (2 * lane)) & 1u;
-                        in1 |= (mk >> (2 * lane + 1)) & 1u;
-                    }
+                    in0 |= win_has(pw, cp.u0);
+                    in1 |= win_has(pw, cp.u1);
                     if (pw.vlast >= uhi || pw.pp + 32 >= pw.pdeg) break;
                     pw.pp += 32;
                     win_load(pw, g);
@@ -636,6 +597,7 @@ __device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const Wa
                     continue;
                 }
                 s = s0 = lr / bkey;  // samplers.hpp:86-89
+                eb = ervs_bound(d - fe, mp.ervs_slack);  // m <= d - seg for the whole segment
                 seg = fe;
                 have = true;
                 pos = fe;
@@ -650,7 +612,6 @@ __device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const Wa
                 double tot = p1;
 #pragma unroll
                 for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(kFull, tot, o);
-                const ErvsBound eb = ervs_bound(cend - seg, mp.ervs_slack);
                 const double A = s - tot;
                 if (A > eb.k * (s0 + tot) + 1.1 * 0x1.0p-53 * fabs(A) + eb.lo) {
                     s = A;
@@ -671,7 +632,6 @@ __device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const Wa
             uint32_t cross = kInvalid;
             bool decided = false;
             if (s > 0.0 && s < DBL_MAX) {
-                const ErvsBound eb = ervs_bound(cend - seg, mp.ervs_slack);
                 const double A0 = s - P0, A1 = s - P1;
                 const double E0 = eb.k * (s0 + P0) + 1.1 * 0x1.0p-53 * fabs(A0) + eb.lo;
                 const double E1 = eb.k * (s0 + P1) + 1.1 * 0x1.0p-53 * fabs(A1) + eb.lo;
@@ -694,6 +654,7 @@ __device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const Wa
                 cross = ervs_replay<M>(mp, S, g, begin, phoff, seg, s0, cend, &sx);
                 if (cross == kInvalid) {  // exact value at the chunk end restarts the bound
                     s = s0 = sx;
+                    eb = ervs_bound(d - cend, mp.ervs_slack);
                     seg = cend;
                     break;
                 }
@@ -973,9 +934,21 @@ struct WalkSmem {
 #ifndef DW_ERVS_MIN_BLOCKS
 #define DW_ERVS_MIN_BLOCKS 2
 #endif
+// PR2 (CoopErjs) kernels too: second-order PageRank on heavy-tailed weights
+// spends its time in hub-row scans (cap overruns, tier-2 hand-offs), which
+// then run inline instead of through an out-of-line call whose register
+// saves spilled ~600 B at 80 registers
+#ifndef DW_PR2_WIDE
+#define DW_PR2_WIDE 1
+#endif
+template <class M, int MODE>
+struct WideKernel {
+    static constexpr bool value = MODE == kForceErvs || MODE == kErvsNoJump ||
+                                  (DW_PR2_WIDE && CoopErjs<M>::value);
+};
 template <class M, int MODE, int FAT>
-__global__ void __launch_bounds__(kThreads, (MODE == kForceErvs || MODE == kErvsNoJump)
-                                                ? DW_ERVS_MIN_BLOCKS : DW_MIN_BLOCKS)
+__global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS_MIN_BLOCKS
+                                                                        : DW_MIN_BLOCKS)
     walk_kernel(const __grid_constant__ WalkParams p) {
     constexpr bool kNoJump = MODE == kErvsNoJump;
     // MetaPath trials judged on a packed label first (DevGraph::lab2); the
@@ -1754,7 +1727,10 @@ __global__ void __launch_bounds__(kThreads, (MODE == kForceErvs || MODE == kErvs
                 st = ervs_warp<M, kNoJump, kTma>(p.mp, T, K, p.rk, g, tb, tph, db, &nx, &ni, &dr,
                                                  ring, T.prev != kInvalid ? tpb : kNoRow);
             }
-            else if constexpr (DW_PR2_PAR && CoopErjs<M>::value)  // PR2: cap overruns, hand-offs
+            else if constexpr (WideKernel<M, MODE>::value)  // PR2: cap overruns, hand-offs
+                st = ervs_warp<M, kNoJump, false>(p.mp, T, K, p.rk, g, tb, tph, db, &nx, &ni, &dr,
+                                                  TmaRing{});
+            else if constexpr (DW_PR2_PAR && CoopErjs<M>::value)
                 st = ervs_warp_cold<M, kNoJump>(p.mp, T, K, p.rk, g, tb, tph, db, &nx, &ni, &dr);
             else
                 st = ervs_warp_seq<M, kNoJump>(p.mp, T, K, p.rk, g, tb, tph, db, &nx, &ni, &dr);
