@@ -344,13 +344,14 @@ dwb::ModelParams model_params(const dw_model_desc* m) {
     // one-multiply weight-sum screen (dw_models.cuh wsum_approx)
     mp.screen = (m->kind == DW_MODEL_NODE2VEC && m->a > 0.0 && m->b > 0.0) ? 1u : 0u;
     mp.wsum_coef = (1.0 / m->a + 1.0 + 1.0 / m->b) / 3.0;
-    // decisions within this relative distance of a compact record's f32 row
-    // sum refetch the exact node record (dw_walk_kernel.cuh); the f32 sum is
-    // within 2^-24 of the double one, so any band >= 1e-6 is exact
-    mp.fat32_band = 1e-6;
+    // decisions within this relative distance of a compact record's row sum
+    // refetch the exact node record (dw_walk_kernel.cuh); the record keeps
+    // the f32 sum truncated to 15 mantissa bits (within 2^-15 = 3.1e-5 of the
+    // double sum), so any band >= 1e-4 is exact
+    mp.fat32_band = 1e-4;
     if (const char* env = std::getenv("DW_FAT32_BAND")) {
         const double b = std::atof(env);
-        if (b >= 1e-6) mp.fat32_band = b;
+        if (b >= 1e-4) mp.fat32_band = b;
     }
     // the warp reservoir's rounding band (dw_walk_kernel.cuh ervs_warp) is
     // rigorous at 1; DW_ERVS_SLACK > 1 widens it so that tests drive the exact

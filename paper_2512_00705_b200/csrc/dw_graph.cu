@@ -166,10 +166,51 @@ __global__ void label_mask_kernel(const NodeRec* __restrict__ nodes, uint32_t nv
     }
 }
 
+// Triangle bound of the step v -> u (record of edge v -> u): the largest prop
+// h(u -> w) over w in N(v), w != v -- the edges whose node2vec/PR2 weight is
+// the "in N(prev)" case at cur = u, prev = v (models.hpp:62-69, 128-138).
+// Encoded in 8 bits against hmax(u): 0 = no such edge; q >= 1: every such
+// prop is <= hmax(u) * (q + 1) / 256 (exact in double); 255 = unknown (the
+// intersection was not computed: more than kTriWork probes).  The walk turns
+// it into a tighter non-return maximum (dw_models.cuh nonreturn_max), so more
+// eRJS trials are rejected without a gather and fewer need a membership
+// probe; outcomes are unchanged because it is an upper bound.
+constexpr uint32_t kTriWork = 4096;
+__device__ uint32_t tri_q(const EdgeRec* __restrict__ edges, const uint32_t* __restrict__ hslots,
+                          uint32_t v, const NodeRec& nvr, uint32_t u, const NodeRec& nur) {
+    const uint32_t du = nur.degree, dv = nvr.degree;
+    const ull work_a = du;                                          // probe N(v) per edge of u
+    const ull work_b = (ull)dv * (ull)(33 - __clz(du | 1u));        // search u's row per w
+    if ((work_a < work_b ? work_a : work_b) > kTriWork) return 255u;
+    DevGraph g{};
+    g.hslots = hslots;
+    float m = -1.0f;
+    if (work_a <= work_b) {
+        for (uint32_t i = 0; i < du; ++i) {
+            const EdgeRec er = edges[nur.begin + i];
+            if (er.col != v && member(g, dv, nvr.hoff, er.col) && er.h > m) m = er.h;
+        }
+    } else {
+        for (uint32_t j = 0; j < dv; ++j) {
+            const uint32_t w = edges[nvr.begin + j].col;
+            if (w == v) continue;
+            uint32_t lo = row_lower_bound(edges, nur.begin, du, w);
+            for (; lo < du && edges[nur.begin + lo].col == w; ++lo)
+                if (edges[nur.begin + lo].h > m) m = edges[nur.begin + lo].h;
+        }
+    }
+    if (m < 0.0f) return 0u;
+    // q = floor(256 m / hmax), nudged up so rounding cannot make it too small
+    const double r = 256.0 * (double)m / nur.hmax * (1.0 + 0x1.0p-40);
+    const uint32_t q = r >= 255.0 ? 255u : (uint32_t)r;
+    return q < 1u ? 1u : q;
+}
+
 __global__ void fat_build_kernel(const NodeRec* __restrict__ nodes, uint32_t nv,
                                  const EdgeRec* __restrict__ edges,
                                  const uint16_t* __restrict__ labels,
-                                 const uint8_t* __restrict__ lmask, FatRec* __restrict__ fat) {
+                                 const uint8_t* __restrict__ lmask, const uint32_t* __restrict__ hslots,
+                                 FatRec* __restrict__ fat) {
     const ull warp = (blockIdx.x * (ull)blockDim.x + threadIdx.x) >> 5;
     const ull nwarps = ((ull)gridDim.x * blockDim.x) >> 5;
     const uint32_t lane = threadIdx.x & 31;
@@ -192,7 +233,9 @@ __global__ void fat_build_kernel(const NodeRec* __restrict__ nodes, uint32_t nv,
             f.tdeg = nu.degree;
             f.thoff = nu.hoff;
             f.twin_lo = lo;
-            f.twin_cnt = hi - lo;
+            // multiplicity (24 bits; 0xFFFFFF = too many to describe) | triangle bound << 24
+            f.twin_cnt = (hi - lo >= 0xFFFFFFu ? 0xFFFFFFu : hi - lo) |
+                         (tri_q(edges, hslots, (uint32_t)v, nr, er.col, nu) << 24);
             f.thmax = nu.hmax;
             f.thsum = nu.hsum;
             f.aux[0] = f.aux[1] = f.aux[2] = f.aux[3] = 0;
@@ -243,7 +286,8 @@ static cudaError_t build_twin(DeviceGraphBuffers& g, cudaStream_t s) {
 }
 
 __global__ void fat32_build_kernel(const NodeRec* __restrict__ nodes, uint32_t nv,
-                                   const EdgeRec* __restrict__ edges, FatRec32* __restrict__ fat) {
+                                   const EdgeRec* __restrict__ edges,
+                                   const uint32_t* __restrict__ hslots, FatRec32* __restrict__ fat) {
     const ull warp = (blockIdx.x * (ull)blockDim.x + threadIdx.x) >> 5;
     const ull nwarps = ((ull)gridDim.x * blockDim.x) >> 5;
     const uint32_t lane = threadIdx.x & 31;
@@ -268,8 +312,13 @@ __global__ void fat32_build_kernel(const NodeRec* __restrict__ nodes, uint32_t n
             f.thmax = (float)nu.hmax;  // exact: a maximum of f32 props
             // a row sum above FLT_MAX has no f32 neighbour: NaN fails both of
             // the decision's band tests, so the exact node record decides
+            // the row sum in the top 24 bits (f32 truncated to 15 mantissa
+            // bits: decisions within fat32_band = 1e-4 of it refetch the
+            // node record), the triangle bound in the low 8
             const float fs = (float)nu.hsum;
-            f.thsum = isfinite(fs) ? fs : __int_as_float(0x7fc00000);
+            const uint32_t sb = isfinite(fs) ? __float_as_uint(fs) : 0x7fc00000u;
+            f.thsum = __uint_as_float((sb & ~0xFFu) |
+                                      tri_q(edges, hslots, (uint32_t)v, nodes[v], er.col, nu));
             fat[e] = f;
         }
     }
@@ -317,7 +366,7 @@ static cudaError_t build_fat(DeviceGraphBuffers& g, cudaStream_t s) {
         if (need32 + (4ull << 30) <= fb) {
             DW_TRY(cudaMallocAsync(&g.fat32, need32, s));
             fat32_build_kernel<<<grid_for((ull)g.nv * 32, 256), 256, 0, s>>>(g.nodes, g.nv, g.edges,
-                                                                             g.fat32);
+                                                                             g.hslots, g.fat32);
             DW_TRY(cudaGetLastError());
             DW_TRY(cudaStreamSynchronize(s));
             used = need32;
@@ -350,7 +399,7 @@ static cudaError_t build_fat(DeviceGraphBuffers& g, cudaStream_t s) {
         DW_TRY(cudaGetLastError());
     }
     fat_build_kernel<<<grid_for((ull)g.nv * 32, 256), 256, 0, s>>>(g.nodes, g.nv, g.edges,
-                                                                   g.labels, lmask, g.fat);
+                                                                   g.labels, lmask, g.hslots, g.fat);
     DW_TRY(cudaGetLastError());
     if (lmask) DW_TRY(cudaFreeAsync(lmask, s));
     return cudaStreamSynchronize(s);
@@ -824,6 +873,7 @@ __global__ void probe_pass_kernel(DevGraph g, __grid_constant__ const ModelParam
         S.degree = P.degree;
         S.hmax = P.hmax;
         S.hsum = P.hsum;
+        S.hin = P.hmax;  // no triangle bound in the probe
         S.lmax = S.lsum = 0.0;
         m.prepare(S);
         const uint32_t k = min(S.degree, npn);

@@ -39,6 +39,10 @@ struct Step {
     uint32_t degree;  // d(cur)
     double hmax, hsum;
     double lmax, lsum;  // per-node label MAX/SUM (DSL models whose estimators read labels)
+    // upper bound of h(cur -> u) over u in N(prev), u != prev (the record's
+    // triangle bound, dw_graph.cu tri_q): 0 when there is no such edge,
+    // hmax when unknown.  Only nonreturn_max reads it.
+    double hin;
     __device__ __forceinline__ bool has_prev() const { return prev != kInvalid; }
 };
 
@@ -144,12 +148,14 @@ struct Node2VecModel {
         }
         return ddiv(da(1.0) + 1.0 + db(1.0), 3.0, i3) * (double)s.degree;
     }
-    // u != prev: weight is h or h/b with h <= hmax (RN is monotone, b > 0)
+    // u != prev: weight is h (u in N(prev): h <= hin, the triangle bound)
+    // or h/b (h <= hmax); RN is monotone and b > 0
     __device__ double nonreturn_max(const Step& s) const {
         const double hmax = W ? s.hmax : 1.0;
         if (!s.has_prev()) return hmax;
+        const double hin = W ? s.hin : (s.hin > 0.0 ? 1.0 : 0.0);
         const double hb = db(hmax);
-        return hb > hmax ? hb : hmax;
+        return hb > hin ? hb : hin;
     }
     __device__ void prepare(const Step&) const {}
     __device__ WeightCase weight(const Step& s, uint32_t u, float hf, uint16_t) const {
@@ -223,12 +229,15 @@ struct Pr2Model {
         const double avg = (x + x * cb * md + x * cp * md) / 3.0;
         return W ? avg : avg * (double)s.degree;
     }
+    // u != prev: boosted h * cb * md when u in N(prev) (h <= hin, the
+    // triangle bound), plain h * cp * md otherwise (h <= hmax)
     __device__ double nonreturn_max(const Step& s) const {
         const double hmax = W ? s.hmax : 1.0;
         if (!s.has_prev()) return hmax;
+        const double hin = W ? s.hin : (s.hin > 0.0 ? 1.0 : 0.0);
         double cp, cb, md;
         factors(s, cp, cb, md);
-        const double x = hmax * cb * md, y = hmax * cp * md;
+        const double x = hin * cb * md, y = hmax * cp * md;
         return x > y ? x : y;
     }
     __device__ void prepare(const Step& s) {

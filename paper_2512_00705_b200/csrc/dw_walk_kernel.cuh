@@ -187,6 +187,7 @@ __device__ __forceinline__ double ervs_weight(const M& m, const Step& S, const D
                                               uint32_t phoff, uint32_t u, float h, uint16_t lab) {
     const WeightCase wc = m.weight(S, u, h, lab);
     if (!M::kSecondOrder || !wc.needs_member) return wc.w;
+    if ((double)h > S.hin) return wc.w_out;  // above the triangle bound: not in N(prev)
     return member(g, S.prev_degree, phoff, u) ? wc.w_in : wc.w_out;
 }
 
@@ -897,6 +898,15 @@ __device__ __forceinline__ ull warp_sum(ull v) {
     return v;
 }
 
+// The record's 8-bit triangle bound (dw_graph.cu tri_q) as f32 bits of an
+// upper bound of the props of the edges (cur -> u), u in N(prev): 0 when
+// there is none, hmax when unknown (255), else hmax (q + 1) / 256 rounded up.
+__device__ __forceinline__ uint32_t tri_bound(uint32_t q, float hmax) {
+    if (q == 0u) return 0u;
+    if (q == 255u) return __float_as_uint(hmax);
+    return __float_as_uint(__fmul_ru(hmax, (float)(q + 1u)) * 0x1.0p-8f);
+}
+
 // ---- K3: adaptive walker loop (runtime.cpp:59-153 + 192-247) --------------
 // Per-lane landing slots and counters, structure-of-arrays ([.][kThreads]) so
 // a warp's 16 B accesses are conflict-free.
@@ -919,6 +929,9 @@ struct WalkSmem {
         twlo[kThreads], twcnt[kThreads], nret[kThreads];
     double bound[kThreads], mnr[kThreads];
     uint32_t qi[kThreads];           // the lane's walker: index in this launch
+    // f32 bits of the current step's triangle bound (Step::hin, rounded up):
+    // props of the edges (cur -> u) with u in N(prev) are <= it
+    uint32_t tq[kThreads];
     ull cnt[kCNum];
     uint32_t hist[66];
     ull lct[LC_NUM];                 // block totals of the lane counters
@@ -1064,6 +1077,7 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
         S.degree = deg;
         S.hmax = hmax;
         S.hsum = hsum;
+        S.hin = hmax;
         return S;
     };
     auto key_of = [&]() {
@@ -1340,6 +1354,7 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
         if (ph0 == P_TRIAL) {
             int acc = -1;
             const Step S = mkstep(0.0, 0.0);
+            const float hin_r = __uint_as_float(sm.tq[tid]);  // triangle bound
             if (mb & kParked) {  // resolve the head's membership probe
                 const uint4 v0 = s_rec[rh][0][tid];
                 const uint32_t u = FAT ? v0.x : (((sel >> rh) & 1) ? v0.z : v0.x);
@@ -1399,8 +1414,21 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
                         break;
                     }
                     if (!ok || y < hi) {  // outcome hinges on u in N(prev)
-                        mb = kParked | hash_bucket(u, plg);
-                        break;
+                        if (h > hin_r) {
+                            // a prop above the triangle bound: u is not in
+                            // N(prev), no probe (weight: the "out" case)
+                            if (!valid_w(wc.w_out)) {
+                                fail(kDevBadWeight);
+                                break;
+                            }
+                            if (y < wc.w_out) {
+                                acc = (int)rh;
+                                break;
+                            }
+                        } else {
+                            mb = kParked | hash_bucket(u, plg);
+                            break;
+                        }
                     }
                 }
                 rh = (rh + 1) & (kRing - 1);
@@ -1455,6 +1483,8 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
             }
             if (r >= 0) {
                 const WeightCase wc = model.weight(mkstep(0.0, 0.0), u, h, lab);
+                if (kSO && r == 2 && wc.needs_member && h > __uint_as_float(sm.tq[tid]))
+                    r = 0;  // prop above the triangle bound: u is not in N(prev)
                 if (kSO && r == 2 && wc.needs_member) {
                     s_rec[kRing - 1][0][tid] = make_uint4(u, __float_as_uint(h), lab, 0u);
                     mb = hash_bucket(u, plg);
@@ -1527,7 +1557,9 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
                 tw_lo = (v1.y >> 24) == 255u ? 0u : (v1.y & 0xFFFFFFu);
                 tw_cnt = (v1.y >> 24) == 255u ? 0xFFFFFFFFu : (v1.y >> 24);
                 hmax = (double)__uint_as_float(v1.z);
-                hsum = (double)__uint_as_float(v1.w);  // rounded: see the decision
+                // row sum truncated to 24 bits (see the decision), triangle bound
+                hsum = (double)__uint_as_float(v1.w & ~0xFFu);
+                sm.tq[tid] = tri_bound(v1.w & 0xFFu, __uint_as_float(v1.z));
                 approx_sum = true;
             } else if (next_ev == E_FAT) {
                 const uint4 v1 = s_rec[next_slot][1][tid], v2 = s_rec[next_slot][2][tid];
@@ -1535,8 +1567,9 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
                 deg = v1.x;
                 hoff = v1.y;
                 tw_lo = v1.z;
-                tw_cnt = v1.w;
+                tw_cnt = (v1.w & 0xFFFFFFu) == 0xFFFFFFu ? 0xFFFFFFFFu : (v1.w & 0xFFFFFFu);
                 hmax = __hiloint2double((int)v2.y, (int)v2.x);
+                sm.tq[tid] = tri_bound(v1.w >> 24, (float)hmax);  // hmax: a max of f32 props
                 hsum = __hiloint2double((int)v2.w, (int)v2.z);
                 lmask = v0.w >> 24;
             } else {
@@ -1561,6 +1594,7 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
             if (FAT != 2 || prev == kInvalid) {
                 tw_lo = 0;
                 tw_cnt = prev == kInvalid ? 0u : 0xFFFFFFFFu;
+                sm.tq[tid] = tri_bound(255u, (float)hmax);  // no triangle bound
             }
             if (!FAT && g.twin && prev != kInvalid) {
                 const uint32_t w = s_t[0][tid];
@@ -1576,6 +1610,7 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
                 end_walk();
             } else {
                 Step S = mkstep(hmax, hsum, lmax, lsum);
+                if (FAT && prev != kInvalid) S.hin = (double)__uint_as_float(sm.tq[tid]);
                 model.prepare(S);
                 bool erjs = false, need_node = false;
                 if (MODE == kAdaptive) {
@@ -1712,6 +1747,7 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
             T.step = __shfl_sync(kFull, step, L);
             T.degree = __shfl_sync(kFull, deg, L);
             T.hmax = T.hsum = 0.0;
+            T.hin = (double)__uint_as_float(sm.tq[(tid & ~31) + L]);
             const uint32_t tph = __shfl_sync(kFull, phoff, L);
             const ull tb = __shfl_sync(kFull, begin, L);
             const ull q = __shfl_sync(kFull, qg, L);
@@ -1782,6 +1818,7 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
                 T.step = __shfl_sync(kFull, step, L);
                 T.degree = __shfl_sync(kFull, deg, L);
                 T.hmax = T.hsum = 0.0;
+                T.hin = (double)__uint_as_float(sm.tq[Lt]);
                 T.lmax = T.lsum = 0.0;
                 M mw(p.mp);
                 mw.prepare(T);
@@ -1824,7 +1861,8 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
                             isret = kSO && u == T.prev;
                             const double w = !wc.needs_member
                                                  ? wc.w
-                                                 : (member(g, T.prev_degree, tph, u) ? wc.w_in : wc.w_out);
+                                                 : ((double)h <= T.hin && member(g, T.prev_degree, tph, u)
+                                                        ? wc.w_in : wc.w_out);
                             if (!valid_w(w))
                                 badw = true;
                             else
