@@ -171,17 +171,19 @@ __global__ void label_mask_kernel(const NodeRec* __restrict__ nodes, uint32_t nv
 // the "in N(prev)" case at cur = u, prev = v (models.hpp:62-69, 128-138).
 // Encoded in 8 bits against hmax(u): 0 = no such edge; q >= 1: every such
 // prop is <= hmax(u) * (q + 1) / 256 (exact in double); 255 = unknown (the
-// intersection was not computed: more than kTriWork probes).  The walk turns
+// intersection was not computed: more than `work` probes; DW_TRI_WORK, default
+// kTriWork, 0 = never).  The walk turns
 // it into a tighter non-return maximum (dw_models.cuh nonreturn_max), so more
 // eRJS trials are rejected without a gather and fewer need a membership
 // probe; outcomes are unchanged because it is an upper bound.
-constexpr uint32_t kTriWork = 4096;
+constexpr uint32_t kTriWork = 1024;
 __device__ uint32_t tri_q(const EdgeRec* __restrict__ edges, const uint32_t* __restrict__ hslots,
-                          uint32_t v, const NodeRec& nvr, uint32_t u, const NodeRec& nur) {
+                          uint32_t v, const NodeRec& nvr, uint32_t u, const NodeRec& nur,
+                          uint32_t work) {
     const uint32_t du = nur.degree, dv = nvr.degree;
     const ull work_a = du;                                          // probe N(v) per edge of u
     const ull work_b = (ull)dv * (ull)(33 - __clz(du | 1u));        // search u's row per w
-    if ((work_a < work_b ? work_a : work_b) > kTriWork) return 255u;
+    if ((work_a < work_b ? work_a : work_b) > work) return 255u;
     DevGraph g{};
     g.hslots = hslots;
     float m = -1.0f;
@@ -210,7 +212,7 @@ __global__ void fat_build_kernel(const NodeRec* __restrict__ nodes, uint32_t nv,
                                  const EdgeRec* __restrict__ edges,
                                  const uint16_t* __restrict__ labels,
                                  const uint8_t* __restrict__ lmask, const uint32_t* __restrict__ hslots,
-                                 FatRec* __restrict__ fat) {
+                                 uint32_t tri_work, FatRec* __restrict__ fat) {
     const ull warp = (blockIdx.x * (ull)blockDim.x + threadIdx.x) >> 5;
     const ull nwarps = ((ull)gridDim.x * blockDim.x) >> 5;
     const uint32_t lane = threadIdx.x & 31;
@@ -235,7 +237,7 @@ __global__ void fat_build_kernel(const NodeRec* __restrict__ nodes, uint32_t nv,
             f.twin_lo = lo;
             // multiplicity (24 bits; 0xFFFFFF = too many to describe) | triangle bound << 24
             f.twin_cnt = (hi - lo >= 0xFFFFFFu ? 0xFFFFFFu : hi - lo) |
-                         (tri_q(edges, hslots, (uint32_t)v, nr, er.col, nu) << 24);
+                         (tri_q(edges, hslots, (uint32_t)v, nr, er.col, nu, tri_work) << 24);
             f.thmax = nu.hmax;
             f.thsum = nu.hsum;
             f.aux[0] = f.aux[1] = f.aux[2] = f.aux[3] = 0;
@@ -287,7 +289,8 @@ static cudaError_t build_twin(DeviceGraphBuffers& g, cudaStream_t s) {
 
 __global__ void fat32_build_kernel(const NodeRec* __restrict__ nodes, uint32_t nv,
                                    const EdgeRec* __restrict__ edges,
-                                   const uint32_t* __restrict__ hslots, FatRec32* __restrict__ fat) {
+                                   const uint32_t* __restrict__ hslots, uint32_t tri_work,
+                                   FatRec32* __restrict__ fat) {
     const ull warp = (blockIdx.x * (ull)blockDim.x + threadIdx.x) >> 5;
     const ull nwarps = ((ull)gridDim.x * blockDim.x) >> 5;
     const uint32_t lane = threadIdx.x & 31;
@@ -318,7 +321,7 @@ __global__ void fat32_build_kernel(const NodeRec* __restrict__ nodes, uint32_t n
             const float fs = (float)nu.hsum;
             const uint32_t sb = isfinite(fs) ? __float_as_uint(fs) : 0x7fc00000u;
             f.thsum = __uint_as_float((sb & ~0xFFu) |
-                                      tri_q(edges, hslots, (uint32_t)v, nodes[v], er.col, nu));
+                                      tri_q(edges, hslots, (uint32_t)v, nr, er.col, nu, tri_work));
             fat[e] = f;
         }
     }
@@ -330,6 +333,11 @@ __global__ void fat32_build_kernel(const NodeRec* __restrict__ nodes, uint32_t n
 // s27 (137 GB) 3.27e9 vs 4.42e9 (random gathers spread over 175 GB of HBM).
 // DW_FAT=0 disables the layout, DW_FAT=1 builds it whenever it fits.
 constexpr unsigned long long kFatMaxBytes = 96ull * 1000 * 1000 * 1000;
+
+static uint32_t tri_work() {
+    if (const char* env = getenv("DW_TRI_WORK")) return (uint32_t)std::strtoul(env, nullptr, 10);
+    return kTriWork;
+}
 
 static cudaError_t build_fat(DeviceGraphBuffers& g, cudaStream_t s) {
     g.fat = nullptr;
@@ -366,7 +374,7 @@ static cudaError_t build_fat(DeviceGraphBuffers& g, cudaStream_t s) {
         if (need32 + (4ull << 30) <= fb) {
             DW_TRY(cudaMallocAsync(&g.fat32, need32, s));
             fat32_build_kernel<<<grid_for((ull)g.nv * 32, 256), 256, 0, s>>>(g.nodes, g.nv, g.edges,
-                                                                             g.hslots, g.fat32);
+                                                                             g.hslots, tri_work(), g.fat32);
             DW_TRY(cudaGetLastError());
             DW_TRY(cudaStreamSynchronize(s));
             used = need32;
@@ -399,7 +407,8 @@ static cudaError_t build_fat(DeviceGraphBuffers& g, cudaStream_t s) {
         DW_TRY(cudaGetLastError());
     }
     fat_build_kernel<<<grid_for((ull)g.nv * 32, 256), 256, 0, s>>>(g.nodes, g.nv, g.edges,
-                                                                   g.labels, lmask, g.hslots, g.fat);
+                                                                   g.labels, lmask, g.hslots, tri_work(),
+                                                                   g.fat);
     DW_TRY(cudaGetLastError());
     if (lmask) DW_TRY(cudaFreeAsync(lmask, s));
     return cudaStreamSynchronize(s);
