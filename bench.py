@@ -59,12 +59,12 @@ CONFIGS = {
             labels=(0, 3), cheaper_mix=True,
             desc="MetaPath schema (0,1,2,3) repeated to length 80, R-MAT s22 ef16, labels "
                  "uniform [0,3], uniform [1,5) weights"),
-    # tier-2 sampling (erjs_handoff = 0.25): the reference's PR2 bounds run
+    # tier-2 sampling (erjs_handoff = 0.05): the reference's PR2 bounds run
     # ~6,100 trials per step at s20 and more at larger scales, so
-    # an eRJS step hands off to the reservoir after trials worth a quarter of
-    # a pass over the row; the distribution is exact (chi-square tested), the
+    # an eRJS step hands off to the reservoir after trials worth 1/20 of a
+    # pass over the row; the distribution is exact (chi-square tested), the
     # random stream differs from the reference's
-    4: dict(scale=25, model="pr2", gamma=0.15, weights="pareto", labels=None, handoff=0.25,
+    4: dict(scale=25, model="pr2", gamma=0.15, weights="pareto", labels=None, handoff=0.05,
             cheaper_mix=True,
             desc="second-order PR gamma=0.15 (no restart in the reference, SURVEY 7.3), "
                  "R-MAT/Kronecker s25 ef16, Pareto alpha=1 weights, tier-2 eRJS hand-off"),
