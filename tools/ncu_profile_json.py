@@ -74,6 +74,8 @@ def main():
     note = sys.argv[5] if len(sys.argv) > 5 else ""
     d = raw(rep)
     b = json.loads(open(bench).read().strip().splitlines()[-1])
+    if "walker_steps_per_step" not in b:
+        raise SystemExit("bench line without walker_steps_per_step")
     steps = float(b["walker_steps_per_step"])
     met = {k: {"value": d[k][0], "unit": d[k][1]} for k in KEYS if k in d}
     rd = to_bytes(*d["dram__bytes_read.sum"])
@@ -84,7 +86,7 @@ def main():
     tot = sum(st.values()) or 1.0
     stalls = {k.replace("smsp__pcsamp_warps_issue_stalled_", ""): round(100 * v / tot, 1)
               for k, v in sorted(st.items(), key=lambda kv: -kv[1])[:10]}
-    per = launches(lcsv)
+    per = launches(lcsv) if lcsv != "-" else {}
     total_ms = sum(t for _, t in per.values())
     walk = {k: v for k, v in per.items() if "walk_kernel" in k}
     walk_ms = sum(t for _, t in walk.values())
@@ -106,7 +108,7 @@ def main():
         },
         "simt_lanes_per_instruction": _num(d["smsp__thread_inst_executed_per_inst_executed.ratio"][0]),
         "stall_pct": stalls,
-        "launch_list": {
+        "launch_list": None if lcsv == "-" else {
             "source": lcsv,
             "kernels": {k: {"launches": n, "ms": round(t, 3)} for k, (n, t) in
                         sorted(per.items(), key=lambda kv: -kv[1][1])[:12]},
