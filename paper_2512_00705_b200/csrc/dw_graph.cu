@@ -334,9 +334,12 @@ __global__ void fat32_build_kernel(const NodeRec* __restrict__ nodes, uint32_t n
 // DW_FAT=0 disables the layout, DW_FAT=1 builds it whenever it fits.
 constexpr unsigned long long kFatMaxBytes = 96ull * 1000 * 1000 * 1000;
 
-static uint32_t tri_work() {
+// s24: 1024 probes per edge build in 10 s and walk at 8.65e9 walker-steps/s,
+// 4096 in 34 s at 8.78e9, 16384 in 59 s at 8.78e9 (profiles/r2_tri_work_s24.txt);
+// graphs above 2^30 edges keep 1024 (s27: the build stays under 20 s)
+static uint32_t tri_work(ull ne) {
     if (const char* env = getenv("DW_TRI_WORK")) return (uint32_t)std::strtoul(env, nullptr, 10);
-    return kTriWork;
+    return ne > (1ull << 30) ? kTriWork : 4 * kTriWork;
 }
 
 static cudaError_t build_fat(DeviceGraphBuffers& g, cudaStream_t s) {
@@ -374,7 +377,7 @@ static cudaError_t build_fat(DeviceGraphBuffers& g, cudaStream_t s) {
         if (need32 + (4ull << 30) <= fb) {
             DW_TRY(cudaMallocAsync(&g.fat32, need32, s));
             fat32_build_kernel<<<grid_for((ull)g.nv * 32, 256), 256, 0, s>>>(g.nodes, g.nv, g.edges,
-                                                                             g.hslots, tri_work(), g.fat32);
+                                                                             g.hslots, tri_work(g.ne), g.fat32);
             DW_TRY(cudaGetLastError());
             DW_TRY(cudaStreamSynchronize(s));
             used = need32;
@@ -407,7 +410,7 @@ static cudaError_t build_fat(DeviceGraphBuffers& g, cudaStream_t s) {
         DW_TRY(cudaGetLastError());
     }
     fat_build_kernel<<<grid_for((ull)g.nv * 32, 256), 256, 0, s>>>(g.nodes, g.nv, g.edges,
-                                                                   g.labels, lmask, g.hslots, tri_work(),
+                                                                   g.labels, lmask, g.hslots, tri_work(g.ne),
                                                                    g.fat);
     DW_TRY(cudaGetLastError());
     if (lmask) DW_TRY(cudaFreeAsync(lmask, s));
