@@ -109,7 +109,9 @@ cudaError_t launch_custom(const dw_custom_model_s* cm_, int mode, const WalkPara
     }
     cudaKernel_t k = cm->kernels[mode];
     constexpr int kThreadsRtc = kThreads;
-    const size_t smem = sizeof(WalkSmem);
+    // reservoir-only modes run the wide kernel (WideKernel, WalkSmemWide)
+    const size_t smem = (mode == kForceErvs || mode == kErvsNoJump) ? sizeof(WalkSmemWide)
+                                                                     : sizeof(WalkSmem);
     if (!cm->attr_set[mode]) {
         e = cudaKernelSetAttributeForDevice(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)smem, dev);

@@ -7,7 +7,7 @@ namespace dwb {
 template <class M, int MODE, int FAT>
 static cudaError_t launch_t(const WalkParams& p, int num_sms, cudaStream_t stream) {
     int per_sm = 0;
-    const size_t smem = sizeof(WalkSmem);
+    const size_t smem = walk_smem_bytes<M, MODE>();
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         cudaError_t ea = cudaFuncSetAttribute(walk_kernel<M, MODE, FAT>,

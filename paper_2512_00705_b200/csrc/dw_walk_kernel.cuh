@@ -959,6 +959,17 @@ struct WideKernel {
     static constexpr bool value = MODE == kForceErvs || MODE == kErvsNoJump ||
                                   (DW_PR2_WIDE && CoopErjs<M>::value);
 };
+// Wide kernels (2 CTAs/SM) have shared memory to spare: each lane also keeps
+// prev's row begin, so the warp reservoir merges cur's row with prev's
+// instead of probing prev's hash set
+struct WalkSmemWide : WalkSmem {
+    ull pbeg[kThreads];
+};
+template <class M, int MODE>
+constexpr size_t walk_smem_bytes() {
+    return WideKernel<M, MODE>::value ? sizeof(WalkSmemWide) : sizeof(WalkSmem);
+}
+
 template <class M, int MODE, int FAT>
 __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS_MIN_BLOCKS
                                                                         : DW_MIN_BLOCKS)
@@ -1173,10 +1184,10 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
     // slim layout: the edge the walker took, whose twin[] word comes with the
     // next node record (s_y[1] is idle between a step's end and its node gather)
     auto twe = [&]() -> ull& { return *reinterpret_cast<ull*>(&s_y[1][tid]); };
-    // reservoir-only modes: prev's row begin (the warp reservoir merges cur's
-    // row with prev's), in ring slot 0's y, idle in those modes
-    constexpr bool kPrevRow = (MODE == kForceErvs || MODE == kErvsNoJump) && M::kSecondOrder;
-    auto pbeg = [&]() -> ull& { return *reinterpret_cast<ull*>(&s_y[0][tid]); };
+    // wide kernels: prev's row begin (the warp reservoir merges cur's row
+    // with prev's; WalkSmemWide)
+    constexpr bool kPrevRow = WideKernel<M, MODE>::value && M::kSecondOrder;
+    auto pbeg = [&]() -> ull& { return reinterpret_cast<WalkSmemWide&>(sm).pbeg[tid]; };
 
     for (;;) {
         // ---- refill idle lanes: one atomic per warp (runtime.cpp:209-211)
@@ -1763,9 +1774,11 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
                 st = ervs_warp<M, kNoJump, kTma>(p.mp, T, K, p.rk, g, tb, tph, db, &nx, &ni, &dr,
                                                  ring, T.prev != kInvalid ? tpb : kNoRow);
             }
-            else if constexpr (WideKernel<M, MODE>::value)  // PR2: cap overruns, hand-offs
+            else if constexpr (WideKernel<M, MODE>::value) {  // PR2: cap overruns, hand-offs
+                const ull tpb = kPrevRow ? __shfl_sync(kFull, pbeg(), L) : kNoRow;
                 st = ervs_warp<M, kNoJump, false>(p.mp, T, K, p.rk, g, tb, tph, db, &nx, &ni, &dr,
-                                                  TmaRing{});
+                                                  TmaRing{}, T.prev != kInvalid ? tpb : kNoRow);
+            }
             else if constexpr (DW_PR2_PAR && CoopErjs<M>::value)
                 st = ervs_warp_cold<M, kNoJump>(p.mp, T, K, p.rk, g, tb, tph, db, &nx, &ni, &dr);
             else
