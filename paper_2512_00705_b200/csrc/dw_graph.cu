@@ -208,11 +208,29 @@ __device__ uint32_t tri_q(const EdgeRec* __restrict__ edges, const uint32_t* __r
     return q < 1u ? 1u : q;
 }
 
+// tri_q of every edge, once for both record layouts (one warp per row)
+__global__ void tri_build_kernel(const NodeRec* __restrict__ nodes, uint32_t nv,
+                                 const EdgeRec* __restrict__ edges,
+                                 const uint32_t* __restrict__ hslots, uint32_t work,
+                                 uint8_t* __restrict__ tq) {
+    const ull warp = (blockIdx.x * (ull)blockDim.x + threadIdx.x) >> 5;
+    const ull nwarps = ((ull)gridDim.x * blockDim.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    for (ull v = warp; v < nv; v += nwarps) {
+        const NodeRec nr = nodes[v];
+        for (ull i = lane; i < nr.degree; i += 32) {
+            const ull e = nr.begin + i;
+            const uint32_t u = load_col(edges + e);
+            tq[e] = (uint8_t)tri_q(edges, hslots, (uint32_t)v, nr, u, nodes[u], work);
+        }
+    }
+}
+
 __global__ void fat_build_kernel(const NodeRec* __restrict__ nodes, uint32_t nv,
                                  const EdgeRec* __restrict__ edges,
                                  const uint16_t* __restrict__ labels,
-                                 const uint8_t* __restrict__ lmask, const uint32_t* __restrict__ hslots,
-                                 uint32_t tri_work, FatRec* __restrict__ fat) {
+                                 const uint8_t* __restrict__ lmask, const uint8_t* __restrict__ tq,
+                                 FatRec* __restrict__ fat) {
     const ull warp = (blockIdx.x * (ull)blockDim.x + threadIdx.x) >> 5;
     const ull nwarps = ((ull)gridDim.x * blockDim.x) >> 5;
     const uint32_t lane = threadIdx.x & 31;
@@ -237,7 +255,7 @@ __global__ void fat_build_kernel(const NodeRec* __restrict__ nodes, uint32_t nv,
             f.twin_lo = lo;
             // multiplicity (24 bits; 0xFFFFFF = too many to describe) | triangle bound << 24
             f.twin_cnt = (hi - lo >= 0xFFFFFFu ? 0xFFFFFFu : hi - lo) |
-                         (tri_q(edges, hslots, (uint32_t)v, nr, er.col, nu, tri_work) << 24);
+                         ((uint32_t)tq[e] << 24);
             f.thmax = nu.hmax;
             f.thsum = nu.hsum;
             f.aux[0] = f.aux[1] = f.aux[2] = f.aux[3] = 0;
@@ -289,8 +307,7 @@ static cudaError_t build_twin(DeviceGraphBuffers& g, cudaStream_t s) {
 
 __global__ void fat32_build_kernel(const NodeRec* __restrict__ nodes, uint32_t nv,
                                    const EdgeRec* __restrict__ edges,
-                                   const uint32_t* __restrict__ hslots, uint32_t tri_work,
-                                   FatRec32* __restrict__ fat) {
+                                   const uint8_t* __restrict__ tq, FatRec32* __restrict__ fat) {
     const ull warp = (blockIdx.x * (ull)blockDim.x + threadIdx.x) >> 5;
     const ull nwarps = ((ull)gridDim.x * blockDim.x) >> 5;
     const uint32_t lane = threadIdx.x & 31;
@@ -321,7 +338,7 @@ __global__ void fat32_build_kernel(const NodeRec* __restrict__ nodes, uint32_t n
             const float fs = (float)nu.hsum;
             const uint32_t sb = isfinite(fs) ? __float_as_uint(fs) : 0x7fc00000u;
             f.thsum = __uint_as_float((sb & ~0xFFu) |
-                                      tri_q(edges, hslots, (uint32_t)v, nr, er.col, nu, tri_work));
+                                      (uint32_t)tq[e]);
             fat[e] = f;
         }
     }
@@ -367,6 +384,17 @@ static cudaError_t build_fat(DeviceGraphBuffers& g, cudaStream_t s) {
     // node2vec walks them (+5 % over the 64 B records at s24, and they fit
     // s27), the other models use the 64 B records built next when those fit.
     // Both layouts together stay under kFatMaxBytes and leave 4 GB free.
+    // the triangle bounds of every edge (1 B each), shared by both layouts
+    uint8_t* tq = nullptr;
+    DW_TRY(cudaMallocAsync(&tq, std::max<ull>(g.ne, 1), s));
+    tri_build_kernel<<<grid_for((ull)g.nv * 32, 256), 256, 0, s>>>(g.nodes, g.nv, g.edges, g.hslots,
+                                                                   tri_work(g.ne), tq);
+    DW_TRY(cudaGetLastError());
+    struct FreeTq {
+        uint8_t* p;
+        cudaStream_t s;
+        ~FreeTq() { cudaFreeAsync(p, s); }
+    } free_tq{tq, s};
     const bool compact_ok = !g.labels && g.max_degree < (1u << 24);
     const char* fenv = getenv("DW_FAT");
     ull used = 0;
@@ -377,7 +405,7 @@ static cudaError_t build_fat(DeviceGraphBuffers& g, cudaStream_t s) {
         if (need32 + (4ull << 30) <= fb) {
             DW_TRY(cudaMallocAsync(&g.fat32, need32, s));
             fat32_build_kernel<<<grid_for((ull)g.nv * 32, 256), 256, 0, s>>>(g.nodes, g.nv, g.edges,
-                                                                             g.hslots, tri_work(g.ne), g.fat32);
+                                                                             tq, g.fat32);
             DW_TRY(cudaGetLastError());
             DW_TRY(cudaStreamSynchronize(s));
             used = need32;
@@ -410,8 +438,7 @@ static cudaError_t build_fat(DeviceGraphBuffers& g, cudaStream_t s) {
         DW_TRY(cudaGetLastError());
     }
     fat_build_kernel<<<grid_for((ull)g.nv * 32, 256), 256, 0, s>>>(g.nodes, g.nv, g.edges,
-                                                                   g.labels, lmask, g.hslots, tri_work(g.ne),
-                                                                   g.fat);
+                                                                   g.labels, lmask, tq, g.fat);
     DW_TRY(cudaGetLastError());
     if (lmask) DW_TRY(cudaFreeAsync(lmask, s));
     return cudaStreamSynchronize(s);
