@@ -286,6 +286,24 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
+// arm a stage's mbarrier with `bytes` and issue its bulk copy, with the
+// shared-memory addresses already in the shared window (one asm block)
+__device__ __forceinline__ void bulk_stage(uint32_t dst, uint32_t bar, const void* src,
+                                           uint32_t bytes) {
+    asm volatile(
+        "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %3;\n"
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%2], %3, [%1];\n"
+        ::"r"(dst), "r"(bar), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+    } while (!done);
+}
 // order this thread's earlier generic shared-memory accesses before later
 // async-proxy (bulk copy) writes to the same bytes
 __device__ __forceinline__ void fence_proxy_async() {
@@ -394,15 +412,18 @@ __device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const Wa
     PrevWindow pw{pbegin, S.prev_degree, 0u, kInvalid, kInvalid, kInvalid};
     uint32_t par = 0;
     EPair nx{};
+    // the ring's shared-window addresses, formed once per row
+    const uint32_t stg0 = TMA ? smem_u32(ring.stage0) : 0u, bar0 = TMA ? smem_u32(ring.bar) : 0u;
+    const uint32_t stgb = ring.stride * 16u;  // bytes between stages
     if (TMA) {
         par = *ring.parity;
         if (lane == 0) {
+            // earlier generic writes to the stages (other phases' landing
+            // slots) before the bulk copies' async-proxy writes
             fence_proxy_async();
-            for (uint32_t c = 0; c < kTmaStages && c < nch; ++c) {
-                mbar_expect_tx(&ring.bar[c], chunk_bytes(c));
-                bulk_g2s(ring.stage0 + c * ring.stride, g.edges + abase + 64ull * c, chunk_bytes(c),
-                         &ring.bar[c]);
-            }
+            for (uint32_t c = 0; c < kTmaStages && c < nch; ++c)
+                bulk_stage(stg0 + c * stgb, bar0 + 8u * c, g.edges + abase + 64ull * c,
+                           chunk_bytes(c));
         }
     } else {
         nx = ervs_load_pair<M>(g, abase, 2u * lane, npos, off, d);
@@ -415,17 +436,16 @@ __device__ __forceinline__ int ervs_warp(const ModelParams& mp, Step S, const Wa
         EPair cp;
         if (TMA) {
             const uint32_t st = c % kTmaStages;
-            mbar_wait(&ring.bar[st], (par >> st) & 1u);
+            mbar_wait_u32(bar0 + 8u * st, (par >> st) & 1u);
             par ^= 1u << st;
             const uint4 v = ring.stage0[st * ring.stride + lane];
             cp = q < npos ? ervs_pair(v, 0u, i0, d) : EPair{kInvalid, kInvalid, 0.f, 0.f, 0u};
+            // every lane's read of the stage precedes its refill (the reads
+            // have completed: their values are consumed above)
             __syncwarp();
-            if (lane == 0 && c + kTmaStages < nch) {  // refill the stage just read
-                fence_proxy_async();
-                mbar_expect_tx(&ring.bar[st], chunk_bytes(c + kTmaStages));
-                bulk_g2s(ring.stage0 + st * ring.stride, g.edges + abase + 64ull * (c + kTmaStages),
-                         chunk_bytes(c + kTmaStages), &ring.bar[st]);
-            }
+            if (lane == 0 && c + kTmaStages < nch)  // refill the stage just read
+                bulk_stage(stg0 + st * stgb, bar0 + 8u * st,
+                           g.edges + abase + 64ull * (c + kTmaStages), chunk_bytes(c + kTmaStages));
         } else {
             cp = nx;
             if (base + 64 < npos) nx = ervs_load_pair<M>(g, abase, q + 64, npos, off, d);
