@@ -13,6 +13,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/dynwalk_b200.h"
@@ -95,6 +96,23 @@ struct Replica {
     ull* h_ends = nullptr;      // pinned [kRingSlots] batch end offsets
     cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
     cudaEvent_t ev_reset = nullptr;
+    // direct compact runs (run_direct): one launch writes the flat layout at
+    // predicted offsets and the host copies finished chunks while it walks
+    struct Direct {
+        uint32_t* q = nullptr;      // [cap_q] queries
+        ull* qids = nullptr;        // [cap_q] global walker ids
+        uint32_t* len = nullptr;    // [cap_q] predicted lengths
+        ull* offs = nullptr;        // [cap_q + 1] predicted offsets
+        uint32_t* flat = nullptr;   // [cap_flat] ids
+        unsigned* done = nullptr;   // [kMaxChunks] finished walkers per chunk
+        int* flag = nullptr;        // scratch (sink_targets)
+        unsigned* h_flag = nullptr; // host-mapped [kMaxChunks] chunk final flags
+        ull* h_bounds = nullptr;    // host-mapped [kMaxChunks + 1] chunk flat bounds
+        ull cap_q = 0, cap_flat = 0;
+        bool has_qids = false;
+        cudaEvent_t pre = nullptr, walk = nullptr, w0 = nullptr, w1 = nullptr;
+    } dir;
+    int sinks = -1;  // -1 unknown, 1: some edge leads to a vertex without neighbours
     // dw_run_device bookkeeping
     bool pending = false;
     ull pending_launches = 0;
@@ -150,6 +168,19 @@ int init_replica(Replica& r, int device) {
     return DW_OK;
 }
 
+// the direct compact runs' per-walker buffers (reallocated on next use)
+void free_direct(Replica::Direct& d) {
+    cudaFree(d.q);
+    cudaFree(d.qids);
+    cudaFree(d.len);
+    cudaFree(d.offs);
+    cudaFree(d.flat);
+    d.q = d.len = d.flat = nullptr;
+    d.qids = d.offs = nullptr;
+    d.cap_q = d.cap_flat = 0;
+    d.has_qids = false;
+}
+
 void free_replica(Replica& r) {
     if (cudaSetDevice(r.device) != cudaSuccess) return;
     if (r.stream) cudaStreamSynchronize(r.stream);
@@ -180,6 +211,13 @@ void free_replica(Replica& r) {
         for (cudaEvent_t e : {sl.h2d, sl.walk, sl.end, sl.d2h})
             if (e) cudaEventDestroy(e);
     }
+    free_direct(r.dir);
+    cudaFree(r.dir.done);
+    cudaFree(r.dir.flag);
+    if (r.dir.h_flag) cudaFreeHost(r.dir.h_flag);
+    if (r.dir.h_bounds) cudaFreeHost(r.dir.h_bounds);
+    for (cudaEvent_t e : {r.dir.pre, r.dir.walk, r.dir.w0, r.dir.w1})
+        if (e) cudaEventDestroy(e);
     cudaFree(r.d_base);
     cudaFree(r.d_scan);
     if (r.h_ends) cudaFreeHost(r.h_ends);
@@ -823,6 +861,246 @@ int run_engine(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries
     return DW_OK;
 }
 
+// ---- direct compact runs ---------------------------------------------------
+// dw_run_compact on one device for walks whose lengths are known before they
+// run: node2vec (a, b > 0: weights positive by construction), adaptive or
+// force-erjs, on a graph where no edge leads to a vertex without neighbours
+// (mirrored graphs: every target has its twin edge back).
+// Then no walk stops early (runtime.cpp:115-153: dead ends need d = 0 or
+// all-zero weights) and a path's length is 0 (start out of range), 1 (start
+// without neighbours) or target + 1.  The offsets of RunResult's flattened
+// paths are therefore a scan of the predicted lengths, computed before the
+// walk, and one launch writes every path straight to its final place.  The
+// walk counts finished walkers per chunk of 2^shift and raises a host-mapped
+// flag per finished chunk; this thread copies each chunk to the caller's
+// buffer as soon as it is final, so the copies overlap the walk and the run
+// ends one chunk copy after the walk does (the batched engine pays a launch
+// tail per batch and the final batch's copy).  A walk that ends up shorter
+// than predicted makes the ids written fall short of the predicted total (the
+// counters tell: every path is at most its predicted length), and the caller
+// re-runs the batched engine.
+constexpr ull kMaxChunks = 1024;
+constexpr int kDirectNo = 1;     // not applicable: use the batched engine
+constexpr int kDirectRetry = 2;  // prediction failed: use the batched engine
+
+int direct_ok(dw_graph_t g, const dw_model_desc* m, const dw_run_opts* o, ull nq) {
+    if (g->reps.size() != 1 || nq == 0 || nq >= (1ull << 32)) return kDirectNo;
+    // DW_DIRECT=0: always the batched engine; =2: predict even on a graph
+    // with sinks (tests of the short-walk -> batched re-run path)
+    bool force = false;
+    if (const char* e = std::getenv("DW_DIRECT")) {
+        if (e[0] == '0') return kDirectNo;
+        force = e[0] == '2';
+    }
+    // the walk kernels with the direct layout: node2vec, adaptive / force-erjs
+    // (dw_walk.cu DirectOk)
+    if (m->kind != DW_MODEL_NODE2VEC || !model_params(m).pos_weights) return kDirectNo;
+    if (o->mode != DW_MODE_ADAPTIVE && o->mode != DW_MODE_FORCE_ERJS) return kDirectNo;
+    Replica& r = g->reps[0];
+    if (force) return DW_OK;
+    if (r.sinks < 0) {
+        CU(cudaSetDevice(r.device), "cudaSetDevice");
+        if (!r.dir.flag) CU(cudaMalloc(&r.dir.flag, sizeof(int)), "cudaMalloc");
+        CU(cudaMemsetAsync(r.dir.flag, 0, sizeof(int), r.stream), "memset");
+        CU(dwb::sink_targets(r.g.nodes, r.g.edges, r.g.ne, r.dir.flag, r.stream), "sinks");
+        int f = 0;
+        CU(cudaMemcpyAsync(&f, r.dir.flag, sizeof(int), cudaMemcpyDeviceToHost, r.stream),
+           "D2H");
+        CU(cudaStreamSynchronize(r.stream), "sinks");
+        r.sinks = f ? 1 : 0;
+    }
+    return r.sinks ? kDirectNo : DW_OK;
+}
+
+// grows the direct buffers to nq walkers / nflat ids; kDirectNo when device
+// memory is short (the batched engine's ring is bounded)
+int direct_buffers(Replica& r, ull nq, ull nflat, bool qids) {
+    Replica::Direct& d = r.dir;
+    if (!d.done) {
+        CU(cudaMalloc(&d.done, kMaxChunks * sizeof(unsigned)), "cudaMalloc");
+        CU(cudaHostAlloc(&d.h_flag, kMaxChunks * sizeof(unsigned), cudaHostAllocMapped),
+           "cudaHostAlloc");
+        CU(cudaHostAlloc(&d.h_bounds, (kMaxChunks + 1) * sizeof(ull), cudaHostAllocMapped),
+           "cudaHostAlloc");
+        for (cudaEvent_t* e : {&d.pre, &d.walk})
+            CU(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "cudaEventCreate");
+        CU(cudaEventCreate(&d.w0), "cudaEventCreate");
+        CU(cudaEventCreate(&d.w1), "cudaEventCreate");
+    }
+    if (!d.flag) CU(cudaMalloc(&d.flag, sizeof(int)), "cudaMalloc");
+    if (nq > d.cap_q || (qids && !d.has_qids) || nflat > d.cap_flat) {
+        CU(cudaStreamSynchronize(r.stream), "sync");
+        CU(cudaStreamSynchronize(r.copy), "sync");
+        ull need = 0;
+        const ull cq = std::max(nq, d.cap_q);
+        const bool hq = qids || d.has_qids;
+        const ull cf = std::max(nflat, d.cap_flat);
+        if (cq > d.cap_q || hq != d.has_qids)
+            need += cq * (sizeof(uint32_t) * 2 + sizeof(ull) * (hq ? 2 : 1));
+        if (cf > d.cap_flat) need += cf * sizeof(uint32_t);
+        size_t fr = 0, tot = 0;
+        CU(cudaMemGetInfo(&fr, &tot), "cudaMemGetInfo");
+        if ((ull)fr < need + (2ull << 30)) return kDirectNo;
+        if (cq > d.cap_q || hq != d.has_qids) {
+            cudaFree(d.q);
+            cudaFree(d.qids);
+            cudaFree(d.len);
+            cudaFree(d.offs);
+            d.q = d.len = nullptr;
+            d.qids = d.offs = nullptr;
+            d.cap_q = 0;
+            CU(cudaMalloc(&d.q, cq * sizeof(uint32_t)), "cudaMalloc queries");
+            CU(cudaMalloc(&d.len, cq * sizeof(uint32_t)), "cudaMalloc lengths");
+            CU(cudaMalloc(&d.offs, (cq + 1) * sizeof(ull)), "cudaMalloc offsets");
+            if (hq) CU(cudaMalloc(&d.qids, cq * sizeof(ull)), "cudaMalloc walker ids");
+            d.cap_q = cq;
+            d.has_qids = hq;
+        }
+        if (cf > d.cap_flat) {
+            cudaFree(d.flat);
+            d.flat = nullptr;
+            d.cap_flat = 0;
+            CU(cudaMalloc(&d.flat, cf * sizeof(uint32_t)), "cudaMalloc flat paths");
+            d.cap_flat = cf;
+        }
+    }
+    size_t need = 0;
+    CU(dwb::path_offsets(nullptr, nq, nullptr, nullptr, nullptr, need, r.stream), "scan size");
+    if (need > r.scan_bytes) {
+        CU(cudaStreamSynchronize(r.stream), "sync");
+        cudaFree(r.d_scan);
+        r.d_scan = nullptr;
+        r.scan_bytes = 0;
+        CU(cudaMalloc(&r.d_scan, need), "cudaMalloc scan");
+        r.scan_bytes = need;
+    }
+    return DW_OK;
+}
+
+int run_direct(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries, ull nq,
+               const dw_run_opts* opts, const RunOut& out, dw_run_stats* st) {
+    int rc;
+    if ((rc = direct_ok(g, model, opts, nq))) return rc;
+    Replica& r = g->reps[0];
+    Replica::Direct& d = r.dir;
+    CU(cudaSetDevice(r.device), "cudaSetDevice");
+    if ((rc = prepare_model(r, model))) return rc;
+    // the flat size is known only after the scan: reserve the bound
+    // nq * (target + 1) (always enough) up front
+    const uint32_t target = target_steps(model, opts);
+    const ull bound = nq * ((ull)target + 1);
+    if ((rc = direct_buffers(r, nq, bound, opts->qids != nullptr))) return rc;
+    // ~256 chunks of >= 16K walkers (a smaller chunk's copy is launch-bound)
+    uint32_t shift = 14;
+    while ((nq >> shift) > 256 && shift < 24) ++shift;
+    while (((nq + (1ull << shift) - 1) >> shift) > kMaxChunks) ++shift;
+    const ull nch = (nq + (1ull << shift) - 1) >> shift;
+    cudaStream_t ws = r.stream, cp = r.copy;
+    std::memset(d.h_flag, 0, nch * sizeof(unsigned));
+    if (st) std::memset(st, 0, sizeof *st);
+    CU(cudaEventRecord(d.w0, ws), "event");
+    CU(cudaMemcpyAsync(d.q, queries, nq * sizeof(uint32_t), cudaMemcpyHostToDevice, ws),
+       "H2D queries");
+    if (opts->qids)
+        CU(cudaMemcpyAsync(d.qids, opts->qids, nq * sizeof(ull), cudaMemcpyHostToDevice, ws),
+           "H2D walker ids");
+    if ((rc = reset_run_state(r))) return rc;
+    CU(cudaMemsetAsync(d.done, 0, nch * sizeof(unsigned), ws), "memset");
+    CU(cudaMemsetAsync(r.d_base, 0, sizeof(ull), ws), "memset");
+    CU(dwb::predict_lengths(d.q, nq, r.g.nodes, r.g.nv, target, d.len, ws), "predict");
+    size_t tb = r.scan_bytes;
+    CU(dwb::path_offsets(d.len, nq, d.offs, r.d_base, r.d_scan, tb, ws), "scan");
+    CU(dwb::chunk_bounds(d.offs, nq, shift, nch, d.h_bounds, ws), "bounds");
+    CU(cudaEventRecord(d.pre, ws), "event");
+    CU(cudaEventSynchronize(d.pre), "predict");
+    const ull total = d.h_bounds[nch];
+    if (total > out.flat_cap)
+        return fail(DW_EINVAL, "flat path buffer too small: need %llu ids",
+                    (unsigned long long)total);
+    if (total && !out.flat) return fail(DW_EINVAL, "flat is NULL");
+    dwb::WalkParams p = make_params(r, model, opts);
+    p.queries = d.q;
+    p.nq = nq;
+    p.qid_base = opts->qid_base;
+    p.qids = opts->qids ? d.qids : nullptr;
+    p.paths = d.flat;
+    p.lengths = nullptr;
+    p.next_walker = r.queues;
+    p.offs = d.offs;
+    p.chunk_done = d.done;
+    p.chunk_flag = d.h_flag;
+    p.chunk_shift = shift;
+    CU(cudaMemsetAsync(p.next_walker, 0, sizeof(ull), ws), "memset");
+    CU(cudaEventRecord(r.ev_start, ws), "event");
+    CU(launch_model(r, model, opts->mode, p, ws), "walk");
+    CU(cudaEventRecord(r.ev_stop, ws), "event");
+    CU(cudaEventRecord(d.walk, ws), "event");
+    // the offsets are final already: their copy overlaps the walk
+    CU(cudaMemcpyAsync(out.offsets, d.offs, (nq + 1) * sizeof(ull), cudaMemcpyDeviceToHost, cp),
+       "D2H offsets");
+    // copy every chunk as soon as its walkers are final
+    volatile unsigned* flag = d.h_flag;
+    bool walk_done = false;
+    for (ull c = 0; c < nch; ++c) {
+        while (!flag[c]) {
+            if (walk_done) break;
+            if (cudaEventQuery(d.walk) == cudaSuccess) walk_done = true;  // recheck the flag
+            else std::this_thread::yield();
+        }
+        if (!flag[c]) break;  // the walk stopped on an error: collect() reports it
+        const ull lo = d.h_bounds[c], hi = d.h_bounds[c + 1];
+        if (hi > lo)
+            CU(cudaMemcpyAsync(out.flat + lo, d.flat + lo, (hi - lo) * sizeof(uint32_t),
+                               cudaMemcpyDeviceToHost, cp),
+               "D2H paths");
+    }
+    CU(cudaStreamWaitEvent(cp, d.walk, 0), "event");
+    CU(cudaEventRecord(d.w1, cp), "event");
+    CU(cudaStreamSynchronize(ws), "walk");
+    if ((rc = collect(r, st, 0))) {
+        cudaStreamSynchronize(cp);
+        return rc;
+    }
+    CU(cudaStreamSynchronize(cp), "copy");
+    // every path is at most its predicted length, so the lengths all match
+    // iff their sum does: ids written = walkers with a start in range + steps
+    // that advanced (runtime.cpp:141-149)
+    dw_run_stats cs;
+    std::memset(&cs, 0, sizeof cs);
+    {
+        ull c[dwb::kCNum];
+        CU(cudaMemcpy(c, r.counters, sizeof c, cudaMemcpyDeviceToHost), "D2H counters");
+        add_counters(&cs, c);
+    }
+    const bool mis = cs.queries - cs.query_errors + cs.steps - cs.dead_ends != total;
+    if (const char* tp = std::getenv("DW_ENGINE_TRACE"))
+        if (FILE* f = std::fopen(tp, "a")) {
+            std::fprintf(f, "X %llu %s\n", (unsigned long long)nq, mis ? "retry" : "ok");
+            std::fclose(f);
+        }
+    if (mis) {
+        r.sinks = 1;  // do not predict on this graph again
+        return kDirectRetry;
+    }
+    if (st) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.ev_start, r.ev_stop);
+        st->kernel_ms = ms;
+        cudaEventElapsedTime(&ms, d.w0, d.w1);
+        st->total_ms = ms;
+        st->kernel_launches = 6;
+    }
+    if (std::getenv("DW_VERBOSE")) {
+        float a = 0.f, b = 0.f, c = 0.f;
+        cudaEventElapsedTime(&a, d.w0, r.ev_start);
+        cudaEventElapsedTime(&b, r.ev_start, r.ev_stop);
+        cudaEventElapsedTime(&c, r.ev_stop, d.w1);
+        std::fprintf(stderr, "dynwalk direct: %llu chunks, before walk %.3f ms, walk %.3f ms, after %.3f ms\n",
+                     (unsigned long long)nch, a, b, c);
+    }
+    return DW_OK;
+}
+
 }  // namespace
 
 // ---- DWG1 binary CSR cache, streamed to the devices (graph.cpp:217-300) ----
@@ -1142,11 +1420,22 @@ int dw_graph_download(dw_graph_t g, uint64_t* row, uint32_t* col, float* prop, u
     if (!g) return fail(DW_EINVAL, "graph handle is NULL");
     Replica& r = g->reps[0];
     CU(cudaSetDevice(r.device), "cudaSetDevice");
+    // the unpacked CSR needs ~8 B per edge of scratch: give back the direct
+    // compact runs' cached buffers first (config 5: 45 GB)
+    CU(cudaStreamSynchronize(r.stream), "sync");
+    CU(cudaStreamSynchronize(r.copy), "sync");
+    free_direct(r.dir);
     const ull nv = g->nv, ne = g->ne;
     ull* d_row = nullptr;
     uint32_t* d_col = nullptr;
     float* d_prop = nullptr;
     double *d_nmax = nullptr, *d_nsum = nullptr;
+    struct Scratch {
+        void** p[5];
+        ~Scratch() {
+            for (void** q : p) cudaFree(*q);
+        }
+    } scratch{{(void**)&d_row, (void**)&d_col, (void**)&d_prop, (void**)&d_nmax, (void**)&d_nsum}};
     if (row) CU(cudaMalloc(&d_row, (nv + 1) * sizeof(ull)), "cudaMalloc");
     if (col) CU(cudaMalloc(&d_col, std::max<ull>(ne, 1) * sizeof(uint32_t)), "cudaMalloc");
     if (prop) CU(cudaMalloc(&d_prop, std::max<ull>(ne, 1) * sizeof(float)), "cudaMalloc");
@@ -1161,11 +1450,6 @@ int dw_graph_download(dw_graph_t g, uint64_t* row, uint32_t* col, float* prop, u
     if (nsum && nv) CU(cudaMemcpy(nsum, d_nsum, nv * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
     if (label && r.g.labels && ne)
         CU(cudaMemcpy(label, r.g.labels, ne * sizeof(uint16_t), cudaMemcpyDeviceToHost), "D2H");
-    cudaFree(d_row);
-    cudaFree(d_col);
-    cudaFree(d_prop);
-    cudaFree(d_nmax);
-    cudaFree(d_nsum);
     return DW_OK;
 }
 
@@ -1402,6 +1686,8 @@ int dw_run_compact(dw_graph_t g, const dw_model_desc* model, const uint32_t* que
     out.offsets = reinterpret_cast<ull*>(offsets);
     out.flat = flat;
     out.flat_cap = flat_capacity;
+    rc = run_direct(g, model, queries, nq, opts, out, st);
+    if (rc != kDirectNo && rc != kDirectRetry) return rc;
     return run_engine(g, model, queries, nq, opts, out, st);
 }
 

@@ -1208,6 +1208,62 @@ cudaError_t compact_paths(const uint32_t* paths, const uint32_t* lengths, ull n,
     return cudaGetLastError();
 }
 
+// ---- direct compact runs (dw_capi.cu run_direct) --------------------------------
+// Predicted path length of each query: 0 for a start out of range (a query
+// error, runtime.cpp:213-217), 1 for a start without neighbours (or a
+// zero-step walk), target + 1 otherwise.  Exact on graphs where no edge
+// leads to a vertex without neighbours and for models whose weights are
+// positive by construction: no walk can then stop early.
+__global__ void predict_lengths_kernel(const uint32_t* __restrict__ q, ull n,
+                                       const NodeRec* __restrict__ nodes, uint32_t nv,
+                                       uint32_t target, uint32_t* __restrict__ len) {
+    for (ull i = (ull)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (ull)gridDim.x * blockDim.x) {
+        const uint32_t v = q[i];
+        len[i] = v >= nv ? 0u : (target && nodes[v].degree) ? target + 1u : 1u;
+    }
+}
+
+cudaError_t predict_lengths(const uint32_t* queries, ull n, const NodeRec* nodes, uint32_t nv,
+                            uint32_t target, uint32_t* lengths, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    predict_lengths_kernel<<<grid_for(n, 256 * 8), 256, 0, s>>>(queries, n, nodes, nv, target,
+                                                                lengths);
+    return cudaGetLastError();
+}
+
+// out[c] = offs[min(c << shift, n)], c = 0..nchunks (out may be host-mapped)
+__global__ void chunk_bounds_kernel(const ull* __restrict__ offs, ull n, uint32_t shift,
+                                    ull nchunks, ull* out) {
+    for (ull c = (ull)blockIdx.x * blockDim.x + threadIdx.x; c <= nchunks;
+         c += (ull)gridDim.x * blockDim.x)
+        out[c] = offs[min(c << shift, n)];
+}
+
+cudaError_t chunk_bounds(const ull* offs, ull n, uint32_t shift, ull nchunks, ull* out,
+                         cudaStream_t s) {
+    chunk_bounds_kernel<<<grid_for(nchunks + 1, 256), 256, 0, s>>>(offs, n, shift, nchunks, out);
+    return cudaGetLastError();
+}
+
+// *flag <- 1 when some edge leads to a vertex without neighbours
+__global__ void sink_targets_kernel(const NodeRec* __restrict__ nodes,
+                                    const EdgeRec* __restrict__ edges, ull ne,
+                                    int* __restrict__ flag) {
+    bool sink = false;
+    for (ull e = (ull)blockIdx.x * blockDim.x + threadIdx.x; e < ne;
+         e += (ull)gridDim.x * blockDim.x)
+        sink |= nodes[edges[e].col].degree == 0;
+    if (__any_sync(0xFFFFFFFFu, sink) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+cudaError_t sink_targets(const NodeRec* nodes, const EdgeRec* edges, ull ne, int* flag,
+                         cudaStream_t s) {
+    if (ne == 0) return cudaSuccess;
+    sink_targets_kernel<<<grid_for(ne, 256 * 16), 256, 0, s>>>(nodes, edges, ne, flag);
+    return cudaGetLastError();
+}
+
 // ---- DWG1 loads ----------------------------------------------------------------
 __global__ void check_props_kernel(const float* __restrict__ prop, ull ne, int* __restrict__ bad) {
     for (ull e = blockIdx.x * (ull)blockDim.x + threadIdx.x; e < ne;

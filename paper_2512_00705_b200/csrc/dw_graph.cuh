@@ -106,4 +106,16 @@ cudaError_t compact_paths(const uint32_t* paths, const uint32_t* lengths, unsign
                           unsigned long long stride, const unsigned long long* offs,
                           uint32_t* flat, cudaStream_t s);
 
+// ---- direct compact runs (dw_capi.cu run_direct) ------------------------------
+// lengths[i] = the path length query i has unless its walk stops early (0 for
+// a start >= nv, 1 for a start without neighbours or target 0, else target+1)
+cudaError_t predict_lengths(const uint32_t* queries, unsigned long long n, const NodeRec* nodes,
+                            uint32_t nv, uint32_t target, uint32_t* lengths, cudaStream_t s);
+// out[c] = offs[min(c << shift, n)] for c = 0..nchunks
+cudaError_t chunk_bounds(const unsigned long long* offs, unsigned long long n, uint32_t shift,
+                         unsigned long long nchunks, unsigned long long* out, cudaStream_t s);
+// *flag |= 1 if some edge's target has no neighbours (a walk can end early)
+cudaError_t sink_targets(const NodeRec* nodes, const EdgeRec* edges, unsigned long long ne,
+                         int* flag, cudaStream_t s);
+
 }  // namespace dwb

@@ -4,26 +4,40 @@
 
 namespace dwb {
 
-template <class M, int MODE, int FAT>
+template <class M, int MODE, int FAT, bool DIRECT>
 static cudaError_t launch_t(const WalkParams& p, int num_sms, cudaStream_t stream) {
     int per_sm = 0;
     const size_t smem = walk_smem_bytes<M, MODE>();
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
-        cudaError_t ea = cudaFuncSetAttribute(walk_kernel<M, MODE, FAT>,
+        cudaError_t ea = cudaFuncSetAttribute(walk_kernel<M, MODE, FAT, DIRECT>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (ea != cudaSuccess) return ea;
         attr_set = true;
     }
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, walk_kernel<M, MODE, FAT>, kThreads, smem);
+        &per_sm, walk_kernel<M, MODE, FAT, DIRECT>, kThreads, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
     unsigned long long blocks = (unsigned long long)num_sms * per_sm;
     const unsigned long long need = (p.nq + kThreads - 1) / kThreads;
     if (need < blocks) blocks = need ? need : 1;
-    walk_kernel<M, MODE, FAT><<<(unsigned)blocks, kThreads, smem, stream>>>(p);
+    walk_kernel<M, MODE, FAT, DIRECT><<<(unsigned)blocks, kThreads, smem, stream>>>(p);
     return cudaGetLastError();
+}
+
+// direct compact runs (p.offs set; dw_capi.cu run_direct) are node2vec's
+// adaptive and force-erjs walks: the kernels with the flat-layout writes and
+// chunk counts are instantiated for those only
+template <class M> struct DirectOk { static constexpr bool value = false; };
+template <bool W> struct DirectOk<Node2VecModel<W>> { static constexpr bool value = true; };
+
+template <class M, int MODE, int FAT>
+static cudaError_t launch_d(const WalkParams& p, int num_sms, cudaStream_t s) {
+    if constexpr (DirectOk<M>::value && (MODE == kAdaptive || MODE == kForceErjs))
+        if (p.offs) return launch_t<M, MODE, FAT, true>(p, num_sms, s);
+    if (p.offs) return cudaErrorInvalidValue;
+    return launch_t<M, MODE, FAT, false>(p, num_sms, s);
 }
 
 // compact 32 B records (FAT = 2) are walked by node2vec, in preference to the
@@ -42,16 +56,16 @@ static cudaError_t launch_m(int mode, const WalkParams& p, int num_sms, cudaStre
     switch (mode) {
     case kAdaptive:
         if constexpr (UsesFat32<M>::value)
-            if (fat32) return launch_t<M, kAdaptive, 2>(p, num_sms, s);
-        if (fat) return launch_t<M, kAdaptive, 1>(p, num_sms, s);
-        return launch_t<M, kAdaptive, 0>(p, num_sms, s);
+            if (fat32) return launch_d<M, kAdaptive, 2>(p, num_sms, s);
+        if (fat) return launch_d<M, kAdaptive, 1>(p, num_sms, s);
+        return launch_d<M, kAdaptive, 0>(p, num_sms, s);
     case kForceErjs:
         if constexpr (UsesFat32<M>::value)
-            if (fat32) return launch_t<M, kForceErjs, 2>(p, num_sms, s);
-        if (fat) return launch_t<M, kForceErjs, 1>(p, num_sms, s);
-        return launch_t<M, kForceErjs, 0>(p, num_sms, s);
-    case kForceErvs: return launch_t<M, kForceErvs, 0>(p, num_sms, s);
-    case kErvsNoJump: return launch_t<M, kErvsNoJump, 0>(p, num_sms, s);
+            if (fat32) return launch_d<M, kForceErjs, 2>(p, num_sms, s);
+        if (fat) return launch_d<M, kForceErjs, 1>(p, num_sms, s);
+        return launch_d<M, kForceErjs, 0>(p, num_sms, s);
+    case kForceErvs: return launch_d<M, kForceErvs, 0>(p, num_sms, s);
+    case kErvsNoJump: return launch_d<M, kErvsNoJump, 0>(p, num_sms, s);
     }
     return cudaErrorInvalidValue;
 }

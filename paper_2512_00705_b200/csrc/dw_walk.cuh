@@ -38,6 +38,13 @@ struct WalkParams {
     int* error;                       // first DevError
     unsigned long long* error_info;   // offending query index
     ModelParams mp;
+    // direct compact output (dw_capi.cu run_direct): paths is the flat id
+    // array and walker i's path starts at offs[i] (offs: [nq + 1], the scan
+    // of the predicted lengths); null: paths is [nq][stride]
+    const unsigned long long* offs;
+    unsigned int* chunk_done;         // [nq >> chunk_shift] finished walkers, or null
+    unsigned int* chunk_flag;         // host-mapped: 1 once every walker of the chunk is final
+    unsigned int chunk_shift;
 };
 
 enum Mode : int { kAdaptive = 0, kForceErvs = 1, kForceErjs = 2, kErvsNoJump = 3 };

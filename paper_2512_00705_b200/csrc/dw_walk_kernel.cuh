@@ -61,6 +61,9 @@ namespace dwb {
 #ifndef DW_MIN_BLOCKS
 #define DW_MIN_BLOCKS 3
 #endif
+#ifndef DW_DONE_MODE
+#define DW_DONE_MODE 0
+#endif
 #ifndef DW_RING
 #define DW_RING 2
 #endif
@@ -89,7 +92,9 @@ constexpr uint32_t kEWait = DW_EWAIT;
 constexpr unsigned kFull = 0xFFFFFFFFu;
 typedef unsigned long long ull;
 
-enum Phase : uint32_t { P_IDLE = 0, P_NODE, P_TRIAL, P_FETCH, P_VREC, P_VMEMB, P_COOP, P_EMATH, P_CJS };
+// P_DONE: the walk just ended; the next iteration's refill site books it
+// (one code site for the direct compact output's chunk accounting)
+enum Phase : uint32_t { P_IDLE = 0, P_NODE, P_TRIAL, P_FETCH, P_VREC, P_VMEMB, P_COOP, P_EMATH, P_CJS, P_DONE };
 
 // Warp-cooperative eRJS for models whose bounds can be far above the typical
 // weight (second-order PageRank: thousands of trials on hub rows, SURVEY
@@ -121,7 +126,7 @@ constexpr uint32_t kCjsMin = DW_CJS_MIN;
 // 64-bit counter.
 enum LaneCounter : int {
     LC_ETRIALS = 0, LC_EREADS, LC_EDRAWS, LC_ALG4, LC_NUM64,
-    LC_ETRIALS1 = LC_NUM64, LC_FALLBACKS, LC_DEADENDS, LC_QERRORS, LC_QUERIES, LC_NUM
+    LC_ETRIALS1 = LC_NUM64, LC_FALLBACKS, LC_DEADENDS, LC_NUM
 };
 
 __device__ __forceinline__ bool valid_w(double w) { return !(w < 0.0) && isfinite(w); }
@@ -949,6 +954,12 @@ struct WalkSmem {
         twlo[kThreads], twcnt[kThreads], nret[kThreads];
     double bound[kThreads], mnr[kThreads];
     uint32_t qi[kThreads];           // the lane's walker: index in this launch
+    // first entry of the lane's path in p.paths: qi * stride (padded rows),
+    // or p.offs[qi] (direct compact output)
+    ull rowb[kThreads];
+    // direct compact output: chunk of the walker that ended last iteration,
+    // booked after this iteration's gathers are issued (0xFFFF: none)
+    uint16_t dchunk[kThreads];
     // f32 bits of the current step's triangle bound (Step::hin, rounded up):
     // props of the edges (cur -> u) with u in N(prev) are <= it
     uint32_t tq[kThreads];
@@ -960,6 +971,11 @@ struct WalkSmem {
     ull mbar[kThreads / 32][kTmaStages];
     uint32_t tmaph[kThreads / 32];
 };
+
+// DW_MIN_BLOCKS CTAs of the narrow kernels must fit one SM's 228 KB of shared
+// memory, 1 KB of which each CTA reserves (one CTA less costs ~30 %)
+static_assert(DW_THREADS != 256 || DW_MIN_BLOCKS * (sizeof(WalkSmem) + 1024) <= 228 * 1024,
+              "WalkSmem too large for DW_MIN_BLOCKS CTAs per SM");
 
 // reservoir-only modes (force-ervs, ervs-nojump) spend their time in the
 // warp-cooperative row scan, whose parallel jump chain needs ~14 more live
@@ -990,7 +1006,10 @@ constexpr size_t walk_smem_bytes() {
     return WideKernel<M, MODE>::value ? sizeof(WalkSmemWide) : sizeof(WalkSmem);
 }
 
-template <class M, int MODE, int FAT>
+// DIRECT: paths go to the flat layout at p.offs (direct compact runs,
+// dw_capi.cu run_direct) with per-chunk completion counts; compiled only into
+// the kernels such runs use, so the padded-row kernels carry none of it
+template <class M, int MODE, int FAT, bool DIRECT = false>
 __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS_MIN_BLOCKS
                                                                         : DW_MIN_BLOCKS)
     walk_kernel(const __grid_constant__ WalkParams p) {
@@ -1018,6 +1037,7 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
     for (int i = tid; i < 66; i += blockDim.x) s_hist[i] = 0;
 #pragma unroll
     for (int c = 0; c < LC_NUM64; ++c) s_lc[c][tid] = 0;
+    sm.dchunk[tid] = 0xFFFFu;
 #pragma unroll
     for (int c = 0; c < LC_NUM - LC_NUM64; ++c) sm.lc32[c][tid] = 0;
     constexpr bool kTma = DW_ERVS_TMA && (MODE == kForceErvs || MODE == kErvsNoJump) &&
@@ -1038,8 +1058,7 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
             x = y;
             if (y < (uint32_t)v) {
                 const int gc = c == LC_ETRIALS1 ? kCTrials : c == LC_FALLBACKS ? kCFallbacks
-                               : c == LC_DEADENDS ? kCDeadEnds : c == LC_QERRORS ? kCQueryErrors
-                                                                                : kCQueries;
+                                                             : kCDeadEnds;
                 atomicAdd(&p.counters[gc], 1ull << 32);
             }
         }
@@ -1124,31 +1143,61 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
         lc_add(LC_ALG4, c_alg4);
         c_trials = c_alg4 = 0;
     };
+    // a walker's path is final (direct compact output): count it in its
+    // chunk; the walker that completes a chunk raises the chunk's host-mapped
+    // flag, so the host copies the chunk while the launch walks on
+    // (acq_rel: every path write of the chunk precedes the flag)
+    auto chunk_done = [&]() {
+        const uint32_t c = sm.dchunk[tid];
+        if (c == 0xFFFFu) return;
+        sm.dchunk[tid] = 0xFFFFu;
+        unsigned old;
+#if DW_DONE_MODE == 0
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                     : "=r"(old) : "l"(p.chunk_done + c) : "memory");
+#elif DW_DONE_MODE == 1  // measurement only: no ordering
+        old = atomicAdd(p.chunk_done + c, 1u);
+#else
+        return;
+#endif
+        const ull lo = (ull)c << p.chunk_shift;
+        const ull n = min(p.nq - lo, 1ull << p.chunk_shift);
+        if ((ull)old + 1 == n) {
+            __threadfence_system();
+            *(volatile unsigned*)(p.chunk_flag + c) = 1u;
+        }
+    };
+    // first entry of the lane's path: its row of the padded [nq][stride]
+    // layout, or its offset in the flat layout (DIRECT)
+    auto row_start = [&]() -> uint32_t* {
+        return DIRECT ? p.paths + sm.rowb[tid] : p.paths + (ull)sm.qi[tid] * p.stride;
+    };
     // path entry `step` (stage; a completed 32 B sector is written whole)
     auto put_path = [&](uint32_t v) {
-        uint32_t* a = p.paths + ((ull)sm.qi[tid] * p.stride + step);
+        uint32_t* const rs = row_start();
+        uint32_t* a = rs + step;
         const uint32_t k = (uint32_t)(reinterpret_cast<unsigned long long>(a) >> 2) & 7u;
         sm.pst[k][tid] = v;
         if (k == 7u) {
             uint32_t* s0 = a - 7;
-            if (s0 >= p.paths + (ull)sm.qi[tid] * p.stride) {  // the sector is this walker's
+            if (s0 >= rs) {  // the sector is this walker's
                 reinterpret_cast<uint4*>(s0)[0] =
                     make_uint4(sm.pst[0][tid], sm.pst[1][tid], sm.pst[2][tid], sm.pst[3][tid]);
                 reinterpret_cast<uint4*>(s0)[1] =
                     make_uint4(sm.pst[4][tid], sm.pst[5][tid], sm.pst[6][tid], sm.pst[7][tid]);
             } else {  // the row's first sector, shared with the previous row
-                for (uint32_t* q = p.paths + (ull)sm.qi[tid] * p.stride; q <= a; ++q)
+                for (uint32_t* q = rs; q <= a; ++q)
                     *q = sm.pst[(uint32_t)(reinterpret_cast<unsigned long long>(q) >> 2) & 7u][tid];
             }
         }
     };
     // the staged entries of the last, incomplete sector
     auto flush_path = [&]() {
-        uint32_t* a = p.paths + ((ull)sm.qi[tid] * p.stride + step);
+        uint32_t* const rs = row_start();
+        uint32_t* a = rs + step;
         const uint32_t k = (uint32_t)(reinterpret_cast<unsigned long long>(a) >> 2) & 7u;
         if (k == 7u) return;
         uint32_t* q = a - k;
-        uint32_t* rs = p.paths + (ull)sm.qi[tid] * p.stride;
         if (q < rs) q = rs;
         for (; q <= a; ++q)
             *q = sm.pst[(uint32_t)(reinterpret_cast<unsigned long long>(q) >> 2) & 7u][tid];
@@ -1157,7 +1206,7 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
         if (p.lengths) p.lengths[sm.qi[tid]] = step + 1;
         if (p.paths) flush_path();
         flush_walker();
-        phase = P_IDLE;
+        phase = DIRECT ? P_DONE : P_IDLE;
     };
     auto start_ervs = [&](ull draw_base) {
         tn = 0;
@@ -1210,6 +1259,11 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
     auto pbeg = [&]() -> ull& { return reinterpret_cast<WalkSmemWide&>(sm).pbeg[tid]; };
 
     for (;;) {
+        // ---- walks that ended last iteration (end_walk)
+        if (DIRECT && phase == P_DONE) {
+            sm.dchunk[tid] = (uint16_t)(sm.qi[tid] >> p.chunk_shift);
+            phase = P_IDLE;
+        }
         // ---- refill idle lanes: one atomic per warp (runtime.cpp:209-211)
         unsigned need = __ballot_sync(kFull, phase == P_IDLE);
         if (need && !drained) {
@@ -1224,21 +1278,25 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
                 base = __shfl_sync(kFull, base, leader);
                 if (base + (ull)n >= p.nq) drained = true;
                 if (lane == leader && base < p.nq)  // one counter add per claim
-                    lc_add(LC_QUERIES, min((ull)n, p.nq - base));
+                    atomicAdd(&p.counters[kCQueries], min((ull)n, p.nq - base));
                 if (phase == P_IDLE) {
                     const ull i = base + (ull)__popc(need & lt_mask);
                     if (i < p.nq) {
                         const uint32_t start = p.queries[i];
+                        const ull rb = DIRECT ? p.offs[i] : i * p.stride;
+                        sm.qi[tid] = (uint32_t)i;
                         if (start >= g.nv) {  // runtime.cpp:213-217
-                            lc_add(LC_QERRORS, 1);
+                            atomicAdd(&p.counters[kCQueryErrors], 1ull);
                             if (p.lengths) p.lengths[i] = 0;
+                            if (DIRECT) phase = P_DONE;  // booked next iteration
                         } else {
                             if (p.target == 0) {
-                                if (p.paths) p.paths[i * p.stride] = start;
+                                if (p.paths) p.paths[rb] = start;
                                 if (p.lengths) p.lengths[i] = 1;
+                                if (DIRECT) phase = P_DONE;
                             } else {
                                 phase = P_NODE;
-                                sm.qi[tid] = (uint32_t)i;
+                                if (DIRECT) sm.rowb[tid] = rb;
                                 qg = p.qids ? p.qids[i] : p.qid_base + i;
                                 step = 0;
                                 if (p.paths) put_path(start);
@@ -1375,6 +1433,10 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
             cp16(&s_mb[0][tid], pair_of(g.edges, e));
             if (M::kUsesLabels && g.labels) cp4(&s_mb[1][tid], g.labels + (e & ~1ull));
         }
+        // a walk that ended last iteration is final: count it in its chunk
+        // (direct compact output; its release and round trip overlap the
+        // gathers just issued)
+        if (DIRECT) chunk_done();
         // ---- B
         cp_wait_all();
 
@@ -1957,6 +2019,7 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
             }
         }
     }
+    if (DIRECT) chunk_done();  // the walks that ended in the last iteration
 
     // ---- flush counters: eRJS trials count as trials, reads and 2 draws each
     __syncthreads();
@@ -1975,8 +2038,6 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
         s_cnt[kCAlgBytes] = 4 * s_lct[LC_ALG4];
         s_cnt[kCFallbacks] += s_lct[LC_FALLBACKS];
         s_cnt[kCDeadEnds] += s_lct[LC_DEADENDS];
-        s_cnt[kCQueryErrors] += s_lct[LC_QERRORS];
-        s_cnt[kCQueries] += s_lct[LC_QUERIES];
     }
     __syncthreads();
     for (int i = tid; i < kCNum; i += blockDim.x)

@@ -387,6 +387,91 @@ def test_compact_output_matches_padded(dw, orc):
         assert st[k] == r.stats[k], k
 
 
+def _compact_pair(dw, dg, model, q, opts, env, trace):
+    """dw_run_compact under `env` and under the batched engine (DW_DIRECT=0);
+    returns both results and the run engine trace lines of the first."""
+    if os.path.exists(trace):
+        os.remove(trace)
+    a = _with_env(dict(env, DW_ENGINE_TRACE=trace),
+                  lambda: dw.run_queries_compact(dg, model, q, opts))
+    lines = open(trace).read().split() if os.path.exists(trace) else []
+    b = _with_env({"DW_DIRECT": "0"}, lambda: dw.run_queries_compact(dg, model, q, opts))
+    return a, b, lines
+
+
+def _assert_compact_equal(a, b, tag):
+    assert np.array_equal(a[0], b[0]), tag
+    assert np.array_equal(a[1], b[1]), tag
+    for k in ("steps", "select_erjs", "select_ervs", "trials", "weight_reads", "rng_draws",
+              "dead_ends", "query_errors", "erjs_fallbacks", "queries"):
+        assert a[2][k] == b[2][k], (tag, k)
+
+
+@pytest.mark.parametrize("layout", ["default", "slim", "fat64"])
+@pytest.mark.parametrize("mk", [dict(kind="node2vec", a=0.5, b=2.0),
+                                dict(kind="node2vec", a=2.0, b=0.5, weighted=False)],
+                         ids=["weighted", "unweighted"])
+def test_direct_compact_output(dw, orc, mk, layout, tmp_path):
+    """dw_run_compact's direct engine (one launch writing every path at its
+    predicted flat offset, chunks copied while the walk runs) gives the
+    batched engine's offsets, ids and counters: mirrored graph, invalid starts
+    (empty paths), isolated starts (length 1), several chunks, every record
+    layout, adaptive and force-erjs; other models keep the batched engine."""
+    og = orc.Graph.rmat(13, 16, 21).synth_philox("uniform", 1.0, 5.0, seed=22)
+    env = {"default": {}, "slim": {"DW_FAT": "0"}, "fat64": {"DW_FAT": "1"}}[layout]
+    dg = _with_env(env, lambda: to_device(dw, og))
+    rng = np.random.default_rng(4)
+    q = rng.integers(0, og.nv + 50, 1_500_000).astype(np.uint32)
+    model = dw.Model(**mk)
+    trace = str(tmp_path / "trace.txt")
+    for mode, L in (("adaptive", 30), ("adaptive", 1), ("adaptive", 0), ("force-erjs", 12)):
+        opts = dw.RunOptions(mode=mode, walk_length=L, seed=5, edge_cost_ratio=1.3)
+        a, b, lines = _compact_pair(dw, dg, model, q, opts, {}, trace)
+        assert lines[:3] == ["X", str(len(q)), "ok"], (mk, mode, L, lines[:6])
+        _assert_compact_equal(a, b, (mk, mode, L))
+    # the padded run agrees too (lengths = offset differences)
+    opts = dw.RunOptions(mode="adaptive", walk_length=20, seed=9, edge_cost_ratio=1.3)
+    r = dw.run_queries(dg, model, q[:200_000], opts)
+    offs, flat, _ = dw.run_queries_compact(dg, model, q[:200_000], opts)
+    assert np.array_equal(np.diff(offs.astype(np.int64)), r.lengths.astype(np.int64))
+    mask = np.arange(r.paths.shape[1])[None, :] < r.lengths[:, None]
+    assert np.array_equal(flat, r.paths[mask])
+    # PR2 and the reservoir-only modes stay on the batched engine
+    for m2, mode in ((dw.Model(kind="pr2", gamma=0.15), "adaptive"), (model, "force-ervs")):
+        opts = dw.RunOptions(mode=mode, walk_length=10, seed=5, edge_cost_ratio=1.3)
+        a, b, lines = _compact_pair(dw, dg, m2, q[:300_000], opts, {}, trace)
+        assert "X" not in lines, (mode, lines[:6])
+        _assert_compact_equal(a, b, ("batched", mode))
+
+
+def test_direct_compact_falls_back_on_sinks(dw, orc, tmp_path):
+    """A directed graph with sinks: walks stop early, so the direct engine is
+    not used (no X trace line); forced (DW_DIRECT=2) it detects the shorter
+    walks, and the batched re-run gives the same output."""
+    rng = np.random.default_rng(6)
+    n = 4000
+    src = rng.integers(0, n, 30000).astype(np.uint32)
+    dst = rng.integers(0, n, 30000).astype(np.uint32)
+    keep = src % 5 != 0  # vertices 0, 5, 10 ... have in-edges only: sinks
+    src, dst = src[keep], dst[keep]
+    prop = rng.uniform(1.0, 5.0, len(src)).astype(np.float32)
+    og = orc.Graph.build(src, dst, prop, mirror=False, nv_hint=n)
+    dg = to_device(dw, og)
+    q = np.arange(og.nv, dtype=np.uint32).repeat(40)
+    model = dw.Model(kind="node2vec", a=0.5, b=2.0)
+    opts = dw.RunOptions(mode="adaptive", walk_length=40, seed=3, edge_cost_ratio=1.3)
+    trace = str(tmp_path / "trace.txt")
+    a, b, lines = _compact_pair(dw, dg, model, q, opts, {"DW_DIRECT": "2"}, trace)
+    assert lines[:3] == ["X", str(len(q)), "retry"], lines[:6]
+    _assert_compact_equal(a, b, "forced")
+    a, b, lines = _compact_pair(dw, dg, model, q, opts, {}, trace)
+    assert "X" not in lines, lines[:6]
+    _assert_compact_equal(a, b, "default")
+    r = dw.run_queries(dg, model, q, opts)
+    assert r.stats["steps"] > 0 and (r.lengths < 41).any()
+    assert np.array_equal(np.diff(a[0].astype(np.int64)), r.lengths.astype(np.int64))
+
+
 def _write_dwg1(path, row, col, prop, label=None):
     """DWG1 as dynwalk::save_binary writes it (graph.cpp:243-256)."""
     with open(path, "wb") as f:
