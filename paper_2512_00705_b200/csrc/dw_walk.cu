@@ -4,25 +4,25 @@
 
 namespace dwb {
 
-template <class M, int MODE, int FAT, bool DIRECT>
+template <class M, int MODE, int FAT, int OUT>
 static cudaError_t launch_t(const WalkParams& p, int num_sms, cudaStream_t stream) {
     int per_sm = 0;
-    const size_t smem = walk_smem_bytes<M, MODE>();
+    const size_t smem = walk_smem_bytes<M, MODE, OUT>();
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
-        cudaError_t ea = cudaFuncSetAttribute(walk_kernel<M, MODE, FAT, DIRECT>,
+        cudaError_t ea = cudaFuncSetAttribute(walk_kernel<M, MODE, FAT, OUT>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (ea != cudaSuccess) return ea;
         attr_set = true;
     }
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, walk_kernel<M, MODE, FAT, DIRECT>, kThreads, smem);
+        &per_sm, walk_kernel<M, MODE, FAT, OUT>, kThreads, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
     unsigned long long blocks = (unsigned long long)num_sms * per_sm;
     const unsigned long long need = (p.nq + kThreads - 1) / kThreads;
     if (need < blocks) blocks = need ? need : 1;
-    walk_kernel<M, MODE, FAT, DIRECT><<<(unsigned)blocks, kThreads, smem, stream>>>(p);
+    walk_kernel<M, MODE, FAT, OUT><<<(unsigned)blocks, kThreads, smem, stream>>>(p);
     return cudaGetLastError();
 }
 
@@ -35,9 +35,9 @@ template <bool W> struct DirectOk<Node2VecModel<W>> { static constexpr bool valu
 template <class M, int MODE, int FAT>
 static cudaError_t launch_d(const WalkParams& p, int num_sms, cudaStream_t s) {
     if constexpr (DirectOk<M>::value && (MODE == kAdaptive || MODE == kForceErjs))
-        if (p.offs) return launch_t<M, MODE, FAT, true>(p, num_sms, s);
+        if (p.offs) return launch_t<M, MODE, FAT, kOutFlat>(p, num_sms, s);
     if (p.offs) return cudaErrorInvalidValue;
-    return launch_t<M, MODE, FAT, false>(p, num_sms, s);
+    return launch_t<M, MODE, FAT, kOutPadded>(p, num_sms, s);
 }
 
 // compact 32 B records (FAT = 2) are walked by node2vec, in preference to the

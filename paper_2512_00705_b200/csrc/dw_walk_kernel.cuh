@@ -126,7 +126,7 @@ constexpr uint32_t kCjsMin = DW_CJS_MIN;
 // 64-bit counter.
 enum LaneCounter : int {
     LC_ETRIALS = 0, LC_EREADS, LC_EDRAWS, LC_ALG4, LC_NUM64,
-    LC_ETRIALS1 = LC_NUM64, LC_FALLBACKS, LC_DEADENDS, LC_NUM
+    LC_ETRIALS1 = LC_NUM64, LC_FALLBACKS, LC_DEADENDS, LC_QERRORS, LC_QUERIES, LC_NUM
 };
 
 __device__ __forceinline__ bool valid_w(double w) { return !(w < 0.0) && isfinite(w); }
@@ -935,13 +935,16 @@ __device__ __forceinline__ uint32_t tri_bound(uint32_t q, float hmax) {
 // ---- K3: adaptive walker loop (runtime.cpp:59-153 + 192-247) --------------
 // Per-lane landing slots and counters, structure-of-arrays ([.][kThreads]) so
 // a warp's 16 B accesses are conflict-free.
-struct WalkSmem {
+// kLc32: rows of 32-bit lane counters (LC_NUM - LC_NUM64; the direct compact
+// kernels count queries per block instead, WalkSmemFlat)
+template <int kLc32>
+struct WalkSmemT {
     uint4 rec[kRing][3][kThreads];   // landing: fat record / slim pair in [0]
     double y[kRing][kThreads];       // y of the queued trials
     uint32_t t[kRing][kThreads];     // trial index of the queued trials
     uint4 mb[2][kThreads];           // node record / hash bucket / eRVS pair
     ull lc[LC_NUM64][kThreads];      // per-lane RunStats counters (64-bit)
-    uint32_t lc32[LC_NUM - LC_NUM64][kThreads];  // (bounded ones)
+    uint32_t lc32[kLc32][kThreads];  // (bounded ones)
     // path entries staged until their 32 B sector is complete: a sector is
     // written whole (two 16 B stores) instead of eight 4 B stores, so L2 never
     // evicts a partly written sector, which HBM's ECC turns into a
@@ -954,12 +957,6 @@ struct WalkSmem {
         twlo[kThreads], twcnt[kThreads], nret[kThreads];
     double bound[kThreads], mnr[kThreads];
     uint32_t qi[kThreads];           // the lane's walker: index in this launch
-    // first entry of the lane's path in p.paths: qi * stride (padded rows),
-    // or p.offs[qi] (direct compact output)
-    ull rowb[kThreads];
-    // direct compact output: chunk of the walker that ended last iteration,
-    // booked after this iteration's gathers are issued (0xFFFF: none)
-    uint16_t dchunk[kThreads];
     // f32 bits of the current step's triangle bound (Step::hin, rounded up):
     // props of the edges (cur -> u) with u in N(prev) are <= it
     uint32_t tq[kThreads];
@@ -972,10 +969,20 @@ struct WalkSmem {
     uint32_t tmaph[kThreads / 32];
 };
 
+using WalkSmem = WalkSmemT<LC_NUM - LC_NUM64>;
+// direct compact kernels (kOutFlat): + each lane's path start in the flat
+// layout (p.offs[qi]) and the chunk of the walker that ended last iteration,
+// booked after this iteration's gathers are issued (0xFFFF: none); room made
+// by counting queries and query errors with global atomics (one per warp
+// claim, one per out-of-range start) instead of per lane
+struct WalkSmemFlat : WalkSmemT<LC_QERRORS - LC_NUM64> {
+    ull rowb[kThreads];
+    uint16_t dchunk[kThreads];
+};
 // DW_MIN_BLOCKS CTAs of the narrow kernels must fit one SM's 228 KB of shared
 // memory, 1 KB of which each CTA reserves (one CTA less costs ~30 %)
-static_assert(DW_THREADS != 256 || DW_MIN_BLOCKS * (sizeof(WalkSmem) + 1024) <= 228 * 1024,
-              "WalkSmem too large for DW_MIN_BLOCKS CTAs per SM");
+static_assert(DW_THREADS != 256 || DW_MIN_BLOCKS * (sizeof(WalkSmemFlat) + 1024) <= 228 * 1024,
+              "WalkSmemFlat too large for DW_MIN_BLOCKS CTAs per SM");
 
 // reservoir-only modes (force-ervs, ervs-nojump) spend their time in the
 // warp-cooperative row scan, whose parallel jump chain needs ~14 more live
@@ -1001,15 +1008,21 @@ struct WideKernel {
 struct WalkSmemWide : WalkSmem {
     ull pbeg[kThreads];
 };
-template <class M, int MODE>
+// OUT: where paths go.  kOutPadded: [nq][stride] rows.  kOutFlat: the flat
+// layout at p.offs, with finished walkers counted per chunk and finished
+// chunks flagged to the host (direct compact runs, dw_capi.cu run_direct);
+// that code and its shared memory are compiled only into the kernels such
+// runs use, so the padded-row kernels are exactly the ones without it
+enum : int { kOutPadded = 0, kOutFlat = 1 };
+template <int OUT> struct OutSmem { using type = WalkSmem; };
+template <> struct OutSmem<kOutFlat> { using type = WalkSmemFlat; };
+template <class M, int MODE, int OUT = kOutPadded>
 constexpr size_t walk_smem_bytes() {
-    return WideKernel<M, MODE>::value ? sizeof(WalkSmemWide) : sizeof(WalkSmem);
+    return WideKernel<M, MODE>::value ? sizeof(WalkSmemWide)
+                                      : sizeof(typename OutSmem<OUT>::type);
 }
 
-// DIRECT: paths go to the flat layout at p.offs (direct compact runs,
-// dw_capi.cu run_direct) with per-chunk completion counts; compiled only into
-// the kernels such runs use, so the padded-row kernels carry none of it
-template <class M, int MODE, int FAT, bool DIRECT = false>
+template <class M, int MODE, int FAT, int OUT = kOutPadded>
 __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS_MIN_BLOCKS
                                                                         : DW_MIN_BLOCKS)
     walk_kernel(const __grid_constant__ WalkParams p) {
@@ -1022,7 +1035,11 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
     constexpr bool kSO = M::kSecondOrder;
     // dynamic shared memory (WalkSmem): may exceed the 48 KB static limit
     extern __shared__ __align__(16) unsigned char dsm[];
-    WalkSmem& sm = *reinterpret_cast<WalkSmem*>(dsm);
+    using SM = typename OutSmem<OUT>::type;
+    SM& sm = *reinterpret_cast<SM*>(dsm);
+    // lane counters with a per-lane row (the direct kernels count queries and
+    // query errors with global atomics: WalkSmemFlat)
+    constexpr int kLcN = OUT == kOutFlat ? (int)LC_QERRORS : (int)LC_NUM;
     auto& s_rec = sm.rec;
     auto& s_y = sm.y;
     auto& s_t = sm.t;
@@ -1037,9 +1054,9 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
     for (int i = tid; i < 66; i += blockDim.x) s_hist[i] = 0;
 #pragma unroll
     for (int c = 0; c < LC_NUM64; ++c) s_lc[c][tid] = 0;
-    sm.dchunk[tid] = 0xFFFFu;
+    if constexpr (OUT != kOutPadded) sm.dchunk[tid] = 0xFFFFu;
 #pragma unroll
-    for (int c = 0; c < LC_NUM - LC_NUM64; ++c) sm.lc32[c][tid] = 0;
+    for (int c = 0; c < kLcN - LC_NUM64; ++c) sm.lc32[c][tid] = 0;
     constexpr bool kTma = DW_ERVS_TMA && (MODE == kForceErvs || MODE == kErvsNoJump) &&
                           !M::kUsesLabels && !M::kLabelAgg;
     if (kTma && (tid & 31) == 0) {
@@ -1058,7 +1075,8 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
             x = y;
             if (y < (uint32_t)v) {
                 const int gc = c == LC_ETRIALS1 ? kCTrials : c == LC_FALLBACKS ? kCFallbacks
-                                                             : kCDeadEnds;
+                               : c == LC_DEADENDS ? kCDeadEnds : c == LC_QERRORS ? kCQueryErrors
+                                                                                : kCQueries;
                 atomicAdd(&p.counters[gc], 1ull << 32);
             }
         }
@@ -1148,6 +1166,7 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
     // flag, so the host copies the chunk while the launch walks on
     // (acq_rel: every path write of the chunk precedes the flag)
     auto chunk_done = [&]() {
+      if constexpr (OUT != kOutPadded) {
         const uint32_t c = sm.dchunk[tid];
         if (c == 0xFFFFu) return;
         sm.dchunk[tid] = 0xFFFFu;
@@ -1166,38 +1185,42 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
             __threadfence_system();
             *(volatile unsigned*)(p.chunk_flag + c) = 1u;
         }
+      }
     };
     // first entry of the lane's path: its row of the padded [nq][stride]
-    // layout, or its offset in the flat layout (DIRECT)
+    // layout, or its offset in the flat layout (kOutFlat)
     auto row_start = [&]() -> uint32_t* {
-        return DIRECT ? p.paths + sm.rowb[tid] : p.paths + (ull)sm.qi[tid] * p.stride;
+        if constexpr (OUT == kOutFlat) return p.paths + sm.rowb[tid];
+        else return p.paths + (ull)sm.qi[tid] * p.stride;
     };
     // path entry `step` (stage; a completed 32 B sector is written whole)
     auto put_path = [&](uint32_t v) {
+        // the row start is read once (the staging stores may alias it)
         uint32_t* const rs = row_start();
         uint32_t* a = rs + step;
         const uint32_t k = (uint32_t)(reinterpret_cast<unsigned long long>(a) >> 2) & 7u;
         sm.pst[k][tid] = v;
         if (k == 7u) {
             uint32_t* s0 = a - 7;
-            if (s0 >= rs) {  // the sector is this walker's
+            if (s0 >= (OUT == kOutFlat ? rs : row_start())) {  // the sector is this walker's
                 reinterpret_cast<uint4*>(s0)[0] =
                     make_uint4(sm.pst[0][tid], sm.pst[1][tid], sm.pst[2][tid], sm.pst[3][tid]);
                 reinterpret_cast<uint4*>(s0)[1] =
                     make_uint4(sm.pst[4][tid], sm.pst[5][tid], sm.pst[6][tid], sm.pst[7][tid]);
             } else {  // the row's first sector, shared with the previous row
-                for (uint32_t* q = rs; q <= a; ++q)
+                for (uint32_t* q = OUT == kOutFlat ? rs : row_start(); q <= a; ++q)
                     *q = sm.pst[(uint32_t)(reinterpret_cast<unsigned long long>(q) >> 2) & 7u][tid];
             }
         }
     };
     // the staged entries of the last, incomplete sector
     auto flush_path = [&]() {
-        uint32_t* const rs = row_start();
-        uint32_t* a = rs + step;
+        uint32_t* const rs0 = row_start();
+        uint32_t* a = rs0 + step;
         const uint32_t k = (uint32_t)(reinterpret_cast<unsigned long long>(a) >> 2) & 7u;
         if (k == 7u) return;
         uint32_t* q = a - k;
+        uint32_t* rs = OUT == kOutFlat ? rs0 : row_start();
         if (q < rs) q = rs;
         for (; q <= a; ++q)
             *q = sm.pst[(uint32_t)(reinterpret_cast<unsigned long long>(q) >> 2) & 7u][tid];
@@ -1206,7 +1229,7 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
         if (p.lengths) p.lengths[sm.qi[tid]] = step + 1;
         if (p.paths) flush_path();
         flush_walker();
-        phase = DIRECT ? P_DONE : P_IDLE;
+        phase = OUT != kOutPadded ? P_DONE : P_IDLE;
     };
     auto start_ervs = [&](ull draw_base) {
         tn = 0;
@@ -1260,10 +1283,11 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
 
     for (;;) {
         // ---- walks that ended last iteration (end_walk)
-        if (DIRECT && phase == P_DONE) {
-            sm.dchunk[tid] = (uint16_t)(sm.qi[tid] >> p.chunk_shift);
-            phase = P_IDLE;
-        }
+        if constexpr (OUT != kOutPadded)
+            if (phase == P_DONE) {
+                sm.dchunk[tid] = (uint16_t)(sm.qi[tid] >> p.chunk_shift);
+                phase = P_IDLE;
+            }
         // ---- refill idle lanes: one atomic per warp (runtime.cpp:209-211)
         unsigned need = __ballot_sync(kFull, phase == P_IDLE);
         if (need && !drained) {
@@ -1278,25 +1302,40 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
                 base = __shfl_sync(kFull, base, leader);
                 if (base + (ull)n >= p.nq) drained = true;
                 if (lane == leader && base < p.nq)  // one counter add per claim
-                    atomicAdd(&p.counters[kCQueries], min((ull)n, p.nq - base));
+                {
+                    if constexpr (OUT == kOutFlat)
+                        atomicAdd(&p.counters[kCQueries], min((ull)n, p.nq - base));
+                    else
+                        lc_add(LC_QUERIES, min((ull)n, p.nq - base));
+                }
                 if (phase == P_IDLE) {
                     const ull i = base + (ull)__popc(need & lt_mask);
                     if (i < p.nq) {
                         const uint32_t start = p.queries[i];
-                        const ull rb = DIRECT ? p.offs[i] : i * p.stride;
-                        sm.qi[tid] = (uint32_t)i;
                         if (start >= g.nv) {  // runtime.cpp:213-217
-                            atomicAdd(&p.counters[kCQueryErrors], 1ull);
+                            if constexpr (OUT == kOutFlat) atomicAdd(&p.counters[kCQueryErrors], 1ull);
+                            else lc_add(LC_QERRORS, 1);
                             if (p.lengths) p.lengths[i] = 0;
-                            if (DIRECT) phase = P_DONE;  // booked next iteration
+                            if constexpr (OUT != kOutPadded) {  // booked next iteration
+                                sm.qi[tid] = (uint32_t)i;
+                                phase = P_DONE;
+                            }
                         } else {
                             if (p.target == 0) {
-                                if (p.paths) p.paths[rb] = start;
+                                if constexpr (OUT == kOutFlat) {
+                                    if (p.paths) p.paths[p.offs[i]] = start;
+                                } else {
+                                    if (p.paths) p.paths[i * p.stride] = start;
+                                }
                                 if (p.lengths) p.lengths[i] = 1;
-                                if (DIRECT) phase = P_DONE;
+                                if constexpr (OUT != kOutPadded) {
+                                    sm.qi[tid] = (uint32_t)i;
+                                    phase = P_DONE;
+                                }
                             } else {
                                 phase = P_NODE;
-                                if (DIRECT) sm.rowb[tid] = rb;
+                                sm.qi[tid] = (uint32_t)i;
+                                if constexpr (OUT == kOutFlat) sm.rowb[tid] = p.offs[i];
                                 qg = p.qids ? p.qids[i] : p.qid_base + i;
                                 step = 0;
                                 if (p.paths) put_path(start);
@@ -1436,7 +1475,7 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
         // a walk that ended last iteration is final: count it in its chunk
         // (direct compact output; its release and round trip overlap the
         // gathers just issued)
-        if (DIRECT) chunk_done();
+        if (OUT != kOutPadded) chunk_done();
         // ---- B
         cp_wait_all();
 
@@ -2019,13 +2058,13 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
             }
         }
     }
-    if (DIRECT) chunk_done();  // the walks that ended in the last iteration
+    if (OUT != kOutPadded) chunk_done();  // the walks that ended in the last iteration
 
     // ---- flush counters: eRJS trials count as trials, reads and 2 draws each
     __syncthreads();
     if (tid < 66 && s_hist[tid]) s_cnt[kCHist + tid] += s_hist[tid];
 #pragma unroll 1
-    for (int c = 0; c < LC_NUM; ++c) {
+    for (int c = 0; c < kLcN; ++c) {
         const ull v = warp_sum(c < LC_NUM64 ? s_lc[c][tid] : (ull)sm.lc32[c - LC_NUM64][tid]);
         if (lane == 0 && v) atomicAdd(&s_lct[c], v);
     }
@@ -2038,6 +2077,8 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
         s_cnt[kCAlgBytes] = 4 * s_lct[LC_ALG4];
         s_cnt[kCFallbacks] += s_lct[LC_FALLBACKS];
         s_cnt[kCDeadEnds] += s_lct[LC_DEADENDS];
+        s_cnt[kCQueryErrors] += s_lct[LC_QERRORS];  // 0 in the direct kernels:
+        s_cnt[kCQueries] += s_lct[LC_QUERIES];      // they count into p.counters
     }
     __syncthreads();
     for (int i = tid; i < kCNum; i += blockDim.x)
