@@ -6,6 +6,9 @@ sampler templates on hub-heavy R-MAT graphs (-m gpu).
   node2vec), at the calibrated ratio the headline runs with (~2.3) and at
   1.6: 50K sampled walkers of length 80, adaptive and force-erjs, bit-exact
   against the oracle in paths, lengths and every RunStats counter.
+* The same graph through dw_run_compact's direct engine (every vertex a
+  start, ratio 0.5 as calibrated at s24): equal to the padded run and, on a
+  sample, to the oracle.
 * R-MAT s13 / s14 (max degree in the thousands): the GPU against
   ref_run_philox, i.e. the reference's samplers.hpp / models.hpp /
   runtime.cpp templates driven by the same Philox stream, for node2vec
@@ -55,6 +58,40 @@ def test_bench_graph_s20_parity(dw, orc, bench_s20, ratio, mode):
     assert r_dev.stats["steps"] > 1_000_000
     if mode == "adaptive":
         assert r_dev.stats["select_ervs"] > 1000 and r_dev.stats["select_erjs"] > 100_000
+
+
+def test_bench_graph_s20_direct_compact(dw, orc, bench_s20, tmp_path):
+    """The headline's end-to-end path at scale 20: dw_run_compact on the
+    bench graph takes the direct engine (trace line "X nq ok"), and its
+    offsets and ids equal the padded run's for every vertex as a start, and
+    the oracle's on a sample."""
+    import bench
+    dg, og = bench_s20
+    nv = og.nv
+    q = np.arange(nv, dtype=np.uint32)
+    model = dw.Model(kind="node2vec", a=0.5, b=2.0)
+    opts = dw.RunOptions(mode="adaptive", walk_length=80, seed=bench.WALK_SEED,
+                         edge_cost_ratio=0.5)
+    trace = str(tmp_path / "trace.txt")
+    os.environ["DW_ENGINE_TRACE"] = trace
+    try:
+        offs, flat, st = dw.run_queries_compact(dg, model, q, opts)
+    finally:
+        os.environ.pop("DW_ENGINE_TRACE", None)
+    assert open(trace).read().split()[:3] == ["X", str(nv), "ok"]
+    r = dw.run_queries(dg, model, q, opts)
+    assert np.array_equal(np.diff(offs.astype(np.int64)), r.lengths.astype(np.int64))
+    mask = np.arange(r.paths.shape[1])[None, :] < r.lengths[:, None]
+    assert np.array_equal(flat, r.paths[mask])
+    assert stats_core(st) == stats_core(r.stats)
+    qs = q[::nv // 20_000][:20_000]
+    r_orc = orc.run(og, orc.Model(kind="node2vec", a=0.5, b=2.0), qs, mode="adaptive",
+                    walk_length=80, seed=bench.WALK_SEED, ratio=0.5, rng="philox",
+                    threads=THREADS, qids=qs.astype(np.uint64))  # walker id = vertex id
+    o = offs.astype(np.int64)
+    sel = np.concatenate([np.arange(o[i], o[i + 1]) for i in qs.astype(np.int64)])
+    assert np.array_equal(flat[sel], r_orc.paths[np.arange(r_orc.paths.shape[1])[None, :]
+                                                 < r_orc.lengths[:, None]])
 
 
 @pytest.fixture(scope="module", params=[13, 14])
