@@ -1312,37 +1312,51 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
                     const ull i = base + (ull)__popc(need & lt_mask);
                     if (i < p.nq) {
                         const uint32_t start = p.queries[i];
-                        if (start >= g.nv) {  // runtime.cpp:213-217
-                            if constexpr (OUT == kOutFlat) atomicAdd(&p.counters[kCQueryErrors], 1ull);
-                            else lc_add(LC_QERRORS, 1);
-                            if (p.lengths) p.lengths[i] = 0;
-                            if constexpr (OUT != kOutPadded) {  // booked next iteration
-                                sm.qi[tid] = (uint32_t)i;
-                                phase = P_DONE;
+                        if constexpr (OUT == kOutFlat) {
+                            // the path's flat offset loads beside the start
+                            // (one load latency per claim, not two)
+                            const ull rb = p.offs[i];
+                            sm.qi[tid] = (uint32_t)i;
+                            if (start >= g.nv) {  // runtime.cpp:213-217
+                                atomicAdd(&p.counters[kCQueryErrors], 1ull);
+                                if (p.lengths) p.lengths[i] = 0;
+                                phase = P_DONE;  // booked next iteration
+                            } else {
+                                if (p.target == 0) {
+                                    if (p.paths) p.paths[rb] = start;
+                                    if (p.lengths) p.lengths[i] = 1;
+                                    phase = P_DONE;
+                                } else {
+                                    phase = P_NODE;
+                                    sm.rowb[tid] = rb;
+                                    qg = p.qids ? p.qids[i] : p.qid_base + i;
+                                    step = 0;
+                                    if (p.paths) put_path(start);
+                                    cur = start;
+                                    prev = kInvalid;
+                                    pdeg = phoff = plg = 0;
+                                    step = 0;
+                                }
                             }
                         } else {
-                            if (p.target == 0) {
-                                if constexpr (OUT == kOutFlat) {
-                                    if (p.paths) p.paths[p.offs[i]] = start;
-                                } else {
-                                    if (p.paths) p.paths[i * p.stride] = start;
-                                }
-                                if (p.lengths) p.lengths[i] = 1;
-                                if constexpr (OUT != kOutPadded) {
-                                    sm.qi[tid] = (uint32_t)i;
-                                    phase = P_DONE;
-                                }
+                            if (start >= g.nv) {  // runtime.cpp:213-217
+                                lc_add(LC_QERRORS, 1);
+                                if (p.lengths) p.lengths[i] = 0;
                             } else {
-                                phase = P_NODE;
-                                sm.qi[tid] = (uint32_t)i;
-                                if constexpr (OUT == kOutFlat) sm.rowb[tid] = p.offs[i];
-                                qg = p.qids ? p.qids[i] : p.qid_base + i;
-                                step = 0;
-                                if (p.paths) put_path(start);
-                                cur = start;
-                                prev = kInvalid;
-                                pdeg = phoff = plg = 0;
-                                step = 0;
+                                if (p.target == 0) {
+                                    if (p.paths) p.paths[i * p.stride] = start;
+                                    if (p.lengths) p.lengths[i] = 1;
+                                } else {
+                                    phase = P_NODE;
+                                    sm.qi[tid] = (uint32_t)i;
+                                    qg = p.qids ? p.qids[i] : p.qid_base + i;
+                                    step = 0;
+                                    if (p.paths) put_path(start);
+                                    cur = start;
+                                    prev = kInvalid;
+                                    pdeg = phoff = plg = 0;
+                                    step = 0;
+                                }
                             }
                         }
                     }
