@@ -444,6 +444,31 @@ def test_direct_compact_output(dw, orc, mk, layout, tmp_path):
         _assert_compact_equal(a, b, ("batched", mode))
 
 
+def test_direct_compact_global_walker_ids(dw, orc, tmp_path):
+    """Direct compact runs keyed by explicit global walker ids (dw_run_opts.qids,
+    as the hash-sharded multi-GPU bench passes them) and by qid_base: equal to
+    the batched engine and to the oracle with the same ids."""
+    og = orc.Graph.rmat(12, 16, 31).synth_philox("uniform", 1.0, 5.0, seed=32)
+    dg = to_device(dw, og)
+    rng = np.random.default_rng(9)
+    q = rng.integers(0, og.nv, 300_000).astype(np.uint32)
+    qids = rng.permutation(10 * len(q))[:len(q)].astype(np.uint64)
+    model = dw.Model(kind="node2vec", a=0.5, b=2.0)
+    trace = str(tmp_path / "trace.txt")
+    for kw in (dict(qids=qids), dict(qid_base=123_456_789)):
+        opts = dw.RunOptions(mode="adaptive", walk_length=40, seed=11, edge_cost_ratio=1.1, **kw)
+        a, b, lines = _compact_pair(dw, dg, model, q, opts, {}, trace)
+        assert lines[:3] == ["X", str(len(q)), "ok"], lines[:6]
+        _assert_compact_equal(a, b, kw.keys())
+        r_orc = orc.run(og, orc.Model(kind="node2vec", a=0.5, b=2.0), q[:20_000], mode="adaptive",
+                        walk_length=40, seed=11, ratio=1.1, rng="philox", threads=4,
+                        qids=qids[:20_000] if "qids" in kw else None,
+                        qid_base=kw.get("qid_base", 0))
+        o = a[0].astype(np.int64)
+        mask = np.arange(r_orc.paths.shape[1])[None, :] < r_orc.lengths[:, None]
+        assert np.array_equal(a[1][:o[20_000]], r_orc.paths[mask]), kw.keys()
+
+
 def test_direct_compact_falls_back_on_sinks(dw, orc, tmp_path):
     """A directed graph with sinks: walks stop early, so the direct engine is
     not used (no X trace line); forced (DW_DIRECT=2) it detects the shorter
