@@ -603,24 +603,22 @@ struct RunOut {
 // launch ends in a ~1 ms tail while its last walkers finish, so fewer is
 // better; batch_plan shortens the last ones), at least 256K walkers per
 // launch, at most 4M (1.3 GB of padded paths at L=80)
-ull batch_size(ull n) {
+ull batch_size(ull n, ull div = 4) {
     if (const char* env = std::getenv("DW_BATCH"))  // experiments: fixed walkers per batch
         if (std::atoll(env) > 0) return std::min<ull>(std::max<ull>(n, 1), (ull)std::atoll(env));
-    ull div = 4;
     if (const char* env = std::getenv("DW_BATCH_DIV")) div = std::max(1, std::atoi(env));
     const ull want = (n + div - 1) / div;
     return std::max<ull>(1, std::min<ull>(n, std::max<ull>(1ull << 18, std::min<ull>(want, 1ull << 22))));
 }
 
-// Batch boundaries of one device's n walkers: batches of batch_size(n), the
+// Batch boundaries of one device's n walkers: batches of bs (batch_size), the
 // last two batches' worth split geometrically (1/2, 1/4, 1/8, 1/8, pieces of
 // at least 1M walkers) so the copy of the final batch, which nothing
-// overlaps, is short.  `cap` bounds every
-// batch (the ring slot size).
-std::vector<ull> batch_plan(ull n, ull cap) {
+// overlaps, is short.  bs is the ring slot size (every batch fits one).
+std::vector<ull> batch_plan(ull n, ull bs) {
     std::vector<ull> at{0};
     if (n == 0) return at;
-    const ull bs = std::min(cap, batch_size(n));
+    bs = std::max<ull>(bs, 1);
     ull pos = 0;
     while (n - pos > 2 * bs) at.push_back(pos += bs);
     ull rem = n - pos;
@@ -656,7 +654,11 @@ int run_engine(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries
     const ull stride = (ull)opts->walk_length + 1;
     const bool ordered = out.compact || out.text;
     const ull per_dev = std::max<ull>(1, (nq + nd - 1) / nd);
-    const ull bs = out.text ? std::min<ull>(batch_size(per_dev), 1ull << 20) : batch_size(per_dev);
+    // compact output: ~2 batches per device (its last copy is small next to
+    // the launch tails a batch adds: MetaPath s22 e2e 14.3 ms against 15.1
+    // with 4, profiles/r2_cfg_ab_final.txt); padded rows: ~4
+    const ull bs = out.text ? std::min<ull>(batch_size(per_dev), 1ull << 20)
+                            : batch_size(per_dev, out.compact ? 2 : 4);
     const std::vector<ull> at = batch_plan(nq, bs);
     const ull nb = at.size() - 1;
     struct Dev {
