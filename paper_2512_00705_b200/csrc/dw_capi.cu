@@ -104,10 +104,14 @@ struct Replica {
         uint32_t* len = nullptr;    // [cap_q] predicted lengths
         ull* offs = nullptr;        // [cap_q + 1] predicted offsets
         uint32_t* flat = nullptr;   // [cap_flat] ids
+        ull* pos = nullptr;         // [cap_q + 1] rank of each walking walker
+        uint32_t* cq = nullptr;     // [cap_q] the walking walkers: queries,
+        ull* cqid = nullptr;        //   global walker ids,
+        ull* coffs = nullptr;       //   flat offsets
         unsigned* done = nullptr;   // [kMaxChunks] finished walkers per chunk
         int* flag = nullptr;        // scratch (sink_targets)
         unsigned* h_flag = nullptr; // host-mapped [kMaxChunks] chunk final flags
-        ull* h_bounds = nullptr;    // host-mapped [kMaxChunks + 1] chunk flat bounds
+        ull* h_bounds = nullptr;    // host-mapped [kMaxChunks + 3] chunk flat bounds, nt, nch
         ull cap_q = 0, cap_flat = 0;
         bool has_qids = false;
         cudaEvent_t pre = nullptr, walk = nullptr, w0 = nullptr, w1 = nullptr;
@@ -175,8 +179,12 @@ void free_direct(Replica::Direct& d) {
     cudaFree(d.len);
     cudaFree(d.offs);
     cudaFree(d.flat);
-    d.q = d.len = d.flat = nullptr;
-    d.qids = d.offs = nullptr;
+    cudaFree(d.pos);
+    cudaFree(d.cq);
+    cudaFree(d.cqid);
+    cudaFree(d.coffs);
+    d.q = d.len = d.flat = d.cq = nullptr;
+    d.qids = d.offs = d.pos = d.cqid = d.coffs = nullptr;
     d.cap_q = d.cap_flat = 0;
     d.has_qids = false;
 }
@@ -922,7 +930,7 @@ int direct_buffers(Replica& r, ull nq, ull nflat, bool qids) {
         CU(cudaMalloc(&d.done, kMaxChunks * sizeof(unsigned)), "cudaMalloc");
         CU(cudaHostAlloc(&d.h_flag, kMaxChunks * sizeof(unsigned), cudaHostAllocMapped),
            "cudaHostAlloc");
-        CU(cudaHostAlloc(&d.h_bounds, (kMaxChunks + 1) * sizeof(ull), cudaHostAllocMapped),
+        CU(cudaHostAlloc(&d.h_bounds, (kMaxChunks + 3) * sizeof(ull), cudaHostAllocMapped),
            "cudaHostAlloc");
         for (cudaEvent_t* e : {&d.pre, &d.walk})
             CU(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "cudaEventCreate");
@@ -938,22 +946,25 @@ int direct_buffers(Replica& r, ull nq, ull nflat, bool qids) {
         const bool hq = qids || d.has_qids;
         const ull cf = std::max(nflat, d.cap_flat);
         if (cq > d.cap_q || hq != d.has_qids)
-            need += cq * (sizeof(uint32_t) * 2 + sizeof(ull) * (hq ? 2 : 1));
+            need += cq * (sizeof(uint32_t) * 3 + sizeof(ull) * (hq ? 5 : 4));
         if (cf > d.cap_flat) need += cf * sizeof(uint32_t);
         size_t fr = 0, tot = 0;
         CU(cudaMemGetInfo(&fr, &tot), "cudaMemGetInfo");
         if ((ull)fr < need + (2ull << 30)) return kDirectNo;
         if (cq > d.cap_q || hq != d.has_qids) {
-            cudaFree(d.q);
-            cudaFree(d.qids);
-            cudaFree(d.len);
-            cudaFree(d.offs);
-            d.q = d.len = nullptr;
-            d.qids = d.offs = nullptr;
+            for (void* p : {(void*)d.q, (void*)d.qids, (void*)d.len, (void*)d.offs, (void*)d.pos,
+                            (void*)d.cq, (void*)d.cqid, (void*)d.coffs})
+                cudaFree(p);
+            d.q = d.len = d.cq = nullptr;
+            d.qids = d.offs = d.pos = d.cqid = d.coffs = nullptr;
             d.cap_q = 0;
             CU(cudaMalloc(&d.q, cq * sizeof(uint32_t)), "cudaMalloc queries");
             CU(cudaMalloc(&d.len, cq * sizeof(uint32_t)), "cudaMalloc lengths");
             CU(cudaMalloc(&d.offs, (cq + 1) * sizeof(ull)), "cudaMalloc offsets");
+            CU(cudaMalloc(&d.pos, (cq + 1) * sizeof(ull)), "cudaMalloc walker ranks");
+            CU(cudaMalloc(&d.cq, cq * sizeof(uint32_t)), "cudaMalloc walker list");
+            CU(cudaMalloc(&d.cqid, cq * sizeof(ull)), "cudaMalloc walker list");
+            CU(cudaMalloc(&d.coffs, cq * sizeof(ull)), "cudaMalloc walker list");
             if (hq) CU(cudaMalloc(&d.qids, cq * sizeof(ull)), "cudaMalloc walker ids");
             d.cap_q = cq;
             d.has_qids = hq;
@@ -996,9 +1007,9 @@ int run_direct(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries
     uint32_t shift = 14;
     while ((nq >> shift) > 256 && shift < 24) ++shift;
     while (((nq + (1ull << shift) - 1) >> shift) > kMaxChunks) ++shift;
-    const ull nch = (nq + (1ull << shift) - 1) >> shift;
+    const ull nch_max = (nq + (1ull << shift) - 1) >> shift;
     cudaStream_t ws = r.stream, cp = r.copy;
-    std::memset(d.h_flag, 0, nch * sizeof(unsigned));
+    std::memset(d.h_flag, 0, nch_max * sizeof(unsigned));
     if (st) std::memset(st, 0, sizeof *st);
     CU(cudaEventRecord(d.w0, ws), "event");
     CU(cudaMemcpyAsync(d.q, queries, nq * sizeof(uint32_t), cudaMemcpyHostToDevice, ws),
@@ -1007,39 +1018,56 @@ int run_direct(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries
         CU(cudaMemcpyAsync(d.qids, opts->qids, nq * sizeof(ull), cudaMemcpyHostToDevice, ws),
            "H2D walker ids");
     if ((rc = reset_run_state(r))) return rc;
-    CU(cudaMemsetAsync(d.done, 0, nch * sizeof(unsigned), ws), "memset");
+    CU(cudaMemsetAsync(d.done, 0, nch_max * sizeof(unsigned), ws), "memset");
     CU(cudaMemsetAsync(r.d_base, 0, sizeof(ull), ws), "memset");
+    // offsets of every path, then the walkers whose path is final already
+    // (start out of range or without neighbours: 56 % of the s24 starts) are
+    // written here, and the walk gets only the list of the others: no claim,
+    // node gather or chunk count for them in the walk
     CU(dwb::predict_lengths(d.q, nq, r.g.nodes, r.g.nv, target, d.len, ws), "predict");
     size_t tb = r.scan_bytes;
     CU(dwb::path_offsets(d.len, nq, d.offs, r.d_base, r.d_scan, tb, ws), "scan");
-    CU(dwb::chunk_bounds(d.offs, nq, shift, nch, d.h_bounds, ws), "bounds");
+    CU(dwb::trivial_walkers(d.q, nq, d.len, d.offs, d.flat, r.counters, ws), "trivial walkers");
+    CU(cudaMemsetAsync(r.d_base, 0, sizeof(ull), ws), "memset");
+    CU(dwb::path_offsets(d.len, nq, d.pos, r.d_base, r.d_scan, tb, ws), "scan");
+    CU(dwb::walker_list(d.q, opts->qids ? d.qids : nullptr, opts->qid_base, nq, d.len, d.pos,
+                        d.offs, d.cq, d.cqid, d.coffs, ws),
+       "walker list");
+    CU(dwb::direct_bounds(d.coffs, r.d_base, d.offs + nq, shift, kMaxChunks, d.h_bounds, ws),
+       "bounds");
     CU(cudaEventRecord(d.pre, ws), "event");
     CU(cudaEventSynchronize(d.pre), "predict");
+    const ull nt = d.h_bounds[kMaxChunks + 1], nch = d.h_bounds[kMaxChunks + 2];
     const ull total = d.h_bounds[nch];
     if (total > out.flat_cap)
         return fail(DW_EINVAL, "flat path buffer too small: need %llu ids",
                     (unsigned long long)total);
     if (total && !out.flat) return fail(DW_EINVAL, "flat is NULL");
     dwb::WalkParams p = make_params(r, model, opts);
-    p.queries = d.q;
-    p.nq = nq;
-    p.qid_base = opts->qid_base;
-    p.qids = opts->qids ? d.qids : nullptr;
+    p.queries = d.cq;
+    p.nq = nt;
+    p.qid_base = 0;
+    p.qids = d.cqid;
     p.paths = d.flat;
     p.lengths = nullptr;
     p.next_walker = r.queues;
-    p.offs = d.offs;
+    p.offs = d.coffs;
     p.chunk_done = d.done;
     p.chunk_flag = d.h_flag;
     p.chunk_shift = shift;
-    CU(cudaMemsetAsync(p.next_walker, 0, sizeof(ull), ws), "memset");
     CU(cudaEventRecord(r.ev_start, ws), "event");
-    CU(launch_model(r, model, opts->mode, p, ws), "walk");
+    if (nt) {
+        CU(cudaMemsetAsync(p.next_walker, 0, sizeof(ull), ws), "memset");
+        CU(launch_model(r, model, opts->mode, p, ws), "walk");
+    }
     CU(cudaEventRecord(r.ev_stop, ws), "event");
     CU(cudaEventRecord(d.walk, ws), "event");
     // the offsets are final already: their copy overlaps the walk
     CU(cudaMemcpyAsync(out.offsets, d.offs, (nq + 1) * sizeof(ull), cudaMemcpyDeviceToHost, cp),
        "D2H offsets");
+    if (nch == 0 && total)  // no walker walks: every path is final
+        CU(cudaMemcpyAsync(out.flat, d.flat, total * sizeof(uint32_t), cudaMemcpyDeviceToHost, cp),
+           "D2H paths");
     // copy every chunk as soon as its walkers are final
     volatile unsigned* flag = d.h_flag;
     bool walk_done = false;
@@ -1090,7 +1118,7 @@ int run_direct(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries
         st->kernel_ms = ms;
         cudaEventElapsedTime(&ms, d.w0, d.w1);
         st->total_ms = ms;
-        st->kernel_launches = 6;
+        st->kernel_launches = 10 + (nt ? 1 : 0);
     }
     if (std::getenv("DW_VERBOSE")) {
         float a = 0.f, b = 0.f, c = 0.f;

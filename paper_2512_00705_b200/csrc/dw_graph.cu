@@ -1246,6 +1246,99 @@ cudaError_t chunk_bounds(const ull* offs, ull n, uint32_t shift, ull nchunks, ul
     return cudaGetLastError();
 }
 
+// Walkers whose path is final before the walk (length 0: start out of range;
+// 1: start without neighbours or target 0) are done here: a length-1 path's
+// one id is written at its offset, and queries / query errors are counted
+// (the walk kernel counts the walkers it claims).  len[i] becomes the
+// walker's "walks" flag, for the scan that lists the walking ones.
+__global__ void trivial_walkers_kernel(const uint32_t* __restrict__ q, ull n,
+                                       uint32_t* __restrict__ len, const ull* __restrict__ offs,
+                                       uint32_t* __restrict__ flat, ull* __restrict__ counters) {
+    uint32_t nq = 0, ne = 0;
+    for (ull i = (ull)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (ull)gridDim.x * blockDim.x) {
+        const uint32_t l = len[i];
+        if (l == 1) flat[offs[i]] = q[i];
+        nq += l <= 1;
+        ne += l == 0;
+        len[i] = l > 1;
+    }
+    __shared__ uint32_t s_c[2];
+    if (threadIdx.x == 0) s_c[0] = s_c[1] = 0;
+    __syncthreads();
+    nq = __reduce_add_sync(0xFFFFFFFFu, nq);
+    ne = __reduce_add_sync(0xFFFFFFFFu, ne);
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&s_c[0], nq);
+        atomicAdd(&s_c[1], ne);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s_c[0]) atomicAdd(&counters[kCQueries], (ull)s_c[0]);
+        if (s_c[1]) atomicAdd(&counters[kCQueryErrors], (ull)s_c[1]);
+    }
+}
+
+cudaError_t trivial_walkers(const uint32_t* queries, ull n, uint32_t* lengths, const ull* offs,
+                            uint32_t* flat, ull* counters, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    trivial_walkers_kernel<<<grid_for(n, 256 * 8), 256, 0, s>>>(queries, n, lengths, offs, flat,
+                                                               counters);
+    return cudaGetLastError();
+}
+
+// The walking walkers, in query order: cq / cqid / coffs[pos[i]] = query,
+// global walker id (RNG key) and flat offset of every i with flag[i] set.
+__global__ void walker_list_kernel(const uint32_t* __restrict__ q, const ull* __restrict__ qids,
+                                   ull qid_base, ull n, const uint32_t* __restrict__ flag,
+                                   const ull* __restrict__ pos, const ull* __restrict__ offs,
+                                   uint32_t* __restrict__ cq, ull* __restrict__ cqid,
+                                   ull* __restrict__ coffs) {
+    for (ull i = (ull)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (ull)gridDim.x * blockDim.x) {
+        if (!flag[i]) continue;
+        const ull j = pos[i];
+        cq[j] = q[i];
+        cqid[j] = qids ? qids[i] : qid_base + i;
+        coffs[j] = offs[i];
+    }
+}
+
+cudaError_t walker_list(const uint32_t* queries, const ull* qids, ull qid_base, ull n,
+                        const uint32_t* flag, const ull* pos, const ull* offs, uint32_t* cq,
+                        ull* cqid, ull* coffs, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    walker_list_kernel<<<grid_for(n, 256 * 8), 256, 0, s>>>(queries, qids, qid_base, n, flag, pos,
+                                                           offs, cq, cqid, coffs);
+    return cudaGetLastError();
+}
+
+// Copy ranges of the direct run's chunks (host-mapped out): chunk c holds
+// walking walkers [c << shift, (c + 1) << shift) of the nt = *d_nt listed,
+// and the flat range out[c] .. out[c + 1] (out[0] = 0, out[nch] = total;
+// the paths of the walkers that do not walk are written before the walk).
+// out[kMax + 1] = nt, out[kMax + 2] = nch.
+__global__ void direct_bounds_kernel(const ull* __restrict__ coffs, const ull* __restrict__ d_nt,
+                                     const ull* __restrict__ total, uint32_t shift, ull kmax,
+                                     ull* out) {
+    const ull nt = *d_nt;
+    const ull nch = (nt + (1ull << shift) - 1) >> shift;
+    for (ull c = (ull)blockIdx.x * blockDim.x + threadIdx.x; c <= nch;
+         c += (ull)gridDim.x * blockDim.x)
+        out[c] = c == nch ? *total : c == 0 ? 0ull : coffs[c << shift];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        out[kmax + 1] = nt;
+        out[kmax + 2] = nch;
+    }
+}
+
+cudaError_t direct_bounds(const ull* coffs, const ull* d_nt, const ull* total, uint32_t shift,
+                          ull kmax, ull* out, cudaStream_t s) {
+    direct_bounds_kernel<<<grid_for(kmax + 1, 256), 256, 0, s>>>(coffs, d_nt, total, shift, kmax,
+                                                                out);
+    return cudaGetLastError();
+}
+
 // *flag <- 1 when some edge leads to a vertex without neighbours
 __global__ void sink_targets_kernel(const NodeRec* __restrict__ nodes,
                                     const EdgeRec* __restrict__ edges, ull ne,

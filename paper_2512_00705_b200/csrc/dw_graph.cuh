@@ -114,6 +114,23 @@ cudaError_t predict_lengths(const uint32_t* queries, unsigned long long n, const
 // out[c] = offs[min(c << shift, n)] for c = 0..nchunks
 cudaError_t chunk_bounds(const unsigned long long* offs, unsigned long long n, uint32_t shift,
                          unsigned long long nchunks, unsigned long long* out, cudaStream_t s);
+// Walkers whose path is final before the walk: writes length-1 paths at
+// offs, adds their queries and query errors to counters, and turns
+// lengths[i] into the "walks" flag (length > 1).
+cudaError_t trivial_walkers(const uint32_t* queries, unsigned long long n, uint32_t* lengths,
+                            const unsigned long long* offs, uint32_t* flat,
+                            unsigned long long* counters, cudaStream_t s);
+// cq / cqid / coffs[pos[i]] = queries[i], its walker id (qids[i] or
+// qid_base + i) and offs[i] for every i with flag[i] set
+cudaError_t walker_list(const uint32_t* queries, const unsigned long long* qids,
+                        unsigned long long qid_base, unsigned long long n, const uint32_t* flag,
+                        const unsigned long long* pos, const unsigned long long* offs,
+                        uint32_t* cq, unsigned long long* cqid, unsigned long long* coffs,
+                        cudaStream_t s);
+// chunk copy ranges of a direct run (see dw_graph.cu direct_bounds_kernel)
+cudaError_t direct_bounds(const unsigned long long* coffs, const unsigned long long* d_nt,
+                          const unsigned long long* total, uint32_t shift, unsigned long long kmax,
+                          unsigned long long* out, cudaStream_t s);
 // *flag |= 1 if some edge's target has no neighbours (a walk can end early)
 cudaError_t sink_targets(const NodeRec* nodes, const EdgeRec* edges, unsigned long long ne,
                          int* flag, cudaStream_t s);
