@@ -118,6 +118,17 @@ struct Replica {
     } dir;
     int sinks = -1;  // -1 unknown, 1: some edge leads to a vertex without neighbours
     // dw_run_device bookkeeping
+    struct Listed {               // a listed walk (run_device_listed) to verify
+        bool on = false;
+        uint32_t target = 0;
+        dw_model_desc model;
+        dw_run_opts opts;
+        const uint32_t* queries = nullptr;
+        ull nq = 0;
+        uint32_t *paths = nullptr, *lengths = nullptr;
+        cudaStream_t stream = nullptr;
+        ull nt = 0;               // walkers the walk was given
+    } listed;
     bool pending = false;
     ull pending_launches = 0;
     ull pending_qbase = 0;
@@ -893,8 +904,15 @@ constexpr ull kMaxChunks = 1024;
 constexpr int kDirectNo = 1;     // not applicable: use the batched engine
 constexpr int kDirectRetry = 2;  // prediction failed: use the batched engine
 
+int listed_ok(Replica& r, const dw_model_desc* m, const dw_run_opts* o);
+
 int direct_ok(dw_graph_t g, const dw_model_desc* m, const dw_run_opts* o, ull nq) {
     if (g->reps.size() != 1 || nq == 0 || nq >= (1ull << 32)) return kDirectNo;
+    return listed_ok(g->reps[0], m, o);
+}
+
+// Every path length is known before the walk (see above) on replica r
+int listed_ok(Replica& r, const dw_model_desc* m, const dw_run_opts* o) {
     // DW_DIRECT=0: always the batched engine; =2: predict even on a graph
     // with sinks (tests of the short-walk -> batched re-run path)
     bool force = false;
@@ -906,7 +924,6 @@ int direct_ok(dw_graph_t g, const dw_model_desc* m, const dw_run_opts* o, ull nq
     // (dw_walk.cu DirectOk)
     if (m->kind != DW_MODEL_NODE2VEC || !model_params(m).pos_weights) return kDirectNo;
     if (o->mode != DW_MODE_ADAPTIVE && o->mode != DW_MODE_FORCE_ERJS) return kDirectNo;
-    Replica& r = g->reps[0];
     if (force) return DW_OK;
     if (r.sinks < 0) {
         CU(cudaSetDevice(r.device), "cudaSetDevice");
@@ -1031,7 +1048,7 @@ int run_direct(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries
     CU(cudaMemsetAsync(r.d_base, 0, sizeof(ull), ws), "memset");
     CU(dwb::path_offsets(d.len, nq, d.pos, r.d_base, r.d_scan, tb, ws), "scan");
     CU(dwb::walker_list(d.q, opts->qids ? d.qids : nullptr, opts->qid_base, nq, d.len, d.pos,
-                        d.offs, d.cq, d.cqid, d.coffs, ws),
+                        d.offs, 0, d.cq, d.cqid, d.coffs, ws),
        "walker list");
     CU(dwb::direct_bounds(d.coffs, r.d_base, d.offs + nq, shift, kMaxChunks, d.h_bounds, ws),
        "bounds");
@@ -1128,6 +1145,70 @@ int run_direct(dw_graph_t g, const dw_model_desc* model, const uint32_t* queries
         std::fprintf(stderr, "dynwalk direct: %llu chunks, before walk %.3f ms, walk %.3f ms, after %.3f ms\n",
                      (unsigned long long)nch, a, b, c);
     }
+    return DW_OK;
+}
+
+// dw_run_device when every path length is known before the walk (listed_ok):
+// `trivial_rows` writes every length (the predicted one) and the padded row
+// of each walker that does not move (start without neighbours: 56 % of the
+// s24 starts), and one walk over the
+// list of the others (`walker_list`, rows at i * stride, walker ids as RNG
+// keys) writes their rows: no claim or node gather for the walkers that
+// cannot move.  The host reads the list's length before the launch (the walk
+// sizes its grid by it).  dw_run_device_sync checks that no walk ended early
+// (steps - dead ends = listed walkers * target) and otherwise re-runs every
+// walker on the padded kernel.
+int run_device_listed(Replica& r, const dw_model_desc* model, const uint32_t* d_queries, ull nq,
+                      const dw_run_opts* opts, uint32_t* d_paths, uint32_t* d_lengths,
+                      cudaStream_t s) {
+    if (nq == 0) return kDirectNo;
+    int rc;
+    if ((rc = listed_ok(r, model, opts))) return rc;
+    if ((rc = direct_buffers(r, nq, 0, false))) return rc;
+    Replica::Direct& d = r.dir;
+    const uint32_t target = target_steps(model, opts);
+    const ull stride = (ull)opts->walk_length + 1;
+    // no memset of the rows: trivial_rows pads the rows of the walkers that
+    // do not move, and the walk fills every row of the others (no walk ends
+    // early here; the sync check re-runs on a memset buffer if one did)
+    CU(cudaMemsetAsync(r.d_base, 0, sizeof(ull), s), "memset");
+    CU(dwb::predict_lengths(d_queries, nq, r.g.nodes, r.g.nv, target, d.len, s), "predict");
+    CU(dwb::trivial_rows(d_queries, nq, d.len, d_paths, stride, d_lengths, r.counters, s),
+       "trivial rows");
+    size_t tb = r.scan_bytes;
+    CU(dwb::path_offsets(d.len, nq, d.pos, r.d_base, r.d_scan, tb, s), "scan");
+    CU(dwb::walker_list(d_queries, reinterpret_cast<const ull*>(opts->qids), opts->qid_base, nq,
+                        d.len, d.pos, nullptr, stride, d.cq, d.cqid, d.coffs, s),
+       "walker list");
+    ull nt = 0;
+    CU(cudaMemcpyAsync(&nt, r.d_base, sizeof(ull), cudaMemcpyDeviceToHost, s), "D2H");
+    CU(cudaStreamSynchronize(s), "walker list");
+    dwb::WalkParams p = make_params(r, model, opts);
+    p.queries = d.cq;
+    p.nq = nt;
+    p.qid_base = 0;
+    p.qids = d.cqid;
+    p.paths = d_paths;
+    p.lengths = nullptr;
+    p.next_walker = r.queues;
+    p.offs = d.coffs;  // kOutFlat kernel: rows at i * stride, no chunk counts
+    CU(cudaEventRecord(r.ev_start, s), "event");
+    if (nt) CU(launch_model(r, model, opts->mode, p, s), "walk");
+    CU(cudaEventRecord(r.ev_stop, s), "event");
+    Replica::Listed& l = r.listed;
+    l.on = true;
+    l.target = target;
+    l.model = *model;
+    l.opts = *opts;
+    l.queries = d_queries;
+    l.nq = nq;
+    l.paths = d_paths;
+    l.lengths = d_lengths;
+    l.stream = s;
+    l.nt = nt;
+    r.pending = true;
+    r.pending_launches = 6 + (nt ? 1 : 0);
+    r.pending_qbase = opts->qid_base;
     return DW_OK;
 }
 
@@ -1626,6 +1707,9 @@ int dw_run_device(dw_graph_t g, int replica, const dw_model_desc* model, const u
         CU(cudaEventRecord(r.ev_reset, r.stream), "event");
         CU(cudaStreamWaitEvent(s, r.ev_reset, 0), "event");
     }
+    r.listed.on = false;
+    rc = run_device_listed(r, model, d_queries, nq, opts, d_paths, d_lengths, s);
+    if (rc != kDirectNo) return rc;
     dwb::WalkParams p = make_params(r, model, opts);
     p.queries = d_queries;
     p.nq = nq;
@@ -1653,6 +1737,48 @@ int dw_run_device_sync(dw_graph_t g, int replica, dw_run_stats* st) {
     CU(cudaSetDevice(r.device), "cudaSetDevice");
     CU(cudaEventSynchronize(r.ev_stop), "walk");
     if (st) std::memset(st, 0, sizeof *st);
+    if (r.listed.on) {
+        // a listed walk (run_device_listed) is exact iff no walk ended early:
+        // steps that advanced = listed walkers * target (runtime.cpp:141-149)
+        Replica::Listed& l = r.listed;
+        l.on = false;
+        dw_run_stats cs;
+        std::memset(&cs, 0, sizeof cs);
+        int rc0 = collect(r, &cs, 0);
+        if (rc0) return rc0;
+        if (cs.steps - cs.dead_ends != l.nt * (ull)l.target) {
+            r.sinks = 1;  // do not list on this graph again; re-run every walker
+            if (const char* tp = std::getenv("DW_ENGINE_TRACE"))
+                if (FILE* f = std::fopen(tp, "a")) {
+                    std::fprintf(f, "L %llu retry\n", (unsigned long long)l.nq);
+                    std::fclose(f);
+                }
+            int rc1;
+            if ((rc1 = reset_run_state(r))) return rc1;
+            CU(cudaStreamSynchronize(r.stream), "reset");
+            dwb::WalkParams p = make_params(r, &l.model, &l.opts);
+            p.queries = l.queries;
+            p.nq = l.nq;
+            p.qid_base = l.opts.qid_base;
+            p.qids = reinterpret_cast<const ull*>(l.opts.qids);
+            p.paths = l.paths;
+            p.lengths = l.lengths;
+            p.next_walker = r.queues;
+            if (l.paths)
+                CU(cudaMemsetAsync(l.paths, 0xFF, l.nq * (ull)p.stride * sizeof(uint32_t), l.stream),
+                   "memset paths");
+            CU(cudaEventRecord(r.ev_start, l.stream), "event");
+            CU(launch_model(r, &l.model, l.opts.mode, p, l.stream), "walk");
+            CU(cudaEventRecord(r.ev_stop, l.stream), "event");
+            CU(cudaEventSynchronize(r.ev_stop), "walk");
+            r.pending_launches = 1;
+        } else if (std::getenv("DW_ENGINE_TRACE")) {
+            if (FILE* f = std::fopen(std::getenv("DW_ENGINE_TRACE"), "a")) {
+                std::fprintf(f, "L %llu ok\n", (unsigned long long)l.nq);
+                std::fclose(f);
+            }
+        }
+    }
     int rc = collect(r, st, r.pending_qbase);
     if (st) {
         float ms = 0.f;

@@ -1287,12 +1287,70 @@ cudaError_t trivial_walkers(const uint32_t* queries, ull n, uint32_t* lengths, c
     return cudaGetLastError();
 }
 
+// dw_run_device's listed walks: every walker's length (the predicted one:
+// exact where listed walks are used), the whole padded row of each walker
+// that does not move (its start or nothing, then 0xFFFFFFFF; a warp writes a
+// row with coalesced stores), queries / query errors counted; len[i] becomes
+// the "walks" flag.  The rows of the walkers that move are written whole by
+// the walk (no walk ends early there), so the rows need no memset.
+__global__ void trivial_rows_kernel(const uint32_t* __restrict__ q, ull n,
+                                    uint32_t* __restrict__ len, uint32_t* __restrict__ paths,
+                                    ull stride, uint32_t* __restrict__ lengths,
+                                    ull* __restrict__ counters) {
+    const int lane = threadIdx.x & 31;
+    uint32_t nq = 0, ne = 0;
+    const ull warps = (ull)gridDim.x * (blockDim.x >> 5);
+    for (ull w = (ull)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w * 32 < n; w += warps) {
+        const ull i = w * 32 + lane;
+        const uint32_t l = i < n ? len[i] : 2u;
+        const uint32_t v = i < n && l == 1 ? q[i] : 0xFFFFFFFFu;
+        if (i < n) {
+            if (lengths) lengths[i] = l;
+            nq += l <= 1;
+            ne += l == 0;
+            len[i] = l > 1;
+        }
+        if (paths) {
+            unsigned triv = __ballot_sync(0xFFFFFFFFu, l <= 1);
+            while (triv) {
+                const int b = __ffs(triv) - 1;
+                triv &= triv - 1;
+                const uint32_t vb = __shfl_sync(0xFFFFFFFFu, v, b);
+                uint32_t* row = paths + (w * 32 + b) * stride;
+                for (ull j = lane; j < stride; j += 32) row[j] = j == 0 ? vb : 0xFFFFFFFFu;
+            }
+        }
+    }
+    __shared__ uint32_t s_c[2];
+    if (threadIdx.x == 0) s_c[0] = s_c[1] = 0;
+    __syncthreads();
+    nq = __reduce_add_sync(0xFFFFFFFFu, nq);
+    ne = __reduce_add_sync(0xFFFFFFFFu, ne);
+    if (lane == 0) {
+        atomicAdd(&s_c[0], nq);
+        atomicAdd(&s_c[1], ne);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s_c[0]) atomicAdd(&counters[kCQueries], (ull)s_c[0]);
+        if (s_c[1]) atomicAdd(&counters[kCQueryErrors], (ull)s_c[1]);
+    }
+}
+
+cudaError_t trivial_rows(const uint32_t* queries, ull n, uint32_t* len, uint32_t* paths,
+                         ull stride, uint32_t* lengths, ull* counters, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    trivial_rows_kernel<<<grid_for(n, 256 * 4), 256, 0, s>>>(queries, n, len, paths, stride,
+                                                            lengths, counters);
+    return cudaGetLastError();
+}
+
 // The walking walkers, in query order: cq / cqid / coffs[pos[i]] = query,
 // global walker id (RNG key) and flat offset of every i with flag[i] set.
 __global__ void walker_list_kernel(const uint32_t* __restrict__ q, const ull* __restrict__ qids,
                                    ull qid_base, ull n, const uint32_t* __restrict__ flag,
                                    const ull* __restrict__ pos, const ull* __restrict__ offs,
-                                   uint32_t* __restrict__ cq, ull* __restrict__ cqid,
+                                   ull stride, uint32_t* __restrict__ cq, ull* __restrict__ cqid,
                                    ull* __restrict__ coffs) {
     for (ull i = (ull)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (ull)gridDim.x * blockDim.x) {
@@ -1300,16 +1358,16 @@ __global__ void walker_list_kernel(const uint32_t* __restrict__ q, const ull* __
         const ull j = pos[i];
         cq[j] = q[i];
         cqid[j] = qids ? qids[i] : qid_base + i;
-        coffs[j] = offs[i];
+        coffs[j] = offs ? offs[i] : i * stride;
     }
 }
 
 cudaError_t walker_list(const uint32_t* queries, const ull* qids, ull qid_base, ull n,
-                        const uint32_t* flag, const ull* pos, const ull* offs, uint32_t* cq,
-                        ull* cqid, ull* coffs, cudaStream_t s) {
+                        const uint32_t* flag, const ull* pos, const ull* offs, ull stride,
+                        uint32_t* cq, ull* cqid, ull* coffs, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     walker_list_kernel<<<grid_for(n, 256 * 8), 256, 0, s>>>(queries, qids, qid_base, n, flag, pos,
-                                                           offs, cq, cqid, coffs);
+                                                           offs, stride, cq, cqid, coffs);
     return cudaGetLastError();
 }
 

@@ -121,12 +121,18 @@ cudaError_t trivial_walkers(const uint32_t* queries, unsigned long long n, uint3
                             const unsigned long long* offs, uint32_t* flat,
                             unsigned long long* counters, cudaStream_t s);
 // cq / cqid / coffs[pos[i]] = queries[i], its walker id (qids[i] or
-// qid_base + i) and offs[i] for every i with flag[i] set
+// qid_base + i) and offs[i] (offs null: i * stride) for every i with flag[i]
 cudaError_t walker_list(const uint32_t* queries, const unsigned long long* qids,
                         unsigned long long qid_base, unsigned long long n, const uint32_t* flag,
                         const unsigned long long* pos, const unsigned long long* offs,
-                        uint32_t* cq, unsigned long long* cqid, unsigned long long* coffs,
-                        cudaStream_t s);
+                        unsigned long long stride, uint32_t* cq, unsigned long long* cqid,
+                        unsigned long long* coffs, cudaStream_t s);
+// dw_run_device's listed walks: lengths[i] = len[i] (predicted), paths[i *
+// stride] = queries[i] for length-1 walkers, queries / query errors counted,
+// len[i] <- (len[i] > 1)
+cudaError_t trivial_rows(const uint32_t* queries, unsigned long long n, uint32_t* len,
+                         uint32_t* paths, unsigned long long stride, uint32_t* lengths,
+                         unsigned long long* counters, cudaStream_t s);
 // chunk copy ranges of a direct run (see dw_graph.cu direct_bounds_kernel)
 cudaError_t direct_bounds(const unsigned long long* coffs, const unsigned long long* d_nt,
                           const unsigned long long* total, uint32_t shift, unsigned long long kmax,

@@ -1285,7 +1285,8 @@ __global__ void __launch_bounds__(kThreads, WideKernel<M, MODE>::value ? DW_ERVS
         // ---- walks that ended last iteration (end_walk)
         if constexpr (OUT != kOutPadded)
             if (phase == P_DONE) {
-                sm.dchunk[tid] = (uint16_t)(sm.qi[tid] >> p.chunk_shift);
+                // (no chunk counts: dw_run_device's listed walkers)
+                if (p.chunk_done) sm.dchunk[tid] = (uint16_t)(sm.qi[tid] >> p.chunk_shift);
                 phase = P_IDLE;
             }
         // ---- refill idle lanes: one atomic per warp (runtime.cpp:209-211)

@@ -182,6 +182,83 @@ def test_run_device_entry_point(dw, orc):
     assert st.steps == r_orc.stats["steps"] and st.kernel_ms > 0
 
 
+def _run_device(dw, dg, q, model, opts, paths=True, qids=None):
+    """dw_run_device on cuda:0 (device queries, padded rows and lengths)."""
+    import ctypes as C
+    import torch
+    L = opts.walk_length
+    dq = torch.from_numpy(q.view(np.int32)).cuda()
+    dp = torch.empty((len(q), L + 1), dtype=torch.int32, device="cuda") if paths else None
+    dl = torch.empty(len(q), dtype=torch.int32, device="cuda")
+    if qids is not None:
+        dqid = torch.from_numpy(qids.view(np.int64)).cuda()
+        opts.qids = dqid.data_ptr()
+    lib = dw.load_library()
+    m = model.c()
+    o = opts.c()
+    torch.cuda.synchronize()
+    assert lib.dw_run_device(dg.h, 0, C.byref(m), C.c_void_p(dq.data_ptr()), len(q), C.byref(o),
+                             C.c_void_p(dp.data_ptr() if paths else None),
+                             C.c_void_p(dl.data_ptr()), None) == 0
+    st = dw.RunStatsC()
+    assert lib.dw_run_device_sync(dg.h, 0, C.byref(st)) == 0
+    opts.qids = None
+    return (dp.cpu().numpy().view(np.uint32) if paths else None,
+            dl.cpu().numpy().view(np.uint32), st.as_dict())
+
+
+@pytest.mark.parametrize("mode", ["adaptive", "force-erjs"])
+def test_run_device_listed_walkers(dw, orc, mode, tmp_path):
+    """dw_run_device walks only the walkers that can move when every length
+    is known before the walk (trace "L nq ok"): padded rows, lengths and
+    counters equal the every-walker launch (DW_DIRECT=0) and the oracle,
+    with invalid and isolated starts, explicit walker ids, qid_base and
+    discarded paths; on a graph with sinks, forced listing (DW_DIRECT=2) is
+    detected and re-run on every walker ("L nq retry")."""
+    og = orc.Graph.rmat(13, 16, 21).synth_philox("uniform", 1.0, 5.0, seed=22)
+    dg = to_device(dw, og)
+    rng = np.random.default_rng(12)
+    q = rng.integers(0, og.nv + 40, 400_000).astype(np.uint32)
+    model = dw.Model(kind="node2vec", a=0.5, b=2.0)
+    trace = str(tmp_path / "trace.txt")
+    qids = rng.permutation(4 * len(q))[:len(q)].astype(np.uint64)
+    for kw, qd in ((dict(), None), (dict(qid_base=77_777), None), (dict(), qids)):
+        opts = dw.RunOptions(mode=mode, walk_length=30, seed=6, edge_cost_ratio=1.3, **kw)
+        if os.path.exists(trace):
+            os.remove(trace)
+        a = _with_env({"DW_ENGINE_TRACE": trace}, lambda: _run_device(dw, dg, q, model, opts,
+                                                                      qids=qd))
+        assert open(trace).read().split() == ["L", str(len(q)), "ok"]
+        b = _with_env({"DW_DIRECT": "0"}, lambda: _run_device(dw, dg, q, model, opts, qids=qd))
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]), kw
+        assert stats_core(a[2]) == stats_core(b[2]), kw
+        assert a[2]["queries"] == b[2]["queries"] and a[2]["query_errors"] == b[2]["query_errors"]
+    r_orc = orc.run(og, orc.Model(kind="node2vec", a=0.5, b=2.0), q[:30_000], mode=mode,
+                    walk_length=30, seed=6, ratio=1.3, rng="philox", threads=4)
+    opts = dw.RunOptions(mode=mode, walk_length=30, seed=6, edge_cost_ratio=1.3)
+    p, l, _ = _run_device(dw, dg, q[:30_000], model, opts)
+    assert np.array_equal(p, r_orc.paths) and np.array_equal(l, r_orc.lengths)
+    _, l2, st2 = _run_device(dw, dg, q[:30_000], model, opts, paths=False)
+    assert np.array_equal(l2, r_orc.lengths) and st2["steps"] == r_orc.stats["steps"]
+    # a directed graph with sinks: listing forced, detected, re-run
+    src = rng.integers(0, 3000, 20000).astype(np.uint32)
+    dst = rng.integers(0, 3000, 20000).astype(np.uint32)
+    keep = src % 5 != 0
+    g2 = orc.Graph.build(src[keep], dst[keep], rng.uniform(1, 5, keep.sum()).astype(np.float32),
+                         mirror=False, nv_hint=3000)
+    dg2 = to_device(dw, g2)
+    q2 = np.arange(g2.nv, dtype=np.uint32).repeat(20)
+    opts = dw.RunOptions(mode=mode, walk_length=25, seed=2, edge_cost_ratio=1.3)
+    if os.path.exists(trace):
+        os.remove(trace)
+    a = _with_env({"DW_DIRECT": "2", "DW_ENGINE_TRACE": trace},
+                  lambda: _run_device(dw, dg2, q2, model, opts))
+    assert open(trace).read().split() == ["L", str(len(q2)), "retry"]
+    b = _with_env({"DW_DIRECT": "0"}, lambda: _run_device(dw, dg2, q2, model, opts))
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert stats_core(a[2]) == stats_core(b[2])
+
+
 def test_chi_square_transition_frequencies(dw, orc):
     """Per-(prev,cur) transition counts vs oracle_enumerate (samplers.hpp:272-288), p > 0.01."""
     from scipy.stats import chisquare
