@@ -218,7 +218,7 @@ def test_run_device_listed_walkers(dw, orc, mode, tmp_path):
     og = orc.Graph.rmat(13, 16, 21).synth_philox("uniform", 1.0, 5.0, seed=22)
     dg = to_device(dw, og)
     rng = np.random.default_rng(12)
-    q = rng.integers(0, og.nv + 40, 400_000).astype(np.uint32)
+    q = rng.integers(0, og.nv + 40, 1_200_000).astype(np.uint32)  # listing needs >= 2^20
     model = dw.Model(kind="node2vec", a=0.5, b=2.0)
     trace = str(tmp_path / "trace.txt")
     qids = rng.permutation(4 * len(q))[:len(q)].astype(np.uint64)
@@ -236,10 +236,10 @@ def test_run_device_listed_walkers(dw, orc, mode, tmp_path):
     r_orc = orc.run(og, orc.Model(kind="node2vec", a=0.5, b=2.0), q[:30_000], mode=mode,
                     walk_length=30, seed=6, ratio=1.3, rng="philox", threads=4)
     opts = dw.RunOptions(mode=mode, walk_length=30, seed=6, edge_cost_ratio=1.3)
-    p, l, _ = _run_device(dw, dg, q[:30_000], model, opts)
-    assert np.array_equal(p, r_orc.paths) and np.array_equal(l, r_orc.lengths)
-    _, l2, st2 = _run_device(dw, dg, q[:30_000], model, opts, paths=False)
-    assert np.array_equal(l2, r_orc.lengths) and st2["steps"] == r_orc.stats["steps"]
+    p, l, st1 = _run_device(dw, dg, q, model, opts)  # listed; walker ids = indices
+    assert np.array_equal(p[:30_000], r_orc.paths) and np.array_equal(l[:30_000], r_orc.lengths)
+    _, l2, st2 = _run_device(dw, dg, q, model, opts, paths=False)
+    assert np.array_equal(l2, l) and st2["steps"] == st1["steps"]
     # a directed graph with sinks: listing forced, detected, re-run
     src = rng.integers(0, 3000, 20000).astype(np.uint32)
     dst = rng.integers(0, 3000, 20000).astype(np.uint32)
@@ -247,7 +247,7 @@ def test_run_device_listed_walkers(dw, orc, mode, tmp_path):
     g2 = orc.Graph.build(src[keep], dst[keep], rng.uniform(1, 5, keep.sum()).astype(np.float32),
                          mirror=False, nv_hint=3000)
     dg2 = to_device(dw, g2)
-    q2 = np.arange(g2.nv, dtype=np.uint32).repeat(20)
+    q2 = np.arange(g2.nv, dtype=np.uint32).repeat(400)
     opts = dw.RunOptions(mode=mode, walk_length=25, seed=2, edge_cost_ratio=1.3)
     if os.path.exists(trace):
         os.remove(trace)
