@@ -241,7 +241,13 @@ int dw_run_write_paths(dw_graph_t g, const dw_model_desc* model, const uint32_t*
 /* Device-resident variant on replica `replica`: d_queries / d_paths /
  * d_lengths are device pointers on that device (d_paths, d_lengths may be
  * NULL), `stream` a cudaStream_t (NULL = the replica's stream).  Enqueues and
- * returns; stats are valid after dw_run_device_sync. */
+ * returns; stats are valid after dw_run_device_sync.  When every path length
+ * is known before the walk (node2vec with a, b > 0, adaptive or force-erjs,
+ * no edge into a vertex without neighbours, >= 2^20 queries) the walkers that
+ * cannot move are written first and the walk runs over the others; the call
+ * then waits for that ~1 ms pre-pass (the walk's grid is sized by its count)
+ * before it enqueues the walk, and dw_run_device_sync verifies the lengths
+ * (re-running every walker if one walk ended early). */
 int dw_run_device(dw_graph_t g, int replica, const dw_model_desc* model,
                   const uint32_t* d_queries, uint64_t nq, const dw_run_opts* opts,
                   uint32_t* d_paths, uint32_t* d_lengths, void* stream);
